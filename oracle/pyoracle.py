@@ -1,0 +1,642 @@
+"""pyoracle -- TEST INFRASTRUCTURE ONLY.
+
+numpy/ctypes front-end over the two CPU checkers in this directory:
+
+* ``liboracle.so``            -- the plain-C restatement (bitgnn_oracle.c);
+* ``_ref/libbitgnn_ref.so``   -- the unmodified reference library compiled
+                                 from /root/reference/proj/src (ref_capi.cpp).
+
+Only tests/, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs import this module.  The product package
+(paper_2305_02522_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libbitgnn_ref.so")
+
+F, B = 0, 1
+BMM, BSPMM, ADD, CONCAT = 0, 1, 2, 3
+ROW, COL = 0, 1
+GCN, SAGE, GRAPHCONV, FC, SOFTMAX = 0, 1, 2, 3, 7
+
+
+def build(quiet: bool = True) -> None:
+    """Compile liboracle.so (and _ref when the reference sources exist)."""
+    out = subprocess.run(["make", "-C", HERE, "-j8", "all"], capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("oracle build failed:\n" + out.stdout + out.stderr)
+    if not quiet:
+        print(out.stdout)
+
+
+def spw(cols: int, word_bits: int) -> int:
+    """Storage u32 words per packed row (bitdense.hpp:72-73)."""
+    return (cols + word_bits - 1) // word_bits * (word_bits // 32)
+
+
+# --------------------------------------------------------------------------- #
+# ctypes plumbing for liboracle.so
+# --------------------------------------------------------------------------- #
+class _Rng(C.Structure):
+    _fields_ = [("mt", C.c_uint64 * 312), ("idx", C.c_int)]
+
+
+class _Frdc(C.Structure):
+    _fields_ = [("rows", C.c_int64), ("cols", C.c_int64), ("nnz", C.c_int64),
+                ("row_ptr", C.POINTER(C.c_uint64)), ("col_ind", C.POINTER(C.c_uint32)),
+                ("tiles", C.POINTER(C.c_uint16))]
+
+
+class _Variant(C.Structure):
+    _fields_ = [("op", C.c_int), ("in1", C.c_int), ("in2", C.c_int), ("out", C.c_int)]
+
+
+class _Mat(C.Structure):
+    _fields_ = [("prec", C.c_int), ("rows", C.c_int64), ("cols", C.c_int64),
+                ("word_bits", C.c_int), ("f", C.POINTER(C.c_float)),
+                ("bits", C.POINTER(C.c_uint32)), ("scale", C.POINTER(C.c_float))]
+
+
+class _Graph(C.Structure):
+    _fields_ = [("n", C.c_int64), ("structure", _Frdc), ("raw", _Frdc),
+                ("norm", C.POINTER(C.c_float)), ("mean_row", C.POINTER(C.c_float)),
+                ("ones", C.POINTER(C.c_float)), ("neighbor_count", C.POINTER(C.c_int64))]
+
+
+class _Layer(C.Structure):
+    _fields_ = [("kind", C.c_int), ("nplan", C.c_int), ("plan", _Variant * 4),
+                ("w1", C.POINTER(C.c_float)), ("w1_rows", C.c_int64), ("w1_cols", C.c_int64),
+                ("w2", C.POINTER(C.c_float)), ("w2_rows", C.c_int64), ("w2_cols", C.c_int64),
+                ("relu", C.c_int)]
+
+
+_TRACE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_char_p, C.POINTER(C.c_uint32), C.c_int64,
+                        C.c_int64, C.c_int)
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(ORACLE_SO):
+            build()
+        L = C.CDLL(ORACLE_SO)
+        L.og_rng_seed.argtypes = [C.POINTER(_Rng), C.c_uint64]
+        L.og_rng_next.restype = C.c_uint64
+        L.og_rng_next.argtypes = [C.POINTER(_Rng)]
+        L.og_rng_uniform.restype = C.c_double
+        L.og_rng_uniform.argtypes = [C.POINTER(_Rng)]
+        L.og_rng_index.restype = C.c_int64
+        L.og_rng_index.argtypes = [C.POINTER(_Rng), C.c_int64]
+        L.og_random_dense.argtypes = [C.POINTER(_Rng), C.c_int64, C.c_int64, C.c_void_p]
+        L.og_random_edges.restype = C.c_int64
+        L.og_random_edges.argtypes = [C.POINTER(_Rng), C.c_int64, C.c_int64, C.c_int,
+                                      C.c_void_p, C.c_void_p]
+        L.og_spw.restype = C.c_int64
+        L.og_binarize.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+        L.og_l1_scales.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+        L.og_transpose_bits.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+        L.og_frdc_from_edges.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_int,
+                                         C.POINTER(_Frdc), C.POINTER(C.c_int64)]
+        L.og_frdc_free.argtypes = [C.POINTER(_Frdc)]
+        L.og_row_popcounts.argtypes = [C.POINTER(_Frdc), C.c_void_p]
+        L.og_mat_free.argtypes = [C.POINTER(_Mat)]
+        L.og_bmm.argtypes = [_Variant, C.POINTER(_Mat), C.POINTER(_Mat), C.c_int, C.POINTER(_Mat)]
+        L.og_bspmm.argtypes = [_Variant, C.POINTER(_Frdc), C.c_void_p, C.c_void_p,
+                               C.POINTER(_Mat), C.c_int, C.POINTER(_Mat)]
+        L.og_add.argtypes = [_Variant, C.POINTER(_Mat), C.POINTER(_Mat), C.POINTER(_Mat)]
+        L.og_relu.argtypes = [C.POINTER(_Mat)]
+        L.og_softmax_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]
+        L.og_error.restype = C.c_char_p
+        L.og_prepare_graph.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
+                                       C.POINTER(_Graph)]
+        L.og_graph_free.argtypes = [C.POINTER(_Graph)]
+        L.og_run_model.argtypes = [C.POINTER(_Layer), C.c_int, C.c_int, C.POINTER(_Graph),
+                                   C.c_void_p, C.c_int64, C.c_int64,
+                                   C.POINTER(C.POINTER(C.c_float)), C.POINTER(C.POINTER(C.c_float)),
+                                   C.POINTER(C.c_int64), _TRACE_FN, C.c_void_p]
+        L.og_free.argtypes = [C.c_void_p]
+        _lib = L
+    return _lib
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _err() -> str:
+    return lib().og_error().decode()
+
+
+# --------------------------------------------------------------------------- #
+# rng.hpp
+# --------------------------------------------------------------------------- #
+class Rng:
+    """std::mt19937_64 + the reference's mappings (rng.hpp:16-80)."""
+
+    def __init__(self, seed: int):
+        self._s = _Rng()
+        lib().og_rng_seed(C.byref(self._s), C.c_uint64(seed))
+
+    def next(self) -> int:
+        return lib().og_rng_next(C.byref(self._s))
+
+    def uniform(self) -> float:
+        return lib().og_rng_uniform(C.byref(self._s))
+
+    def index(self, n: int) -> int:
+        return lib().og_rng_index(C.byref(self._s), n)
+
+    def range(self, lo: int, hi: int) -> int:
+        return lo + self.index(hi - lo + 1)
+
+    def random_dense(self, rows: int, cols: int) -> np.ndarray:
+        out = np.empty((rows, cols), dtype=np.float32)
+        lib().og_random_dense(C.byref(self._s), rows, cols, _ptr(out))
+        return out
+
+    def random_edges(self, nodes: int, m: int, allow_self: bool = False) -> Tuple[np.ndarray, np.ndarray]:
+        src = np.empty(max(m, 1), dtype=np.int64)
+        dst = np.empty(max(m, 1), dtype=np.int64)
+        k = lib().og_random_edges(C.byref(self._s), nodes, m, int(allow_self), _ptr(src), _ptr(dst))
+        return src[:k].copy(), dst[:k].copy()
+
+
+# --------------------------------------------------------------------------- #
+# bitdense / bitsparse
+# --------------------------------------------------------------------------- #
+def binarize(x: np.ndarray, word_bits: int = 32) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    rows, cols = x.shape
+    out = np.empty((rows, spw(cols, word_bits)), dtype=np.uint32)
+    lib().og_binarize(_ptr(x), rows, cols, word_bits, _ptr(out))
+    return out
+
+
+def l1_scales(x: np.ndarray, axis: int) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    rows, cols = x.shape
+    out = np.empty(rows if axis == ROW else cols, dtype=np.float32)
+    lib().og_l1_scales(_ptr(x), rows, cols, axis, _ptr(out))
+    return out
+
+
+def transpose_bits(bits: np.ndarray, rows: int, cols: int, word_bits: int = 32) -> np.ndarray:
+    bits = np.ascontiguousarray(bits, dtype=np.uint32)
+    out = np.empty((cols, spw(rows, word_bits)), dtype=np.uint32)
+    lib().og_transpose_bits(_ptr(bits), rows, cols, word_bits, _ptr(out))
+    return out
+
+
+@dataclass
+class Frdc:
+    rows: int
+    cols: int
+    row_ptr: np.ndarray
+    col_ind: np.ndarray
+    tiles: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.tiles.shape[0])
+
+    def nnz_bits(self) -> int:
+        return int(np.unpackbits(self.tiles.view(np.uint8)).sum())
+
+    def _c(self) -> _Frdc:
+        s = _Frdc()
+        s.rows, s.cols, s.nnz = self.rows, self.cols, self.nnz
+        s.row_ptr = self.row_ptr.ctypes.data_as(C.POINTER(C.c_uint64))
+        s.col_ind = self.col_ind.ctypes.data_as(C.POINTER(C.c_uint32))
+        s.tiles = self.tiles.ctypes.data_as(C.POINTER(C.c_uint16))
+        return s
+
+    def row_popcounts(self) -> np.ndarray:
+        deg = np.empty(self.rows, dtype=np.int64)
+        s = self._c()
+        lib().og_row_popcounts(C.byref(s), _ptr(deg))
+        return deg
+
+
+def _frdc_copy(s: _Frdc) -> Frdc:
+    tr = (s.rows + 3) // 4
+    rp = np.ctypeslib.as_array(s.row_ptr, shape=(tr + 1,)).copy()
+    if s.nnz:
+        ci = np.ctypeslib.as_array(s.col_ind, shape=(s.nnz,)).copy()
+        ti = np.ctypeslib.as_array(s.tiles, shape=(s.nnz,)).copy()
+    else:
+        ci = np.zeros(0, dtype=np.uint32)
+        ti = np.zeros(0, dtype=np.uint16)
+    return Frdc(s.rows, s.cols, rp, ci, ti)
+
+
+def frdc_from_edges(n: int, src: np.ndarray, dst: np.ndarray, self_loops: bool) -> Frdc:
+    src = np.ascontiguousarray(src, dtype=np.int64)
+    dst = np.ascontiguousarray(dst, dtype=np.int64)
+    s = _Frdc()
+    bad = C.c_int64(-1)
+    rc = lib().og_frdc_from_edges(n, _ptr(src), _ptr(dst), src.shape[0], int(self_loops),
+                                  C.byref(s), C.byref(bad))
+    if rc:
+        raise ValueError(f"edge {bad.value} out of range for {n} nodes")
+    out = _frdc_copy(s)
+    lib().og_frdc_free(C.byref(s))
+    return out
+
+
+# --------------------------------------------------------------------------- #
+# kernels.cpp
+# --------------------------------------------------------------------------- #
+_OPS = {"BMM": BMM, "MM": BMM, "BSPMM": BSPMM, "ADD": ADD, "CONCAT": CONCAT}
+
+
+def parse_variant(text: str) -> Tuple[int, int, int, int]:
+    op, tags = text.split(".")
+    p = [F if c in "Ff" else B for c in tags]
+    return (_OPS[op.upper()], p[0], p[1], p[2])
+
+
+def _variant(v) -> _Variant:
+    if isinstance(v, str):
+        v = parse_variant(v)
+    return _Variant(*v)
+
+
+@dataclass
+class Mat:
+    """F operand (f: float32 rows x cols) or B operand (bits: u32 rows x spw)."""
+    prec: int
+    rows: int
+    cols: int
+    word_bits: int = 32
+    f: Optional[np.ndarray] = None
+    bits: Optional[np.ndarray] = None
+    scale: Optional[np.ndarray] = None
+
+    @staticmethod
+    def dense(x: np.ndarray) -> "Mat":
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        return Mat(F, x.shape[0], x.shape[1], 32, f=x)
+
+    @staticmethod
+    def binary(bits: np.ndarray, rows: int, cols: int, word_bits: int = 32,
+               scale: Optional[np.ndarray] = None) -> "Mat":
+        return Mat(B, rows, cols, word_bits, bits=np.ascontiguousarray(bits, dtype=np.uint32),
+                   scale=None if scale is None else np.ascontiguousarray(scale, dtype=np.float32))
+
+    def _c(self) -> _Mat:
+        m = _Mat()
+        m.prec, m.rows, m.cols, m.word_bits = self.prec, self.rows, self.cols, self.word_bits
+        if self.f is not None:
+            m.f = self.f.ctypes.data_as(C.POINTER(C.c_float))
+        if self.bits is not None:
+            m.bits = self.bits.ctypes.data_as(C.POINTER(C.c_uint32))
+        if self.scale is not None:
+            m.scale = self.scale.ctypes.data_as(C.POINTER(C.c_float))
+        return m
+
+
+def _take(m: _Mat) -> Mat:
+    if m.prec == F:
+        f = np.ctypeslib.as_array(m.f, shape=(m.rows * m.cols,)).reshape(m.rows, m.cols).copy() \
+            if m.rows * m.cols else np.zeros((m.rows, m.cols), np.float32)
+        out = Mat(F, m.rows, m.cols, m.word_bits, f=f)
+    else:
+        n = m.rows * spw(m.cols, m.word_bits)
+        bits = np.ctypeslib.as_array(m.bits, shape=(n,)).reshape(m.rows, -1).copy() \
+            if n else np.zeros((m.rows, spw(m.cols, m.word_bits)), np.uint32)
+        out = Mat(B, m.rows, m.cols, m.word_bits, bits=bits)
+    lib().og_mat_free(C.byref(m))
+    return out
+
+
+def bmm(v, a: Mat, w: Mat, word_bits: int = 32) -> Mat:
+    ca, cw, out = a._c(), w._c(), _Mat()
+    if lib().og_bmm(_variant(v), C.byref(ca), C.byref(cw), word_bits, C.byref(out)):
+        raise ValueError(_err())
+    return _take(out)
+
+
+def bspmm(v, adj: Frdc, x: Mat, row_scale: Optional[np.ndarray] = None,
+          col_scale: Optional[np.ndarray] = None, word_bits: int = 32) -> Mat:
+    cadj, cx, out = adj._c(), x._c(), _Mat()
+    if lib().og_bspmm(_variant(v), C.byref(cadj), _ptr(row_scale), _ptr(col_scale), C.byref(cx),
+                      word_bits, C.byref(out)):
+        raise ValueError(_err())
+    return _take(out)
+
+
+def add(v, a: Mat, b: Mat) -> Mat:
+    ca, cb, out = a._c(), b._c(), _Mat()
+    if lib().og_add(_variant(v), C.byref(ca), C.byref(cb), C.byref(out)):
+        raise ValueError(_err())
+    return _take(out)
+
+
+def softmax_rows(x: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty_like(x)
+    lib().og_softmax_rows(_ptr(x), x.shape[0], x.shape[1], _ptr(out))
+    return out
+
+
+# --------------------------------------------------------------------------- #
+# graphops.cpp / modelconfig.cpp
+# --------------------------------------------------------------------------- #
+class Graph:
+    """prepare_graph (graphops.cpp:146-170)."""
+
+    def __init__(self, n: int, src: np.ndarray, dst: np.ndarray):
+        self.n = n
+        self._src = np.ascontiguousarray(src, dtype=np.int64)
+        self._dst = np.ascontiguousarray(dst, dtype=np.int64)
+        self._g = _Graph()
+        if lib().og_prepare_graph(n, _ptr(self._src), _ptr(self._dst), self._src.shape[0],
+                                  C.byref(self._g)):
+            raise ValueError(_err())
+        self.structure = _frdc_copy(self._g.structure)
+        self.raw = _frdc_copy(self._g.raw)
+        self.norm = np.ctypeslib.as_array(self._g.norm, shape=(n,)).copy() if n else np.zeros(0, np.float32)
+        self.mean_row = np.ctypeslib.as_array(self._g.mean_row, shape=(n,)).copy() if n else np.zeros(0, np.float32)
+        self.neighbor_count = np.ctypeslib.as_array(self._g.neighbor_count, shape=(n,)).copy() if n else np.zeros(0, np.int64)
+
+    def __del__(self):
+        try:
+            lib().og_graph_free(C.byref(self._g))
+        except Exception:
+            pass
+
+
+@dataclass
+class Layer:
+    kind: int
+    plan: List[str] = field(default_factory=list)
+    w1: Optional[np.ndarray] = None
+    w2: Optional[np.ndarray] = None
+    relu: bool = False
+
+
+DEFAULT_PLANS = {  # modelconfig.cpp:49-60
+    "gcn": ["MM.FBB+BSpMM.BBB", "MM.BBF+BSpMM.FBF"],
+    "sage": ["MM.FBB+MM.FBB+BSpMM.BBB+ADD.BBF", "MM.FBF+MM.FBF+BSpMM.FFF+ADD.FFF"],
+    "saint": ["MM.FBB+MM.FBB+BSpMM.BBB+ADD.BBF", "MM.FBB+MM.FBB+BSpMM.BBB+ADD.BBF", "MM.FBF"],
+}
+
+
+def build_model(model: str, features: int, hidden: int, classes: int, seed: int, nodes: int,
+                plan: Optional[Sequence[str]] = None) -> Tuple[List[Layer], np.ndarray]:
+    """build_model (modelconfig.cpp:99-173): X first, then W1 (and W2) per
+    layer from one mt19937_64 stream; softmax appended."""
+    plan = list(plan) if plan else DEFAULT_PLANS[model]
+    rng = Rng(seed)
+    X = rng.random_dense(nodes, features)
+
+    def dims(n):
+        d, fin = [], features
+        for i in range(n):
+            fout = classes if i + 1 == n else hidden
+            d.append((fin, fout))
+            fin = fout
+        return d
+
+    layers: List[Layer] = []
+    if model == "gcn":
+        dd = dims(len(plan))
+        for i, chain in enumerate(plan):
+            w1 = rng.random_dense(*dd[i])
+            layers.append(Layer(GCN, chain.split("+"), w1, None, i + 1 < len(plan)))
+    else:
+        conv = len(plan) - 1 if model == "saint" else len(plan)
+        dd = dims(conv + (1 if model == "saint" else 0))
+        for i in range(conv):
+            w1 = rng.random_dense(*dd[i])
+            w2 = rng.random_dense(*dd[i])
+            layers.append(Layer(SAGE if model == "sage" else GRAPHCONV, plan[i].split("+"), w1, w2, True))
+        if model == "saint":
+            layers.append(Layer(FC, plan[-1].split("+"), rng.random_dense(*dd[-1]), None, False))
+        else:
+            layers[-1].relu = False
+    layers.append(Layer(SOFTMAX))
+    return layers, X
+
+
+@dataclass
+class TracePoint:
+    label: str
+    bits: np.ndarray
+    rows: int
+    cols: int
+    word_bits: int
+
+
+def run_model(layers: Sequence[Layer], graph: Optional[Graph], x0: np.ndarray, word_bits: int = 32,
+              trace: bool = True):
+    """run_model (graphops.cpp:390-484).  Returns (out, logits, trace points)."""
+    x0 = np.ascontiguousarray(x0, dtype=np.float32)
+    cl = (_Layer * len(layers))()
+    keep = []
+    for i, l in enumerate(layers):
+        cl[i].kind = l.kind
+        cl[i].nplan = len(l.plan)
+        for k, p in enumerate(l.plan):
+            cl[i].plan[k] = _variant(p)
+        for name in ("w1", "w2"):
+            w = getattr(l, name)
+            if w is not None:
+                w = np.ascontiguousarray(w, dtype=np.float32)
+                keep.append(w)
+                setattr(cl[i], name, w.ctypes.data_as(C.POINTER(C.c_float)))
+                setattr(cl[i], name + "_rows", w.shape[0])
+                setattr(cl[i], name + "_cols", w.shape[1])
+        cl[i].relu = int(l.relu)
+    points: List[TracePoint] = []
+
+    def sink(_ctx, label, bits, rows, cols, wb):
+        n = rows * spw(cols, wb)
+        arr = np.ctypeslib.as_array(bits, shape=(n,)).reshape(rows, -1).copy() if n else \
+            np.zeros((rows, spw(cols, wb)), np.uint32)
+        points.append(TracePoint(label.decode(), arr, rows, cols, wb))
+
+    cb = _TRACE_FN(sink) if trace else _TRACE_FN()
+    out_p, log_p = C.POINTER(C.c_float)(), C.POINTER(C.c_float)()
+    oc = C.c_int64(0)
+    gp = C.byref(graph._g) if graph is not None else None
+    rc = lib().og_run_model(cl, len(layers), word_bits, gp, _ptr(x0), x0.shape[0], x0.shape[1],
+                            C.byref(out_p), C.byref(log_p), C.byref(oc), cb, None)
+    if rc:
+        raise ValueError(_err())
+    rows = x0.shape[0]
+    out = np.ctypeslib.as_array(out_p, shape=(rows * oc.value,)).reshape(rows, -1).copy()
+    logits = np.ctypeslib.as_array(log_p, shape=(rows * oc.value,)).reshape(rows, -1).copy()
+    lib().og_free(C.cast(out_p, C.c_void_p))
+    lib().og_free(C.cast(log_p, C.c_void_p))
+    return out, logits, points
+
+
+# --------------------------------------------------------------------------- #
+# The real reference (oracle/_ref) -- present when built in the dev container.
+# --------------------------------------------------------------------------- #
+_ref = None
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref() -> C.CDLL:
+    global _ref
+    if _ref is None:
+        if not os.path.exists(REF_SO):
+            raise FileNotFoundError(REF_SO)
+        L = C.CDLL(REF_SO)
+        L.ref_error.restype = C.c_char_p
+        L.ref_max_threads.restype = C.c_int
+        L.ref_set_threads.argtypes = [C.c_int]
+        L.ref_random_edges.restype = C.c_int64
+        L.ref_random_edges.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_void_p]
+        L.ref_random_dense.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_void_p]
+        L.ref_graph_create.restype = C.c_void_p
+        L.ref_graph_create.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int64]
+        L.ref_graph_free.argtypes = [C.c_void_p]
+        L.ref_graph_frdc.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int64),
+                                     C.POINTER(C.POINTER(C.c_uint64)), C.POINTER(C.POINTER(C.c_uint32)),
+                                     C.POINTER(C.POINTER(C.c_uint16))]
+        L.ref_graph_scales.argtypes = [C.c_void_p, C.POINTER(C.POINTER(C.c_float)),
+                                       C.POINTER(C.POINTER(C.c_float)), C.POINTER(C.POINTER(C.c_int64))]
+        L.ref_model_build.restype = C.c_void_p
+        L.ref_model_build.argtypes = [C.c_void_p, C.c_char_p, C.c_int64, C.c_int64, C.c_int64,
+                                      C.c_uint64, C.c_int, C.c_char_p, C.c_int64]
+        L.ref_model_free.argtypes = [C.c_void_p]
+        L.ref_model_features.restype = C.POINTER(C.c_float)
+        L.ref_model_features.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.ref_model_layers.argtypes = [C.c_void_p]
+        L.ref_model_weight.restype = C.POINTER(C.c_float)
+        L.ref_model_weight.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.ref_model_run.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
+                                    C.c_void_p, _TRACE_FN, C.c_void_p]
+        L.ref_model_time_forward.restype = C.c_double
+        L.ref_model_time_forward.argtypes = [C.c_void_p]
+        L.ref_model_kernel_times.argtypes = [C.c_void_p, C.c_int, C.c_char_p, C.c_int, C.c_void_p]
+        L.ref_binarize.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+        _ref = L
+    return _ref
+
+
+def ref_random_edges(seed: int, nodes: int, m: int, allow_self: bool = False):
+    src = np.empty(max(m, 1), np.int64)
+    dst = np.empty(max(m, 1), np.int64)
+    k = ref().ref_random_edges(seed, nodes, m, int(allow_self), _ptr(src), _ptr(dst))
+    return src[:k].copy(), dst[:k].copy()
+
+
+class RefGraph:
+    def __init__(self, n: int, src: np.ndarray, dst: np.ndarray):
+        src = np.ascontiguousarray(src, dtype=np.int64)
+        dst = np.ascontiguousarray(dst, dtype=np.int64)
+        self.n = n
+        self.h = ref().ref_graph_create(n, _ptr(src), _ptr(dst), src.shape[0])
+        if not self.h:
+            raise ValueError(ref().ref_error().decode())
+
+    def frdc(self, which: int) -> Frdc:
+        nnz = C.c_int64()
+        rp, ci, ti = C.POINTER(C.c_uint64)(), C.POINTER(C.c_uint32)(), C.POINTER(C.c_uint16)()
+        ref().ref_graph_frdc(self.h, which, C.byref(nnz), C.byref(rp), C.byref(ci), C.byref(ti))
+        tr = (self.n + 3) // 4
+        s = _Frdc(self.n, self.n, nnz.value, rp, ci, ti)
+        return _frdc_copy(s)
+
+    def scales(self):
+        a, b, c = C.POINTER(C.c_float)(), C.POINTER(C.c_float)(), C.POINTER(C.c_int64)()
+        ref().ref_graph_scales(self.h, C.byref(a), C.byref(b), C.byref(c))
+        n = self.n
+        return (np.ctypeslib.as_array(a, shape=(n,)).copy(), np.ctypeslib.as_array(b, shape=(n,)).copy(),
+                np.ctypeslib.as_array(c, shape=(n,)).copy())
+
+    def __del__(self):
+        try:
+            if self.h:
+                ref().ref_graph_free(self.h)
+        except Exception:
+            pass
+
+
+class RefModel:
+    def __init__(self, graph: Optional[RefGraph], model: str, features: int, hidden: int,
+                 classes: int, seed: int, nodes: int, word_bits: int = 32,
+                 plan: Optional[Sequence[str]] = None):
+        p = "|".join(plan) if plan else ""
+        self.h = ref().ref_model_build(graph.h if graph else None, model.encode(), features, hidden,
+                                       classes, seed, word_bits, p.encode(), nodes)
+        if not self.h:
+            raise ValueError(ref().ref_error().decode())
+        self.graph = graph
+
+    def features(self) -> np.ndarray:
+        r, c = C.c_int64(), C.c_int64()
+        p = ref().ref_model_features(self.h, C.byref(r), C.byref(c))
+        return np.ctypeslib.as_array(p, shape=(r.value * c.value,)).reshape(r.value, c.value).copy()
+
+    def weights(self):
+        out = []
+        for i in range(ref().ref_model_layers(self.h)):
+            ws = []
+            for which in (1, 2):
+                r, c = C.c_int64(), C.c_int64()
+                p = ref().ref_model_weight(self.h, i, which, C.byref(r), C.byref(c))
+                ws.append(None if not p else
+                          np.ctypeslib.as_array(p, shape=(r.value * c.value,)).reshape(r.value, c.value).copy())
+            out.append(tuple(ws))
+        return out
+
+    def run(self, out_cols: int, x: Optional[np.ndarray] = None, trace: bool = True):
+        rows = self.features().shape[0] if x is None else x.shape[0]
+        logits = np.empty((rows, out_cols), np.float32)
+        out = np.empty((rows, out_cols), np.float32)
+        points: List[TracePoint] = []
+
+        def sink(_ctx, label, bits, r, c, wb):
+            n = r * spw(c, wb)
+            arr = np.ctypeslib.as_array(bits, shape=(n,)).reshape(r, -1).copy() if n else \
+                np.zeros((r, spw(c, wb)), np.uint32)
+            points.append(TracePoint(label.decode(), arr, r, c, wb))
+
+        cb = _TRACE_FN(sink) if trace else _TRACE_FN()
+        xp = None
+        if x is not None:
+            x = np.ascontiguousarray(x, dtype=np.float32)
+            xp = _ptr(x)
+        rc = ref().ref_model_run(self.h, xp, rows, 0 if x is None else x.shape[1],
+                                 _ptr(logits), _ptr(out), cb, None)
+        if rc:
+            raise ValueError(ref().ref_error().decode())
+        return out, logits, points
+
+    def time_forward(self) -> float:
+        return ref().ref_model_time_forward(self.h)
+
+    def kernel_times(self):
+        cap, ll = 64, 96
+        labels = C.create_string_buffer(cap * ll)
+        ms = np.zeros(cap, np.float64)
+        n = ref().ref_model_kernel_times(self.h, cap, labels, ll, _ptr(ms))
+        raw = labels.raw
+        return [(raw[i * ll:(i + 1) * ll].split(b"\0")[0].decode(), float(ms[i])) for i in range(max(n, 0))]
+
+    def __del__(self):
+        try:
+            if self.h:
+                ref().ref_model_free(self.h)
+        except Exception:
+            pass

@@ -1,0 +1,255 @@
+// ref_capi.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// A thin extern "C" shim over the UNMODIFIED reference library, compiled
+// straight from /root/reference/proj/src by oracle/Makefile into
+// oracle/_ref/libbitgnn_ref.so.  It lets the Python tests and bench.py's
+// reference arm drive the real reference (bitgnn::prepare_graph,
+// bitgnn::build_model, bitgnn::run_model, bitgnn::bench_model) without
+// linking it into the product.  No reference source is copied here; only the
+// reference's public headers are included.
+#include <omp.h>
+
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "bitgnn/bitsparse.hpp"
+#include "bitgnn/graphops.hpp"
+#include "bitgnn/kernels.hpp"
+#include "bitgnn/modelconfig.hpp"
+#include "bitgnn/rng.hpp"
+#include "bitgnn/runreport.hpp"
+
+using namespace bitgnn;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct RefGraph {
+  std::shared_ptr<const GraphBundle> g;
+  EdgeList edges;
+};
+
+struct RefModel {
+  BuiltModel bm;
+};
+
+int guard(const std::exception& e) {
+  g_err = e.what();
+  return 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+typedef void (*ref_trace_fn)(void* ctx, const char* label, const uint32_t* bits, int64_t rows,
+                             int64_t cols, int word_bits);
+
+const char* ref_error(void) { return g_err.c_str(); }
+
+int ref_max_threads(void) { return omp_get_max_threads(); }
+void ref_set_threads(int n) {
+  if (n > 0) omp_set_num_threads(n);
+}
+
+// rng.hpp:66-80 through the reference's own Rng.
+int64_t ref_random_edges(uint64_t seed, int64_t nodes, int64_t m, int allow_self, int64_t* src,
+                         int64_t* dst) {
+  Rng rng(seed);
+  EdgeList e = random_edges(rng, nodes, m, allow_self != 0);
+  for (size_t k = 0; k < e.edges.size(); ++k) {
+    src[k] = e.edges[k].first;
+    dst[k] = e.edges[k].second;
+  }
+  return static_cast<int64_t>(e.edges.size());
+}
+
+void ref_random_dense(uint64_t seed, int64_t rows, int64_t cols, float* out) {
+  Rng rng(seed);
+  DenseMatrix m = random_dense(rng, rows, cols);
+  std::memcpy(out, m.row(0), static_cast<size_t>(rows * cols) * sizeof(float));
+}
+
+// graphops.cpp:146-170 (prepare_graph) on the given edges.
+void* ref_graph_create(int64_t n, const int64_t* src, const int64_t* dst, int64_t e) {
+  try {
+    auto h = std::make_unique<RefGraph>();
+    h->edges.node_count = n;
+    h->edges.edges.reserve(static_cast<size_t>(e));
+    for (int64_t k = 0; k < e; ++k) h->edges.edges.emplace_back(src[k], dst[k]);
+    h->g = prepare_graph(h->edges);
+    return h.release();
+  } catch (const std::exception& ex) {
+    guard(ex);
+    return nullptr;
+  }
+}
+
+void ref_graph_free(void* h) { delete static_cast<RefGraph*>(h); }
+
+// which: 0 = A+I (structure), 1 = loop-free A (raw).
+int ref_graph_frdc(void* h, int which, int64_t* nnz, const uint64_t** row_ptr,
+                   const uint32_t** col_ind, const uint16_t** tiles) {
+  auto* g = static_cast<RefGraph*>(h);
+  const FrdcMatrix& m = which == 0 ? g->g->structure : g->g->raw;
+  *nnz = m.nnz_tiles();
+  *row_ptr = m.row_ptr().data();
+  *col_ind = m.col_ind().data();
+  *tiles = m.tiles().data();
+  return 0;
+}
+
+int ref_graph_scales(void* h, const float** norm, const float** mean_row,
+                     const int64_t** neighbor_count) {
+  auto* g = static_cast<RefGraph*>(h);
+  *norm = g->g->norm_row.values().data();
+  *mean_row = g->g->mean_row.values().data();
+  *neighbor_count = g->g->neighbor_count.data();
+  return 0;
+}
+
+// modelconfig.cpp:99-173 (build_model).  plan: '|'-separated chains, empty
+// for the default plan of `model`.
+void* ref_model_build(void* graph, const char* model, int64_t features, int64_t hidden,
+                      int64_t classes, uint64_t seed, int word_bits, const char* plan,
+                      int64_t nodes) {
+  try {
+    ModelConfig cfg;
+    cfg.model = model;
+    cfg.features = features;
+    cfg.hidden = hidden;
+    cfg.classes = classes;
+    cfg.seed = seed;
+    cfg.word_bits = word_bits;
+    if (plan && *plan) {
+      std::string p(plan);
+      size_t s = 0;
+      while (s <= p.size()) {
+        size_t e = p.find('|', s);
+        if (e == std::string::npos) e = p.size();
+        if (e > s) cfg.plan.push_back(p.substr(s, e - s));
+        s = e + 1;
+      }
+    }
+    auto h = std::make_unique<RefModel>();
+    std::shared_ptr<const GraphBundle> g =
+        graph ? static_cast<RefGraph*>(graph)->g : std::shared_ptr<const GraphBundle>();
+    h->bm = build_model(cfg, g, nodes);
+    return h.release();
+  } catch (const std::exception& ex) {
+    guard(ex);
+    return nullptr;
+  }
+}
+
+void ref_model_free(void* h) { delete static_cast<RefModel*>(h); }
+
+const float* ref_model_features(void* h, int64_t* rows, int64_t* cols) {
+  auto* m = static_cast<RefModel*>(h);
+  *rows = m->bm.features.rows();
+  *cols = m->bm.features.cols();
+  return m->bm.features.row(0);
+}
+
+int ref_model_layers(void* h) { return static_cast<int>(static_cast<RefModel*>(h)->bm.spec.layers.size()); }
+
+// which: 1 = w1, 2 = w2.  Returns NULL when the layer has no such weight.
+const float* ref_model_weight(void* h, int layer, int which, int64_t* rows, int64_t* cols) {
+  auto* m = static_cast<RefModel*>(h);
+  const LayerSpec& l = m->bm.spec.layers[static_cast<size_t>(layer)];
+  const auto& w = which == 1 ? l.w1 : l.w2;
+  if (!w) return nullptr;
+  *rows = w->rows();
+  *cols = w->cols();
+  return w->row(0);
+}
+
+// graphops.cpp:390-484 with a RunTrace; logits = softmax input.
+int ref_model_run(void* h, const float* x, int64_t rows, int64_t cols, float* logits,
+                  float* out, ref_trace_fn trace, void* ctx) {
+  try {
+    auto* m = static_cast<RefModel*>(h);
+    const DenseMatrix* x0 = &m->bm.features;
+    DenseMatrix own;
+    if (x) {
+      own = DenseMatrix(rows, cols);
+      std::memcpy(own.row(0), x, static_cast<size_t>(rows * cols) * sizeof(float));
+      x0 = &own;
+    }
+    RunTrace tr;
+    DenseMatrix o = run_model(m->bm.spec, MatOperand(*x0), &tr);
+    if (trace)
+      for (const auto& p : tr.points) {
+        std::vector<uint32_t> words(static_cast<size_t>(p.bits.rows() * p.bits.storage_words_per_row()));
+        for (int64_t i = 0; i < p.bits.rows(); ++i) {
+          auto r = p.bits.row_span(i);
+          std::memcpy(words.data() + i * p.bits.storage_words_per_row(), r.data(), r.size() * 4);
+        }
+        trace(ctx, p.label.c_str(), words.data(), p.bits.rows(), p.bits.cols(), p.bits.word_bits());
+      }
+    if (logits)
+      std::memcpy(logits, tr.logits.row(0),
+                  static_cast<size_t>(tr.logits.rows() * tr.logits.cols()) * sizeof(float));
+    if (out) std::memcpy(out, o.row(0), static_cast<size_t>(o.rows() * o.cols()) * sizeof(float));
+    return 0;
+  } catch (const std::exception& ex) {
+    return guard(ex);
+  }
+}
+
+// Wall-clock forward timing through the reference's own run_model (the body
+// of bench_model, runreport.cpp:241-277), one call per invocation so the
+// caller controls warm-up/steps.  Returns milliseconds, or -1 on error.
+double ref_model_time_forward(void* h) {
+  try {
+    auto* m = static_cast<RefModel*>(h);
+    auto t0 = std::chrono::steady_clock::now();
+    DenseMatrix o = run_model(m->bm.spec, MatOperand(m->bm.features));
+    auto t1 = std::chrono::steady_clock::now();
+    volatile float sink = o.rows() ? o.at(0, 0) : 0.0f;
+    (void)sink;
+    return std::chrono::duration<double, std::milli>(t1 - t0).count();
+  } catch (const std::exception& ex) {
+    guard(ex);
+    return -1.0;
+  }
+}
+
+// Per-kernel breakdown of one forward (graphops.cpp:53-55 record_ns hooks).
+int ref_model_kernel_times(void* h, int cap, char* labels, int label_len, double* ms) {
+  try {
+    auto* m = static_cast<RefModel*>(h);
+    std::vector<KernelTiming> t;
+    run_model(m->bm.spec, MatOperand(m->bm.features), nullptr, &t);
+    int n = 0;
+    for (const auto& k : t) {
+      if (n >= cap) break;
+      std::strncpy(labels + n * label_len, k.label.c_str(), static_cast<size_t>(label_len - 1));
+      labels[n * label_len + label_len - 1] = 0;
+      ms[n] = static_cast<double>(k.ns) / 1e6;
+      ++n;
+    }
+    return n;
+  } catch (const std::exception& ex) {
+    guard(ex);
+    return -1;
+  }
+}
+
+// Kernel-level access for fixtures: binarize (bitdense.cpp:71-88).
+void ref_binarize(const float* x, int64_t rows, int64_t cols, int word_bits, uint32_t* out) {
+  DenseMatrix m(rows, cols);
+  std::memcpy(m.row(0), x, static_cast<size_t>(rows * cols) * sizeof(float));
+  BitDenseMatrix b = binarize(m, word_bits);
+  for (int64_t i = 0; i < rows; ++i) {
+    auto r = b.row_span(i);
+    std::memcpy(out + i * b.storage_words_per_row(), r.data(), r.size() * 4);
+  }
+}
+
+}  // extern "C"
