@@ -1,0 +1,275 @@
+/*
+ * bitgnn_b200.h -- C ABI of the B200-native binary-GNN inference path.
+ *
+ * This is the drop-in boundary for the reference's operator API in
+ * /root/reference/proj/include/bitgnn (abbreviated "ref:").  Each entry point
+ * names the reference interface it replaces.  Plain pointers and sizes only:
+ * device buffers are CUDA device pointers, streams are cudaStream_t passed as
+ * void*.  Every call returns a status code; bg_last_error() holds the message
+ * (thread-local), worded like the reference's exception text so the C++ shim
+ * (include/bitgnn_b200/bitgnn.hpp) can rethrow the reference's exception types:
+ *
+ *   BG_INVALID_ARGUMENT -> std::invalid_argument   (contract violations)
+ *   BG_RUNTIME_ERROR    -> std::runtime_error      (layer failures, I/O)
+ *   BG_LOGIC_ERROR      -> std::logic_error
+ *   BG_CUDA_ERROR       -> std::runtime_error      (device failure)
+ *
+ * Layouts are the reference's (ref: bitdense.hpp:55-60, bitsparse.hpp:22-25):
+ * row-major; packed rows of ceil(cols/word_bits)*(word_bits/32) u32 words,
+ * column j at bit 31 - j%32 of word j/32 (MSB first), padding bits zero;
+ * FRDC = CSR over 4x4 bit tiles (u64 row_ptr, u32 col_ind, u16 tiles with
+ * bit (r,c) at 15-(4r+c)).  All kernels are sm_100a CUDA; there is no CPU
+ * fallback: a call on a machine without a B200 fails with BG_CUDA_ERROR.
+ */
+#ifndef BITGNN_B200_H
+#define BITGNN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BG_OK 0
+#define BG_INVALID_ARGUMENT 1
+#define BG_RUNTIME_ERROR 2
+#define BG_LOGIC_ERROR 3
+#define BG_CUDA_ERROR 4
+
+typedef void* bg_stream; /* cudaStream_t; NULL = legacy default stream */
+
+const char* bg_last_error(void);
+int bg_version(void);
+
+/* ---- enums (ref: kernels.hpp:15-33, bitdense.hpp:15-16, graphops.hpp:44-55) */
+enum { BG_F = 0, BG_B = 1 };                                  /* Precision */
+enum { BG_BMM = 0, BG_BSPMM = 1, BG_ADD = 2, BG_CONCAT = 3 }; /* KernelOp */
+enum { BG_AXIS_ROW = 0, BG_AXIS_COL = 1 };                    /* Axis */
+enum { BG_ZERO_ONE = 0, BG_PLUS_MINUS = 1 };                  /* BitSemantics */
+enum { /* TrinaryStrategy; accepted and semantically inert (ref: test_kernels.cpp:276-303) */
+       BG_STRATEGY_DEFAULT = -1,
+       BG_IF_ELSE = 0,
+       BG_AND_ANDNOT = 1,
+       BG_TWO_AND_MINUS_POPC = 2 };
+enum { /* LayerKind */
+       BG_LAYER_GCN = 0,
+       BG_LAYER_SAGE = 1,
+       BG_LAYER_GRAPHCONV = 2,
+       BG_LAYER_FC = 3,
+       BG_LAYER_AGGREGATE = 4,
+       BG_LAYER_RELU = 5,
+       BG_LAYER_BATCHNORM = 6,
+       BG_LAYER_SOFTMAX = 7,
+       BG_LAYER_BINARIZE = 8,
+       BG_LAYER_SCALE = 9 };
+
+/* ref: KernelVariant (kernels.hpp:23-33) */
+typedef struct bg_variant {
+  int32_t op, in1, in2, out;
+} bg_variant;
+
+int bg_variant_parse(const char* text, bg_variant* out);      /* ref: KernelVariant::parse */
+int bg_variant_valid(bg_variant v);                           /* ref: KernelVariant::valid, 1/0 */
+int bg_variant_name(bg_variant v, char* buf, size_t buf_len); /* ref: KernelVariant::name */
+
+/* A matrix operand in device memory: ref MatOperand = variant<DenseMatrix,
+ * BitOperand> (kernels.hpp:37-42).  F: data = float[rows*cols].  B: data =
+ * uint32[rows*bg_storage_words_per_row(cols, word_bits)], optional scale
+ * (float[rows] for Axis::Row, float[cols] for Axis::Col), NULL when absent. */
+typedef struct bg_mat {
+  int32_t precision;
+  int32_t word_bits;
+  int32_t semantics;
+  int32_t scale_axis;
+  int64_t rows, cols;
+  void* data;
+  float* scale;
+} bg_mat;
+
+/* ref: BitDenseMatrix::storage_words_per_row (bitdense.hpp:72-73) */
+int64_t bg_storage_words_per_row(int64_t cols, int word_bits);
+
+/* ---- bitdense (ref: bitdense.hpp:110-141) ------------------------------- */
+/* ref: binarize (bitdense.cpp:71-88): bit = (x >= 0) */
+int bg_binarize(const float* x, int64_t rows, int64_t cols, int word_bits, uint32_t* out,
+                bg_stream stream);
+/* ref: binarize_with_scale (bitdense.cpp:90-104): mean |x| in double, floor 1e-12 */
+int bg_binarize_with_scale(const float* x, int64_t rows, int64_t cols, int axis, int word_bits,
+                           uint32_t* out_bits, float* out_scale, bg_stream stream);
+/* ref: unpack (bitdense.cpp:106-114) */
+int bg_unpack(const uint32_t* bits, int64_t rows, int64_t cols, int word_bits, int semantics,
+              float* out, bg_stream stream);
+/* ref: transpose (bitdense.cpp:189-210): out is cols x rows bits */
+int bg_transpose(const uint32_t* in, int64_t rows, int64_t cols, int word_bits, uint32_t* out,
+                 bg_stream stream);
+
+/* ---- bitsparse (ref: bitsparse.hpp:26-81) -------------------------------- */
+typedef struct bg_frdc bg_frdc; /* device-resident FrdcMatrix, immutable after build */
+
+typedef struct bg_frdc_info {
+  int64_t node_rows, node_cols, tile_rows, tile_cols, nnz_tiles, nnz_bits, max_row_degree;
+  const uint64_t* row_ptr; /* device, tile_rows + 1 */
+  const uint32_t* col_ind; /* device, nnz_tiles */
+  const uint16_t* tiles;   /* device, nnz_tiles */
+  const int32_t* degree;   /* device, node_rows: set bits per node row */
+} bg_frdc_info;
+
+/* ref: frdc_from_edges (bitsparse.cpp:72-112), built on the device.  src/dst
+ * are DEVICE int64 arrays of n_edges directed (src, dst) pairs. */
+int bg_frdc_from_edges(const int64_t* src, const int64_t* dst, int64_t n_edges, int64_t n_nodes,
+                       int add_self_loops, bg_frdc** out, bg_stream stream);
+/* ref: FrdcMatrix constructor (bitsparse.cpp:40-70) with its validation; HOST arrays. */
+int bg_frdc_from_host(int64_t node_rows, int64_t node_cols, const uint64_t* row_ptr,
+                      const uint32_t* col_ind, const uint16_t* tiles, int64_t nnz_tiles,
+                      bg_frdc** out, bg_stream stream);
+int bg_frdc_info_get(const bg_frdc* m, bg_frdc_info* info);
+/* Copy the three FRDC arrays to HOST buffers (row_ptr: tile_rows+1, others nnz). */
+int bg_frdc_download(const bg_frdc* m, uint64_t* row_ptr, uint32_t* col_ind, uint16_t* tiles);
+/* Fault hook (ref: runreport.cpp:55-63): flip bit 0 of stored tile k % nnz. */
+int bg_frdc_corrupt_tile(bg_frdc* m, int64_t k);
+void bg_frdc_destroy(bg_frdc* m);
+
+/* ---- graph bundle (ref: GraphBundle, prepare_graph, graphops.hpp:17-40) --- */
+typedef struct bg_graph bg_graph;
+typedef struct bg_graph_info {
+  int64_t n;
+  const bg_frdc* structure;      /* A + I */
+  const bg_frdc* raw;            /* A, explicit self edges stripped */
+  const float* norm;             /* device: float(1/sqrt(double deg(A+I))) */
+  const float* mean_row;         /* device: 1.0f / float(max(1, neighbor_count)) */
+  const float* ones;             /* device: 1.0f */
+  const int64_t* neighbor_count; /* device */
+} bg_graph_info;
+
+/* ref: prepare_graph (graphops.cpp:146-170); src/dst DEVICE int64 arrays. */
+int bg_prepare_graph(const int64_t* src, const int64_t* dst, int64_t n_edges, int64_t n_nodes,
+                     bg_graph** out, bg_stream stream);
+int bg_graph_info_get(const bg_graph* g, bg_graph_info* info);
+/* Engine-side fault hook for verify (ref: runreport.cpp:55-63): corrupts A+I. */
+int bg_graph_corrupt_tile(bg_graph* g, int64_t k);
+void bg_graph_destroy(bg_graph* g);
+
+/* ---- kernel families (ref: kernels.hpp:63-97) -------------------------- */
+/* Output descriptors: fill precision/shape/word_bits of the result the op
+ * would produce (data/scale left NULL) so callers can allocate it. */
+int bg_bmm_out_desc(bg_variant v, const bg_mat* a, const bg_mat* w, int word_bits, bg_mat* out);
+int bg_bspmm_out_desc(bg_variant v, const bg_frdc* adj, const bg_mat* x, int word_bits,
+                      bg_mat* out);
+
+/* ref: bmm (kernels.cpp:140-191).  out is caller-allocated per bg_bmm_out_desc. */
+int bg_bmm(bg_variant v, const bg_mat* a, const bg_mat* w, int word_bits, bg_mat* out,
+           bg_stream stream);
+/* ref: bspmm (kernels.cpp:413-556).  row_scale/col_scale (device, len
+ * node_rows/node_cols) factorize the adjacency; both NULL for in2 = B. */
+int bg_bspmm(bg_variant v, const bg_frdc* adj, const float* row_scale, const float* col_scale,
+             const bg_mat* x, int strategy, int word_bits, bg_mat* out, bg_stream stream);
+/* ref: add (kernels.cpp:593-625) */
+int bg_add(bg_variant v, const bg_mat* a, const bg_mat* b, bg_mat* out, bg_stream stream);
+/* ref: concat (kernels.cpp:627-668) */
+int bg_concat(bg_variant v, const bg_mat* a, const bg_mat* b, bg_mat* out, bg_stream stream);
+/* ref: scl (kernels.cpp:560-571) */
+int bg_scl(const float* x, int64_t rows, int64_t cols, const float* row, const float* col,
+           float* out, bg_stream stream);
+/* ref: dense_mm (kernels.cpp:193-212), double accumulation in k order */
+int bg_dense_mm(const float* a, const float* w, int64_t rows, int64_t k, int64_t cols, float* out,
+                bg_stream stream);
+/* ref: relu_inplace (graphops.cpp:89-97); binary operands are left untouched */
+int bg_relu_inplace(bg_mat* x, bg_stream stream);
+/* ref: softmax_rows (graphops.cpp:372-386) */
+int bg_softmax_rows(const float* x, int64_t rows, int64_t cols, float* out, bg_stream stream);
+/* ref: batchnorm_infer (graphops.cpp:337-355); parameters are device arrays of len cols */
+int bg_batchnorm_infer(const float* x, int64_t rows, int64_t cols, const float* gamma,
+                       const float* beta, const float* mean, const float* sigma, float* out,
+                       bg_stream stream);
+/* ref: fused_mm_spmm (kernels.cpp:670-677): adj * (x * w), requires mm.out == spmm.in1 */
+int bg_fused_mm_spmm(bg_variant mm, bg_variant spmm, const bg_mat* x, const bg_mat* w,
+                     const bg_frdc* adj, const float* row_scale, const float* col_scale,
+                     int strategy, bg_mat* out, bg_stream stream);
+
+/* ---- models (ref: LayerSpec / ModelSpec / run_model, graphops.hpp:57-133) --- */
+typedef struct bg_layer_desc {
+  int32_t kind; /* BG_LAYER_* */
+  int32_t n_plan;
+  bg_variant plan[4];
+  const float* w1; /* HOST fp32, row-major */
+  int64_t w1_rows, w1_cols;
+  const float* w2;
+  int64_t w2_rows, w2_cols;
+  int32_t relu;
+  const float *bn_gamma, *bn_beta, *bn_mean, *bn_sigma; /* HOST, optional (BatchNorm) */
+  int64_t bn_len;
+  const float* scale_row; /* HOST, optional (Scale) */
+  int64_t scale_row_len;
+  const float* scale_col;
+  int64_t scale_col_len;
+} bg_layer_desc;
+
+typedef struct bg_model bg_model;
+
+/* ref: validate_model (graphops.cpp:245-268).  Returns the number of
+ * problems; the messages, '\n'-separated and worded like the reference's,
+ * go to buf. */
+int bg_validate_model(int has_graph, int input_precision, const bg_layer_desc* layers,
+                      int n_layers, char* buf, size_t buf_len);
+
+/* Builds a device-resident model; weights are uploaded and binarized once
+ * with their column scales, as run_mm_slot does per call (graphops.cpp:47-77).
+ * Invalid models fail with BG_INVALID_ARGUMENT and the run_model message. */
+int bg_model_create(const bg_graph* graph, int input_precision, int strategy, int word_bits,
+                    const bg_layer_desc* layers, int n_layers, bg_model** out, bg_stream stream);
+void bg_model_destroy(bg_model* m);
+/* Shape of the model output for an input with `rows` rows. */
+int bg_model_output_cols(const bg_model* m, int64_t* cols);
+/* Capture each forward as one CUDA graph after the first run (default on). */
+int bg_model_set_graph_capture(bg_model* m, int enable);
+
+/* ref: run_model (graphops.cpp:390-484).  x0 in device memory; out and
+ * logits (softmax input; may be NULL) are device float[rows*out_cols]. */
+int bg_model_forward(bg_model* m, const bg_mat* x0, float* out, float* logits, bg_stream stream);
+
+/* End-to-end call with HOST buffers: H2D of x (pipelined with the first
+ * layer), forward, D2H of out/logits (logits may be NULL).  Synchronous. */
+int bg_model_forward_host(bg_model* m, const float* x_host, int64_t rows, int64_t cols,
+                          float* out_host, float* logits_host, bg_stream stream);
+
+/* BIN-point trace (ref: RunTrace, graphops.hpp:114-122) */
+typedef struct bg_trace bg_trace;
+int bg_trace_create(bg_trace** out);
+void bg_trace_destroy(bg_trace* t);
+int bg_model_forward_traced(bg_model* m, const bg_mat* x0, float* out, float* logits,
+                            bg_trace* trace, bg_stream stream);
+int bg_trace_size(const bg_trace* t);
+/* bits: device pointer owned by the trace, rows x storage_words_per_row(cols) */
+int bg_trace_point(const bg_trace* t, int i, const char** label, int64_t* rows, int64_t* cols,
+                   int* word_bits, const uint32_t** bits);
+
+/* Per-kernel timing (ref: KernelTiming + record_ns hooks, graphops.cpp:53-84),
+ * measured with CUDA events on `stream`. */
+typedef struct bg_kernel_timing {
+  char label[64];
+  double ms;
+} bg_kernel_timing;
+int bg_model_forward_timed(bg_model* m, const bg_mat* x0, float* out, float* logits,
+                           bg_kernel_timing* timings, int cap, int* n, bg_stream stream);
+
+/* ---- row-sharded multi-GPU forward (one process per GPU) ---------------- */
+/* Row range [row_begin, row_end) of a model's graph owned by this rank: tile
+ * rows split so every rank holds about the same number of FRDC tiles. */
+int bg_partition_rows(const bg_graph* g, int world_size, int rank, int64_t* row_begin,
+                      int64_t* row_end);
+
+/* ---- deterministic synthetic inputs (ref: rng.hpp:16-80) --------------- */
+typedef struct bg_rng bg_rng;
+int bg_rng_create(uint64_t seed, bg_rng** out);
+void bg_rng_destroy(bg_rng* r);
+/* float(uniform*2-1) draws, row-major, into a HOST buffer (ref: random_dense) */
+int bg_rng_dense(bg_rng* r, int64_t rows, int64_t cols, float* out_host);
+/* ref: random_edges; HOST outputs of capacity m; *count = edges written */
+int bg_rng_edges(bg_rng* r, int64_t nodes, int64_t m, int allow_self, int64_t* src_host,
+                 int64_t* dst_host, int64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BITGNN_B200_H */

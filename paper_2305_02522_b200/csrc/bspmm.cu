@@ -1,0 +1,352 @@
+// Binary sparse aggregation over FRDC 4x4 bit tiles (ref: bspmm,
+// kernels.cpp:413-556).
+//
+// Integer path (BBB / BBF, kernels.cpp:254-465): out(i,k) = 2*cnt(i,k) - deg(i)
+// with cnt = #{j in N(i): x_jk = 1}; BBB keeps the sign bit (>= 0).
+//
+//   One warp per tile row.  The warp streams the tile row's col_ind/tiles
+//   with coalesced loads (one tile per lane), counting-sorts the set bits by
+//   local node row into four shared-memory rings (a packed 4x8-bit warp scan
+//   gives every lane its slots), and drains each ring in batches of 8 edges
+//   per slot lane.  Lane (slot s, word g) gathers word g of 8 neighbour rows
+//   and adds them into bit-sliced (vertical) counters with a Harley-Seal
+//   carry-save tree: ~4 LOP3 per gathered word, no per-feature unpacking.
+//   At the end the slot lanes are summed with a bit-sliced butterfly and the
+//   BBB threshold cnt >= ceil(deg/2) is evaluated plane-wise, producing the
+//   packed output word directly (north-star item 4: no unpacked round trip).
+//
+// Real-valued path (FBF/FFF/FBB/FFB and BFF/BFB, kernels.cpp:467-555): one
+// warp per node row walks its neighbours in ascending column order (ballot
+// over the tile chunk, then ascending lane, then ascending local column --
+// the order of walk_tile_row, :218-234) and accumulates in double, lanes over
+// features, so every output is bit-identical to the reference's sequential sum.
+#include <algorithm>
+
+#include "ops.cuh"
+
+namespace bg {
+namespace {
+
+constexpr int kRing = 256;  // ring entries per node row per warp
+constexpr int kBBWarps = 8;
+
+__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) {
+  return (a & b) | (c & (a ^ b));
+}
+
+// Harley-Seal: add 8 words into bit-sliced planes P[0..NP) (P[q] weight 2^q).
+template <int NP>
+__device__ __forceinline__ void hs_add8(uint32_t (&P)[NP], const uint32_t (&x)[8]) {
+  uint32_t t1, t2, f1, f2, e, s;
+  s = P[0] ^ x[0] ^ x[1]; t1 = maj3(P[0], x[0], x[1]); P[0] = s;
+  s = P[0] ^ x[2] ^ x[3]; t2 = maj3(P[0], x[2], x[3]); P[0] = s;
+  s = P[1] ^ t1 ^ t2;     f1 = maj3(P[1], t1, t2);     P[1] = s;
+  s = P[0] ^ x[4] ^ x[5]; t1 = maj3(P[0], x[4], x[5]); P[0] = s;
+  s = P[0] ^ x[6] ^ x[7]; t2 = maj3(P[0], x[6], x[7]); P[0] = s;
+  s = P[1] ^ t1 ^ t2;     f2 = maj3(P[1], t1, t2);     P[1] = s;
+  s = P[2] ^ f1 ^ f2;     e = maj3(P[2], f1, f2);      P[2] = s;
+#pragma unroll
+  for (int q = 3; q < NP; ++q) {
+    const uint32_t nq = P[q] ^ e;
+    e &= P[q];
+    P[q] = nq;
+  }
+}
+
+// G = word lanes (power of two), S = 32/G slot lanes.  NP planes per lane.
+template <int G, int NP, bool OUTB>
+__global__ void __launch_bounds__(kBBWarps * 32)
+    k_bspmm_bb(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+               const uint16_t* __restrict__ ti, int64_t trows, int64_t rows,
+               const uint32_t* __restrict__ x, int64_t xspw, int64_t f,
+               uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
+  constexpr int S = 32 / G;
+  constexpr int B = 8 * S;  // edges per batch
+  constexpr int LOGS = S == 1 ? 0 : S == 2 ? 1 : S == 4 ? 2 : S == 8 ? 3 : S == 16 ? 4 : 5;
+  constexpr int NQ = NP + LOGS;  // planes after the slot reduction
+  __shared__ uint32_t ring_all[kBBWarps][4][kRing];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane % G, slot = lane / G;
+  const int64_t word = static_cast<int64_t>(blockIdx.y) * G + g;
+  const bool word_ok = word < xspw;
+  uint32_t(*ring)[kRing] = ring_all[warp];
+
+  for (int64_t tr = static_cast<int64_t>(blockIdx.x) * kBBWarps + warp; tr < trows;
+       tr += static_cast<int64_t>(gridDim.x) * kBBWarps) {
+    uint32_t P[4][NP];
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int q = 0; q < NP; ++q) P[n][q] = 0;
+    uint32_t fill[4] = {0, 0, 0, 0}, head[4] = {0, 0, 0, 0};
+
+    auto batch = [&](auto nc, uint32_t h, uint32_t cnt) {
+      constexpr int n = decltype(nc)::value;
+      uint32_t xv[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const uint32_t e = static_cast<uint32_t>(slot + S * m);
+        xv[m] = 0;
+        if (e < cnt && word_ok) {
+          const uint32_t j = ring[n][(h + e) & (kRing - 1)];
+          xv[m] = __ldg(x + static_cast<int64_t>(j) * xspw + word);
+        }
+      }
+      hs_add8<NP>(P[n], xv);
+    };
+
+    const uint64_t t0 = rp[tr], t1 = rp[tr + 1];
+    for (uint64_t base = t0; base < t1; base += 32) {
+      __syncwarp();
+      const uint64_t t = base + lane;
+      uint32_t tile = 0, col = 0;
+      if (t < t1) {
+        tile = __ldg(ti + t);
+        col = __ldg(ci + t);
+      }
+      const uint32_t packed = __popc(tile >> 12) | (__popc((tile >> 8) & 0xFu) << 8) |
+                              (__popc((tile >> 4) & 0xFu) << 16) | (__popc(tile & 0xFu) << 24);
+      uint32_t incl = packed;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+        if (lane >= d) incl += v;
+      }
+      const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      const uint32_t excl = incl - packed;
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        uint32_t pos = fill[n] + ((excl >> (8 * n)) & 0xFFu);
+        uint32_t nib = (tile >> (12 - 4 * n)) & 0xFu;
+        while (nib) {
+          const int b = __ffs(nib) - 1;  // bit b of the nibble is local column 3 - b
+          nib &= nib - 1;
+          ring[n][pos & (kRing - 1)] = 4 * col + (3 - b);
+          ++pos;
+        }
+        fill[n] += (total >> (8 * n)) & 0xFFu;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        while (fill[n] - head[n] >= static_cast<uint32_t>(B)) {
+          switch (n) {
+            case 0: batch(std::integral_constant<int, 0>{}, head[n], B); break;
+            case 1: batch(std::integral_constant<int, 1>{}, head[n], B); break;
+            case 2: batch(std::integral_constant<int, 2>{}, head[n], B); break;
+            default: batch(std::integral_constant<int, 3>{}, head[n], B); break;
+          }
+          head[n] += B;
+        }
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      if (fill[n] > head[n]) {
+        const uint32_t cnt = fill[n] - head[n];
+        switch (n) {
+          case 0: batch(std::integral_constant<int, 0>{}, head[n], cnt); break;
+          case 1: batch(std::integral_constant<int, 1>{}, head[n], cnt); break;
+          case 2: batch(std::integral_constant<int, 2>{}, head[n], cnt); break;
+          default: batch(std::integral_constant<int, 3>{}, head[n], cnt); break;
+        }
+      }
+    }
+
+    // Slot reduction (bit-sliced butterfly) and epilogue per node row.
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      uint32_t Q[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) Q[q] = q < NP ? P[n][q] : 0u;
+#pragma unroll
+      for (int d = G; d < 32; d <<= 1) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const uint32_t a = Q[q], b = __shfl_xor_sync(0xFFFFFFFFu, Q[q], d);
+          Q[q] = a ^ b ^ c;
+          c = maj3(a, b, c);
+        }
+      }
+      const int64_t row = 4 * tr + n;
+      if (row >= rows) continue;
+      const uint32_t deg = fill[n];
+      if (OUTB) {
+        // cnt >= ceil(deg/2)  <=>  2*cnt - deg >= 0   (kernels.cpp:440-454)
+        const uint32_t T = (deg + 1) >> 1;
+        uint32_t gt = 0, eq = 0xFFFFFFFFu;
+#pragma unroll
+        for (int q = NQ - 1; q >= 0; --q) {
+          if ((T >> q) & 1u) {
+            eq &= Q[q];
+          } else {
+            gt |= eq & Q[q];
+            eq &= ~Q[q];
+          }
+        }
+        if (T >> NQ) gt = eq = 0;  // unreachable for supported degrees
+        uint32_t ge = gt | eq;
+        if (32 * (word + 1) > f) ge &= (32 * word >= f) ? 0u : tail_mask32(f);
+        if (slot == 0 && word_ok) out_bits[row * xspw + word] = ge;
+      } else if (word_ok) {
+        for (int b = slot; b < 32; b += S) {
+          const int64_t k = 32 * word + b;
+          if (k >= f) break;
+          uint32_t cnt = 0;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) cnt |= ((Q[q] >> (31 - b)) & 1u) << q;
+          out_f[row * f + k] = static_cast<float>(2 * static_cast<int64_t>(cnt) -
+                                                  static_cast<int64_t>(deg));
+        }
+      }
+    }
+  }
+}
+
+template <int G, int NP, bool OUTB>
+void launch_bb(const bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uint32_t* ob,
+               float* of, cudaStream_t s) {
+  const int64_t groups = cdiv(xspw, G);
+  const int64_t blocks = std::max<int64_t>(
+      1, std::min<int64_t>(cdiv(A.tile_rows, kBBWarps), static_cast<int64_t>(sm_count()) * 64));
+  dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(groups));
+  k_bspmm_bb<G, NP, OUTB><<<grid, kBBWarps * 32, 0, s>>>(A.rp(), A.ci(), A.ti(), A.tile_rows,
+                                                         A.rows, x, xspw, f, ob, of);
+  BG_LAUNCH_CHECK();
+}
+
+template <int G, bool OUTB>
+void launch_bb_np(const bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uint32_t* ob,
+                  float* of, cudaStream_t s) {
+  constexpr int S = 32 / G;
+  // Per slot lane at most deg/S + 8 edges land in its counters.
+  const int64_t per_lane = A.max_deg / S + 8;
+  if (per_lane < (1 << 11)) return launch_bb<G, 11, OUTB>(A, x, f, xspw, ob, of, s);
+  if (per_lane < (1 << 16)) return launch_bb<G, 16, OUTB>(A, x, f, xspw, ob, of, s);
+  fail("bspmm: node degree " + std::to_string(A.max_deg) + " exceeds the counter range");
+}
+
+// ---- real-valued walk ------------------------------------------------------
+template <int M, bool XBITS, bool OUTB>
+__global__ void __launch_bounds__(256)
+    k_bspmm_f(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+              const uint16_t* __restrict__ ti, int64_t rows, const float* __restrict__ xf,
+              const uint32_t* __restrict__ xb, int64_t xspw, const float* __restrict__ rs,
+              const float* __restrict__ cs, int64_t f, int64_t ospw,
+              uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (i >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t fbase = static_cast<int64_t>(blockIdx.y) * 32 * M;
+  const int64_t tr = i >> 2;
+  const int shift = 12 - 4 * static_cast<int>(i & 3);
+  double d[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) d[m] = 0.0;
+  const uint64_t t1 = rp[tr + 1];
+  for (uint64_t base = rp[tr]; base < t1; base += 32) {
+    const uint64_t t = base + lane;
+    uint32_t nib = 0, col = 0;
+    if (t < t1) {
+      nib = (__ldg(ti + t) >> shift) & 0xFu;
+      col = __ldg(ci + t);
+    }
+    uint32_t mask = __ballot_sync(0xFFFFFFFFu, nib != 0);
+    while (mask) {
+      const int L = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const uint32_t nl = __shfl_sync(0xFFFFFFFFu, nib, L);
+      const uint32_t cl = __shfl_sync(0xFFFFFFFFu, col, L);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (!(nl & (8u >> c))) continue;
+        const int64_t j = 4 * static_cast<int64_t>(cl) + c;
+        const double w = cs ? static_cast<double>(__ldg(cs + j)) : 1.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const int64_t k = fbase + 32 * m + lane;
+          if (k < f) {
+            if (XBITS) {
+              const uint32_t bit = (__ldg(xb + j * xspw + (k >> 5)) >> (31 - (k & 31))) & 1u;
+              d[m] = __dadd_rn(d[m], bit ? w : -w);
+            } else {
+              d[m] = __dadd_rn(d[m], __dmul_rn(w, static_cast<double>(__ldg(xf + j * f + k))));
+            }
+          }
+        }
+      }
+    }
+  }
+  const double si = rs ? static_cast<double>(rs[i]) : 1.0;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int64_t k = fbase + 32 * m + lane;
+    const double v = __dmul_rn(si, d[m]);
+    if (OUTB) {
+      const uint32_t word = __brev(__ballot_sync(0xFFFFFFFFu, k < f && v >= 0.0));
+      const int64_t w = (fbase >> 5) + m;
+      if (lane == 0 && w < ospw) out_bits[i * ospw + w] = word;
+    } else if (k < f) {
+      out_f[i * f + k] = __double2float_rn(v);
+    }
+  }
+  if (OUTB && lane == 0 && blockIdx.y == gridDim.y - 1)
+    for (int64_t w = (f + 31) / 32; w < ospw; ++w) out_bits[i * ospw + w] = 0;
+}
+
+template <int M, bool XBITS, bool OUTB>
+void launch_f(const bg_frdc& A, const SpmmFArgs& a, cudaStream_t s) {
+  const int64_t passes = cdiv(a.f, 32 * M);
+  dim3 grid(static_cast<unsigned>(cdiv(A.rows * 32, 256)), static_cast<unsigned>(passes));
+  const int64_t xspw = XBITS ? spw(a.f, a.xwb) : 0;
+  const int64_t ospw = OUTB ? spw(a.f, a.owb) : 0;
+  k_bspmm_f<M, XBITS, OUTB><<<grid, 256, 0, s>>>(A.rp(), A.ci(), A.ti(), A.rows, a.x_f, a.x_bits,
+                                                 xspw, a.row_scale, a.col_scale, a.f, ospw,
+                                                 a.out_bits, a.out_f);
+  BG_LAUNCH_CHECK();
+}
+
+template <bool XBITS, bool OUTB>
+void launch_f_m(const bg_frdc& A, const SpmmFArgs& a, cudaStream_t s) {
+  if (a.f <= 32) launch_f<1, XBITS, OUTB>(A, a, s);
+  else if (a.f <= 64) launch_f<2, XBITS, OUTB>(A, a, s);
+  else launch_f<4, XBITS, OUTB>(A, a, s);
+}
+
+}  // namespace
+
+void bspmm_bb(const bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* out_bits,
+              float* out_f, cudaStream_t s) {
+  if (A.rows == 0) return;
+  const int64_t xspw = spw(f, wb);
+  if (xspw == 0) {
+    return;
+  }
+  const bool ob = out_bits != nullptr;
+  if (xspw <= 4) {
+    if (ob) launch_bb_np<4, true>(A, x, f, xspw, out_bits, out_f, s);
+    else launch_bb_np<4, false>(A, x, f, xspw, out_bits, out_f, s);
+  } else if (xspw <= 8) {
+    if (ob) launch_bb_np<8, true>(A, x, f, xspw, out_bits, out_f, s);
+    else launch_bb_np<8, false>(A, x, f, xspw, out_bits, out_f, s);
+  } else if (xspw <= 16) {
+    if (ob) launch_bb_np<16, true>(A, x, f, xspw, out_bits, out_f, s);
+    else launch_bb_np<16, false>(A, x, f, xspw, out_bits, out_f, s);
+  } else {
+    if (ob) launch_bb_np<32, true>(A, x, f, xspw, out_bits, out_f, s);
+    else launch_bb_np<32, false>(A, x, f, xspw, out_bits, out_f, s);
+  }
+}
+
+void bspmm_f(const bg_frdc& A, const SpmmFArgs& a, cudaStream_t s) {
+  if (A.rows == 0 || a.f == 0) return;
+  const bool xb = a.x_bits != nullptr, ob = a.out_bits != nullptr;
+  if (xb && ob) launch_f_m<true, true>(A, a, s);
+  else if (xb) launch_f_m<true, false>(A, a, s);
+  else if (ob) launch_f_m<false, true>(A, a, s);
+  else launch_f_m<false, false>(A, a, s);
+}
+
+}  // namespace bg

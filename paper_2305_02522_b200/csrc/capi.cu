@@ -1,0 +1,614 @@
+// extern "C" entry points (include/bitgnn_b200.h).  Every function converts
+// exceptions into status codes; the message stays in bg_last_error().
+#include <algorithm>
+#include <cstring>
+#include <random>
+#include <sstream>
+
+#include "engine.cuh"
+#include "model.cuh"
+
+namespace bg {
+
+namespace {
+thread_local std::string g_last_error;
+thread_local Pool g_op_pool;  // temporaries of op-level calls (synchronous)
+}  // namespace
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+    return v;
+  }();
+  return n;
+}
+
+namespace {
+
+void need(const void* p, const char* what) {
+  if (!p) fail(std::string("null ") + what);
+}
+
+void copy_out(const Op& r, bg_mat* out, cudaStream_t s) {
+  need(out, "output operand");
+  if (out->precision != r.prec || out->rows != r.rows || out->cols != r.cols ||
+      (r.prec == BG_B && out->word_bits != r.wb))
+    fail("output operand shape/precision does not match the result");
+  need(out->data, "output data");
+  const void* src = r.prec == BG_F ? static_cast<const void*>(r.f) : static_cast<const void*>(r.bits);
+  if (r.bytes()) BG_CUDA(cudaMemcpyAsync(out->data, src, r.bytes(), cudaMemcpyDeviceToDevice, s));
+  out->semantics = BG_PLUS_MINUS;
+  out->scale = nullptr;
+}
+
+void sync(cudaStream_t s) { BG_CUDA(cudaStreamSynchronize(s)); }
+
+}  // namespace
+}  // namespace bg
+
+using namespace bg;
+
+extern "C" {
+
+const char* bg_last_error(void) { return bg::g_last_error.c_str(); }
+int bg_version(void) { return 100; }
+
+int64_t bg_storage_words_per_row(int64_t cols, int word_bits) { return spw(cols, word_bits); }
+
+int bg_variant_parse(const char* text, bg_variant* out) {
+  return guard([&] {
+    need(text, "text");
+    need(out, "output");
+    *out = variant_parse(text);
+  });
+}
+int bg_variant_valid(bg_variant v) { return variant_valid(v) ? 1 : 0; }
+int bg_variant_name(bg_variant v, char* buf, size_t len) {
+  return guard([&] {
+    const std::string n = variant_name(v);
+    if (!buf || len <= n.size()) fail("buffer too small");
+    std::memcpy(buf, n.c_str(), n.size() + 1);
+  });
+}
+
+// ---- bitdense ---------------------------------------------------------------
+static void check_wb(int wb) {
+  if (wb != 32 && wb != 64) fail("BitDenseMatrix: word_bits must be 32 or 64");
+}
+
+int bg_binarize(const float* x, int64_t rows, int64_t cols, int wb, uint32_t* out, bg_stream s) {
+  return guard([&] {
+    check_wb(wb);
+    if (rows < 0 || cols < 0) fail("BitDenseMatrix: negative dimension");
+    binarize(x, rows, cols, wb, out, S(s));
+  });
+}
+
+int bg_binarize_with_scale(const float* x, int64_t rows, int64_t cols, int axis, int wb,
+                           uint32_t* out_bits, float* out_scale, bg_stream s) {
+  return guard([&] {
+    check_wb(wb);
+    if (rows < 0 || cols < 0) fail("BitDenseMatrix: negative dimension");
+    binarize(x, rows, cols, wb, out_bits, S(s));
+    l1_scales(x, rows, cols, axis, out_scale, S(s));
+  });
+}
+
+int bg_unpack(const uint32_t* bits, int64_t rows, int64_t cols, int wb, int semantics, float* out,
+              bg_stream s) {
+  return guard([&] {
+    check_wb(wb);
+    unpack(bits, rows, cols, wb, semantics, out, S(s));
+  });
+}
+
+int bg_transpose(const uint32_t* in, int64_t rows, int64_t cols, int wb, uint32_t* out,
+                 bg_stream s) {
+  return guard([&] {
+    check_wb(wb);
+    transpose_bits(in, rows, cols, wb, out, S(s));
+  });
+}
+
+// ---- FRDC / graph --------------------------------------------------------------
+int bg_frdc_from_edges(const int64_t* src, const int64_t* dst, int64_t e, int64_t n, int loops,
+                       bg_frdc** out, bg_stream s) {
+  return guard([&] {
+    need(out, "output");
+    *out = frdc_build(src, dst, e, n, loops != 0, false, S(s)).release();
+  });
+}
+
+int bg_frdc_from_host(int64_t rows, int64_t cols, const uint64_t* rp, const uint32_t* ci,
+                      const uint16_t* ti, int64_t nnz, bg_frdc** out, bg_stream s) {
+  return guard([&] {
+    need(out, "output");
+    *out = frdc_from_host(rows, cols, rp, ci, ti, nnz, S(s)).release();
+  });
+}
+
+int bg_frdc_info_get(const bg_frdc* m, bg_frdc_info* info) {
+  return guard([&] {
+    need(m, "frdc");
+    need(info, "info");
+    info->node_rows = m->rows;
+    info->node_cols = m->cols;
+    info->tile_rows = m->tile_rows;
+    info->tile_cols = m->tile_cols;
+    info->nnz_tiles = m->nnz;
+    info->nnz_bits = m->nnz_bits;
+    info->max_row_degree = m->max_deg;
+    info->row_ptr = m->rp();
+    info->col_ind = m->ci();
+    info->tiles = m->ti();
+    info->degree = m->deg();
+  });
+}
+
+int bg_frdc_download(const bg_frdc* m, uint64_t* rp, uint32_t* ci, uint16_t* ti) {
+  return guard([&] {
+    need(m, "frdc");
+    if (rp) BG_CUDA(cudaMemcpy(rp, m->row_ptr.p, static_cast<size_t>(m->tile_rows + 1) * 8, cudaMemcpyDeviceToHost));
+    if (ci && m->nnz) BG_CUDA(cudaMemcpy(ci, m->col_ind.p, static_cast<size_t>(m->nnz) * 4, cudaMemcpyDeviceToHost));
+    if (ti && m->nnz) BG_CUDA(cudaMemcpy(ti, m->tiles.p, static_cast<size_t>(m->nnz) * 2, cudaMemcpyDeviceToHost));
+  });
+}
+
+int bg_frdc_corrupt_tile(bg_frdc* m, int64_t k) {
+  return guard([&] {
+    need(m, "frdc");
+    if (m->nnz == 0) return;
+    const int64_t i = ((k % m->nnz) + m->nnz) % m->nnz;
+    uint16_t t = 0;
+    BG_CUDA(cudaMemcpy(&t, m->tiles.as<uint16_t>() + i, 2, cudaMemcpyDeviceToHost));
+    t = static_cast<uint16_t>(t ^ 1u);
+    BG_CUDA(cudaMemcpy(m->tiles.as<uint16_t>() + i, &t, 2, cudaMemcpyHostToDevice));
+    frdc_finalize(*m, nullptr);
+  });
+}
+
+void bg_frdc_destroy(bg_frdc* m) { delete m; }
+
+int bg_prepare_graph(const int64_t* src, const int64_t* dst, int64_t e, int64_t n, bg_graph** out,
+                     bg_stream s) {
+  return guard([&] {
+    need(out, "output");
+    *out = prepare_graph(src, dst, e, n, S(s)).release();
+  });
+}
+
+int bg_graph_info_get(const bg_graph* g, bg_graph_info* info) {
+  return guard([&] {
+    need(g, "graph");
+    need(info, "info");
+    info->n = g->n;
+    info->structure = g->structure.get();
+    info->raw = g->raw.get();
+    info->norm = g->norm.as<float>();
+    info->mean_row = g->mean_row.as<float>();
+    info->ones = g->ones.as<float>();
+    info->neighbor_count = g->neighbor_count.as<int64_t>();
+  });
+}
+
+int bg_graph_corrupt_tile(bg_graph* g, int64_t k) {
+  need(g, "graph");
+  return bg_frdc_corrupt_tile(g->structure.get(), k);
+}
+
+void bg_graph_destroy(bg_graph* g) { delete g; }
+
+// ---- ops ---------------------------------------------------------------------
+int bg_bmm_out_desc(bg_variant v, const bg_mat* a, const bg_mat* w, int wb, bg_mat* out) {
+  return guard([&] {
+    need(out, "output");
+    Op o = bmm_out_desc(v, op_from_mat(a), op_from_mat(w), wb);
+    std::memset(out, 0, sizeof *out);
+    op_to_mat(o, out);
+  });
+}
+
+int bg_bspmm_out_desc(bg_variant v, const bg_frdc* adj, const bg_mat* x, int wb, bg_mat* out) {
+  return guard([&] {
+    need(out, "output");
+    Op o = bspmm_out_desc(v, adj, op_from_mat(x), wb);
+    std::memset(out, 0, sizeof *out);
+    op_to_mat(o, out);
+  });
+}
+
+int bg_bmm(bg_variant v, const bg_mat* a, const bg_mat* w, int wb, bg_mat* out, bg_stream s) {
+  return guard([&] {
+    g_op_pool.reset();
+    const Op wo = op_from_mat(w);
+    Op r = run_bmm(v, op_from_mat(a), &wo, nullptr, wb, g_op_pool, S(s));
+    copy_out(r, out, S(s));
+    sync(S(s));
+  });
+}
+
+int bg_bspmm(bg_variant v, const bg_frdc* adj, const float* rs, const float* cs, const bg_mat* x,
+             int strategy, int wb, bg_mat* out, bg_stream s) {
+  (void)strategy;  // all TrinaryStrategy rewritings produce identical results
+  return guard([&] {
+    g_op_pool.reset();
+    Op r = run_bspmm(v, adj, rs, cs, op_from_mat(x), wb, g_op_pool, S(s));
+    copy_out(r, out, S(s));
+    sync(S(s));
+  });
+}
+
+int bg_add(bg_variant v, const bg_mat* a, const bg_mat* b, bg_mat* out, bg_stream s) {
+  return guard([&] {
+    g_op_pool.reset();
+    Op r = run_add(v, op_from_mat(a), op_from_mat(b), g_op_pool, S(s));
+    copy_out(r, out, S(s));
+    sync(S(s));
+  });
+}
+
+int bg_concat(bg_variant v, const bg_mat* a, const bg_mat* b, bg_mat* out, bg_stream s) {
+  return guard([&] {
+    g_op_pool.reset();
+    Op r = run_concat(v, op_from_mat(a), op_from_mat(b), g_op_pool, S(s));
+    copy_out(r, out, S(s));
+    sync(S(s));
+  });
+}
+
+int bg_scl(const float* x, int64_t rows, int64_t cols, const float* r, const float* c, float* out,
+           bg_stream s) {
+  return guard([&] { scl(x, rows, cols, r, c, out, S(s)); });
+}
+
+int bg_dense_mm(const float* a, const float* w, int64_t rows, int64_t k, int64_t cols, float* out,
+                bg_stream s) {
+  return guard([&] { dense_mm(a, w, rows, k, cols, out, S(s)); });
+}
+
+int bg_relu_inplace(bg_mat* x, bg_stream s) {
+  return guard([&] {
+    Op o = op_from_mat(x);
+    if (o.prec == BG_F) relu(o.f, o.rows * o.cols, S(s));
+  });
+}
+
+int bg_softmax_rows(const float* x, int64_t rows, int64_t cols, float* out, bg_stream s) {
+  return guard([&] { softmax_rows(x, rows, cols, out, S(s)); });
+}
+
+int bg_batchnorm_infer(const float* x, int64_t rows, int64_t cols, const float* g, const float* b,
+                       const float* m, const float* sg, float* out, bg_stream s) {
+  return guard([&] { batchnorm(x, rows, cols, g, b, m, sg, out, S(s)); });
+}
+
+int bg_fused_mm_spmm(bg_variant mm, bg_variant sp, const bg_mat* x, const bg_mat* w,
+                     const bg_frdc* adj, const float* rs, const float* cs, int strategy,
+                     bg_mat* out, bg_stream s) {
+  (void)strategy;
+  return guard([&] {
+    if (mm.out != sp.in1)
+      fail("fused_mm_spmm: precision chain mismatch (" + variant_name(mm) + " -> " +
+           variant_name(sp) + ")");
+    g_op_pool.reset();
+    const Op wo = op_from_mat(w);
+    Op h = run_bmm(mm, op_from_mat(x), &wo, nullptr, 32, g_op_pool, S(s));
+    Op r = run_bspmm(sp, adj, rs, cs, h, 32, g_op_pool, S(s));
+    copy_out(r, out, S(s));
+    sync(S(s));
+  });
+}
+
+// ---- models -----------------------------------------------------------------
+int bg_validate_model(int has_graph, int input_precision, const bg_layer_desc* layers, int n,
+                      char* buf, size_t len) {
+  std::vector<LayerInfo> infos;
+  for (int i = 0; i < n; ++i) infos.push_back(layer_info(layers[i]));
+  const auto errs = validate_model(has_graph != 0, input_precision, infos);
+  std::string joined;
+  for (size_t i = 0; i < errs.size(); ++i) joined += (i ? "\n" : "") + errs[i];
+  if (buf && len) {
+    const size_t k = std::min(len - 1, joined.size());
+    std::memcpy(buf, joined.data(), k);
+    buf[k] = 0;
+  }
+  return static_cast<int>(errs.size());
+}
+
+int bg_model_create(const bg_graph* graph, int input_precision, int strategy, int wb,
+                    const bg_layer_desc* layers, int n, bg_model** out, bg_stream s) {
+  return guard([&] {
+    need(out, "output");
+    check_wb(wb);
+    auto m = std::make_unique<bg_model>();
+    m->graph = graph;
+    m->input_prec = input_precision;
+    m->strategy = strategy;
+    m->wb = wb;
+    for (int i = 0; i < n; ++i) m->infos.push_back(layer_info(layers[i]));
+    {
+      const auto errs = validate_model(graph != nullptr, input_precision, m->infos);
+      if (!errs.empty()) {
+        std::ostringstream os;
+        os << "invalid model:";
+        for (const auto& e : errs) os << "\n  " << e;
+        fail(os.str());
+      }
+    }
+    m->layers.resize(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+      const bg_layer_desc& d = layers[i];
+      ModelLayer& l = m->layers[static_cast<size_t>(i)];
+      l.info = m->infos[static_cast<size_t>(i)];
+      l.relu = d.relu != 0;
+      if (d.w1) l.w1.upload(d.w1, d.w1_rows, d.w1_cols, wb, S(s));
+      if (d.w2) l.w2.upload(d.w2, d.w2_rows, d.w2_cols, wb, S(s));
+      auto up = [&](DevBuf& b, const float* h, int64_t len) {
+        b.alloc(static_cast<size_t>(std::max<int64_t>(len, 1)) * 4);
+        if (len) BG_CUDA(cudaMemcpyAsync(b.p, h, static_cast<size_t>(len) * 4, cudaMemcpyHostToDevice, S(s)));
+      };
+      if (l.info.has_bn) {
+        l.bn_len = d.bn_len;
+        up(l.bn_g, d.bn_gamma, d.bn_len);
+        up(l.bn_b, d.bn_beta, d.bn_len);
+        up(l.bn_m, d.bn_mean, d.bn_len);
+        up(l.bn_s, d.bn_sigma, d.bn_len);
+      }
+      if (l.info.has_scale) {
+        l.sr_len = d.scale_row_len;
+        l.sc_len = d.scale_col_len;
+        up(l.sr, d.scale_row, d.scale_row_len);
+        up(l.sc, d.scale_col, d.scale_col_len);
+      }
+    }
+    BG_CUDA(cudaStreamSynchronize(S(s)));
+    *out = m.release();
+  });
+}
+
+void bg_model_destroy(bg_model* m) { delete m; }
+
+int bg_model_output_cols(const bg_model* m, int64_t* cols) {
+  return guard([&] {
+    need(m, "model");
+    need(cols, "cols");
+    int64_t c = -1;
+    for (const auto& l : m->layers)
+      if (l.info.has_w1) c = l.w1.cols;
+    if (c < 0) c = m->last_out_cols;
+    if (c < 0) fail("output width depends on the input (no weighted layer)");
+    *cols = c;
+  });
+}
+
+int bg_model_set_graph_capture(bg_model* m, int enable) {
+  return guard([&] {
+    need(m, "model");
+    m->capture = enable != 0;
+    if (!m->capture && m->exec) {
+      cudaGraphExecDestroy(m->exec);
+      m->exec = nullptr;
+    }
+    m->key_runs = 0;
+  });
+}
+
+int bg_model_forward(bg_model* m, const bg_mat* x0, float* out, float* logits, bg_stream s) {
+  return guard([&] {
+    need(m, "model");
+    const Op x = op_from_mat(x0);
+    cudaStream_t st = S(s);
+    if (!m->capture || st == nullptr) {
+      forward_impl(*m, x, out, logits, nullptr, nullptr, st);
+      return;
+    }
+    bg_model::Key k;
+    k.x = x.prec == BG_F ? static_cast<const void*>(x.f) : static_cast<const void*>(x.bits);
+    k.rows = x.rows;
+    k.cols = x.cols;
+    k.prec = x.prec;
+    k.wb = x.wb;
+    k.out = out;
+    k.logits = logits;
+    k.s = st;
+    if (m->exec && k == m->key) {
+      BG_CUDA(cudaGraphLaunch(m->exec, st));
+      return;
+    }
+    if (!(k == m->key)) {
+      // First run with this binding: eager, which also sizes the pool.
+      if (m->exec) {
+        cudaGraphExecDestroy(m->exec);
+        m->exec = nullptr;
+      }
+      m->key = k;
+      forward_impl(*m, x, out, logits, nullptr, nullptr, st);
+      return;
+    }
+    // Second run with the same binding: capture and replay from now on.
+    cudaGraph_t graph = nullptr;
+    BG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+      forward_impl(*m, x, out, logits, nullptr, nullptr, st);
+    } catch (...) {
+      cudaStreamEndCapture(st, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    BG_CUDA(cudaStreamEndCapture(st, &graph));
+    BG_CUDA(cudaGraphInstantiate(&m->exec, graph, 0));
+    cudaGraphDestroy(graph);
+    BG_CUDA(cudaGraphLaunch(m->exec, st));
+  });
+}
+
+int bg_model_forward_host(bg_model* m, const float* xh, int64_t rows, int64_t cols, float* outh,
+                          float* logh, bg_stream s) {
+  int64_t oc = 0;
+  int rc = bg_model_output_cols(m, &oc);
+  if (rc) return rc;
+  rc = guard([&] {
+    const size_t xb = static_cast<size_t>(rows * cols) * 4, ob = static_cast<size_t>(rows * oc) * 4;
+    if (m->hx.bytes < xb) m->hx.alloc(xb);
+    if (m->hout.bytes < ob) m->hout.alloc(ob);
+    if (logh && m->hlog.bytes < ob) m->hlog.alloc(ob);
+    BG_CUDA(cudaMemcpyAsync(m->hx.p, xh, xb, cudaMemcpyHostToDevice, S(s)));
+  });
+  if (rc) return rc;
+  bg_mat x{};
+  x.precision = BG_F;
+  x.rows = rows;
+  x.cols = cols;
+  x.data = m->hx.p;
+  rc = bg_model_forward(m, &x, m->hout.as<float>(), logh ? m->hlog.as<float>() : nullptr, s);
+  if (rc) return rc;
+  return guard([&] {
+    const size_t ob = static_cast<size_t>(rows * oc) * 4;
+    BG_CUDA(cudaMemcpyAsync(outh, m->hout.p, ob, cudaMemcpyDeviceToHost, S(s)));
+    if (logh) BG_CUDA(cudaMemcpyAsync(logh, m->hlog.p, ob, cudaMemcpyDeviceToHost, S(s)));
+    BG_CUDA(cudaStreamSynchronize(S(s)));
+  });
+}
+
+int bg_trace_create(bg_trace** out) {
+  return guard([&] {
+    need(out, "output");
+    *out = new bg_trace();
+  });
+}
+void bg_trace_destroy(bg_trace* t) { delete t; }
+
+int bg_model_forward_traced(bg_model* m, const bg_mat* x0, float* out, float* logits, bg_trace* t,
+                            bg_stream s) {
+  return guard([&] {
+    need(m, "model");
+    need(t, "trace");
+    t->pts.clear();
+    forward_impl(*m, op_from_mat(x0), out, logits, t, nullptr, S(s));
+    BG_CUDA(cudaStreamSynchronize(S(s)));
+  });
+}
+
+int bg_trace_size(const bg_trace* t) { return t ? static_cast<int>(t->pts.size()) : 0; }
+
+int bg_trace_point(const bg_trace* t, int i, const char** label, int64_t* rows, int64_t* cols,
+                   int* wb, const uint32_t** bits) {
+  return guard([&] {
+    need(t, "trace");
+    if (i < 0 || i >= static_cast<int>(t->pts.size())) fail("trace point index out of range");
+    const TracePoint& p = t->pts[static_cast<size_t>(i)];
+    if (label) *label = p.label.c_str();
+    if (rows) *rows = p.rows;
+    if (cols) *cols = p.cols;
+    if (wb) *wb = p.wb;
+    if (bits) *bits = p.bits.as<uint32_t>();
+  });
+}
+
+int bg_model_forward_timed(bg_model* m, const bg_mat* x0, float* out, float* logits,
+                           bg_kernel_timing* timings, int cap, int* n, bg_stream s) {
+  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+  int rc = guard([&] {
+    need(m, "model");
+    forward_impl(*m, op_from_mat(x0), out, logits, nullptr, &ev, S(s));
+    BG_CUDA(cudaStreamSynchronize(S(s)));
+    int k = 0;
+    for (const auto& e : ev) {
+      if (k >= cap) break;
+      float ms = 0.0f;
+      BG_CUDA(cudaEventElapsedTime(&ms, e.second.first, e.second.second));
+      std::memset(timings[k].label, 0, sizeof timings[k].label);
+      std::strncpy(timings[k].label, e.first.c_str(), sizeof timings[k].label - 1);
+      timings[k].ms = ms;
+      ++k;
+    }
+    if (n) *n = k;
+  });
+  for (auto& e : ev) {
+    cudaEventDestroy(e.second.first);
+    cudaEventDestroy(e.second.second);
+  }
+  return rc;
+}
+
+// ---- multi-GPU row partition ------------------------------------------------
+int bg_partition_rows(const bg_graph* g, int world, int rank, int64_t* r0, int64_t* r1) {
+  return guard([&] {
+    need(g, "graph");
+    if (world < 1 || rank < 0 || rank >= world) fail("partition: bad rank/world size");
+    const bg_frdc& A = *g->structure;
+    std::vector<uint64_t> rp(static_cast<size_t>(A.tile_rows + 1));
+    BG_CUDA(cudaMemcpy(rp.data(), A.row_ptr.p, rp.size() * 8, cudaMemcpyDeviceToHost));
+    auto bound = [&](int k) -> int64_t {
+      if (k <= 0) return 0;
+      if (k >= world) return A.tile_rows;
+      const uint64_t target = (rp.back() * static_cast<uint64_t>(k) + world - 1) / world;
+      return std::lower_bound(rp.begin(), rp.end(), target) - rp.begin();
+    };
+    const int64_t t0 = std::min<int64_t>(bound(rank), A.tile_rows);
+    const int64_t t1 = std::max<int64_t>(t0, std::min<int64_t>(bound(rank + 1), A.tile_rows));
+    *r0 = std::min<int64_t>(4 * t0, g->n);
+    *r1 = std::min<int64_t>(4 * t1, g->n);
+  });
+}
+
+// ---- synthetic inputs (ref: rng.hpp:16-80) ------------------------------------
+}  // extern "C"
+
+struct bg_rng {
+  std::mt19937_64 g;
+  explicit bg_rng(uint64_t seed) : g(seed) {}
+  double uniform() { return static_cast<double>(g() >> 11) * 0x1.0p-53; }
+  int64_t index(int64_t n) {
+    const uint64_t un = static_cast<uint64_t>(n);
+    const uint64_t limit = UINT64_MAX - UINT64_MAX % un;
+    uint64_t v;
+    do v = g();
+    while (v >= limit);
+    return static_cast<int64_t>(v % un);
+  }
+};
+
+extern "C" {
+
+int bg_rng_create(uint64_t seed, bg_rng** out) {
+  return guard([&] {
+    need(out, "output");
+    *out = new bg_rng(seed);
+  });
+}
+void bg_rng_destroy(bg_rng* r) { delete r; }
+
+int bg_rng_dense(bg_rng* r, int64_t rows, int64_t cols, float* out) {
+  return guard([&] {
+    need(r, "rng");
+    for (int64_t i = 0; i < rows * cols; ++i) out[i] = static_cast<float>(r->uniform() * 2.0 - 1.0);
+  });
+}
+
+int bg_rng_edges(bg_rng* r, int64_t nodes, int64_t m, int allow_self, int64_t* src, int64_t* dst,
+                 int64_t* count) {
+  return guard([&] {
+    need(r, "rng");
+    if (nodes <= 0) fail("random_edges: nodes must be positive");
+    int64_t k = 0;
+    for (int64_t t = 0; t < m; ++t) {
+      const int64_t a = r->index(nodes);
+      int64_t b = r->index(nodes);
+      if (!allow_self && a == b) {
+        b = (b + 1) % nodes;
+        if (a == b) continue;
+      }
+      src[k] = a;
+      dst[k] = b;
+      ++k;
+    }
+    if (count) *count = k;
+  });
+}
+
+}  // extern "C"

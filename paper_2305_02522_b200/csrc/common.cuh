@@ -1,0 +1,110 @@
+// Shared internals of the B200 binary-GNN library: error plumbing, device
+// buffers, launch helpers, bit utilities.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+#include "bitgnn_b200.h"
+
+namespace bg {
+
+// Thrown for device failures; mapped to BG_CUDA_ERROR.
+struct cuda_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void set_last_error(const std::string& msg);
+
+#define BG_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      throw ::bg::cuda_error(std::string("CUDA error: ") + cudaGetErrorString(e_) +     \
+                             " at " __FILE__ ":" + std::to_string(__LINE__));           \
+  } while (0)
+
+#define BG_LAUNCH_CHECK() BG_CUDA(cudaGetLastError())
+
+// Runs f and converts exceptions into status codes + bg_last_error().
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return BG_OK;
+  } catch (const cuda_error& e) {
+    set_last_error(e.what());
+    return BG_CUDA_ERROR;
+  } catch (const std::invalid_argument& e) {
+    set_last_error(e.what());
+    return BG_INVALID_ARGUMENT;
+  } catch (const std::logic_error& e) {
+    set_last_error(e.what());
+    return BG_LOGIC_ERROR;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return BG_RUNTIME_ERROR;
+  } catch (...) {
+    set_last_error("unknown error");
+    return BG_RUNTIME_ERROR;
+  }
+}
+
+[[noreturn]] inline void fail(const std::string& m) { throw std::invalid_argument(m); }
+
+inline cudaStream_t S(bg_stream s) { return static_cast<cudaStream_t>(s); }
+
+inline int64_t spw(int64_t cols, int wb) { return (cols + wb - 1) / wb * (wb / 32); }
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Owning device allocation.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t n) { alloc(n); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr, o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(bytes, o.bytes);
+    return *this;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t n) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = n;
+    if (n) BG_CUDA(cudaMalloc(&p, n));
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+int sm_count();
+
+// ---- device helpers ---------------------------------------------------- //
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+// Valid-bit mask of the last u32 word of an n-bit row (MSB-first).
+__host__ __device__ __forceinline__ uint32_t tail_mask32(int64_t n) {
+  const int rem = static_cast<int>(n & 31);
+  return rem == 0 ? 0xFFFFFFFFu : (0xFFFFFFFFu << (32 - rem));
+}
+
+template <class T>
+__device__ __forceinline__ T ldg(const T* p) {
+  return __ldg(p);
+}
+
+}  // namespace bg

@@ -1,0 +1,71 @@
+// Engine internals: operand views, workspace pool, operator dispatch with the
+// reference's validation, and the device-resident model.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "ops.cuh"
+
+namespace bg {
+
+// Device operand view (ref: MatOperand, kernels.hpp:37-42).
+struct Op {
+  int prec = BG_F;
+  int64_t rows = 0, cols = 0;
+  int wb = 32;
+  int sem = BG_PLUS_MINUS;
+  float* f = nullptr;
+  uint32_t* bits = nullptr;
+  const float* scale = nullptr;
+  int scale_axis = BG_AXIS_ROW;
+  size_t bytes() const {
+    return prec == BG_F ? static_cast<size_t>(rows * cols) * 4
+                        : static_cast<size_t>(rows * spw(cols, wb)) * 4;
+  }
+};
+
+Op op_from_mat(const bg_mat* m);
+void op_to_mat(const Op& o, bg_mat* m);
+
+// Deterministic bump pool: the same call sequence gets the same buffers, so a
+// forward can be captured once and replayed as a CUDA graph.
+struct Pool {
+  std::vector<DevBuf> bufs;
+  size_t next = 0;
+  void reset() { next = 0; }
+  void* get(size_t bytes);
+};
+
+std::string variant_name(bg_variant v);
+bool variant_valid(bg_variant v);
+bg_variant variant_parse(const std::string& text);
+const char* layer_kind_name(int kind);
+
+// Ops with the reference's checks.  Outputs come from `pool`.
+// wt_cache/scale_cache: optional pre-binarized transposed weight bits and
+// column scales for w (the model precomputes them once).
+struct WeightCache {
+  const uint32_t* wbits = nullptr;  // w rows x spw(cols) (for traces)
+  const uint32_t* wt = nullptr;     // cols x spw(rows)
+  const float* scale = nullptr;     // column scales
+  const float* f = nullptr;         // fp32 weights (MM.FFF)
+  int64_t rows = 0, cols = 0;
+  int wb = 32;
+};
+Op run_bmm(bg_variant v, const Op& a, const Op* w, const WeightCache* wc, int word_bits, Pool& pool,
+           cudaStream_t s);
+Op run_bspmm(bg_variant v, const bg_frdc* adj, const float* rs, const float* cs, const Op& x,
+             int word_bits, Pool& pool, cudaStream_t s);
+Op run_add(bg_variant v, const Op& a, const Op& b, Pool& pool, cudaStream_t s);
+Op run_concat(bg_variant v, const Op& a, const Op& b, Pool& pool, cudaStream_t s);
+
+// Output shapes (for caller allocation through the C ABI).
+Op bmm_out_desc(bg_variant v, const Op& a, const Op& w, int word_bits);
+Op bspmm_out_desc(bg_variant v, const bg_frdc* adj, const Op& x, int word_bits);
+
+}  // namespace bg

@@ -1,0 +1,401 @@
+// Device-resident model and the layer-chain executor (ref: graphops.cpp:172-484).
+//
+// run_model's semantics are kept operation for operation (validation
+// messages, trace labels and order, timing labels, exception wrapping); the
+// difference is where the work happens: weights are uploaded and binarized
+// once, every operator is a CUDA kernel on the caller's stream, and a forward
+// with a fixed input binding is captured into one CUDA graph and replayed.
+#include <algorithm>
+#include <sstream>
+
+#include "engine.cuh"
+#include "model.cuh"
+
+namespace bg {
+
+// ---- validation (ref: graphops.cpp:103-268) ---------------------------------
+namespace {
+
+bool is_dense_fff(bg_variant v) {
+  return v.op == BG_BMM && v.in1 == BG_F && v.in2 == BG_F && v.out == BG_F;
+}
+
+void check_slot(std::vector<std::string>* errors, const std::string& where, bg_variant v, int want) {
+  if (v.op != want) {
+    static const char* names[] = {"MM", "SpMM", "ADD", "CONCAT"};
+    if (errors)
+      errors->push_back(where + ": expected a " + names[want] + " variant, got " + variant_name(v));
+    return;
+  }
+  if (!variant_valid(v) && !is_dense_fff(v))
+    if (errors) errors->push_back(where + ": unsupported variant " + variant_name(v));
+}
+
+}  // namespace
+
+int layer_output_precision(const LayerInfo& l, int in, std::vector<std::string>* errors) {
+  auto err = [&](const std::string& m) {
+    if (errors) errors->push_back(std::string(layer_kind_name(l.kind)) + ": " + m);
+  };
+  auto need_plan = [&](size_t n) {
+    if (l.plan.size() != n) {
+      err("expected " + std::to_string(n) + " plan slots, got " + std::to_string(l.plan.size()));
+      return false;
+    }
+    return true;
+  };
+  const auto& p = l.plan;
+  switch (l.kind) {
+    case BG_LAYER_GCN: {
+      if (!need_plan(2)) return in;
+      check_slot(errors, "gcn_conv mm", p[0], BG_BMM);
+      check_slot(errors, "gcn_conv spmm", p[1], BG_BSPMM);
+      if (!l.has_w1) err("missing weights");
+      if (p[0].in1 != in) err("mm input tag does not match incoming value");
+      if (p[0].out != p[1].in1) err("mm output tag does not feed the spmm input");
+      return p[1].out;
+    }
+    case BG_LAYER_SAGE:
+    case BG_LAYER_GRAPHCONV: {
+      if (!need_plan(4)) return in;
+      check_slot(errors, "mm_self", p[0], BG_BMM);
+      check_slot(errors, "mm_neigh", p[1], BG_BMM);
+      check_slot(errors, "spmm", p[2], BG_BSPMM);
+      check_slot(errors, "add", p[3], BG_ADD);
+      if (!l.has_w1 || !l.has_w2) err("missing weights");
+      if (p[0].in1 != in || p[1].in1 != in) err("mm input tags do not match incoming value");
+      if (p[1].out != p[2].in1) err("mm_neigh output tag does not feed the spmm input");
+      if (p[3].in1 != p[0].out) err("add input 1 tag does not match mm_self output");
+      if (p[3].in2 != p[2].out) err("add input 2 tag does not match spmm output");
+      return p[3].out;
+    }
+    case BG_LAYER_FC: {
+      if (!need_plan(1)) return in;
+      check_slot(errors, "fc mm", p[0], BG_BMM);
+      if (!l.has_w1) err("missing weights");
+      if (p[0].in1 != in) err("mm input tag does not match incoming value");
+      return p[0].out;
+    }
+    case BG_LAYER_AGGREGATE: {
+      if (!need_plan(1)) return in;
+      check_slot(errors, "aggregate spmm", p[0], BG_BSPMM);
+      if (p[0].in1 != in) err("spmm input tag does not match incoming value");
+      return p[0].out;
+    }
+    case BG_LAYER_RELU:
+      need_plan(0);
+      return in;
+    case BG_LAYER_BATCHNORM:
+      need_plan(0);
+      if (in != BG_F) err("expects a full-precision input");
+      if (!l.has_bn) err("missing parameters");
+      return BG_F;
+    case BG_LAYER_SOFTMAX:
+      need_plan(0);
+      if (in != BG_F) err("expects a full-precision input");
+      return BG_F;
+    case BG_LAYER_BINARIZE:
+      need_plan(0);
+      if (in != BG_F) err("expects a full-precision input");
+      return BG_B;
+    case BG_LAYER_SCALE:
+      need_plan(0);
+      if (in != BG_F) err("expects a full-precision input");
+      if (!l.has_scale) err("missing factors");
+      return BG_F;
+  }
+  return in;
+}
+
+std::vector<std::string> validate_model(bool has_graph, int input_prec,
+                                        const std::vector<LayerInfo>& layers) {
+  std::vector<std::string> errors;
+  if (!has_graph) {
+    bool needs_graph = false;
+    for (const auto& l : layers)
+      if (l.kind == BG_LAYER_GCN || l.kind == BG_LAYER_SAGE || l.kind == BG_LAYER_GRAPHCONV ||
+          l.kind == BG_LAYER_AGGREGATE)
+        needs_graph = true;
+    if (needs_graph) errors.push_back("model uses graph layers but carries no graph");
+  }
+  if (layers.empty()) errors.push_back("model has no layers");
+  int cur = input_prec;
+  for (size_t i = 0; i < layers.size(); ++i) {
+    std::vector<std::string> local;
+    cur = layer_output_precision(layers[i], cur, &local);
+    for (auto& e : local) errors.push_back("layer " + std::to_string(i) + " " + e);
+  }
+  if (!layers.empty() && cur != BG_F)
+    errors.push_back("model output must be full precision, got a binary tail");
+  return errors;
+}
+
+LayerInfo layer_info(const bg_layer_desc& d) {
+  LayerInfo l;
+  l.kind = d.kind;
+  for (int k = 0; k < d.n_plan && k < 4; ++k) l.plan.push_back(d.plan[k]);
+  if (d.n_plan > 4) l.plan.resize(static_cast<size_t>(d.n_plan), bg_variant{});
+  l.has_w1 = d.w1 != nullptr;
+  l.has_w2 = d.w2 != nullptr;
+  l.has_bn = d.bn_gamma && d.bn_beta && d.bn_mean && d.bn_sigma;
+  l.has_scale = d.scale_row && d.scale_col;
+  return l;
+}
+
+// ---- weights ------------------------------------------------------------------
+void WeightDev::upload(const float* host, int64_t r, int64_t c, int wb_, cudaStream_t s) {
+  rows = r;
+  cols = c;
+  wb = wb_;
+  f.alloc(static_cast<size_t>(std::max<int64_t>(r * c, 1)) * 4);
+  bits.alloc(static_cast<size_t>(std::max<int64_t>(r * spw(c, wb), 1)) * 4);
+  scale.alloc(static_cast<size_t>(std::max<int64_t>(c, 1)) * 4);
+  wt.alloc(static_cast<size_t>(std::max<int64_t>(c * spw(r, wb), 1)) * 4);
+  if (r * c) BG_CUDA(cudaMemcpyAsync(f.p, host, static_cast<size_t>(r * c) * 4, cudaMemcpyHostToDevice, s));
+  binarize(f.as<float>(), r, c, wb, bits.as<uint32_t>(), s);
+  l1_scales(f.as<float>(), r, c, BG_AXIS_COL, scale.as<float>(), s);
+  transpose_bits(bits.as<uint32_t>(), r, c, wb, wt.as<uint32_t>(), s);
+}
+
+WeightCache WeightDev::cache() const {
+  WeightCache c;
+  c.wbits = bits.as<uint32_t>();
+  c.wt = wt.as<uint32_t>();
+  c.scale = scale.as<float>();
+  c.f = f.as<float>();
+  c.rows = rows;
+  c.cols = cols;
+  c.wb = wb;
+  return c;
+}
+
+// ---- executor -------------------------------------------------------------------
+namespace {
+
+struct Hooks {
+  bg_trace* trace = nullptr;
+  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>>* timing = nullptr;
+  cudaStream_t s = nullptr;
+
+  void bits(const std::string& label, const uint32_t* b, int64_t rows, int64_t cols, int wb) {
+    if (!trace) return;
+    TracePoint p;
+    p.label = label;
+    p.rows = rows;
+    p.cols = cols;
+    p.wb = wb;
+    const size_t bytes = static_cast<size_t>(rows * spw(cols, wb)) * 4;
+    p.bits.alloc(std::max<size_t>(bytes, 4));
+    if (bytes) BG_CUDA(cudaMemcpyAsync(p.bits.p, b, bytes, cudaMemcpyDeviceToDevice, s));
+    trace->pts.push_back(std::move(p));
+  }
+  void begin(const std::string& label) {
+    if (!timing) return;
+    cudaEvent_t a, b;
+    BG_CUDA(cudaEventCreate(&a));
+    BG_CUDA(cudaEventCreate(&b));
+    BG_CUDA(cudaEventRecord(a, s));
+    timing->push_back({label, {a, b}});
+  }
+  void end() {
+    if (!timing) return;
+    BG_CUDA(cudaEventRecord(timing->back().second.second, s));
+  }
+};
+
+struct Exec {
+  bg_model& m;
+  Hooks& h;
+  cudaStream_t s;
+
+  // ref: run_mm_slot (graphops.cpp:47-77)
+  Op mm_slot(bg_variant mm, const Op& x, const WeightDev& w, const std::string& label) {
+    if (mm.op != BG_BMM) fail(label + ": plan slot expects an MM variant");
+    if (is_dense_fff(mm)) {
+      if (x.prec != BG_F) fail(label + ": MM.FFF expects a full-precision input");
+      if (x.cols != w.rows) fail("dense_mm: inner dimensions disagree");
+      Op o;
+      o.prec = BG_F;
+      o.rows = x.rows;
+      o.cols = w.cols;
+      o.f = static_cast<float*>(m.pool.get(o.bytes()));
+      h.begin(label + "[MM.FFF]");
+      dense_mm(x.f, w.f.as<float>(), x.rows, x.cols, w.cols, o.f, s);
+      h.end();
+      return o;
+    }
+    if (h.trace) {
+      if (mm.in1 == BG_F && x.prec == BG_F) {
+        auto* b = static_cast<uint32_t*>(m.pool.get(static_cast<size_t>(x.rows * spw(x.cols, m.wb)) * 4));
+        binarize(x.f, x.rows, x.cols, m.wb, b, s);
+        h.bits(label + ".bin_in", b, x.rows, x.cols, m.wb);
+      }
+      h.bits(label + ".bin_w", w.bits.as<uint32_t>(), w.rows, w.cols, w.wb);
+    }
+    const WeightCache wc = w.cache();
+    h.begin(label + "[" + variant_name(mm) + "]");
+    Op r = run_bmm(mm, x, nullptr, &wc, m.wb, m.pool, s);
+    h.end();
+    if (mm.out == BG_B) h.bits(label + ".out", r.bits, r.rows, r.cols, r.wb);
+    return r;
+  }
+
+  Op spmm_slot(bg_variant sp, const bg_frdc* adj, const float* rs, const float* cs, const Op& x,
+               const std::string& label) {
+    h.begin(label + "[" + variant_name(sp) + "]");
+    Op r = run_bspmm(sp, adj, rs, cs, x, m.wb, m.pool, s);
+    h.end();
+    if (sp.out == BG_B) h.bits(label + ".out", r.bits, r.rows, r.cols, r.wb);
+    return r;
+  }
+
+  Op own_f(const Op& x) {  // fresh copy for in-place ops on caller memory
+    Op o = x;
+    o.f = static_cast<float*>(m.pool.get(x.bytes()));
+    BG_CUDA(cudaMemcpyAsync(o.f, x.f, x.bytes(), cudaMemcpyDeviceToDevice, s));
+    return o;
+  }
+
+  void relu_inplace(Op& x, const Op& x0) {
+    if (x.prec != BG_F) return;  // ref: graphops.cpp:89-97
+    if (x.f == x0.f) x = own_f(x);
+    relu(x.f, x.rows * x.cols, s);
+  }
+};
+
+}  // namespace
+
+void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace* trace,
+                  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>>* timing,
+                  cudaStream_t s) {
+  {
+    std::vector<std::string> errors = validate_model(m.graph != nullptr, m.input_prec, m.infos);
+    if (!errors.empty()) {
+      std::ostringstream os;
+      os << "invalid model:";
+      for (const auto& e : errors) os << "\n  " << e;
+      fail(os.str());
+    }
+  }
+  if (x0.prec != m.input_prec) fail("model input tag does not match the provided operand");
+  m.pool.reset();
+  Hooks h;
+  h.trace = trace;
+  h.timing = timing;
+  h.s = s;
+  Exec ex{m, h, s};
+  Op cur = x0;
+  bool logits_set = false;
+  const size_t nl = m.layers.size();
+  for (size_t i = 0; i < nl; ++i) {
+    ModelLayer& l = m.layers[i];
+    const std::string prefix = "layer" + std::to_string(i) + ".";
+    try {
+      switch (l.info.kind) {
+        case BG_LAYER_GCN: {  // ref: gcn_layer, graphops.cpp:270-285
+          Op hh = ex.mm_slot(l.info.plan[0], cur, l.w1, prefix + "mm");
+          const bg_variant sp = l.info.plan[1];
+          const bool fac = sp.in2 == BG_F;
+          cur = ex.spmm_slot(sp, m.graph->structure.get(), fac ? m.graph->norm.as<float>() : nullptr,
+                             fac ? m.graph->norm.as<float>() : nullptr, hh, prefix + "spmm");
+          if (l.relu) ex.relu_inplace(cur, x0);
+          break;
+        }
+        case BG_LAYER_SAGE:
+        case BG_LAYER_GRAPHCONV: {  // ref: neighborhood_layer, graphops.cpp:289-321
+          const bool mean = l.info.kind == BG_LAYER_SAGE;
+          Op hs = ex.mm_slot(l.info.plan[0], cur, l.w1, prefix + "mm_self");
+          Op hn = ex.mm_slot(l.info.plan[1], cur, l.w2, prefix + "mm_neigh");
+          const bg_variant sp = l.info.plan[2];
+          const bool fac = sp.in2 == BG_F;
+          const float* rs = fac ? (mean ? m.graph->mean_row.as<float>() : m.graph->ones.as<float>()) : nullptr;
+          const float* cs = fac ? m.graph->ones.as<float>() : nullptr;
+          Op agg = ex.spmm_slot(sp, m.graph->raw.get(), rs, cs, hn, prefix + "spmm");
+          if (mean && sp.in2 == BG_B && sp.out == BG_F)
+            scale_rows_double(agg.f, agg.rows, agg.cols, m.graph->neighbor_count.as<int64_t>(), s);
+          cur = run_add(l.info.plan[3], hs, agg, m.pool, s);
+          if (l.info.plan[3].out == BG_B) h.bits(prefix + "add.out", cur.bits, cur.rows, cur.cols, cur.wb);
+          if (l.relu) ex.relu_inplace(cur, x0);
+          break;
+        }
+        case BG_LAYER_FC: {
+          cur = ex.mm_slot(l.info.plan[0], cur, l.w1, prefix + "mm");
+          if (l.relu) ex.relu_inplace(cur, x0);
+          break;
+        }
+        case BG_LAYER_AGGREGATE: {
+          const bg_variant sp = l.info.plan[0];
+          const bool fac = sp.in2 == BG_F;
+          cur = ex.spmm_slot(sp, m.graph->structure.get(), fac ? m.graph->norm.as<float>() : nullptr,
+                             fac ? m.graph->norm.as<float>() : nullptr, cur, prefix + "spmm");
+          break;
+        }
+        case BG_LAYER_RELU:
+          ex.relu_inplace(cur, x0);
+          break;
+        case BG_LAYER_BATCHNORM: {
+          if (cur.prec != BG_F) fail("bad variant access");
+          if (l.bn_len != cur.cols)
+            fail("batchnorm: parameter lengths do not match " + std::to_string(cur.cols) + " columns");
+          Op o = cur;
+          o.f = static_cast<float*>(m.pool.get(cur.bytes()));
+          batchnorm(cur.f, cur.rows, cur.cols, l.bn_g.as<float>(), l.bn_b.as<float>(),
+                    l.bn_m.as<float>(), l.bn_s.as<float>(), o.f, s);
+          cur = o;
+          break;
+        }
+        case BG_LAYER_SOFTMAX: {
+          if (cur.prec != BG_F) fail("bad variant access");
+          if (logits) {
+            BG_CUDA(cudaMemcpyAsync(logits, cur.f, cur.bytes(), cudaMemcpyDeviceToDevice, s));
+            logits_set = true;
+          }
+          Op o = cur;
+          o.f = (i + 1 == nl && out) ? out : static_cast<float*>(m.pool.get(cur.bytes()));
+          h.begin(prefix + "softmax");
+          softmax_rows(cur.f, cur.rows, cur.cols, o.f, s);
+          h.end();
+          cur = o;
+          break;
+        }
+        case BG_LAYER_BINARIZE: {
+          if (cur.prec != BG_F) fail("bad variant access");
+          Op o;
+          o.prec = BG_B;
+          o.rows = cur.rows;
+          o.cols = cur.cols;
+          o.wb = m.wb;
+          o.bits = static_cast<uint32_t*>(m.pool.get(o.bytes()));
+          binarize(cur.f, cur.rows, cur.cols, m.wb, o.bits, s);
+          h.bits(prefix + "bin.out", o.bits, o.rows, o.cols, o.wb);
+          cur = o;
+          break;
+        }
+        case BG_LAYER_SCALE: {
+          if (cur.prec != BG_F) fail("bad variant access");
+          if (l.sr_len != cur.rows || l.sc_len != cur.cols) fail("scl: scale length mismatch");
+          Op o = cur;
+          o.f = static_cast<float*>(m.pool.get(cur.bytes()));
+          scl(cur.f, cur.rows, cur.cols, l.sr.as<float>(), l.sc.as<float>(), o.f, s);
+          cur = o;
+          break;
+        }
+        default:
+          fail("unknown layer kind");
+      }
+    } catch (const cuda_error&) {
+      throw;
+    } catch (const std::exception& e) {
+      throw std::runtime_error("layer " + std::to_string(i) + " (" + layer_kind_name(l.info.kind) +
+                               "): " + e.what());
+    }
+  }
+  if (cur.prec != BG_F) fail("model output must be full precision");
+  if (out && cur.f != out)
+    BG_CUDA(cudaMemcpyAsync(out, cur.f, cur.bytes(), cudaMemcpyDeviceToDevice, s));
+  if (logits && !logits_set)
+    BG_CUDA(cudaMemcpyAsync(logits, cur.f, cur.bytes(), cudaMemcpyDeviceToDevice, s));
+  m.last_out_cols = cur.cols;
+}
+
+}  // namespace bg

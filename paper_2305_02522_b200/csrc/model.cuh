@@ -1,0 +1,90 @@
+// Model / trace objects behind the C ABI handles.
+#pragma once
+
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "engine.cuh"
+
+namespace bg {
+
+struct LayerInfo {
+  int kind = BG_LAYER_FC;
+  std::vector<bg_variant> plan;
+  bool has_w1 = false, has_w2 = false, has_bn = false, has_scale = false;
+};
+
+struct WeightDev {
+  int64_t rows = 0, cols = 0;
+  int wb = 32;
+  DevBuf f, bits, scale, wt;
+  void upload(const float* host, int64_t r, int64_t c, int wb, cudaStream_t s);
+  WeightCache cache() const;
+};
+
+struct ModelLayer {
+  LayerInfo info;
+  bool relu = false;
+  WeightDev w1, w2;
+  DevBuf bn_g, bn_b, bn_m, bn_s;
+  int64_t bn_len = 0;
+  DevBuf sr, sc;
+  int64_t sr_len = 0, sc_len = 0;
+};
+
+struct TracePoint {
+  std::string label;
+  int64_t rows = 0, cols = 0;
+  int wb = 32;
+  DevBuf bits;
+};
+
+int layer_output_precision(const LayerInfo& l, int in, std::vector<std::string>* errors);
+std::vector<std::string> validate_model(bool has_graph, int input_prec,
+                                        const std::vector<LayerInfo>& layers);
+LayerInfo layer_info(const bg_layer_desc& d);
+
+}  // namespace bg
+
+struct bg_trace {
+  std::vector<bg::TracePoint> pts;
+};
+
+struct bg_model {
+  const bg_graph* graph = nullptr;
+  int input_prec = BG_F;
+  int strategy = -1;
+  int wb = 32;
+  std::vector<bg::LayerInfo> infos;
+  std::vector<bg::ModelLayer> layers;
+  bg::Pool pool;
+  int64_t last_out_cols = -1;
+  // CUDA-graph replay of a forward bound to fixed buffers.
+  bool capture = true;
+  struct Key {
+    const void* x = nullptr;
+    int64_t rows = 0, cols = 0;
+    int prec = 0, wb = 0;
+    float* out = nullptr;
+    float* logits = nullptr;
+    cudaStream_t s = nullptr;
+    bool operator==(const Key& o) const {
+      return x == o.x && rows == o.rows && cols == o.cols && prec == o.prec && wb == o.wb &&
+             out == o.out && logits == o.logits && s == o.s;
+    }
+  } key;
+  int key_runs = 0;
+  cudaGraphExec_t exec = nullptr;
+  // Buffers of the host-pointer entry point.
+  bg::DevBuf hx, hout, hlog;
+  ~bg_model() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
+namespace bg {
+void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace* trace,
+                  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>>* timing,
+                  cudaStream_t s);
+}

@@ -1,0 +1,108 @@
+// Internal launchers shared by the C ABI entry points and the model engine.
+#pragma once
+
+#include <memory>
+
+#include "common.cuh"
+
+// Device-resident FRDC matrix (ref: FrdcMatrix, bitsparse.hpp:26-60) plus the
+// per-node-row degree the aggregation kernels use for thresholds.
+struct bg_frdc {
+  int64_t rows = 0, cols = 0, tile_rows = 0, tile_cols = 0, nnz = 0, nnz_bits = 0;
+  int64_t max_deg = 0;
+  bg::DevBuf row_ptr;  // u64[tile_rows + 1]
+  bg::DevBuf col_ind;  // u32[nnz]
+  bg::DevBuf tiles;    // u16[nnz]
+  bg::DevBuf degree;   // i32[rows]
+  const uint64_t* rp() const { return row_ptr.as<uint64_t>(); }
+  const uint32_t* ci() const { return col_ind.as<uint32_t>(); }
+  const uint16_t* ti() const { return tiles.as<uint16_t>(); }
+  const int32_t* deg() const { return degree.as<int32_t>(); }
+};
+
+struct bg_graph {
+  int64_t n = 0;
+  std::unique_ptr<bg_frdc> structure, raw;
+  bg::DevBuf norm, mean_row, ones, neighbor_count;
+};
+
+namespace bg {
+
+// ---- bitdense.cu ---------------------------------------------------------
+void binarize(const float* x, int64_t rows, int64_t cols, int wb, uint32_t* out, cudaStream_t s);
+// mean |x| per row (axis 0) or column (axis 1), double in index order.
+void l1_scales(const float* x, int64_t rows, int64_t cols, int axis, float* out, cudaStream_t s);
+void unpack(const uint32_t* bits, int64_t rows, int64_t cols, int wb, int semantics, float* out,
+            cudaStream_t s);
+void transpose_bits(const uint32_t* in, int64_t rows, int64_t cols, int wb, uint32_t* out,
+                    cudaStream_t s);
+
+// ---- frdc.cu -------------------------------------------------------------
+// drop_self_edges: skip (s, s) input edges (the loop-free structure of
+// prepare_graph, graphops.cpp:149-154).
+std::unique_ptr<bg_frdc> frdc_build(const int64_t* src, const int64_t* dst, int64_t e, int64_t n,
+                                    bool add_self_loops, bool drop_self_edges, cudaStream_t s);
+std::unique_ptr<bg_frdc> frdc_from_host(int64_t rows, int64_t cols, const uint64_t* rp,
+                                        const uint32_t* ci, const uint16_t* ti, int64_t nnz,
+                                        cudaStream_t s);
+void frdc_finalize(bg_frdc& m, cudaStream_t s);  // degree, nnz_bits, max_deg
+std::unique_ptr<bg_graph> prepare_graph(const int64_t* src, const int64_t* dst, int64_t e,
+                                        int64_t n, cudaStream_t s);
+
+// ---- bmm.cu --------------------------------------------------------------
+// Binary product against transposed weight bits wt (n x spw(k)).
+//   a_bits != nullptr: packed +-1 rows (rows x spw(k)); else a_f fp32 rows x k,
+//   binarized on the fly (fused FBB/FBF prologue).
+// out_bits: B output (dot >= 0, no scale), else out_f = float((alpha*dot)*beta).
+struct BmmArgs {
+  const uint32_t* a_bits = nullptr;
+  const float* a_f = nullptr;
+  const float* alpha = nullptr;  // per-row scale or null (1.0)
+  const uint32_t* wt = nullptr;
+  const float* beta = nullptr;  // per-column scale or null (1.0)
+  int64_t rows = 0, k = 0, n = 0;
+  int wb = 32;
+  uint32_t* out_bits = nullptr;
+  float* out_f = nullptr;
+};
+void bmm(const BmmArgs& a, cudaStream_t s);
+
+// ---- bspmm.cu ------------------------------------------------------------
+// Integer path (BBB / BBF): out(i,k) = 2*#{j in N(i): x_jk = 1} - deg_i.
+void bspmm_bb(const bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* out_bits,
+              float* out_f, cudaStream_t s);
+// Real-valued walk: F activations (x_f) or B activations with factorized
+// adjacency (x_bits + col_scale).  Ascending-j double accumulation.
+struct SpmmFArgs {
+  const float* x_f = nullptr;
+  const uint32_t* x_bits = nullptr;
+  int xwb = 32;
+  const float* row_scale = nullptr;
+  const float* col_scale = nullptr;
+  int64_t f = 0;
+  uint32_t* out_bits = nullptr;
+  int owb = 32;
+  float* out_f = nullptr;
+};
+void bspmm_f(const bg_frdc& A, const SpmmFArgs& a, cudaStream_t s);
+
+// ---- elementwise.cu ------------------------------------------------------
+void add_bbb(const uint32_t* a, const uint32_t* b, int64_t words, uint32_t* out, cudaStream_t s);
+void add_bbf(const uint32_t* a, const uint32_t* b, int64_t rows, int64_t cols, int wb, float* out,
+             cudaStream_t s);
+void add_fff(const float* a, const float* b, int64_t n, float* out, cudaStream_t s);
+void relu(float* x, int64_t n, cudaStream_t s);
+void softmax_rows(const float* x, int64_t rows, int64_t cols, float* out, cudaStream_t s);
+void scale_rows_double(float* x, int64_t rows, int64_t cols, const int64_t* cnt, cudaStream_t s);
+void batchnorm(const float* x, int64_t rows, int64_t cols, const float* g, const float* b,
+               const float* m, const float* sg, float* out, cudaStream_t s);
+void scl(const float* x, int64_t rows, int64_t cols, const float* r, const float* c, float* out,
+         cudaStream_t s);
+void dense_mm(const float* a, const float* w, int64_t rows, int64_t k, int64_t cols, float* out,
+              cudaStream_t s);
+void concat_bits(const uint32_t* a, int64_t ca, const uint32_t* b, int64_t cb, int64_t rows,
+                 int wb, uint32_t* out, cudaStream_t s);
+void concat_f(const float* a, int64_t ca, const float* b, int64_t cb, int64_t rows, float* out,
+              cudaStream_t s);
+
+}  // namespace bg
