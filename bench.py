@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark driver: full-graph binary-GNN inference on B200 vs the CPU reference.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {b200,reference}]
+                    [--workload reddit|pubmed|flickr|products|cora]
+
+Workload (BASELINE.json configs[3]): 2-layer binary GCN, default plan
+MM.FBB+BSpMM.BBB / MM.BBF+BSpMM.FBF (modelconfig.cpp:49-51), on a synthetic
+Reddit-shape graph (232,965 nodes, 114,615,892 edge draws, 602 features,
+hidden 128, 41 classes) generated with the reference's own generators
+(random_edges seed 100, build_model seed 99).  A "step" is one full-graph
+forward.  Prints ONE JSON line (rank 0).
+
+Arms:
+  --impl b200 (default)  the CUDA path through the C ABI (device-resident
+                         inputs for `value`; host buffers for `e2e`).
+  --impl reference       the reference's own CPU implementation
+                         (oracle/_ref = /root/reference/proj/src compiled
+                         unmodified), all host threads, same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+WORKLOADS = {
+    # name: (model, nodes, edge draws, features, hidden, classes, plan)
+    "reddit": ("gcn", 232_965, 114_615_892, 602, 128, 41, None),
+    "pubmed": ("gcn", 19_717, 88_648, 500, 64, 3,
+               ["MM.FBB+BSpMM.BBB", "MM.BBB+BSpMM.BBB", "MM.BBF+BSpMM.FBF"]),
+    "flickr": ("sage", 89_250, 899_756, 500, 256, 7, None),
+    "products": ("saint", 2_449_029, 61_859_140, 100, 128, 47, None),
+    "cora": ("gcn", 2_708, 10_556, 1_433, 64, 7, None),
+}
+GRAPH_SEED, MODEL_SEED = 100, 99
+METRIC = "full-graph inference ms & bit-SpMM GTEPS at 1/2/4/8 B200 vs CPU ref"
+
+
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------------------- #
+# clocks (B200_PROFILING.md "clocks DURING the timed region")
+# --------------------------------------------------------------------------- #
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, device: int, enabled: bool = True):
+        self.enabled = enabled
+        self.device = device
+        self.samples = []
+        self.proc = None
+        self.mark = None
+
+    def start(self):
+        if not self.enabled:
+            return
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception as e:  # nvidia-smi missing: report no clocks
+            log("clock sampler unavailable:", e)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append((time.time(), parts))
+
+    def begin_window(self):
+        self.mark = time.time()
+
+    def end_window(self):
+        self.window = (self.mark, time.time())
+
+    def stop(self):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.kill()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                pass
+            self.proc = None
+
+    def summary(self):
+        t0, t1 = getattr(self, "window", (0, time.time()))
+        sel = [p for (t, p) in self.samples if t0 - 0.05 <= t <= t1 + 0.05] or [p for _, p in self.samples]
+        if not sel:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [int(p[0]) for p in sel if p[0].isdigit()]
+        mx = [int(p[1]) for p in sel if p[1].isdigit()]
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        reasons = sorted({names[i] for p in sel for i in range(4) if p[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sel)}
+
+
+# --------------------------------------------------------------------------- #
+# roofline bookkeeping (SURVEY.md §8d algorithmic bytes)
+# --------------------------------------------------------------------------- #
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def spw(cols, wb=32):
+    return (cols + wb - 1) // wb * (wb // 32)
+
+
+def kernel_bytes(label: str, shapes: dict) -> int:
+    """Algorithmic HBM bytes of one launch: every array counted once."""
+    n, f, h, c = shapes["nodes"], shapes["features"], shapes["hidden"], shapes["classes"]
+    frdc = lambda which: 8 * (shapes[f"{which}_tile_rows"] + 1) + 6 * shapes[f"{which}_nnz_tiles"]
+    layer = int(label[5:label.index(".")]) if label.startswith("layer") else 0
+    fin = f if layer == 0 else h
+    fout = c if label.startswith(f"layer{shapes['last_conv']}") else h
+    if "softmax" in label:
+        return 8 * n * c
+    v = label[label.index("[") + 1:-1] if "[" in label else ""
+    tags = v.split(".")[-1] if v else ""
+    if v.startswith("BMM"):
+        a = 4 * n * fin if tags[0] == "F" else 4 * n * spw(fin)
+        o = 4 * n * spw(fout) if tags[2] == "B" else 4 * n * fout
+        return a + 4 * fout * spw(fin) + 4 * fout + o
+    if v.startswith("BSpMM"):
+        which = "loops" if shapes["model"] == "gcn" else "raw"
+        x = 4 * n * spw(fout) if tags[0] == "B" else 4 * n * fout
+        o = 4 * n * spw(fout) if tags[2] == "B" else 4 * n * fout
+        return frdc(which) + x + o
+    return 0
+
+
+# --------------------------------------------------------------------------- #
+# reference arm
+# --------------------------------------------------------------------------- #
+def run_reference(args, wl):
+    import pyoracle as po
+
+    model, n, e, f, h, c, plan = WORKLOADS[wl]
+    po.ref()
+    threads = po.ref().ref_max_threads()
+    t = time.time()
+    src, dst = po.ref_random_edges(GRAPH_SEED, n, e, False)
+    rg = po.RefGraph(n, src, dst)  # reference prepare_graph (its own sort)
+    rm = po.RefModel(rg, model, f, h, c, MODEL_SEED, n, 32, plan)
+    log(f"reference setup {time.time() - t:.1f}s, {threads} threads")
+    for _ in range(args.warmup):
+        rm.time_forward()
+    times = [rm.time_forward() for _ in range(args.steps)]
+    ms = float(np.mean(times))
+    nnz_bits = int(rg.frdc(0 if model == "gcn" else 1).nnz_bits())
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(ms, 3), "unit": "ms",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "b1+f64",
+        "data": "synthetic (reference generators: random_edges seed 100, build_model seed 99)",
+        "config": workload_config(wl, nnz_bits),
+        "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} full-graph forwards (bitgnn::run_model, OpenMP, "
+                                   f"{threads} threads) after {args.warmup} warm-up"},
+        "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "median_ms": round(float(np.median(times)), 3),
+        "kernels_ms": rm.kernel_times(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(wl, nnz_bits=None):
+    model, n, e, f, h, c, plan = WORKLOADS[wl]
+    from paper_2305_02522_b200.bitgnn import DEFAULT_PLANS
+    return {"workload": f"{wl}-shape {model}", "model_family": model, "nodes": n, "edge_draws": e,
+            "adjacency_bits": nnz_bits, "features": f, "hidden": h, "classes": c,
+            "plan": plan or DEFAULT_PLANS[model], "word_bits": 32,
+            "l2": "inputs larger than L2 (X fp32 and the FRDC adjacency each exceed 126 MB)"
+                  if wl in ("reddit", "products") else "inputs smaller than L2 (launch-bound)"}
+
+
+# --------------------------------------------------------------------------- #
+# B200 arm
+# --------------------------------------------------------------------------- #
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="reddit", choices=list(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true", help="no nvidia-smi sampler (profiling runs)")
+    ap.add_argument("--cpu-budget-s", type=float, default=25.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, args.workload)
+        return
+
+    import torch
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2305_02522_b200 as bg
+    from paper_2305_02522_b200 import sharded
+
+    model_name, n, e, f, h, c, plan = WORKLOADS[args.workload]
+    t = time.time()
+    src, dst = bg.Rng(GRAPH_SEED).random_edges(n, e, False)
+    layers, X = bg.build_model_spec(model_name, f, h, c, MODEL_SEED, n, plan)
+    t_gen = time.time() - t
+    stream = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        t = time.time()
+        graph = bg.prepare_graph(n, src, dst)
+        torch.cuda.synchronize()
+        t_frdc = (time.time() - t) * 1e3
+        if world > 1:
+            runner = sharded.ShardedModel(layers, graph, dist, world, rank)
+        else:
+            runner = bg.Model(layers, graph)
+        x = torch.from_numpy(X).cuda()
+        out = torch.empty((n, c), dtype=torch.float32, device="cuda")
+        loops = graph.structure if model_name == "gcn" else graph.raw
+        shapes = {"nodes": n, "features": f, "hidden": h, "classes": c, "model": model_name,
+                  "last_conv": 1 if model_name != "saint" else 2,
+                  "loops_tile_rows": graph.structure.tile_rows, "loops_nnz_tiles": graph.structure.nnz_tiles,
+                  "raw_tile_rows": graph.raw.tile_rows, "raw_nnz_tiles": graph.raw.nnz_tiles}
+        nnz_bits = loops.nnz_bits
+        log(f"inputs {t_gen:.1f}s, device FRDC build {t_frdc:.0f} ms, nnz_bits {nnz_bits}")
+
+        for _ in range(args.warmup):
+            runner.forward(x, out)
+        stream.synchronize()
+
+        under_profiler = any(k.startswith(("NV_COMPUTE_PROFILER", "NSIGHT", "NV_NSIGHT")) for k in os.environ)
+        clocks = ClockSampler(local, enabled=not (args.no_clocks or under_profiler))
+        clocks.start()
+        t_soak = time.time()
+        while time.time() - t_soak < 0.6:  # steady clocks + sampler coverage
+            runner.forward(x, out)
+        stream.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clocks.begin_window()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            runner.forward(x, out)
+        ev1.record(stream)
+        ev1.synchronize()
+        clocks.end_window()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ms = ev0.elapsed_time(ev1) / args.steps
+        if dist:
+            tt = torch.tensor([ms], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        clocks.stop()
+
+        # Per-kernel device times (CUDA events on the launching stream).
+        per = {}
+        reps = max(3, min(args.steps, 10))
+        for _ in range(reps):
+            _, tl = runner.forward_timed(x)
+            for k in tl:
+                per.setdefault(k.label, []).append(k.ms)
+        kernels = []
+        for lab, v in per.items():
+            kms = float(np.mean(v))
+            b = kernel_bytes(lab, shapes)
+            kernels.append({"label": lab, "ms": round(kms, 4), "alg_bytes": b,
+                            "gb_s": round(b / (kms * 1e-3) / 1e9, 1) if kms > 0 else None})
+        launches_per_step = len(per)
+
+        # End-to-end through the C ABI with host buffers (H2D + forward + D2H).
+        xh = torch.from_numpy(X).pin_memory()
+        e2e_steps = max(2, min(args.steps, 10))
+        runner.forward_host(xh)
+        stream.synchronize()
+        t = time.perf_counter()
+        for _ in range(e2e_steps):
+            runner.forward_host(xh)
+        e2e_ms = (time.perf_counter() - t) * 1e3 / e2e_steps
+
+    peak, peak_kind = peaks()
+    dom = max(kernels, key=lambda k: k["ms"])
+    spmm = [k for k in kernels if "BSpMM.BBB" in k["label"]]
+    gteps = (nnz_bits / (spmm[0]["ms"] * 1e-3) / 1e9) if spmm else None
+    achieved = dom["alg_bytes"] / (dom["ms"] * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "b1+f64",
+        "data": "synthetic (reference generators: random_edges seed 100, build_model seed 99)",
+        "config": workload_config(args.workload, nnz_bits),
+        "bit_spmm_gteps": round(gteps, 1) if gteps else None,
+        "roofline": {"bound": "hbm", "kernel": dom["label"], "achieved": round(achieved, 1),
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dom["label"])},
+        "kernels": kernels,
+        "e2e": {"value": round(e2e_ms, 3), "unit": "ms",
+                "h2d_bytes_per_step": int(X.nbytes), "d2h_bytes_per_step": int(n * c * 4)},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks.summary(),
+        "frdc_build_ms": round(t_frdc, 1),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, graph, out, model_name, n, f, h, c, plan)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def ncu_traffic(label):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        return json.load(fh).get(label)
+
+
+def cpu_baseline(args, graph, out, model_name, n, f, h, c, plan):
+    """Reference run_model on the host cores, bounded sample: full-graph
+    forwards until ~cpu_budget_s.  The reference graph is assembled from the
+    device-built FRDC arrays (byte-identical, see tests) through the
+    reference's validating FrdcMatrix constructor."""
+    try:
+        import pyoracle as po
+        if not po.ref_available():
+            return None
+        t = time.time()
+        a, r = graph.structure.download(), graph.raw.download()
+        rg = po.RefGraph.from_frdc(n, po.Frdc(n, n, *a), po.Frdc(n, n, *r))
+        rm = po.RefModel(rg, model_name, f, h, c, MODEL_SEED, n, 32, plan)
+        threads = po.ref().ref_max_threads()
+        setup = time.time() - t
+        rm.time_forward()  # warm-up
+        times = []
+        t = time.time()
+        while not times or (time.time() - t < args.cpu_budget_s and len(times) < 5):
+            times.append(rm.time_forward())
+        ms = float(np.median(times))
+        # parity of this run: GPU logits-side output vs the reference output
+        rout, _, _ = rm.run(c, trace=False)
+        got = out.cpu().numpy()
+        return {"value": round(ms, 2), "unit": "ms", "cores": threads, "kind": "reference",
+                "sample": f"{len(times)} full-graph forwards of the same workload (median) after 1 "
+                          f"warm-up; bitgnn::run_model built from /root/reference/proj/src, "
+                          f"{threads} OpenMP threads; setup {setup:.1f}s",
+                "speedup_vs_value": None,
+                "output_max_abs_diff": float(np.max(np.abs(got - rout)))}
+    except Exception as ex:  # the baseline is reported, never required
+        log("cpu baseline failed:", ex)
+        return None
+
+
+if __name__ == "__main__":
+    main()

@@ -509,6 +509,9 @@ def ref() -> C.CDLL:
         L.ref_graph_create.restype = C.c_void_p
         L.ref_graph_create.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int64]
         L.ref_graph_free.argtypes = [C.c_void_p]
+        L.ref_graph_from_frdc.restype = C.c_void_p
+        L.ref_graph_from_frdc.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
         L.ref_graph_frdc.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int64),
                                      C.POINTER(C.POINTER(C.c_uint64)), C.POINTER(C.POINTER(C.c_uint32)),
                                      C.POINTER(C.POINTER(C.c_uint16))]
@@ -541,6 +544,18 @@ def ref_random_edges(seed: int, nodes: int, m: int, allow_self: bool = False):
 
 
 class RefGraph:
+    @staticmethod
+    def from_frdc(n: int, loops: "Frdc", raw: "Frdc") -> "RefGraph":
+        g = RefGraph.__new__(RefGraph)
+        g.n = n
+        a = [np.ascontiguousarray(x) for x in (loops.row_ptr, loops.col_ind, loops.tiles,
+                                               raw.row_ptr, raw.col_ind, raw.tiles)]
+        g.h = ref().ref_graph_from_frdc(n, _ptr(a[0]), _ptr(a[1]), _ptr(a[2]), loops.nnz,
+                                        _ptr(a[3]), _ptr(a[4]), _ptr(a[5]), raw.nnz)
+        if not g.h:
+            raise ValueError(ref().ref_error().decode())
+        return g
+
     def __init__(self, n: int, src: np.ndarray, dst: np.ndarray):
         src = np.ascontiguousarray(src, dtype=np.int64)
         dst = np.ascontiguousarray(dst, dtype=np.int64)
