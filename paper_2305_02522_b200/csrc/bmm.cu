@@ -20,7 +20,7 @@ namespace {
 constexpr int kWarps = 8;
 constexpr int kMaxOutPerLane = 8;  // output columns per lane per pass (256 per pass)
 
-template <bool AF, bool OUTB>
+template <bool AF, bool OUTB, int M>
 __global__ void __launch_bounds__(kWarps * 32)
     k_bmm(const uint32_t* __restrict__ a_bits, const float* __restrict__ a_f,
           const float* __restrict__ alpha, const uint32_t* __restrict__ wt,
@@ -37,7 +37,6 @@ __global__ void __launch_bounds__(kWarps * 32)
   }
   __syncthreads();
   uint32_t* arow = srow + warp * kspw;
-  const int m_count = static_cast<int>((nc + 31) / 32);
   for (int64_t row = static_cast<int64_t>(blockIdx.x) * kWarps + warp; row < rows;
        row += static_cast<int64_t>(gridDim.x) * kWarps) {
     if (AF) {
@@ -59,20 +58,19 @@ __global__ void __launch_bounds__(kWarps * 32)
       for (int64_t w = lane; w < kspw; w += 32) arow[w] = __ldg(a_bits + row * kspw + w);
     }
     __syncwarp();
-    int diff[kMaxOutPerLane];
+    int diff[M];
 #pragma unroll
-    for (int m = 0; m < kMaxOutPerLane; ++m) diff[m] = 0;
+    for (int m = 0; m < M; ++m) diff[m] = 0;
+    const uint32_t* swl = sw + lane * ld;
     for (int64_t w = 0; w < kspw; ++w) {
       const uint32_t aw = arow[w];
 #pragma unroll
-      for (int m = 0; m < kMaxOutPerLane; ++m)
-        if (m < m_count) diff[m] += __popc(aw ^ sw[(32 * m + lane) * ld + w]);
+      for (int m = 0; m < M; ++m) diff[m] += __popc(aw ^ swl[32 * m * ld + w]);
     }
     __syncwarp();
     if (OUTB) {
 #pragma unroll
-      for (int m = 0; m < kMaxOutPerLane; ++m) {
-        if (m >= m_count) break;
+      for (int m = 0; m < M; ++m) {
         const int64_t j = 32 * m + lane;
         const bool bit = j < nc && (k - 2 * static_cast<int64_t>(diff[m])) >= 0;
         const uint32_t word = __brev(__ballot_sync(0xFFFFFFFFu, bit));
@@ -84,8 +82,7 @@ __global__ void __launch_bounds__(kWarps * 32)
     } else {
       const double al = alpha ? static_cast<double>(alpha[row]) : 1.0;
 #pragma unroll
-      for (int m = 0; m < kMaxOutPerLane; ++m) {
-        if (m >= m_count) break;
+      for (int m = 0; m < M; ++m) {
         const int64_t j = 32 * m + lane;
         if (j < nc) {
           const double be = beta ? static_cast<double>(beta[c0 + j]) : 1.0;
@@ -99,6 +96,10 @@ __global__ void __launch_bounds__(kWarps * 32)
 
 template <bool AF, bool OUTB>
 void launch(const BmmArgs& a, cudaStream_t s) {
+  auto pick = [](int64_t nc) {
+    return nc <= 32 ? k_bmm<AF, OUTB, 1> : nc <= 64 ? k_bmm<AF, OUTB, 2>
+         : nc <= 128 ? k_bmm<AF, OUTB, 4> : k_bmm<AF, OUTB, 8>;
+  };
   const int64_t kspw = spw(a.k, a.wb);
   const int64_t ld = kspw | 1;
   const int64_t ospw = spw(a.n, a.wb);
@@ -108,7 +109,7 @@ void launch(const BmmArgs& a, cudaStream_t s) {
   for (int64_t c0 = 0; c0 < a.n; c0 += pass) {
     const int64_t nc = std::min(pass, a.n - c0);
     const size_t smem = static_cast<size_t>(cdiv(nc, 32) * 32 * ld + kWarps * kspw) * 4;
-    auto kern = k_bmm<AF, OUTB>;
+    auto kern = pick(nc);
     if (smem > 48 * 1024) BG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                       static_cast<int>(smem)));
     if (smem > 200 * 1024) fail("bmm: inner dimension too large for one pass");

@@ -23,45 +23,22 @@
 #include <algorithm>
 
 #include "ops.cuh"
+#include "tilewalk.cuh"
 
 namespace bg {
 namespace {
 
-constexpr int kRing = 256;  // ring entries per node row per warp
 constexpr int kBBWarps = 8;
 
-__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) {
-  return (a & b) | (c & (a ^ b));
-}
-
-// Harley-Seal: add 8 words into bit-sliced planes P[0..NP) (P[q] weight 2^q).
-template <int NP>
-__device__ __forceinline__ void hs_add8(uint32_t (&P)[NP], const uint32_t (&x)[8]) {
-  uint32_t t1, t2, f1, f2, e, s;
-  s = P[0] ^ x[0] ^ x[1]; t1 = maj3(P[0], x[0], x[1]); P[0] = s;
-  s = P[0] ^ x[2] ^ x[3]; t2 = maj3(P[0], x[2], x[3]); P[0] = s;
-  s = P[1] ^ t1 ^ t2;     f1 = maj3(P[1], t1, t2);     P[1] = s;
-  s = P[0] ^ x[4] ^ x[5]; t1 = maj3(P[0], x[4], x[5]); P[0] = s;
-  s = P[0] ^ x[6] ^ x[7]; t2 = maj3(P[0], x[6], x[7]); P[0] = s;
-  s = P[1] ^ t1 ^ t2;     f2 = maj3(P[1], t1, t2);     P[1] = s;
-  s = P[2] ^ f1 ^ f2;     e = maj3(P[2], f1, f2);      P[2] = s;
-#pragma unroll
-  for (int q = 3; q < NP; ++q) {
-    const uint32_t nq = P[q] ^ e;
-    e &= P[q];
-    P[q] = nq;
-  }
-}
-
-// G = word lanes (power of two), S = 32/G slot lanes.  NP planes per lane.
+// G = word lanes (power of two), S = 32/G slot lanes, NP planes per lane.
 template <int G, int NP, bool OUTB>
 __global__ void __launch_bounds__(kBBWarps * 32)
     k_bspmm_bb(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ ci,
                const uint16_t* __restrict__ ti, int64_t trows, int64_t rows,
-               const uint32_t* __restrict__ x, int64_t xspw, int64_t f,
-               uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
+               const int32_t* __restrict__ degree, const uint32_t* __restrict__ x, int64_t xspw,
+               int64_t f, uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
   constexpr int S = 32 / G;
-  constexpr int B = 8 * S;  // edges per batch
+  constexpr int B = 8 * S;  // edges per drained batch
   constexpr int LOGS = S == 1 ? 0 : S == 2 ? 1 : S == 4 ? 2 : S == 8 ? 3 : S == 16 ? 4 : 5;
   constexpr int NQ = NP + LOGS;  // planes after the slot reduction
   __shared__ uint32_t ring_all[kBBWarps][4][kRing];
@@ -70,6 +47,11 @@ __global__ void __launch_bounds__(kBBWarps * 32)
   const int64_t word = static_cast<int64_t>(blockIdx.y) * G + g;
   const bool word_ok = word < xspw;
   uint32_t(*ring)[kRing] = ring_all[warp];
+  // Lanes past the row's last word gather word 0 and discard it, so the
+  // batch loop below needs no per-load predicate.
+  const uint32_t* xw = x + (word_ok ? word : 0);
+  const uint32_t xstride = static_cast<uint32_t>(xspw);
+  (void)degree;
 
   for (int64_t tr = static_cast<int64_t>(blockIdx.x) * kBBWarps + warp; tr < trows;
        tr += static_cast<int64_t>(gridDim.x) * kBBWarps) {
@@ -78,126 +60,47 @@ __global__ void __launch_bounds__(kBBWarps * 32)
     for (int n = 0; n < 4; ++n)
 #pragma unroll
       for (int q = 0; q < NP; ++q) P[n][q] = 0;
-    uint32_t fill[4] = {0, 0, 0, 0}, head[4] = {0, 0, 0, 0};
 
-    auto batch = [&](auto nc, uint32_t h, uint32_t cnt) {
+    auto drain = [&](auto nc, uint32_t h, uint32_t cnt) {
       constexpr int n = decltype(nc)::value;
       uint32_t xv[8];
+      if (cnt == static_cast<uint32_t>(B)) {
 #pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        const uint32_t e = static_cast<uint32_t>(slot + S * m);
-        xv[m] = 0;
-        if (e < cnt && word_ok) {
-          const uint32_t j = ring[n][(h + e) & (kRing - 1)];
-          xv[m] = __ldg(x + static_cast<int64_t>(j) * xspw + word);
+        for (int m = 0; m < 8; ++m) {
+          const uint32_t j = ring[n][(h + slot + S * m) & (kRing - 1)];
+          xv[m] = __ldg(xw + j * xstride);
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const uint32_t e = static_cast<uint32_t>(slot + S * m);
+          xv[m] = 0;
+          if (e < cnt) xv[m] = __ldg(xw + ring[n][(h + e) & (kRing - 1)] * xstride);
         }
       }
       hs_add8<NP>(P[n], xv);
     };
+    uint32_t fill[4];
+    walk_tile_row<B>(rp, ci, ti, tr, ring, fill, drain);
 
-    const uint64_t t0 = rp[tr], t1 = rp[tr + 1];
-    for (uint64_t base = t0; base < t1; base += 32) {
-      __syncwarp();
-      const uint64_t t = base + lane;
-      uint32_t tile = 0, col = 0;
-      if (t < t1) {
-        tile = __ldg(ti + t);
-        col = __ldg(ci + t);
-      }
-      const uint32_t packed = __popc(tile >> 12) | (__popc((tile >> 8) & 0xFu) << 8) |
-                              (__popc((tile >> 4) & 0xFu) << 16) | (__popc(tile & 0xFu) << 24);
-      uint32_t incl = packed;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-        if (lane >= d) incl += v;
-      }
-      const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-      const uint32_t excl = incl - packed;
-#pragma unroll
-      for (int n = 0; n < 4; ++n) {
-        uint32_t pos = fill[n] + ((excl >> (8 * n)) & 0xFFu);
-        uint32_t nib = (tile >> (12 - 4 * n)) & 0xFu;
-        while (nib) {
-          const int b = __ffs(nib) - 1;  // bit b of the nibble is local column 3 - b
-          nib &= nib - 1;
-          ring[n][pos & (kRing - 1)] = 4 * col + (3 - b);
-          ++pos;
-        }
-        fill[n] += (total >> (8 * n)) & 0xFFu;
-      }
-      __syncwarp();
-#pragma unroll
-      for (int n = 0; n < 4; ++n) {
-        while (fill[n] - head[n] >= static_cast<uint32_t>(B)) {
-          switch (n) {
-            case 0: batch(std::integral_constant<int, 0>{}, head[n], B); break;
-            case 1: batch(std::integral_constant<int, 1>{}, head[n], B); break;
-            case 2: batch(std::integral_constant<int, 2>{}, head[n], B); break;
-            default: batch(std::integral_constant<int, 3>{}, head[n], B); break;
-          }
-          head[n] += B;
-        }
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int n = 0; n < 4; ++n) {
-      if (fill[n] > head[n]) {
-        const uint32_t cnt = fill[n] - head[n];
-        switch (n) {
-          case 0: batch(std::integral_constant<int, 0>{}, head[n], cnt); break;
-          case 1: batch(std::integral_constant<int, 1>{}, head[n], cnt); break;
-          case 2: batch(std::integral_constant<int, 2>{}, head[n], cnt); break;
-          default: batch(std::integral_constant<int, 3>{}, head[n], cnt); break;
-        }
-      }
-    }
-
-    // Slot reduction (bit-sliced butterfly) and epilogue per node row.
+    // Slot reduction and epilogue per node row.
 #pragma unroll
     for (int n = 0; n < 4; ++n) {
       uint32_t Q[NQ];
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) Q[q] = q < NP ? P[n][q] : 0u;
-#pragma unroll
-      for (int d = G; d < 32; d <<= 1) {
-        uint32_t c = 0;
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          const uint32_t a = Q[q], b = __shfl_xor_sync(0xFFFFFFFFu, Q[q], d);
-          Q[q] = a ^ b ^ c;
-          c = maj3(a, b, c);
-        }
-      }
+      slot_reduce<G, NP, NQ>(P[n], Q);
       const int64_t row = 4 * tr + n;
-      if (row >= rows) continue;
+      if (row >= rows || !word_ok) continue;
       const uint32_t deg = fill[n];
       if (OUTB) {
         // cnt >= ceil(deg/2)  <=>  2*cnt - deg >= 0   (kernels.cpp:440-454)
-        const uint32_t T = (deg + 1) >> 1;
-        uint32_t gt = 0, eq = 0xFFFFFFFFu;
-#pragma unroll
-        for (int q = NQ - 1; q >= 0; --q) {
-          if ((T >> q) & 1u) {
-            eq &= Q[q];
-          } else {
-            gt |= eq & Q[q];
-            eq &= ~Q[q];
-          }
-        }
-        if (T >> NQ) gt = eq = 0;  // unreachable for supported degrees
-        uint32_t ge = gt | eq;
+        uint32_t ge = planes_ge<NQ>(Q, (deg + 1) >> 1);
         if (32 * (word + 1) > f) ge &= (32 * word >= f) ? 0u : tail_mask32(f);
-        if (slot == 0 && word_ok) out_bits[row * xspw + word] = ge;
-      } else if (word_ok) {
+        if (slot == 0) out_bits[row * xspw + word] = ge;
+      } else {
         for (int b = slot; b < 32; b += S) {
           const int64_t k = 32 * word + b;
           if (k >= f) break;
-          uint32_t cnt = 0;
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) cnt |= ((Q[q] >> (31 - b)) & 1u) << q;
-          out_f[row * f + k] = static_cast<float>(2 * static_cast<int64_t>(cnt) -
+          out_f[row * f + k] = static_cast<float>(2 * static_cast<int64_t>(plane_count<NQ>(Q, b)) -
                                                   static_cast<int64_t>(deg));
         }
       }
@@ -213,7 +116,7 @@ void launch_bb(const bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uin
       1, std::min<int64_t>(cdiv(A.tile_rows, kBBWarps), static_cast<int64_t>(sm_count()) * 64));
   dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(groups));
   k_bspmm_bb<G, NP, OUTB><<<grid, kBBWarps * 32, 0, s>>>(A.rp(), A.ci(), A.ti(), A.tile_rows,
-                                                         A.rows, x, xspw, f, ob, of);
+                                                         A.rows, A.deg(), x, xspw, f, ob, of);
   BG_LAUNCH_CHECK();
 }
 
@@ -221,9 +124,12 @@ template <int G, bool OUTB>
 void launch_bb_np(const bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uint32_t* ob,
                   float* of, cudaStream_t s) {
   constexpr int S = 32 / G;
-  // Per slot lane at most deg/S + 8 edges land in its counters.
-  const int64_t per_lane = A.max_deg / S + 8;
-  if (per_lane < (1 << 11)) return launch_bb<G, 11, OUTB>(A, x, f, xspw, ob, of, s);
+  // The ring deals a row's edges round-robin to the S slot lanes in batches
+  // of 8 each, so a lane's counters see at most ceil(deg/(8S))*8 edges.
+  const int64_t per_lane = (A.max_deg + 8 * S - 1) / (8 * S) * 8;
+  if (per_lane < (1 << 7)) return launch_bb<G, 7, OUTB>(A, x, f, xspw, ob, of, s);
+  if (per_lane < (1 << 10)) return launch_bb<G, 10, OUTB>(A, x, f, xspw, ob, of, s);
+  if (per_lane < (1 << 13)) return launch_bb<G, 13, OUTB>(A, x, f, xspw, ob, of, s);
   if (per_lane < (1 << 16)) return launch_bb<G, 16, OUTB>(A, x, f, xspw, ob, of, s);
   fail("bspmm: node degree " + std::to_string(A.max_deg) + " exceeds the counter range");
 }

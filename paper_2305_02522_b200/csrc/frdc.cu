@@ -99,6 +99,36 @@ __global__ void k_degree(const uint64_t* __restrict__ rp, const uint16_t* __rest
   }
 }
 
+// Warp per tile row: lane p sums, per node row, the bits of tiles p, p+32, ...;
+// groups of G lanes are then summed and the maximum kept (G = 4 and 8).
+__global__ void k_slot_max(const uint64_t* __restrict__ rp, const uint16_t* __restrict__ tiles,
+                           int64_t trows, int* __restrict__ out) {
+  const int64_t tr = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (tr >= trows) return;
+  const int lane = threadIdx.x & 31;
+  int c[4] = {0, 0, 0, 0};
+  for (uint64_t k = rp[tr] + lane; k < rp[tr + 1]; k += 32) {
+    const uint32_t t = tiles[k];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) c[r] += __popc((t >> (12 - 4 * r)) & 0xFu);
+  }
+  int m4 = 0, m8 = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    int v = c[r];
+    v += __shfl_xor_sync(0xFFFFFFFFu, v, 1);
+    v += __shfl_xor_sync(0xFFFFFFFFu, v, 2);
+    m4 = v > m4 ? v : m4;
+    v += __shfl_xor_sync(0xFFFFFFFFu, v, 4);
+    m8 = v > m8 ? v : m8;
+  }
+  if (lane == 0 || lane == 4 || lane == 8 || lane == 12 || lane == 16 || lane == 20 ||
+      lane == 24 || lane == 28) {
+    atomicMax(out, m4);
+    atomicMax(out + 1, m8);
+  }
+}
+
 __global__ void k_graph_scales(const int32_t* __restrict__ deg_loops,
                                const int32_t* __restrict__ deg_raw, int64_t n,
                                float* __restrict__ norm, float* __restrict__ mean,
@@ -128,11 +158,20 @@ void frdc_finalize(bg_frdc& m, cudaStream_t s) {
     k_degree<<<grid1(m.tile_rows * 32), 256, 0, s>>>(m.rp(), m.ti(), m.tile_rows, m.rows,
                                                      m.degree.as<int32_t>(), nbits, maxdeg);
   BG_LAUNCH_CHECK();
+  DevBuf slots(8);
+  BG_CUDA(cudaMemsetAsync(slots.p, 0, 8, s));
+  if (m.tile_rows > 0)
+    k_slot_max<<<grid1(m.tile_rows * 32), 256, 0, s>>>(m.rp(), m.ti(), m.tile_rows, slots.as<int>());
+  BG_LAUNCH_CHECK();
   unsigned long long h[2] = {0, 0};
+  int hs[2] = {0, 0};
   BG_CUDA(cudaMemcpyAsync(h, stats.p, 16, cudaMemcpyDeviceToHost, s));
+  BG_CUDA(cudaMemcpyAsync(hs, slots.p, 8, cudaMemcpyDeviceToHost, s));
   BG_CUDA(cudaStreamSynchronize(s));
   m.nnz_bits = static_cast<int64_t>(h[0]);
   m.max_deg = static_cast<int64_t>(static_cast<int>(h[1] & 0xFFFFFFFFull));
+  m.max_slot[0] = hs[0];
+  m.max_slot[1] = hs[1];
 }
 
 std::unique_ptr<bg_frdc> frdc_build(const int64_t* src, const int64_t* dst, int64_t e, int64_t n,

@@ -286,6 +286,8 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
   Exec ex{m, h, s};
   Op cur = x0;
   bool logits_set = false;
+  float* fused_probs = nullptr;   // softmax already produced by a fused epilogue
+  const float* fused_logits = nullptr;
   const size_t nl = m.layers.size();
   for (size_t i = 0; i < nl; ++i) {
     ModelLayer& l = m.layers[i];
@@ -293,8 +295,41 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
     try {
       switch (l.info.kind) {
         case BG_LAYER_GCN: {  // ref: gcn_layer, graphops.cpp:270-285
+          const bg_variant mm = l.info.plan[0], sp = l.info.plan[1];
+          const bool bbf_fbf = mm.op == BG_BMM && mm.in1 == BG_B && mm.in2 == BG_B &&
+                               mm.out == BG_F && sp.op == BG_BSPMM && sp.in1 == BG_F &&
+                               sp.in2 == BG_B && sp.out == BG_F;
+          if (bbf_fbf && !l.relu && cur.prec == BG_B && cur.sem == BG_PLUS_MINUS && !cur.scale &&
+              cur.wb == m.wb && cur.cols == l.w1.rows && cur.rows == m.graph->structure->cols &&
+              gcn1_fused_supported(*m.graph->structure, cur.cols, cur.wb, l.w1.cols)) {
+            // Fused MM.BBF + BSpMM.FBF (+ the following Softmax): bit-identical
+            // logits without materializing the N x C intermediate (gcn_fused.cu).
+            if (h.trace) h.bits(prefix + "mm.bin_w", l.w1.bits.as<uint32_t>(), l.w1.rows, l.w1.cols, l.w1.wb);
+            const bg_frdc& A = *m.graph->structure;
+            auto* recs = static_cast<uint32_t*>(m.pool.get(static_cast<size_t>(A.cols) * 64));
+            h.begin(prefix + "mm[" + variant_name(mm) + "]");
+            gcn1_records(cur.bits, A.cols, cur.cols, cur.wb, l.w1.wt.as<uint32_t>(),
+                         l.w1.scale.as<float>(), l.w1.cols, recs, s);
+            h.end();
+            Op o;
+            o.prec = BG_F;
+            o.rows = A.rows;
+            o.cols = l.w1.cols;
+            o.f = static_cast<float*>(m.pool.get(o.bytes()));
+            float* probs = nullptr;
+            if (i + 1 < nl && m.layers[i + 1].info.kind == BG_LAYER_SOFTMAX) {
+              probs = (i + 2 == nl && out) ? out : static_cast<float*>(m.pool.get(o.bytes()));
+              fused_probs = probs;
+              fused_logits = o.f;
+            }
+            h.begin(prefix + "spmm[" + variant_name(sp) + "]");
+            gcn1_aggregate(A, recs, cur.cols, cur.wb, l.w1.wt.as<uint32_t>(), l.w1.scale.as<float>(),
+                           l.w1.cols, o.f, probs, s);
+            h.end();
+            cur = o;
+            break;
+          }
           Op hh = ex.mm_slot(l.info.plan[0], cur, l.w1, prefix + "mm");
-          const bg_variant sp = l.info.plan[1];
           const bool fac = sp.in2 == BG_F;
           cur = ex.spmm_slot(sp, m.graph->structure.get(), fac ? m.graph->norm.as<float>() : nullptr,
                              fac ? m.graph->norm.as<float>() : nullptr, hh, prefix + "spmm");
@@ -351,10 +386,16 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
             logits_set = true;
           }
           Op o = cur;
-          o.f = (i + 1 == nl && out) ? out : static_cast<float*>(m.pool.get(cur.bytes()));
-          h.begin(prefix + "softmax");
-          softmax_rows(cur.f, cur.rows, cur.cols, o.f, s);
-          h.end();
+          if (fused_probs && cur.f == fused_logits) {
+            o.f = fused_probs;  // computed in the fused aggregation epilogue
+            h.begin(prefix + "softmax");
+            h.end();
+          } else {
+            o.f = (i + 1 == nl && out) ? out : static_cast<float*>(m.pool.get(cur.bytes()));
+            h.begin(prefix + "softmax");
+            softmax_rows(cur.f, cur.rows, cur.cols, o.f, s);
+            h.end();
+          }
           cur = o;
           break;
         }

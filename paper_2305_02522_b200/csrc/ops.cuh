@@ -10,6 +10,10 @@
 struct bg_frdc {
   int64_t rows = 0, cols = 0, tile_rows = 0, tile_cols = 0, nnz = 0, nnz_bits = 0;
   int64_t max_deg = 0;
+  // Most bits of one node row that land in the tiles of G consecutive lanes
+  // (tile k of a tile row goes to lane k % 32) -- sizes the bit-sliced
+  // counters of the aggregation kernels.  Index: 0 -> G=4, 1 -> G=8.
+  int64_t max_slot[2] = {0, 0};
   bg::DevBuf row_ptr;  // u64[tile_rows + 1]
   bg::DevBuf col_ind;  // u32[nnz]
   bg::DevBuf tiles;    // u16[nnz]
@@ -85,6 +89,14 @@ struct SpmmFArgs {
   float* out_f = nullptr;
 };
 void bspmm_f(const bg_frdc& A, const SpmmFArgs& a, cudaStream_t s);
+
+// ---- gcn_fused.cu: MM.BBF + BSpMM.FBF (+ softmax) without materializing Y ----
+bool gcn1_fused_supported(const bg_frdc& A, int64_t K, int wb, int64_t C);
+void gcn1_records(const uint32_t* h, int64_t n, int64_t K, int wb, const uint32_t* wt,
+                  const float* beta, int64_t C, uint32_t* rec_buf, cudaStream_t s);
+void gcn1_aggregate(const bg_frdc& A, const uint32_t* rec_buf, int64_t K, int wb,
+                    const uint32_t* wt, const float* beta, int64_t C, float* logits, float* probs,
+                    cudaStream_t s);
 
 // ---- elementwise.cu ------------------------------------------------------
 void add_bbb(const uint32_t* a, const uint32_t* b, int64_t words, uint32_t* out, cudaStream_t s);
