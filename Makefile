@@ -19,7 +19,7 @@ build/%.o: $(CSRC)/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 
 $(LIB): $(OBJS) $(CSRC)/exports.map
-	$(NVCC) $(ARCH) -shared -cudart static -Xlinker --version-script=$(CSRC)/exports.map -o $@ $(OBJS)
+	$(NVCC) $(ARCH) -shared -cudart static -Xlinker --version-script=$(CSRC)/exports.map -o $@ $(OBJS) -ldl
 
 oracle:
 	$(MAKE) -C oracle all

@@ -249,7 +249,9 @@ def main():
         else:
             runner = bg.Model(layers, graph)
         x = torch.from_numpy(X).cuda()
-        out = torch.empty((n, c), dtype=torch.float32, device="cuda")
+        if world > 1:  # this rank's rows of X stay resident; out holds its rows
+            x = runner._local(x).contiguous()
+        out = torch.empty((x.shape[0], c), dtype=torch.float32, device="cuda")
         loops = graph.structure if model_name == "gcn" else graph.raw
         shapes = {"nodes": n, "features": f, "hidden": h, "classes": c, "model": model_name,
                   "last_conv": 1 if model_name != "saint" else 2,

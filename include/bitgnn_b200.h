@@ -254,10 +254,33 @@ int bg_model_forward_timed(bg_model* m, const bg_mat* x0, float* out, float* log
                            bg_kernel_timing* timings, int cap, int* n, bg_stream stream);
 
 /* ---- row-sharded multi-GPU forward (one process per GPU) ---------------- */
-/* Row range [row_begin, row_end) of a model's graph owned by this rank: tile
- * rows split so every rank holds about the same number of FRDC tiles. */
+/* New capability (the reference is single-process): node rows
+ * are split into contiguous tile-row ranges with about equal FRDC tiles; each
+ * rank computes its rows of every layer and the operand of every neighbour
+ * aggregation is all-gathered over NVLink with NCCL. */
+
+/* HOST: bounds[0..world] (multiples of 4, bounds[world] = n) from an FRDC
+ * row_ptr (tile_rows + 1 entries). */
+int bg_partition_bounds(const uint64_t* row_ptr, int64_t tile_rows, int64_t n, int world_size,
+                        int64_t* bounds);
+/* Row range [row_begin, row_end) of rank `rank` for the graph's A+I structure. */
 int bg_partition_rows(const bg_graph* g, int world_size, int rank, int64_t* row_begin,
                       int64_t* row_end);
+
+typedef struct bg_comm bg_comm; /* NCCL communicator, one rank per GPU */
+/* Rank 0 creates the id and ships its bytes to every rank (e.g. through
+ * torch.distributed); every rank then calls bg_comm_create on its device. */
+int bg_comm_unique_id(uint8_t* id, size_t id_len);
+int bg_comm_create(int world_size, int rank, const uint8_t* id, size_t id_len, bg_comm** out);
+void bg_comm_destroy(bg_comm* c);
+
+/* Sharded ref: run_model.  With a communicator, x/out/logits hold this
+ * rank's rows [bounds[rank], bounds[rank+1]) only.  With comm == NULL every
+ * rank's range is computed in this process on this device ("virtual ranks",
+ * x/out/logits full size) -- the same per-range kernels, no exchange. */
+int bg_model_forward_sharded(bg_model* m, bg_comm* comm, const bg_mat* x, const int64_t* bounds,
+                             int world_size, int rank, float* out, float* logits,
+                             bg_stream stream);
 
 /* ---- deterministic synthetic inputs (ref: rng.hpp:16-80) --------------- */
 typedef struct bg_rng bg_rng;

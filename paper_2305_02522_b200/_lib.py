@@ -117,6 +117,11 @@ PROTOTYPES = {
     "bg_model_forward_timed": (I32, [P, C.POINTER(Mat), P, P, C.POINTER(KernelTiming), I32,
                                      C.POINTER(C.c_int), P]),
     "bg_partition_rows": (I32, [P, I32, I32, PI64, PI64]),
+    "bg_partition_bounds": (I32, [P, I64, I64, I32, P]),
+    "bg_comm_unique_id": (I32, [P, C.c_size_t]),
+    "bg_comm_create": (I32, [I32, I32, P, C.c_size_t, C.POINTER(P)]),
+    "bg_comm_destroy": (None, [P]),
+    "bg_model_forward_sharded": (I32, [P, P, C.POINTER(Mat), P, I32, I32, P, P, P]),
     "bg_rng_create": (I32, [C.c_uint64, C.POINTER(P)]),
     "bg_rng_destroy": (None, [P]),
     "bg_rng_dense": (I32, [P, I64, I64, P]),

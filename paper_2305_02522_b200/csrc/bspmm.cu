@@ -34,7 +34,7 @@ constexpr int kBBWarps = 8;
 template <int G, int NP, bool OUTB>
 __global__ void __launch_bounds__(kBBWarps * 32)
     k_bspmm_bb(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ ci,
-               const uint16_t* __restrict__ ti, int64_t trows, int64_t rows,
+               const uint16_t* __restrict__ ti, int64_t tr0, int64_t trows, int64_t rows,
                const int32_t* __restrict__ degree, const uint32_t* __restrict__ x, int64_t xspw,
                int64_t f, uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
   constexpr int S = 32 / G;
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kBBWarps * 32)
   const uint32_t xstride = static_cast<uint32_t>(xspw);
   (void)degree;
 
-  for (int64_t tr = static_cast<int64_t>(blockIdx.x) * kBBWarps + warp; tr < trows;
+  for (int64_t tr = tr0 + static_cast<int64_t>(blockIdx.x) * kBBWarps + warp; tr < trows;
        tr += static_cast<int64_t>(gridDim.x) * kBBWarps) {
     uint32_t P[4][NP];
 #pragma unroll
@@ -110,27 +110,27 @@ __global__ void __launch_bounds__(kBBWarps * 32)
 
 template <int G, int NP, bool OUTB>
 void launch_bb(const bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uint32_t* ob,
-               float* of, cudaStream_t s) {
+               float* of, int64_t t0, int64_t t1, cudaStream_t s) {
   const int64_t groups = cdiv(xspw, G);
   const int64_t blocks = std::max<int64_t>(
-      1, std::min<int64_t>(cdiv(A.tile_rows, kBBWarps), static_cast<int64_t>(sm_count()) * 64));
+      1, std::min<int64_t>(cdiv(t1 - t0, kBBWarps), static_cast<int64_t>(sm_count()) * 64));
   dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(groups));
-  k_bspmm_bb<G, NP, OUTB><<<grid, kBBWarps * 32, 0, s>>>(A.rp(), A.ci(), A.ti(), A.tile_rows,
+  k_bspmm_bb<G, NP, OUTB><<<grid, kBBWarps * 32, 0, s>>>(A.rp(), A.ci(), A.ti(), t0, t1,
                                                          A.rows, A.deg(), x, xspw, f, ob, of);
   BG_LAUNCH_CHECK();
 }
 
 template <int G, bool OUTB>
 void launch_bb_np(const bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uint32_t* ob,
-                  float* of, cudaStream_t s) {
+                  float* of, int64_t t0, int64_t t1, cudaStream_t s) {
   constexpr int S = 32 / G;
   // The ring deals a row's edges round-robin to the S slot lanes in batches
   // of 8 each, so a lane's counters see at most ceil(deg/(8S))*8 edges.
   const int64_t per_lane = (A.max_deg + 8 * S - 1) / (8 * S) * 8;
-  if (per_lane < (1 << 7)) return launch_bb<G, 7, OUTB>(A, x, f, xspw, ob, of, s);
-  if (per_lane < (1 << 10)) return launch_bb<G, 10, OUTB>(A, x, f, xspw, ob, of, s);
-  if (per_lane < (1 << 13)) return launch_bb<G, 13, OUTB>(A, x, f, xspw, ob, of, s);
-  if (per_lane < (1 << 16)) return launch_bb<G, 16, OUTB>(A, x, f, xspw, ob, of, s);
+  if (per_lane < (1 << 7)) return launch_bb<G, 7, OUTB>(A, x, f, xspw, ob, of, t0, t1, s);
+  if (per_lane < (1 << 10)) return launch_bb<G, 10, OUTB>(A, x, f, xspw, ob, of, t0, t1, s);
+  if (per_lane < (1 << 13)) return launch_bb<G, 13, OUTB>(A, x, f, xspw, ob, of, t0, t1, s);
+  if (per_lane < (1 << 16)) return launch_bb<G, 16, OUTB>(A, x, f, xspw, ob, of, t0, t1, s);
   fail("bspmm: node degree " + std::to_string(A.max_deg) + " exceeds the counter range");
 }
 
@@ -141,8 +141,8 @@ __global__ void __launch_bounds__(256)
               const uint16_t* __restrict__ ti, int64_t rows, const float* __restrict__ xf,
               const uint32_t* __restrict__ xb, int64_t xspw, const float* __restrict__ rs,
               const float* __restrict__ cs, int64_t f, int64_t ospw,
-              uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
-  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+              uint32_t* __restrict__ out_bits, float* __restrict__ out_f, int64_t row0) {
+  const int64_t i = row0 + ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
   if (i >= rows) return;
   const int lane = threadIdx.x & 31;
   const int64_t fbase = static_cast<int64_t>(blockIdx.y) * 32 * M;
@@ -203,56 +203,59 @@ __global__ void __launch_bounds__(256)
 }
 
 template <int M, bool XBITS, bool OUTB>
-void launch_f(const bg_frdc& A, const SpmmFArgs& a, cudaStream_t s) {
+void launch_f(const bg_frdc& A, const SpmmFArgs& a, int64_t row0, int64_t row1, cudaStream_t s) {
   const int64_t passes = cdiv(a.f, 32 * M);
-  dim3 grid(static_cast<unsigned>(cdiv(A.rows * 32, 256)), static_cast<unsigned>(passes));
+  dim3 grid(static_cast<unsigned>(cdiv((row1 - row0) * 32, 256)), static_cast<unsigned>(passes));
   const int64_t xspw = XBITS ? spw(a.f, a.xwb) : 0;
   const int64_t ospw = OUTB ? spw(a.f, a.owb) : 0;
-  k_bspmm_f<M, XBITS, OUTB><<<grid, 256, 0, s>>>(A.rp(), A.ci(), A.ti(), A.rows, a.x_f, a.x_bits,
+  k_bspmm_f<M, XBITS, OUTB><<<grid, 256, 0, s>>>(A.rp(), A.ci(), A.ti(), row1, a.x_f, a.x_bits,
                                                  xspw, a.row_scale, a.col_scale, a.f, ospw,
-                                                 a.out_bits, a.out_f);
+                                                 a.out_bits, a.out_f, row0);
   BG_LAUNCH_CHECK();
 }
 
 template <bool XBITS, bool OUTB>
-void launch_f_m(const bg_frdc& A, const SpmmFArgs& a, cudaStream_t s) {
-  if (a.f <= 32) launch_f<1, XBITS, OUTB>(A, a, s);
-  else if (a.f <= 64) launch_f<2, XBITS, OUTB>(A, a, s);
-  else launch_f<4, XBITS, OUTB>(A, a, s);
+void launch_f_m(const bg_frdc& A, const SpmmFArgs& a, int64_t r0, int64_t r1, cudaStream_t s) {
+  if (a.f <= 32) launch_f<1, XBITS, OUTB>(A, a, r0, r1, s);
+  else if (a.f <= 64) launch_f<2, XBITS, OUTB>(A, a, r0, r1, s);
+  else launch_f<4, XBITS, OUTB>(A, a, r0, r1, s);
 }
 
 }  // namespace
 
 void bspmm_bb(const bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* out_bits,
-              float* out_f, cudaStream_t s) {
-  if (A.rows == 0) return;
+              float* out_f, cudaStream_t s, int64_t row0, int64_t row1) {
+  if (row1 < 0) row1 = A.rows;
+  const int64_t t0 = row0 / 4, t1 = (row1 + 3) / 4;
+  if (A.rows == 0 || t1 <= t0) return;
   const int64_t xspw = spw(f, wb);
   if (xspw == 0) {
     return;
   }
   const bool ob = out_bits != nullptr;
   if (xspw <= 4) {
-    if (ob) launch_bb_np<4, true>(A, x, f, xspw, out_bits, out_f, s);
-    else launch_bb_np<4, false>(A, x, f, xspw, out_bits, out_f, s);
+    if (ob) launch_bb_np<4, true>(A, x, f, xspw, out_bits, out_f, t0, t1, s);
+    else launch_bb_np<4, false>(A, x, f, xspw, out_bits, out_f, t0, t1, s);
   } else if (xspw <= 8) {
-    if (ob) launch_bb_np<8, true>(A, x, f, xspw, out_bits, out_f, s);
-    else launch_bb_np<8, false>(A, x, f, xspw, out_bits, out_f, s);
+    if (ob) launch_bb_np<8, true>(A, x, f, xspw, out_bits, out_f, t0, t1, s);
+    else launch_bb_np<8, false>(A, x, f, xspw, out_bits, out_f, t0, t1, s);
   } else if (xspw <= 16) {
-    if (ob) launch_bb_np<16, true>(A, x, f, xspw, out_bits, out_f, s);
-    else launch_bb_np<16, false>(A, x, f, xspw, out_bits, out_f, s);
+    if (ob) launch_bb_np<16, true>(A, x, f, xspw, out_bits, out_f, t0, t1, s);
+    else launch_bb_np<16, false>(A, x, f, xspw, out_bits, out_f, t0, t1, s);
   } else {
-    if (ob) launch_bb_np<32, true>(A, x, f, xspw, out_bits, out_f, s);
-    else launch_bb_np<32, false>(A, x, f, xspw, out_bits, out_f, s);
+    if (ob) launch_bb_np<32, true>(A, x, f, xspw, out_bits, out_f, t0, t1, s);
+    else launch_bb_np<32, false>(A, x, f, xspw, out_bits, out_f, t0, t1, s);
   }
 }
 
-void bspmm_f(const bg_frdc& A, const SpmmFArgs& a, cudaStream_t s) {
-  if (A.rows == 0 || a.f == 0) return;
+void bspmm_f(const bg_frdc& A, const SpmmFArgs& a, cudaStream_t s, int64_t row0, int64_t row1) {
+  if (row1 < 0) row1 = A.rows;
+  if (A.rows == 0 || a.f == 0 || row1 <= row0) return;
   const bool xb = a.x_bits != nullptr, ob = a.out_bits != nullptr;
-  if (xb && ob) launch_f_m<true, true>(A, a, s);
-  else if (xb) launch_f_m<true, false>(A, a, s);
-  else if (ob) launch_f_m<false, true>(A, a, s);
-  else launch_f_m<false, false>(A, a, s);
+  if (xb && ob) launch_f_m<true, true>(A, a, row0, row1, s);
+  else if (xb) launch_f_m<true, false>(A, a, row0, row1, s);
+  else if (ob) launch_f_m<false, true>(A, a, row0, row1, s);
+  else launch_f_m<false, false>(A, a, row0, row1, s);
 }
 
 }  // namespace bg

@@ -537,23 +537,24 @@ int bg_model_forward_timed(bg_model* m, const bg_mat* x0, float* out, float* log
 
 // ---- multi-GPU row partition ------------------------------------------------
 int bg_partition_rows(const bg_graph* g, int world, int rank, int64_t* r0, int64_t* r1) {
-  return guard([&] {
+  int rc = guard([&] {
     need(g, "graph");
     if (world < 1 || rank < 0 || rank >= world) fail("partition: bad rank/world size");
-    const bg_frdc& A = *g->structure;
-    std::vector<uint64_t> rp(static_cast<size_t>(A.tile_rows + 1));
-    BG_CUDA(cudaMemcpy(rp.data(), A.row_ptr.p, rp.size() * 8, cudaMemcpyDeviceToHost));
-    auto bound = [&](int k) -> int64_t {
-      if (k <= 0) return 0;
-      if (k >= world) return A.tile_rows;
-      const uint64_t target = (rp.back() * static_cast<uint64_t>(k) + world - 1) / world;
-      return std::lower_bound(rp.begin(), rp.end(), target) - rp.begin();
-    };
-    const int64_t t0 = std::min<int64_t>(bound(rank), A.tile_rows);
-    const int64_t t1 = std::max<int64_t>(t0, std::min<int64_t>(bound(rank + 1), A.tile_rows));
-    *r0 = std::min<int64_t>(4 * t0, g->n);
-    *r1 = std::min<int64_t>(4 * t1, g->n);
   });
+  if (rc) return rc;
+  std::vector<uint64_t> rp;
+  std::vector<int64_t> bounds(static_cast<size_t>(world) + 1);
+  rc = guard([&] {
+    const bg_frdc& A = *g->structure;
+    rp.resize(static_cast<size_t>(A.tile_rows + 1));
+    BG_CUDA(cudaMemcpy(rp.data(), A.row_ptr.p, rp.size() * 8, cudaMemcpyDeviceToHost));
+  });
+  if (rc) return rc;
+  rc = bg_partition_bounds(rp.data(), g->structure->tile_rows, g->n, world, bounds.data());
+  if (rc) return rc;
+  *r0 = bounds[static_cast<size_t>(rank)];
+  *r1 = bounds[static_cast<size_t>(rank) + 1];
+  return BG_OK;
 }
 
 // ---- synthetic inputs (ref: rng.hpp:16-80) ------------------------------------

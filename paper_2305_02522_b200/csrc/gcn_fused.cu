@@ -74,7 +74,7 @@ __global__ void k_gcn1_records(const uint32_t* __restrict__ h, int64_t rows, int
 template <int NP>
 __global__ void __launch_bounds__(kFWarps * 32)
     k_gcn1_aggregate(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ ci,
-                     const uint16_t* __restrict__ ti, int64_t trows, int64_t rows,
+                     const uint16_t* __restrict__ ti, int64_t tr0, int64_t trows, int64_t rows,
                      const int32_t* __restrict__ degree, const uint32_t* __restrict__ rec,
                      const uint32_t* __restrict__ wt, int hspw, int K,
                      const float* __restrict__ beta, int C, float* __restrict__ logits,
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kFWarps * 32)
   const bool hlane = g < 4;
   (void)degree;
 
-  for (int64_t tr = static_cast<int64_t>(blockIdx.x) * kFWarps + warp; tr < trows;
+  for (int64_t tr = tr0 + static_cast<int64_t>(blockIdx.x) * kFWarps + warp; tr < trows;
        tr += static_cast<int64_t>(gridDim.x) * kFWarps) {
     uint32_t P[4][NP];
     uint32_t alo[4], ahi[4];
@@ -221,14 +221,17 @@ void gcn1_records(const uint32_t* h, int64_t n, int64_t K, int wb, const uint32_
 
 void gcn1_aggregate(const bg_frdc& A, const uint32_t* rec_buf, int64_t K, int wb,
                     const uint32_t* wt, const float* beta, int64_t C, float* logits, float* probs,
-                    cudaStream_t s) {
+                    cudaStream_t s, int64_t row0, int64_t row1) {
+  if (row1 < 0) row1 = A.rows;
+  const int64_t t0 = row0 / 4, t1 = (row1 + 3) / 4;
+  if (t1 <= t0) return;
   const int hspw = static_cast<int>(spw(K, wb));
   const int64_t blocks = std::max<int64_t>(
-      1, std::min<int64_t>(cdiv(A.tile_rows, kFWarps), static_cast<int64_t>(sm_count()) * 64));
+      1, std::min<int64_t>(cdiv(t1 - t0, kFWarps), static_cast<int64_t>(sm_count()) * 64));
   const int64_t per_lane = (A.max_deg + 15) / 16 * 8;  // ring deals edges to 2 slots
   auto go = [&](auto kern) {
     kern<<<static_cast<unsigned>(blocks), kFWarps * 32, 0, s>>>(
-        A.rp(), A.ci(), A.ti(), A.tile_rows, A.rows, A.deg(), rec_buf, wt, hspw,
+        A.rp(), A.ci(), A.ti(), t0, t1, A.rows, A.deg(), rec_buf, wt, hspw,
         static_cast<int>(K), beta, static_cast<int>(C), logits, probs);
   };
   if (per_lane < (1 << 7)) go(k_gcn1_aggregate<7>);

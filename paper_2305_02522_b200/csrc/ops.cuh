@@ -73,8 +73,9 @@ void bmm(const BmmArgs& a, cudaStream_t s);
 
 // ---- bspmm.cu ------------------------------------------------------------
 // Integer path (BBB / BBF): out(i,k) = 2*#{j in N(i): x_jk = 1} - deg_i.
+// [row0, row1): node rows to produce (tile-row aligned start); -1 = all.
 void bspmm_bb(const bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* out_bits,
-              float* out_f, cudaStream_t s);
+              float* out_f, cudaStream_t s, int64_t row0 = 0, int64_t row1 = -1);
 // Real-valued walk: F activations (x_f) or B activations with factorized
 // adjacency (x_bits + col_scale).  Ascending-j double accumulation.
 struct SpmmFArgs {
@@ -88,7 +89,8 @@ struct SpmmFArgs {
   int owb = 32;
   float* out_f = nullptr;
 };
-void bspmm_f(const bg_frdc& A, const SpmmFArgs& a, cudaStream_t s);
+void bspmm_f(const bg_frdc& A, const SpmmFArgs& a, cudaStream_t s, int64_t row0 = 0,
+             int64_t row1 = -1);
 
 // ---- gcn_fused.cu: MM.BBF + BSpMM.FBF (+ softmax) without materializing Y ----
 bool gcn1_fused_supported(const bg_frdc& A, int64_t K, int wb, int64_t C);
@@ -96,7 +98,7 @@ void gcn1_records(const uint32_t* h, int64_t n, int64_t K, int wb, const uint32_
                   const float* beta, int64_t C, uint32_t* rec_buf, cudaStream_t s);
 void gcn1_aggregate(const bg_frdc& A, const uint32_t* rec_buf, int64_t K, int wb,
                     const uint32_t* wt, const float* beta, int64_t C, float* logits, float* probs,
-                    cudaStream_t s);
+                    cudaStream_t s, int64_t row0 = 0, int64_t row1 = -1);
 
 // ---- elementwise.cu ------------------------------------------------------
 void add_bbb(const uint32_t* a, const uint32_t* b, int64_t words, uint32_t* out, cudaStream_t s);

@@ -1,0 +1,430 @@
+// Row-sharded multi-GPU forward (one process per GPU).
+//
+// Nodes are split into contiguous tile-row ranges balanced by FRDC tiles
+// (bg_partition_bounds).  Every rank holds the whole graph and the weights and
+// computes its own node rows of every layer; the only exchange is the one the
+// algorithm needs: before each neighbour aggregation the rank's rows of the
+// aggregated operand (packed activations for the binary plans: 16 B per node
+// at hidden 128) are all-gathered over NVLink with NCCL (a group of in-place
+// broadcasts, so uneven row ranges need no padding).  Row partitioning does not
+// change any per-row accumulation order, so every shard count produces output
+// bit-identical to the single-GPU forward.
+//
+// "Virtual" mode (no communicator) computes every rank's range in one process
+// on one device, exercising exactly the per-range kernels and exchange points;
+// the tests use it to check the sharded path on a single B200.
+#include <dlfcn.h>
+#include <nccl.h>  // types and signatures only: NCCL is loaded lazily (see nccl())
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "engine.cuh"
+#include "model.cuh"
+
+namespace bg {
+namespace {
+
+// NCCL is resolved at first use with dlopen("libnccl.so.2"): inside a torch
+// process that returns the NCCL torch already loaded (same soname), and a
+// plain C++ host gets the system library.  Linking it at load time instead
+// would pin whichever NCCL the dynamic linker found first for the whole
+// process.
+struct Nccl {
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclBroadcast) broadcast = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+};
+
+const Nccl& nccl() {
+  static Nccl n = [] {
+    Nccl r;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return r;
+    r.get_unique_id = reinterpret_cast<decltype(r.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    r.comm_init_rank = reinterpret_cast<decltype(r.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    r.comm_destroy = reinterpret_cast<decltype(r.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    r.group_start = reinterpret_cast<decltype(r.group_start)>(dlsym(h, "ncclGroupStart"));
+    r.group_end = reinterpret_cast<decltype(r.group_end)>(dlsym(h, "ncclGroupEnd"));
+    r.broadcast = reinterpret_cast<decltype(r.broadcast)>(dlsym(h, "ncclBroadcast"));
+    r.error_string = reinterpret_cast<decltype(r.error_string)>(dlsym(h, "ncclGetErrorString"));
+    return r;
+  }();
+  if (!n.get_unique_id || !n.comm_init_rank || !n.broadcast)
+    throw std::runtime_error("NCCL (libnccl.so.2) is not available");
+  return n;
+}
+
+}  // namespace
+}  // namespace bg
+
+struct bg_comm {
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0;
+  ~bg_comm() {
+    if (comm) bg::nccl().comm_destroy(comm);
+  }
+};
+
+namespace bg {
+namespace {
+
+#define BG_NCCL(call)                                                                       \
+  do {                                                                                      \
+    ncclResult_t r_ = (call);                                                               \
+    if (r_ != ncclSuccess)                                                                  \
+      throw ::bg::cuda_error(std::string("NCCL error: ") + ::bg::nccl().error_string(r_) +  \
+                             " at " __FILE__ ":" + std::to_string(__LINE__));               \
+  } while (0)
+
+struct Shard {
+  bg_model& m;
+  const std::vector<int64_t>& bounds;  // world + 1 node-row boundaries
+  std::vector<std::pair<int64_t, int64_t>> ranges;  // ranges computed by this process
+  bg_comm* comm;                       // null: virtual ranks in one process
+  cudaStream_t s;
+
+  // Make rows [bounds[q], bounds[q+1]) of a full-size buffer valid on every rank.
+  void allgather(void* buf, int64_t row_bytes) {
+    if (!comm || comm->world == 1) return;
+    BG_NCCL(nccl().group_start());
+    for (int q = 0; q < comm->world; ++q) {
+      const int64_t r0 = bounds[q], r1 = bounds[q + 1];
+      if (r1 <= r0) continue;
+      char* p = static_cast<char*>(buf) + r0 * row_bytes;
+      BG_NCCL(nccl().broadcast(p, p, static_cast<size_t>((r1 - r0) * row_bytes), ncclUint8, q,
+                            comm->comm, s));
+    }
+    BG_NCCL(nccl().group_end());
+  }
+
+  int64_t row_bytes(const Op& o) const {
+    return o.prec == BG_F ? o.cols * 4 : spw(o.cols, o.wb) * 4;
+  }
+
+  Op alloc_like(int prec, int64_t cols, int wb) {
+    Op o;
+    o.prec = prec;
+    o.rows = m.graph->n;
+    o.cols = cols;
+    o.wb = wb;
+    if (prec == BG_F) o.f = static_cast<float*>(m.pool.get(o.bytes()));
+    else o.bits = static_cast<uint32_t*>(m.pool.get(o.bytes()));
+    return o;
+  }
+
+  // ref: run_mm_slot on rows [r0, r1) (row-local).
+  Op mm(bg_variant v, const Op& x, const WeightDev& w) {
+    if (v.in1 == BG_F && v.in2 == BG_F && v.out == BG_F) fail("sharded forward: MM.FFF not supported");
+    if (v.in1 == BG_B && x.wb != w.wb) fail("bmm: operand word widths disagree");
+    if (x.cols != w.rows) fail("bmm: inner dimensions disagree");
+    const int wb = w.wb;
+    Op out = alloc_like(v.out, w.cols, wb);
+    float* alpha_all = nullptr;
+    if (v.in1 == BG_F && v.out == BG_F)
+      alpha_all = static_cast<float*>(m.pool.get(static_cast<size_t>(x.rows) * 4));
+    for (auto [r0, r1] : ranges) {
+      if (r1 <= r0) continue;
+      BmmArgs k;
+      k.rows = r1 - r0;
+      k.k = x.cols;
+      k.n = w.cols;
+      k.wb = wb;
+      k.wt = w.wt.as<uint32_t>();
+      if (v.in1 == BG_F) {
+        k.a_f = x.f + r0 * x.cols;
+        if (alpha_all) {
+          l1_scales(k.a_f, k.rows, x.cols, BG_AXIS_ROW, alpha_all + r0, s);
+          k.alpha = alpha_all + r0;
+        }
+      } else {
+        k.a_bits = x.bits + r0 * spw(x.cols, x.wb);
+        k.alpha = x.scale ? x.scale + r0 : nullptr;
+      }
+      if (v.out == BG_B) {
+        k.out_bits = out.bits + r0 * spw(w.cols, wb);
+      } else {
+        k.out_f = out.f + r0 * w.cols;
+        k.beta = w.scale.as<float>();
+      }
+      bmm(k, s);
+    }
+    return out;
+  }
+
+  Op spmm(bg_variant v, const bg_frdc* A, const float* rs, const float* cs, const Op& x,
+          bool& x_full) {
+    if (!x_full) {
+      allgather(x.prec == BG_F ? static_cast<void*>(x.f) : static_cast<void*>(x.bits), row_bytes(x));
+      x_full = true;
+    }
+    Op out = alloc_like(v.out, x.cols, v.in1 == BG_B ? x.wb : m.wb);
+    for (auto [r0, r1] : ranges) {
+      if (r1 <= r0) continue;
+      if (v.in1 == BG_B && v.in2 == BG_B) {
+        bspmm_bb(*A, x.bits, x.cols, x.wb, out.bits, out.f, s, r0, r1);
+      } else {
+        SpmmFArgs a;
+        a.f = x.cols;
+        if (v.in1 == BG_B) {
+          a.x_bits = x.bits;
+          a.xwb = x.wb;
+        } else {
+          a.x_f = x.f;
+        }
+        a.row_scale = v.in2 == BG_F ? rs : nullptr;
+        a.col_scale = v.in2 == BG_F ? cs : nullptr;
+        a.out_bits = out.bits;
+        a.owb = out.wb;
+        a.out_f = out.f;
+        bspmm_f(*A, a, s, r0, r1);
+      }
+    }
+    return out;
+  }
+
+  Op add(bg_variant v, const Op& a, const Op& b) {
+    Op out = alloc_like(v.out, a.cols, a.wb);
+    for (auto [r0, r1] : ranges) {
+      if (r1 <= r0) continue;
+      if (v.in1 == BG_F) {
+        add_fff(a.f + r0 * a.cols, b.f + r0 * b.cols, (r1 - r0) * a.cols, out.f + r0 * a.cols, s);
+      } else if (v.out == BG_B) {
+        const int64_t w = spw(a.cols, a.wb);
+        add_bbb(a.bits + r0 * w, b.bits + r0 * w, (r1 - r0) * w, out.bits + r0 * w, s);
+      } else {
+        const int64_t w = spw(a.cols, a.wb);
+        add_bbf(a.bits + r0 * w, b.bits + r0 * w, r1 - r0, a.cols, a.wb, out.f + r0 * a.cols, s);
+      }
+    }
+    return out;
+  }
+
+  void relu_rows(Op& x) {
+    if (x.prec != BG_F) return;
+    for (auto [r0, r1] : ranges)
+      if (r1 > r0) relu(x.f + r0 * x.cols, (r1 - r0) * x.cols, s);
+  }
+};
+
+void forward_sharded(bg_model& m, const Op& x0, const std::vector<int64_t>& bounds, int world,
+                     int rank, bg_comm* comm, float* out_base, float* logits_base, cudaStream_t s) {
+  if (!m.graph) fail("sharded forward: model carries no graph");
+  const int64_t n = m.graph->n;
+  if (static_cast<int>(bounds.size()) != world + 1 || bounds.front() != 0 || bounds.back() != n)
+    fail("sharded forward: bounds must run from 0 to the node count");
+  for (int q = 0; q < world; ++q)
+    if (bounds[q] > bounds[q + 1] || (bounds[q] % 4 != 0))
+      fail("sharded forward: bounds must be non-decreasing tile-row (multiple of 4) offsets");
+  if (x0.prec != m.input_prec) fail("model input tag does not match the provided operand");
+  {
+    std::vector<std::string> errors = validate_model(true, m.input_prec, m.infos);
+    if (!errors.empty()) fail("invalid model: " + errors.front());
+  }
+  m.pool.reset();
+  Shard sh{m, bounds, {}, comm, s};
+  if (comm) sh.ranges.push_back({bounds[rank], bounds[rank + 1]});
+  else
+    for (int q = 0; q < world; ++q) sh.ranges.push_back({bounds[q], bounds[q + 1]});
+
+  Op cur = x0;
+  bool cur_full = comm == nullptr;  // virtual mode: every range is computed here
+  const size_t nl = m.layers.size();
+  float* probs_done = nullptr;
+  for (size_t i = 0; i < nl; ++i) {
+    ModelLayer& l = m.layers[i];
+    try {
+      switch (l.info.kind) {
+        case BG_LAYER_GCN: {
+          const bg_variant mm = l.info.plan[0], sp = l.info.plan[1];
+          const bg_frdc& A = *m.graph->structure;
+          const bool fused = mm.in1 == BG_B && mm.in2 == BG_B && mm.out == BG_F &&
+                             sp.in1 == BG_F && sp.in2 == BG_B && sp.out == BG_F && !l.relu &&
+                             cur.prec == BG_B && !cur.scale && cur.wb == m.wb &&
+                             gcn1_fused_supported(A, cur.cols, cur.wb, l.w1.cols);
+          if (fused) {
+            if (!cur_full) {
+              sh.allgather(cur.bits, sh.row_bytes(cur));
+              cur_full = true;
+            }
+            auto* recs = static_cast<uint32_t*>(m.pool.get(static_cast<size_t>(n) * 64));
+            gcn1_records(cur.bits, n, cur.cols, cur.wb, l.w1.wt.as<uint32_t>(), l.w1.scale.as<float>(),
+                         l.w1.cols, recs, s);
+            Op o = sh.alloc_like(BG_F, l.w1.cols, m.wb);
+            float* probs = nullptr;
+            if (i + 1 < nl && m.layers[i + 1].info.kind == BG_LAYER_SOFTMAX)
+              probs = (i + 2 == nl && out_base) ? out_base : static_cast<float*>(m.pool.get(o.bytes()));
+            for (auto [r0, r1] : sh.ranges)
+              if (r1 > r0)
+                gcn1_aggregate(A, recs, cur.cols, cur.wb, l.w1.wt.as<uint32_t>(), l.w1.scale.as<float>(),
+                               l.w1.cols, o.f, probs, s, r0, r1);
+            probs_done = probs;
+            cur = o;
+            cur_full = comm == nullptr;
+            break;
+          }
+          Op h = sh.mm(mm, cur, l.w1);
+          bool h_full = comm == nullptr;
+          const bool fac = sp.in2 == BG_F;
+          cur = sh.spmm(sp, &A, fac ? m.graph->norm.as<float>() : nullptr,
+                        fac ? m.graph->norm.as<float>() : nullptr, h, h_full);
+          cur_full = comm == nullptr;
+          if (l.relu) sh.relu_rows(cur);
+          break;
+        }
+        case BG_LAYER_SAGE:
+        case BG_LAYER_GRAPHCONV: {
+          const bool mean = l.info.kind == BG_LAYER_SAGE;
+          Op hs = sh.mm(l.info.plan[0], cur, l.w1);
+          Op hn = sh.mm(l.info.plan[1], cur, l.w2);
+          bool hn_full = comm == nullptr;
+          const bg_variant sp = l.info.plan[2];
+          const bool fac = sp.in2 == BG_F;
+          const float* rs = fac ? (mean ? m.graph->mean_row.as<float>() : m.graph->ones.as<float>()) : nullptr;
+          const float* cs = fac ? m.graph->ones.as<float>() : nullptr;
+          Op agg = sh.spmm(sp, m.graph->raw.get(), rs, cs, hn, hn_full);
+          if (mean && sp.in2 == BG_B && sp.out == BG_F)
+            for (auto [r0, r1] : sh.ranges)
+              if (r1 > r0)
+                scale_rows_double(agg.f + r0 * agg.cols, r1 - r0, agg.cols,
+                                  m.graph->neighbor_count.as<int64_t>() + r0, s);
+          cur = sh.add(l.info.plan[3], hs, agg);
+          cur_full = comm == nullptr;
+          if (l.relu) sh.relu_rows(cur);
+          break;
+        }
+        case BG_LAYER_FC:
+          cur = sh.mm(l.info.plan[0], cur, l.w1);
+          cur_full = comm == nullptr;
+          if (l.relu) sh.relu_rows(cur);
+          break;
+        case BG_LAYER_RELU:
+          if (cur.f == x0.f) fail("sharded forward: a leading ReLU layer is not supported");
+          sh.relu_rows(cur);
+          break;
+        case BG_LAYER_SOFTMAX: {
+          if (logits_base)
+            for (auto [r0, r1] : sh.ranges)
+              if (r1 > r0)
+                BG_CUDA(cudaMemcpyAsync(logits_base + r0 * cur.cols, cur.f + r0 * cur.cols,
+                                        static_cast<size_t>((r1 - r0) * cur.cols) * 4,
+                                        cudaMemcpyDeviceToDevice, s));
+          float* dst = (i + 1 == nl && out_base) ? out_base : static_cast<float*>(m.pool.get(cur.bytes()));
+          if (probs_done && i == nl - 1 && probs_done == out_base) {
+            // already produced by the fused aggregation epilogue
+          } else {
+            for (auto [r0, r1] : sh.ranges)
+              if (r1 > r0) softmax_rows(cur.f + r0 * cur.cols, r1 - r0, cur.cols, dst + r0 * cur.cols, s);
+          }
+          cur.f = dst;
+          break;
+        }
+        default:
+          fail(std::string("sharded forward: layer kind ") + layer_kind_name(l.info.kind) +
+               " is not supported");
+      }
+    } catch (const cuda_error&) {
+      throw;
+    } catch (const std::exception& e) {
+      throw std::runtime_error("layer " + std::to_string(i) + " (" + layer_kind_name(l.info.kind) +
+                               "): " + e.what());
+    }
+  }
+  if (cur.prec != BG_F) fail("model output must be full precision");
+  const bool last_softmax = nl && m.layers[nl - 1].info.kind == BG_LAYER_SOFTMAX;
+  for (auto [r0, r1] : sh.ranges) {
+    if (r1 <= r0) continue;
+    const size_t bytes = static_cast<size_t>((r1 - r0) * cur.cols) * 4;
+    if (out_base && cur.f != out_base)
+      BG_CUDA(cudaMemcpyAsync(out_base + r0 * cur.cols, cur.f + r0 * cur.cols, bytes,
+                              cudaMemcpyDeviceToDevice, s));
+    if (logits_base && !last_softmax)
+      BG_CUDA(cudaMemcpyAsync(logits_base + r0 * cur.cols, cur.f + r0 * cur.cols, bytes,
+                              cudaMemcpyDeviceToDevice, s));
+  }
+}
+
+}  // namespace
+}  // namespace bg
+
+using namespace bg;
+
+extern "C" {
+
+int bg_partition_bounds(const uint64_t* rp, int64_t tile_rows, int64_t n, int world,
+                        int64_t* bounds) {
+  return guard([&] {
+    if (world < 1) fail("partition: world size must be positive");
+    if (!rp || !bounds) fail("partition: null pointer");
+    const uint64_t total = rp[tile_rows];
+    bounds[0] = 0;
+    for (int k = 1; k < world; ++k) {
+      const uint64_t target = (total * static_cast<uint64_t>(k) + world - 1) / world;
+      const int64_t t = std::lower_bound(rp, rp + tile_rows + 1, target) - rp;
+      bounds[k] = std::max<int64_t>(bounds[k - 1], std::min<int64_t>(4 * t, n));
+      bounds[k] -= bounds[k] % 4;
+      bounds[k] = std::max<int64_t>(bounds[k - 1], bounds[k]);
+    }
+    bounds[world] = n;
+  });
+}
+
+int bg_comm_unique_id(uint8_t* out, size_t len) {
+  return guard([&] {
+    if (!out || len < sizeof(ncclUniqueId)) fail("unique id buffer too small");
+    ncclUniqueId id;
+    BG_NCCL(nccl().get_unique_id(&id));
+    std::memcpy(out, &id, sizeof id);
+  });
+}
+
+int bg_comm_create(int world, int rank, const uint8_t* id, size_t len, bg_comm** out) {
+  return guard([&] {
+    if (!out || !id || len < sizeof(ncclUniqueId)) fail("bad communicator arguments");
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof uid);
+    auto c = std::make_unique<bg_comm>();
+    c->world = world;
+    c->rank = rank;
+    BG_NCCL(nccl().comm_init_rank(&c->comm, world, uid, rank));
+    *out = c.release();
+  });
+}
+
+void bg_comm_destroy(bg_comm* c) { delete c; }
+
+int bg_model_forward_sharded(bg_model* m, bg_comm* comm, const bg_mat* x, const int64_t* bounds,
+                             int world, int rank, float* out, float* logits, bg_stream stream) {
+  return guard([&] {
+    if (!m || !x || !bounds) fail("sharded forward: null argument");
+    if (comm && (comm->world != world || comm->rank != rank))
+      fail("sharded forward: communicator does not match world/rank");
+    if (rank < 0 || rank >= world) fail("sharded forward: bad rank");
+    std::vector<int64_t> b(bounds, bounds + world + 1);
+    Op x0 = op_from_mat(x);
+    const int64_t r0 = b[rank], r1 = b[rank + 1];
+    int64_t oc = 0;
+    for (const auto& l : m->layers)
+      if (l.info.has_w1) oc = l.w1.cols;
+    float* out_base = out;
+    float* log_base = logits;
+    if (comm) {
+      // x and out hold this rank's rows only: index them through shifted bases
+      if (x0.rows != r1 - r0) fail("sharded forward: x must hold this rank's rows");
+      if (x0.prec == BG_F) x0.f -= r0 * x0.cols;
+      else x0.bits -= r0 * spw(x0.cols, x0.wb);
+      x0.rows = m->graph ? m->graph->n : x0.rows;
+      if (out) out_base = out - r0 * oc;
+      if (logits) log_base = logits - r0 * oc;
+    }
+    forward_sharded(*m, x0, b, world, rank, comm, out_base, log_base, S(stream));
+  });
+}
+
+}  // extern "C"

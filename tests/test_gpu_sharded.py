@@ -1,0 +1,51 @@
+"""GPU: the row-sharded forward on one B200 in "virtual
+ranks" mode -- every rank's row range runs through the same per-range
+kernels -- is bit-identical to the single-GPU forward and to the oracle for
+1/2/3/4/8 shards (the row partition never changes an accumulation order)."""
+import numpy as np
+import pytest
+import torch
+
+import pyoracle as po
+from helpers import to_layer_specs
+
+import paper_2305_02522_b200 as bg
+from paper_2305_02522_b200.sharded import forward_virtual_ranks, partition_bounds
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("model,n,e,f,h,c,plan", [
+    ("gcn", 2708, 13264, 1433, 64, 7, None),
+    ("sage", 2708, 10556, 1433, 64, 7, None),
+    ("saint", 2708, 10556, 1433, 64, 7, None),
+    ("gcn", 19717, 88648, 500, 64, 3, ["MM.FBB+BSpMM.BBB", "MM.BBB+BSpMM.BBB", "MM.BBF+BSpMM.FBF"]),
+    ("gcn", 1003, 9000, 70, 40, 5, ["MM.FBF+BSpMM.FFF", "MM.FBB+BSpMM.BBB", "MM.BBF+BSpMM.FBF"]),
+])
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_sharded_matches_single_gpu(model, n, e, f, h, c, plan, world):
+    s, d = po.Rng(100).random_edges(n, e, False)
+    layers, X = po.build_model(model, f, h, c, 99, n, plan)
+    g = bg.prepare_graph(n, s, d)
+    m = bg.Model(to_layer_specs(bg, layers), g)
+    x = torch.from_numpy(X).cuda()
+    ref_out, ref_log, _ = m.forward_traced(x)
+    rp, _, _ = g.structure.download()
+    bounds = partition_bounds(rp, n, world)
+    assert bounds[0] == 0 and bounds[-1] == n and all(b % 4 == 0 for b in bounds[:-1])
+    out, lg = forward_virtual_ranks(m, x, bounds, logits=True)
+    torch.cuda.synchronize()
+    assert torch.equal(lg, ref_log)
+    assert torch.equal(out, ref_out)
+    o_out, o_log, _ = po.run_model(layers, po.Graph(n, s, d), X)
+    assert np.array_equal(lg.cpu().numpy(), o_log)
+
+
+def test_partition_is_balanced_by_tiles():
+    s, d = po.Rng(3).random_edges(20000, 400000, False)
+    g = bg.prepare_graph(20000, s, d)
+    rp, _, _ = g.structure.download()
+    b = partition_bounds(rp, 20000, 8)
+    tiles = [int(rp[b[k + 1] // 4] if b[k + 1] < 20000 else rp[-1]) - int(rp[b[k] // 4]) for k in range(8)]
+    assert max(tiles) - min(tiles) <= 0.02 * sum(tiles) / 8 + 64
+    assert [g.partition_rows(8, k) for k in range(8)] == [(b[k], b[k + 1]) for k in range(8)]
