@@ -225,6 +225,7 @@ void launch_f_m(const bg_frdc& A, const SpmmFArgs& a, int64_t r0, int64_t r1, cu
 
 void bspmm_bb(const bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* out_bits,
               float* out_f, cudaStream_t s, int64_t row0, int64_t row1) {
+  if (use_slivers()) return sliver_bb(const_cast<bg_frdc&>(A), x, f, wb, out_bits, out_f, s, row0, row1);
   if (row1 < 0) row1 = A.rows;
   const int64_t t0 = row0 / 4, t1 = (row1 + 3) / 4;
   if (A.rows == 0 || t1 <= t0) return;
@@ -249,6 +250,7 @@ void bspmm_bb(const bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* 
 }
 
 void bspmm_f(const bg_frdc& A, const SpmmFArgs& a, cudaStream_t s, int64_t row0, int64_t row1) {
+  if (use_slivers()) return sliver_f(const_cast<bg_frdc&>(A), a, s, row0, row1);
   if (row1 < 0) row1 = A.rows;
   if (A.rows == 0 || a.f == 0 || row1 <= row0) return;
   const bool xb = a.x_bits != nullptr, ob = a.out_bits != nullptr;

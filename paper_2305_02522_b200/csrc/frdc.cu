@@ -129,6 +129,60 @@ __global__ void k_slot_max(const uint64_t* __restrict__ rp, const uint16_t* __re
   }
 }
 
+// Warp per tile row: nonzero nibbles per node row.
+__global__ void k_sliver_count(const uint64_t* __restrict__ rp, const uint16_t* __restrict__ tiles,
+                               int64_t trows, int64_t rows, const int32_t* __restrict__ deg,
+                               unsigned long long* __restrict__ cnt, int* __restrict__ maxima) {
+  const int64_t tr = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (tr >= trows) return;
+  const int lane = threadIdx.x & 31;
+  int c[4] = {0, 0, 0, 0};
+  for (uint64_t k = rp[tr] + lane; k < rp[tr + 1]; k += 32) {
+    const uint32_t t = tiles[k];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) c[r] += ((t >> (12 - 4 * r)) & 0xFu) != 0;
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    for (int o = 16; o; o >>= 1) c[r] += __shfl_xor_sync(0xFFFFFFFFu, c[r], o);
+    if (lane == 0 && 4 * tr + r < rows) {
+      cnt[4 * tr + r] = static_cast<unsigned long long>(c[r]);
+      atomicMax(maxima, c[r]);
+      atomicMax(maxima + 1, deg[4 * tr + r] - c[r]);
+    }
+  }
+}
+
+// Warp per tile row: ballot-compact each row's nonzero nibbles in tile order.
+__global__ void k_sliver_fill(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+                              const uint16_t* __restrict__ tiles, int64_t trows, int64_t rows,
+                              const unsigned long long* __restrict__ srp,
+                              uint32_t* __restrict__ out) {
+  const int64_t tr = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (tr >= trows) return;
+  const int lane = threadIdx.x & 31;
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  unsigned long long pos[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) pos[r] = 4 * tr + r < rows ? srp[4 * tr + r] : 0;
+  for (uint64_t base = rp[tr]; base < rp[tr + 1]; base += 32) {
+    const uint64_t k = base + lane;
+    uint32_t t = 0, col = 0;
+    if (k < rp[tr + 1]) {
+      t = tiles[k];
+      col = ci[k];
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t nib = (t >> (12 - 4 * r)) & 0xFu;
+      const uint32_t mask = __ballot_sync(0xFFFFFFFFu, nib != 0);
+      if (nib) out[pos[r] + __popc(mask & lt)] = (col << 4) | nib;
+      pos[r] += __popc(mask);
+    }
+  }
+}
+
 __global__ void k_graph_scales(const int32_t* __restrict__ deg_loops,
                                const int32_t* __restrict__ deg_raw, int64_t n,
                                float* __restrict__ norm, float* __restrict__ mean,
@@ -148,6 +202,7 @@ unsigned grid1(int64_t n, int bs = 256) { return static_cast<unsigned>(cdiv(n, b
 }  // namespace
 
 void frdc_finalize(bg_frdc& m, cudaStream_t s) {
+  m.nslivers = -1;  // derived views are rebuilt on next use
   m.degree.alloc(static_cast<size_t>(std::max<int64_t>(m.rows, 1)) * 4);
   BG_CUDA(cudaMemsetAsync(m.degree.p, 0, m.degree.bytes, s));
   DevBuf stats(16);
@@ -172,6 +227,46 @@ void frdc_finalize(bg_frdc& m, cudaStream_t s) {
   m.max_deg = static_cast<int64_t>(static_cast<int>(h[1] & 0xFFFFFFFFull));
   m.max_slot[0] = hs[0];
   m.max_slot[1] = hs[1];
+}
+
+void frdc_slivers(bg_frdc& m, cudaStream_t s) {
+  if (m.nslivers >= 0) return;
+  if (m.tile_cols >= (int64_t{1} << 28)) fail("FRDC: too many tile columns for the sliver view");
+  const size_t n1 = static_cast<size_t>(m.rows) + 1;
+  DevBuf cnt(n1 * 8), maxima(8);
+  m.sliver_ptr.alloc(n1 * 8);
+  BG_CUDA(cudaMemsetAsync(cnt.p, 0, cnt.bytes, s));
+  BG_CUDA(cudaMemsetAsync(maxima.p, 0, 8, s));
+  BG_CUDA(cudaMemsetAsync(m.sliver_ptr.p, 0, m.sliver_ptr.bytes, s));
+  if (m.tile_rows > 0)
+    k_sliver_count<<<grid1(m.tile_rows * 32), 256, 0, s>>>(m.rp(), m.ti(), m.tile_rows, m.rows,
+                                                           m.deg(), cnt.as<unsigned long long>(),
+                                                           maxima.as<int>());
+  BG_LAUNCH_CHECK();
+  int hm[2] = {0, 0};
+  BG_CUDA(cudaMemcpyAsync(hm, maxima.p, 8, cudaMemcpyDeviceToHost, s));
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, cnt.as<unsigned long long>(),
+                                m.sliver_ptr.as<unsigned long long>() + 1, static_cast<int>(m.rows), s);
+  DevBuf tmp(std::max<size_t>(tmp_bytes, 1));
+  if (m.rows > 0)
+    cub::DeviceScan::InclusiveSum(tmp.p, tmp_bytes, cnt.as<unsigned long long>(),
+                                  m.sliver_ptr.as<unsigned long long>() + 1, static_cast<int>(m.rows), s);
+  BG_LAUNCH_CHECK();
+  unsigned long long total = 0;
+  BG_CUDA(cudaMemcpyAsync(&total, m.sliver_ptr.as<unsigned long long>() + m.rows, 8,
+                          cudaMemcpyDeviceToHost, s));
+  BG_CUDA(cudaStreamSynchronize(s));
+  m.slivers.alloc(std::max<size_t>(static_cast<size_t>(total) * 4, 4));
+  if (m.tile_rows > 0)
+    k_sliver_fill<<<grid1(m.tile_rows * 32), 256, 0, s>>>(
+        m.rp(), m.ci(), m.ti(), m.tile_rows, m.rows, m.sliver_ptr.as<unsigned long long>(),
+        m.slivers.as<uint32_t>());
+  BG_LAUNCH_CHECK();
+  BG_CUDA(cudaStreamSynchronize(s));
+  m.nslivers = static_cast<int64_t>(total);
+  m.max_sl_row = hm[0];
+  m.max_extra_bits = hm[1];
 }
 
 std::unique_ptr<bg_frdc> frdc_build(const int64_t* src, const int64_t* dst, int64_t e, int64_t n,

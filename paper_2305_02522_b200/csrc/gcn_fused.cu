@@ -213,6 +213,7 @@ bool gcn1_fused_supported(const bg_frdc& A, int64_t K, int wb, int64_t C) {
 
 void gcn1_records(const uint32_t* h, int64_t n, int64_t K, int wb, const uint32_t* wt,
                   const float* beta, int64_t C, uint32_t* rec_buf, cudaStream_t s) {
+  if (use_slivers()) return sliver_gcn1_records(h, n, K, wb, wt, beta, C, rec_buf, s);
   const int hspw = static_cast<int>(spw(K, wb));
   k_gcn1_records<<<static_cast<unsigned>(cdiv(n * kRecWords, 256)), 256, 0, s>>>(
       h, n, hspw, static_cast<int>(K), wt, beta, static_cast<int>(C), rec_buf);
@@ -222,6 +223,8 @@ void gcn1_records(const uint32_t* h, int64_t n, int64_t K, int wb, const uint32_
 void gcn1_aggregate(const bg_frdc& A, const uint32_t* rec_buf, int64_t K, int wb,
                     const uint32_t* wt, const float* beta, int64_t C, float* logits, float* probs,
                     cudaStream_t s, int64_t row0, int64_t row1) {
+  if (use_slivers())
+    return sliver_gcn1_aggregate(const_cast<bg_frdc&>(A), rec_buf, K, wb, wt, beta, C, logits, probs, s, row0, row1);
   if (row1 < 0) row1 = A.rows;
   const int64_t t0 = row0 / 4, t1 = (row1 + 3) / 4;
   if (t1 <= t0) return;

@@ -18,6 +18,17 @@ struct bg_frdc {
   bg::DevBuf col_ind;  // u32[nnz]
   bg::DevBuf tiles;    // u16[nnz]
   bg::DevBuf degree;   // i32[rows]
+  // Node-major view of the same bit tiles, built once on first use
+  // (frdc_slivers): for node row i, the nonzero 1x4 nibbles of its tiles as
+  // u32 (tile_col << 4 | nibble), ascending tile column (the reference's walk
+  // order, kernels.cpp:218-234).  Nibble bit 3-c is local column c.
+  bg::DevBuf sliver_ptr;  // u64[rows + 1]
+  bg::DevBuf slivers;     // u32[nslivers]
+  int64_t nslivers = -1;  // -1: not built
+  int64_t max_sl_row = 0;      // most slivers in one node row
+  int64_t max_extra_bits = 0;  // most (bits - slivers) in one node row
+  const uint64_t* srp() const { return sliver_ptr.as<uint64_t>(); }
+  const uint32_t* sl() const { return slivers.as<uint32_t>(); }
   const uint64_t* rp() const { return row_ptr.as<uint64_t>(); }
   const uint32_t* ci() const { return col_ind.as<uint32_t>(); }
   const uint16_t* ti() const { return tiles.as<uint16_t>(); }
@@ -50,6 +61,7 @@ std::unique_ptr<bg_frdc> frdc_from_host(int64_t rows, int64_t cols, const uint64
                                         const uint32_t* ci, const uint16_t* ti, int64_t nnz,
                                         cudaStream_t s);
 void frdc_finalize(bg_frdc& m, cudaStream_t s);  // degree, nnz_bits, max_deg
+void frdc_slivers(bg_frdc& m, cudaStream_t s);   // build the node-major sliver view once
 std::unique_ptr<bg_graph> prepare_graph(const int64_t* src, const int64_t* dst, int64_t e,
                                         int64_t n, cudaStream_t s);
 
@@ -99,6 +111,20 @@ void gcn1_records(const uint32_t* h, int64_t n, int64_t K, int wb, const uint32_
 void gcn1_aggregate(const bg_frdc& A, const uint32_t* rec_buf, int64_t K, int wb,
                     const uint32_t* wt, const float* beta, int64_t C, float* logits, float* probs,
                     cudaStream_t s, int64_t row0 = 0, int64_t row1 = -1);
+
+// ---- sliver.cu: the same aggregations over the node-major sliver view -----
+// (builds the view on first use, so the first call synchronizes once)
+void sliver_bb(bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* out_bits, float* out_f,
+               cudaStream_t s, int64_t r0 = 0, int64_t r1 = -1);
+void sliver_f(bg_frdc& A, const SpmmFArgs& a, cudaStream_t s, int64_t r0 = 0, int64_t r1 = -1);
+void sliver_gcn1_records(const uint32_t* h, int64_t n, int64_t K, int wb, const uint32_t* wt,
+                         const float* beta, int64_t C, uint32_t* rec, cudaStream_t s);
+void sliver_gcn1_aggregate(bg_frdc& A, const uint32_t* rec, int64_t K, int wb, const uint32_t* wt,
+                           const float* beta, int64_t C, float* logits, float* probs,
+                           cudaStream_t s, int64_t r0 = 0, int64_t r1 = -1);
+// Aggregation layout switch: true (default) = slivers, false = tile-row
+// walker (env BG_AGGREGATION=tiles); both produce identical results.
+bool use_slivers();
 
 // ---- elementwise.cu ------------------------------------------------------
 void add_bbb(const uint32_t* a, const uint32_t* b, int64_t words, uint32_t* out, cudaStream_t s);

@@ -1,0 +1,452 @@
+// Aggregation kernels over the node-major sliver view of the FRDC bit tiles
+// (ops.cuh bg_frdc::slivers): one warp per node row reads its nonzero 1x4
+// nibbles with coalesced 4-byte loads -- no per-forward routing of tile bits
+// to rows.  Same results as the tile-row walker kernels (bspmm.cu,
+// gcn_fused.cu) and the reference (kernels.cpp:254-555).
+//
+//   k_sl_bb        BSpMM.BBB / BBF: lanes (word g, slot s) gather word g of the
+//                  neighbour rows of 8 slivers per slot and count them with
+//                  Harley-Seal planes; epilogue as in bspmm.cu.
+//   k_sl_gcn1      fused layer-1 GCN (gcn_fused.cu): 64-byte records laid out
+//                  so every lane owns one h word and three q words -- all lanes
+//                  run the same Harley-Seal + SWAR code, no divergence.
+//   k_sl_f         real-valued walk in ascending column order (exact double
+//                  accumulation order of the reference).
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
+#include "ops.cuh"
+#include "tilewalk.cuh"
+
+namespace bg {
+namespace {
+
+constexpr int kSlWarps = 8;
+
+// Column of the lowest set bit of a nibble (bit 3 - c is local column c).
+__device__ __forceinline__ uint32_t nib_col(uint32_t low) { return 4u - __ffs(low); }
+
+template <int G, int NP, bool OUTB>
+__global__ void __launch_bounds__(kSlWarps * 32)
+    k_sl_bb(const uint64_t* __restrict__ srp, const uint32_t* __restrict__ sl, int64_t row0,
+            int64_t row1, const int32_t* __restrict__ degree, const uint32_t* __restrict__ x,
+            int64_t xspw, int64_t f, uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
+  constexpr int S = 32 / G, B = 8 * S;
+  constexpr int LOGS = S == 1 ? 0 : S == 2 ? 1 : S == 4 ? 2 : S == 8 ? 3 : S == 16 ? 4 : 5;
+  constexpr int NQ = NP + LOGS;
+  const int lane = threadIdx.x & 31;
+  const int g = lane % G, slot = lane / G;
+  const int64_t word = static_cast<int64_t>(blockIdx.y) * G + g;
+  const bool word_ok = word < xspw;
+  const uint32_t* xw = x + (word_ok ? word : 0);
+  const uint32_t xs = static_cast<uint32_t>(xspw);
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t i = row0 + wid; i < row1; i += nw) {
+    uint32_t P[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) P[q] = 0;
+    const uint64_t e0 = srp[i], e1 = srp[i + 1];
+    for (uint64_t base = e0; base < e1; base += B) {
+      uint32_t rest[8], xv[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const uint64_t e = base + slot + S * m;
+        const uint32_t ent = e < e1 ? ld_nc_u32(sl + e) : 0u;
+        const uint32_t nib = ent & 0xFu, low = nib & (0u - nib);
+        rest[m] = nib ^ low;
+        xv[m] = low ? __ldg(xw + ((ent >> 4) * 4 + nib_col(low)) * xs) : 0u;
+        rest[m] |= ent & ~0xFu;  // keep the column for the rare extra rounds
+      }
+      hs_add8<NP>(P, xv);
+      // nibbles holding several bits: at most three further rounds (rare)
+#pragma unroll 1
+      for (int round = 1; round < 4; ++round) {
+        const uint32_t any = __ballot_sync(
+            0xFFFFFFFFu, ((rest[0] | rest[1] | rest[2] | rest[3] | rest[4] | rest[5] | rest[6] |
+                           rest[7]) & 0xFu) != 0);
+        if (any == 0) break;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const uint32_t nib = rest[m] & 0xFu, low = nib & (0u - nib);
+          xv[m] = low ? __ldg(xw + ((rest[m] >> 4) * 4 + nib_col(low)) * xs) : 0u;
+          rest[m] ^= low;
+        }
+        hs_add8<NP>(P, xv);
+      }
+    }
+    __syncwarp();
+    uint32_t Q[NQ];
+    slot_reduce<G, NP, NQ>(P, Q);
+    const uint32_t deg = static_cast<uint32_t>(__ldg(degree + i));
+    if (!word_ok) {
+    } else if (OUTB) {
+      // cnt >= ceil(deg/2)  <=>  2*cnt - deg >= 0   (kernels.cpp:440-454)
+      uint32_t ge = planes_ge<NQ>(Q, (deg + 1) >> 1);
+      if (32 * (word + 1) > f) ge &= (32 * word >= f) ? 0u : tail_mask32(f);
+      if (slot == 0) out_bits[i * xspw + word] = ge;
+    } else {
+      for (int b = slot; b < 32; b += S) {
+        const int64_t k = 32 * word + b;
+        if (k >= f) break;
+        out_f[i * f + k] = static_cast<float>(2 * static_cast<int64_t>(plane_count<NQ>(Q, b)) -
+                                              static_cast<int64_t>(deg));
+      }
+    }
+  }
+}
+
+// ---- fused layer-1 GCN over slivers ----------------------------------------
+// Record of node j (16 words): word 4g = h word g, words 4g+1..4g+3 = bytes
+// q_jk + 32 of classes 12g .. 12g+11 (4 per word, little-endian).
+constexpr int kRec = 16;
+
+template <int NP>
+__global__ void __launch_bounds__(kSlWarps * 32)
+    k_sl_gcn1(const uint64_t* __restrict__ srp, const uint32_t* __restrict__ sl, int64_t row0,
+              int64_t row1, const int32_t* __restrict__ degree, const uint32_t* __restrict__ rec,
+              const uint32_t* __restrict__ wt, int hspw, int K, const float* __restrict__ beta,
+              int C, float* __restrict__ logits, float* __restrict__ probs) {
+  constexpr int G = 4, S = 8, B = 8 * S, NQ = NP + 3;
+  __shared__ uint32_t planes_all[kSlWarps][4][NQ];
+  __shared__ int qsum_all[kSlWarps][48];
+  __shared__ uint32_t wt_s[48 * 4];
+  for (int t = threadIdx.x; t < C * hspw; t += blockDim.x) wt_s[t] = wt[t];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane % G, slot = lane / G;
+  const uint4* rw = reinterpret_cast<const uint4*>(rec) + g;
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t i = row0 + wid; i < row1; i += nw) {
+    uint32_t P[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) P[q] = 0;
+    uint32_t lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    auto consume = [&](const uint4 (&v)[8]) {
+      uint32_t h[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) h[m] = v[m].x;
+      hs_add8<NP>(P, h);
+      // q bytes are <= 64: three words add byte-wise without carries
+#pragma unroll
+      for (int w = 0; w < 3; ++w) {
+        auto qw = [&](int m) { return w == 0 ? v[m].y : w == 1 ? v[m].z : v[m].w; };
+        const uint32_t a = qw(0) + qw(1) + qw(2), b = qw(3) + qw(4) + qw(5), c = qw(6) + qw(7);
+        lo[w] += (a & 0x00FF00FFu) + (b & 0x00FF00FFu) + (c & 0x00FF00FFu);
+        hi[w] += ((a >> 8) & 0x00FF00FFu) + ((b >> 8) & 0x00FF00FFu) + ((c >> 8) & 0x00FF00FFu);
+      }
+    };
+    const uint64_t e0 = srp[i], e1 = srp[i + 1];
+    for (uint64_t base = e0; base < e1; base += B) {
+      uint32_t rest[8];
+      uint4 v[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const uint64_t e = base + slot + S * m;
+        const uint32_t ent = e < e1 ? ld_nc_u32(sl + e) : 0u;
+        const uint32_t nib = ent & 0xFu, low = nib & (0u - nib);
+        rest[m] = (nib ^ low) | (ent & ~0xFu);
+        v[m] = low ? __ldg(rw + static_cast<size_t>((ent >> 4) * 4 + nib_col(low)) * (kRec / 4))
+                   : make_uint4(0u, 0u, 0u, 0u);
+      }
+      consume(v);
+#pragma unroll 1
+      for (int round = 1; round < 4; ++round) {
+        const uint32_t any = __ballot_sync(
+            0xFFFFFFFFu, ((rest[0] | rest[1] | rest[2] | rest[3] | rest[4] | rest[5] | rest[6] |
+                           rest[7]) & 0xFu) != 0);
+        if (any == 0) break;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const uint32_t nib = rest[m] & 0xFu, low = nib & (0u - nib);
+          v[m] = low ? __ldg(rw + static_cast<size_t>((rest[m] >> 4) * 4 + nib_col(low)) * (kRec / 4))
+                     : make_uint4(0u, 0u, 0u, 0u);
+          rest[m] ^= low;
+        }
+        consume(v);
+      }
+    }
+    __syncwarp();
+    // slot reductions: h planes (bit-sliced butterfly) and q sums (16-bit lanes)
+    uint32_t Q[NQ];
+    slot_reduce<G, NP, NQ>(P, Q);
+#pragma unroll
+    for (int w = 0; w < 3; ++w)
+      for (int d = G; d < 32; d <<= 1) {
+        lo[w] += __shfl_xor_sync(0xFFFFFFFFu, lo[w], d);
+        hi[w] += __shfl_xor_sync(0xFFFFFFFFu, hi[w], d);
+      }
+    const int deg = __ldg(degree + i);
+    if (slot == 0) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) planes_all[warp][g][q] = Q[q];
+      const int bias = 32 * deg;
+#pragma unroll
+      for (int w = 0; w < 3; ++w) {
+        const int k0 = 12 * g + 4 * w;
+        qsum_all[warp][k0 + 0] = static_cast<int>(lo[w] & 0xFFFFu) - bias;
+        qsum_all[warp][k0 + 1] = static_cast<int>(hi[w] & 0xFFFFu) - bias;
+        qsum_all[warp][k0 + 2] = static_cast<int>(lo[w] >> 16) - bias;
+        qsum_all[warp][k0 + 3] = static_cast<int>(hi[w] >> 16) - bias;
+      }
+    }
+    __syncwarp();
+    // Per class: sum_j dot_jk = 2*(2*sum_b [w_bk] cnt_b - sum_b cnt_b) - deg*(2*popc(w_k) - K),
+    // with sum_b [mask_b] cnt_b = sum_q 2^q popc(mask & Q_q); then the exact
+    // combination of gcn_fused.cu and the fused softmax.
+    float lg[2];
+    double mx = -INFINITY;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {
+      const int k = lane + 32 * pass;
+      lg[pass] = -INFINITY;
+      if (k < C) {
+        int64_t sw = 0, sall = 0;
+        int wpop = 0;
+        for (int w = 0; w < hspw; ++w) {
+          const uint32_t wk = wt_s[k * hspw + w];
+          wpop += __popc(wk);
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const uint32_t pl = planes_all[warp][w][q];
+            sw += static_cast<int64_t>(__popc(wk & pl)) << q;
+            sall += static_cast<int64_t>(__popc(pl)) << q;
+          }
+        }
+        const int64_t sdot = 2 * (2 * sw - sall) - static_cast<int64_t>(deg) * (2 * wpop - K);
+        const float bk = beta[k];
+        const int ex = ((__float_as_int(bk) >> 23) & 0xFF) - 127;
+        const double two_u = ldexp(1.0, ex - 22);
+        const double val = __dsub_rn(__dmul_rn(static_cast<double>(bk), static_cast<double>(sdot)),
+                                     __dmul_rn(two_u, static_cast<double>(qsum_all[warp][k])));
+        lg[pass] = __double2float_rn(val);
+        if (logits) logits[i * C + k] = lg[pass];
+        mx = fmax(mx, static_cast<double>(lg[pass]));
+      }
+    }
+    // warp reductions run unconditionally (uniform control flow); only the
+    // stores depend on probs
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    const double x0 = lane < C ? exp(static_cast<double>(lg[0]) - mx) : 0.0;
+    const double x1 = lane + 32 < C ? exp(static_cast<double>(lg[1]) - mx) : 0.0;
+    double sum = x0 + x1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+    if (probs) {
+      if (lane < C) probs[i * C + lane] = __double2float_rn(x0 / sum);
+      if (lane + 32 < C) probs[i * C + lane + 32] = __double2float_rn(x1 / sum);
+    }
+    __syncwarp();
+  }
+}
+
+// Record producer for k_sl_gcn1 (layout above); thread per (node, word).
+__global__ void k_sl_gcn1_records(const uint32_t* __restrict__ h, int64_t rows, int hspw, int K,
+                                  const uint32_t* __restrict__ wt, const float* __restrict__ beta,
+                                  int C, uint32_t* __restrict__ rec) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= rows * kRec) return;
+  const int64_t j = t / kRec;
+  const int w = static_cast<int>(t % kRec);
+  uint32_t hw[4] = {0, 0, 0, 0};
+  for (int q = 0; q < hspw; ++q) hw[q] = __ldg(h + j * hspw + q);
+  const int g = w >> 2, part = w & 3;
+  if (part == 0) {
+    rec[t] = hw[g];
+    return;
+  }
+  uint32_t out = 0;
+  for (int b = 0; b < 4; ++b) {
+    const int k = 12 * g + 4 * (part - 1) + b;
+    if (k >= C) break;
+    int diff = 0;
+    for (int q = 0; q < hspw; ++q) diff += __popc(hw[q] ^ __ldg(wt + k * hspw + q));
+    const float fd = static_cast<float>(K - 2 * diff);  // exact
+    const float bk = __ldg(beta + k);
+    const float x = __fmul_rn(fd, bk);
+    const float e = __fmaf_rn(fd, bk, -x);  // exact rounding error of the product
+    const int ex = ((__float_as_int(bk) >> 23) & 0xFF) - 127;
+    const float inv2u = __int_as_float((127 + 22 - ex) << 23);
+    const int q = __float2int_rn(e * inv2u);  // in [-32, 32]
+    out |= static_cast<uint32_t>(q + 32) << (8 * b);
+  }
+  rec[t] = out;
+}
+
+// ---- real-valued walk in ascending column order ------------------------------
+template <int M, bool XBITS, bool OUTB>
+__global__ void __launch_bounds__(256)
+    k_sl_f(const uint64_t* __restrict__ srp, const uint32_t* __restrict__ sl, int64_t row0,
+           int64_t row1, const float* __restrict__ xf, const uint32_t* __restrict__ xb,
+           int64_t xspw, const float* __restrict__ rs, const float* __restrict__ cs, int64_t f,
+           int64_t ospw, uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
+  const int64_t i = row0 + ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  if (i >= row1) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t fbase = static_cast<int64_t>(blockIdx.y) * 32 * M;
+  double d[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) d[m] = 0.0;
+  const uint64_t e1 = srp[i + 1];
+  for (uint64_t base = srp[i]; base < e1; base += 32) {
+    const uint64_t e = base + lane;
+    const uint32_t mine = e < e1 ? ld_nc_u32(sl + e) : 0u;
+    const int cnt = static_cast<int>(e1 - base < 32 ? e1 - base : 32);
+    for (int L = 0; L < cnt; ++L) {  // slivers in order, then columns in order
+      const uint32_t ent = __shfl_sync(0xFFFFFFFFu, mine, L);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (!(ent & (8u >> c))) continue;
+        const int64_t j = 4 * static_cast<int64_t>(ent >> 4) + c;
+        const double w = cs ? static_cast<double>(__ldg(cs + j)) : 1.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const int64_t k = fbase + 32 * m + lane;
+          if (k < f) {
+            if (XBITS) {
+              const uint32_t bit = (__ldg(xb + j * xspw + (k >> 5)) >> (31 - (k & 31))) & 1u;
+              d[m] = __dadd_rn(d[m], bit ? w : -w);
+            } else {
+              d[m] = __dadd_rn(d[m], __dmul_rn(w, static_cast<double>(__ldg(xf + j * f + k))));
+            }
+          }
+        }
+      }
+    }
+  }
+  const double si = rs ? static_cast<double>(rs[i]) : 1.0;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int64_t k = fbase + 32 * m + lane;
+    const double v = __dmul_rn(si, d[m]);
+    if (OUTB) {
+      const uint32_t word = __brev(__ballot_sync(0xFFFFFFFFu, k < f && v >= 0.0));
+      const int64_t w = (fbase >> 5) + m;
+      if (lane == 0 && w < ospw) out_bits[i * ospw + w] = word;
+    } else if (k < f) {
+      out_f[i * f + k] = __double2float_rn(v);
+    }
+  }
+  if (OUTB && lane == 0 && blockIdx.y == gridDim.y - 1)
+    for (int64_t w = (f + 31) / 32; w < ospw; ++w) out_bits[i * ospw + w] = 0;
+}
+
+int64_t grid_warps(int64_t rows) {
+  return std::max<int64_t>(1, std::min<int64_t>(cdiv(rows, kSlWarps), static_cast<int64_t>(sm_count()) * 32));
+}
+
+// Most bits a slot lane can count: its share of the row's slivers (batches
+// of 8 per slot) plus every extra bit of multi-bit nibbles.
+int64_t lane_bound(const bg_frdc& A, int S) {
+  return (A.max_sl_row + 8 * S - 1) / (8 * S) * 8 + A.max_extra_bits;
+}
+
+template <int G, bool OUTB>
+void launch_sl_bb(const bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uint32_t* ob,
+                  float* of, int64_t r0, int64_t r1, cudaStream_t s) {
+  const int64_t per_lane = lane_bound(A, 32 / G);
+  dim3 grid(static_cast<unsigned>(grid_warps(r1 - r0)), static_cast<unsigned>(cdiv(xspw, G)));
+  auto go = [&](auto kern) {
+    kern<<<grid, kSlWarps * 32, 0, s>>>(A.srp(), A.sl(), r0, r1, A.deg(), x, xspw, f, ob, of);
+  };
+  if (per_lane < (1 << 7)) go(k_sl_bb<G, 7, OUTB>);
+  else if (per_lane < (1 << 10)) go(k_sl_bb<G, 10, OUTB>);
+  else if (per_lane < (1 << 13)) go(k_sl_bb<G, 13, OUTB>);
+  else if (per_lane < (1 << 16)) go(k_sl_bb<G, 16, OUTB>);
+  else fail("bspmm: node degree " + std::to_string(A.max_deg) + " exceeds the counter range");
+  BG_LAUNCH_CHECK();
+}
+
+template <int M, bool XBITS, bool OUTB>
+void launch_sl_f(const bg_frdc& A, const SpmmFArgs& a, int64_t r0, int64_t r1, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>(cdiv((r1 - r0) * 32, 256)), static_cast<unsigned>(cdiv(a.f, 32 * M)));
+  const int64_t xspw = XBITS ? spw(a.f, a.xwb) : 0;
+  const int64_t ospw = OUTB ? spw(a.f, a.owb) : 0;
+  k_sl_f<M, XBITS, OUTB><<<grid, 256, 0, s>>>(A.srp(), A.sl(), r0, r1, a.x_f, a.x_bits, xspw,
+                                              a.row_scale, a.col_scale, a.f, ospw, a.out_bits,
+                                              a.out_f);
+  BG_LAUNCH_CHECK();
+}
+
+template <bool XBITS, bool OUTB>
+void launch_sl_f_m(const bg_frdc& A, const SpmmFArgs& a, int64_t r0, int64_t r1, cudaStream_t s) {
+  if (a.f <= 32) launch_sl_f<1, XBITS, OUTB>(A, a, r0, r1, s);
+  else if (a.f <= 64) launch_sl_f<2, XBITS, OUTB>(A, a, r0, r1, s);
+  else launch_sl_f<4, XBITS, OUTB>(A, a, r0, r1, s);
+}
+
+}  // namespace
+
+void sliver_bb(bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* out_bits, float* out_f,
+               cudaStream_t s, int64_t r0, int64_t r1) {
+  if (r1 < 0) r1 = A.rows;
+  const int64_t xspw = spw(f, wb);
+  if (r1 <= r0 || xspw == 0) return;
+  frdc_slivers(A, s);
+  const bool ob = out_bits != nullptr;
+  if (xspw <= 4) {
+    if (ob) launch_sl_bb<4, true>(A, x, f, xspw, out_bits, out_f, r0, r1, s);
+    else launch_sl_bb<4, false>(A, x, f, xspw, out_bits, out_f, r0, r1, s);
+  } else if (xspw <= 8) {
+    if (ob) launch_sl_bb<8, true>(A, x, f, xspw, out_bits, out_f, r0, r1, s);
+    else launch_sl_bb<8, false>(A, x, f, xspw, out_bits, out_f, r0, r1, s);
+  } else if (xspw <= 16) {
+    if (ob) launch_sl_bb<16, true>(A, x, f, xspw, out_bits, out_f, r0, r1, s);
+    else launch_sl_bb<16, false>(A, x, f, xspw, out_bits, out_f, r0, r1, s);
+  } else {
+    if (ob) launch_sl_bb<32, true>(A, x, f, xspw, out_bits, out_f, r0, r1, s);
+    else launch_sl_bb<32, false>(A, x, f, xspw, out_bits, out_f, r0, r1, s);
+  }
+}
+
+void sliver_f(bg_frdc& A, const SpmmFArgs& a, cudaStream_t s, int64_t r0, int64_t r1) {
+  if (r1 < 0) r1 = A.rows;
+  if (r1 <= r0 || a.f == 0) return;
+  frdc_slivers(A, s);
+  const bool xb = a.x_bits != nullptr, ob = a.out_bits != nullptr;
+  if (xb && ob) launch_sl_f_m<true, true>(A, a, r0, r1, s);
+  else if (xb) launch_sl_f_m<true, false>(A, a, r0, r1, s);
+  else if (ob) launch_sl_f_m<false, true>(A, a, r0, r1, s);
+  else launch_sl_f_m<false, false>(A, a, r0, r1, s);
+}
+
+void sliver_gcn1_records(const uint32_t* h, int64_t n, int64_t K, int wb, const uint32_t* wt,
+                         const float* beta, int64_t C, uint32_t* rec, cudaStream_t s) {
+  k_sl_gcn1_records<<<static_cast<unsigned>(cdiv(n * kRec, 256)), 256, 0, s>>>(
+      h, n, static_cast<int>(spw(K, wb)), static_cast<int>(K), wt, beta, static_cast<int>(C), rec);
+  BG_LAUNCH_CHECK();
+}
+
+void sliver_gcn1_aggregate(bg_frdc& A, const uint32_t* rec, int64_t K, int wb, const uint32_t* wt,
+                           const float* beta, int64_t C, float* logits, float* probs,
+                           cudaStream_t s, int64_t r0, int64_t r1) {
+  if (r1 < 0) r1 = A.rows;
+  if (r1 <= r0) return;
+  frdc_slivers(A, s);
+  const int64_t per_lane = lane_bound(A, 8);
+  const int hspw = static_cast<int>(spw(K, wb));
+  auto go = [&](auto kern) {
+    kern<<<static_cast<unsigned>(grid_warps(r1 - r0)), kSlWarps * 32, 0, s>>>(
+        A.srp(), A.sl(), r0, r1, A.deg(), rec, wt, hspw, static_cast<int>(K), beta,
+        static_cast<int>(C), logits, probs);
+  };
+  if (per_lane < (1 << 7)) go(k_sl_gcn1<7>);
+  else if (per_lane < (1 << 10)) go(k_sl_gcn1<10>);
+  else go(k_sl_gcn1<13>);
+  BG_LAUNCH_CHECK();
+}
+
+}  // namespace bg
+
+namespace bg {
+bool use_slivers() {
+  static const bool v = [] {
+    const char* e = std::getenv("BG_AGGREGATION");
+    return !(e && std::string(e) == "tiles");
+  }();
+  return v;
+}
+}  // namespace bg
