@@ -10,8 +10,8 @@ OBJS    := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 HDRS    := $(wildcard $(CSRC)/*.cuh) include/bitgnn_b200.h
 LIB     := paper_2305_02522_b200/libbitgnn_b200.so
 
-.PHONY: all lib oracle clean
-all: lib oracle
+.PHONY: all lib oracle cpptest clean
+all: lib oracle cpptest
 lib: $(LIB)
 
 build/%.o: $(CSRC)/%.cu $(HDRS)
@@ -23,7 +23,19 @@ $(LIB): $(OBJS) $(CSRC)/exports.map
 
 oracle:
 	$(MAKE) -C oracle all
+oracle/liboracle.so:
+	$(MAKE) -C oracle all
+
+# C++ host-API test program (tests/cpp): the header-only shim over the C ABI,
+# checked against the C oracle (test infrastructure).
+CPPTEST := tests/cpp/bin/test_shim
+cpptest: $(CPPTEST)
+$(CPPTEST): tests/cpp/test_shim.cpp include/bitgnn_b200/bitgnn.hpp include/bitgnn_b200.h $(LIB) oracle/liboracle.so
+	@mkdir -p tests/cpp/bin
+	g++ -std=c++20 -O1 -Wall -Wextra -Wno-missing-field-initializers -Iinclude -Ioracle -o $@ $< \
+	    -L paper_2305_02522_b200 -lbitgnn_b200 -L oracle -loracle \
+	    -Wl,-rpath,'$$ORIGIN/../../../paper_2305_02522_b200' -Wl,-rpath,'$$ORIGIN/../../../oracle'
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) tests/cpp/bin
 	$(MAKE) -C oracle clean

@@ -42,6 +42,16 @@ typedef void* bg_stream; /* cudaStream_t; NULL = legacy default stream */
 const char* bg_last_error(void);
 int bg_version(void);
 
+/* ---- device memory (so C/C++ hosts need no CUDA headers) ---------------- */
+enum { BG_COPY_H2D = 0, BG_COPY_D2H = 1, BG_COPY_D2D = 2 };
+int bg_device_count(int* count);
+int bg_device_alloc(size_t bytes, void** out); /* cudaMalloc; 0 bytes -> NULL */
+int bg_device_free(void* p);
+/* Copy on `stream`, then wait for the stream (synchronous for the caller). */
+int bg_memcpy(void* dst, const void* src, size_t bytes, int kind, bg_stream stream);
+int bg_memset(void* dst, int value, size_t bytes, bg_stream stream);
+int bg_stream_synchronize(bg_stream stream);
+
 /* ---- enums (ref: kernels.hpp:15-33, bitdense.hpp:15-16, graphops.hpp:44-55) */
 enum { BG_F = 0, BG_B = 1 };                                  /* Precision */
 enum { BG_BMM = 0, BG_BSPMM = 1, BG_ADD = 2, BG_CONCAT = 3 }; /* KernelOp */

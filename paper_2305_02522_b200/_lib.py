@@ -70,6 +70,12 @@ PI64 = C.POINTER(C.c_int64)
 PROTOTYPES = {
     "bg_last_error": (C.c_char_p, []),
     "bg_version": (I32, []),
+    "bg_device_count": (I32, [C.POINTER(C.c_int)]),
+    "bg_device_alloc": (I32, [C.c_size_t, C.POINTER(C.c_void_p)]),
+    "bg_device_free": (I32, [P]),
+    "bg_memcpy": (I32, [P, P, C.c_size_t, I32, P]),
+    "bg_memset": (I32, [P, I32, C.c_size_t, P]),
+    "bg_stream_synchronize": (I32, [P]),
     "bg_variant_parse": (I32, [C.c_char_p, C.POINTER(Variant)]),
     "bg_variant_valid": (I32, [Variant]),
     "bg_variant_name": (I32, [Variant, C.c_char_p, C.c_size_t]),

@@ -57,6 +57,48 @@ extern "C" {
 const char* bg_last_error(void) { return bg::g_last_error.c_str(); }
 int bg_version(void) { return 100; }
 
+int bg_device_count(int* count) {
+  return guard([&] {
+    need(count, "output");
+    BG_CUDA(cudaGetDeviceCount(count));
+  });
+}
+int bg_device_alloc(size_t bytes, void** out) {
+  return guard([&] {
+    need(out, "output");
+    *out = nullptr;
+    if (bytes) BG_CUDA(cudaMalloc(out, bytes));
+  });
+}
+int bg_device_free(void* p) {
+  return guard([&] {
+    if (p) BG_CUDA(cudaFree(p));
+  });
+}
+int bg_memcpy(void* dst, const void* src, size_t bytes, int kind, bg_stream s) {
+  return guard([&] {
+    if (!bytes) return;
+    need(dst, "destination");
+    need(src, "source");
+    const cudaMemcpyKind k = kind == BG_COPY_H2D   ? cudaMemcpyHostToDevice
+                             : kind == BG_COPY_D2H ? cudaMemcpyDeviceToHost
+                             : kind == BG_COPY_D2D ? cudaMemcpyDeviceToDevice
+                                                   : (fail("bg_memcpy: unknown copy kind"), cudaMemcpyDefault);
+    BG_CUDA(cudaMemcpyAsync(dst, src, bytes, k, S(s)));
+    sync(S(s));
+  });
+}
+int bg_memset(void* dst, int value, size_t bytes, bg_stream s) {
+  return guard([&] {
+    if (!bytes) return;
+    need(dst, "destination");
+    BG_CUDA(cudaMemsetAsync(dst, value, bytes, S(s)));
+  });
+}
+int bg_stream_synchronize(bg_stream s) {
+  return guard([&] { sync(S(s)); });
+}
+
 int64_t bg_storage_words_per_row(int64_t cols, int word_bits) { return spw(cols, word_bits); }
 
 int bg_variant_parse(const char* text, bg_variant* out) {
