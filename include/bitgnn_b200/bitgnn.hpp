@@ -6,7 +6,7 @@
 // reference:
 //   * value types own host storage (ref: bitdense.hpp:18-107, bitsparse.hpp:26-60);
 //   * contract violations throw std::invalid_argument, layer failures
-//     std::runtime_error("layer i (Kind): ..."), trace misuse std::logic_error
+//     std::runtime_error("layer i (kind): ..."), trace misuse std::logic_error
 //     (ref: kernels.cpp:17, graphops.cpp:476-479), with the reference's messages;
 //   * ops are pure; every computation runs on the B200 (no CPU fallback).
 // Each host-typed op uploads its operands, runs the sm_100a kernels and
@@ -597,18 +597,19 @@ inline std::shared_ptr<const GraphBundle> prepare_graph(const EdgeList& e) {
 }
 
 // ---- models (ref: LayerSpec / ModelSpec / RunTrace / run_model, graphops.hpp:61-133) ----
+// ref: layer_kind_name (graphops.cpp:119-133)
 inline const char* layer_kind_name(LayerKind k) {
   switch (k) {
-    case LayerKind::GcnConv: return "GcnConv";
-    case LayerKind::SageConv: return "SageConv";
-    case LayerKind::GraphConv: return "GraphConv";
-    case LayerKind::FullyConnected: return "FullyConnected";
-    case LayerKind::Aggregate: return "Aggregate";
-    case LayerKind::Relu: return "Relu";
-    case LayerKind::BatchNorm: return "BatchNorm";
-    case LayerKind::Softmax: return "Softmax";
-    case LayerKind::Binarize: return "Binarize";
-    case LayerKind::Scale: return "Scale";
+    case LayerKind::GcnConv: return "gcn_conv";
+    case LayerKind::SageConv: return "sage_conv";
+    case LayerKind::GraphConv: return "graph_conv";
+    case LayerKind::FullyConnected: return "fc";
+    case LayerKind::Aggregate: return "aggregate";
+    case LayerKind::Relu: return "relu";
+    case LayerKind::BatchNorm: return "batchnorm";
+    case LayerKind::Softmax: return "softmax";
+    case LayerKind::Binarize: return "binarize";
+    case LayerKind::Scale: return "scale";
   }
   return "?";
 }

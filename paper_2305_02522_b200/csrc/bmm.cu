@@ -11,6 +11,7 @@
 // binarized in the prologue by warp ballots on coalesced loads, so FBB/FBF
 // read X exactly once and never write packed X back (north-star item 4).
 #include <algorithm>
+#include <cstdlib>
 
 #include "ops.cuh"
 
@@ -94,6 +95,314 @@ __global__ void __launch_bounds__(kWarps * 32)
   }
 }
 
+// ---- B-output products with one node row per lane ---------------------------
+// Binary output needs no scales (kernels.cpp:159-161), so the product is pure
+// popcount work: each lane owns one activation row (its KW packed words in
+// registers) and every weight word is a warp-uniform shared-memory broadcast
+// (LDS.128, four output columns at a time), i.e. XOR + POPC + 1/2 IADD3 per
+// (row, column, word) and no per-lane weight traffic.  With fp32 input the
+// warp first binarizes its 32 rows with ballots on coalesced loads (the row
+// goes through shared memory, never through HBM packed).
+constexpr int kLrWarps = 8;
+
+template <bool AF, int KW>
+__global__ void __launch_bounds__(kLrWarps * 32)
+    k_bmm_lanerow(const uint32_t* __restrict__ a_bits, const float* __restrict__ a_f,
+                  const uint32_t* __restrict__ wt, int64_t rows, int k, int kspw, int n, int npad,
+                  int ospw, uint32_t* __restrict__ out_bits) {
+  extern __shared__ uint4 smem4[];
+  uint32_t* sw = reinterpret_cast<uint32_t*>(smem4);  // kspw x npad: W[w][o]
+  const int ld = kspw | 1;                             // stage row stride (odd: no conflicts)
+  uint32_t* stage = sw + kspw * npad + (threadIdx.x >> 5) * 32 * ld;
+  for (int t = threadIdx.x; t < kspw * npad; t += blockDim.x) {
+    const int w = t / npad, o = t % npad;
+    sw[t] = o < n ? __ldg(wt + static_cast<int64_t>(o) * kspw + w) : 0u;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = static_cast<int64_t>(blockIdx.x) * kLrWarps + (threadIdx.x >> 5);
+  for (int64_t base = warp0 * 32; base < rows; base += static_cast<int64_t>(gridDim.x) * kLrWarps * 32) {
+    const int64_t row = base + lane;
+    uint32_t a[KW];
+    if (AF) {
+      const int nr = rows - base < 32 ? static_cast<int>(rows - base) : 32;
+      for (int r = 0; r < nr; ++r) {
+        const float* xr = a_f + (base + r) * k;
+        float v[KW];
+#pragma unroll
+        for (int w = 0; w < KW; ++w) {
+          const int j = 32 * w + lane;
+          v[w] = (w < kspw && j < k) ? __ldg(xr + j) : -1.0f;
+        }
+#pragma unroll
+        for (int w = 0; w < KW; ++w) {
+          const uint32_t word = __brev(__ballot_sync(0xFFFFFFFFu, v[w] >= 0.0f));
+          if (lane == 0 && w < kspw) stage[r * ld + w] = word;
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int w = 0; w < KW; ++w) a[w] = w < kspw ? stage[lane * ld + w] : 0u;
+      __syncwarp();
+    } else {
+#pragma unroll
+      for (int w = 0; w < KW; ++w) a[w] = (w < kspw && row < rows) ? __ldg(a_bits + row * kspw + w) : 0u;
+    }
+    for (int oc = 0; oc < ospw; ++oc) {
+      uint32_t bits = 0;
+      if (32 * oc < n) {
+        int d[32];
+#pragma unroll
+        for (int o = 0; o < 32; ++o) d[o] = 0;
+#pragma unroll
+        for (int w = 0; w < KW; ++w) {
+          if (w < kspw) {
+            const uint4* wv = reinterpret_cast<const uint4*>(sw + w * npad + 32 * oc);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const uint4 c = wv[q];
+              d[4 * q + 0] += __popc(a[w] ^ c.x);
+              d[4 * q + 1] += __popc(a[w] ^ c.y);
+              d[4 * q + 2] += __popc(a[w] ^ c.z);
+              d[4 * q + 3] += __popc(a[w] ^ c.w);
+            }
+          }
+        }
+        // dot = K - 2*diff >= 0 (padding bits are zero on both sides and cancel)
+#pragma unroll
+        for (int o = 0; o < 32; ++o)
+          if (32 * oc + o < n && 2 * d[o] <= k) bits |= 0x80000000u >> o;
+      }
+      if (row < rows) out_bits[row * ospw + oc] = bits;
+    }
+  }
+}
+
+// ---- fp32-input products on the int8 tensor cores ---------------------------
+// sign(x) in {+1, -1} (bit = x >= 0, bitdense.cpp:71-88) is an exact int8, so
+// the +-1 dot of FBB/FBF is an int8 GEMM with int32 accumulation: dot =
+// sum_k s(a_ik) s(w_kj), |dot| <= K, exact.  One warp owns 16 rows (one
+// m16n8k32 A tile) and converts them straight from fp32 registers to int8
+// fragments -- X is read from HBM exactly once and never materialised packed.
+// The weights live in shared memory as +-1 bytes (0 past K / past n), each
+// 32-k block permuted so a B fragment (k 4t..4t+3 and 16+4t..16+4t+3 of
+// column g) is one 8-byte load, rows padded to a conflict-free stride.
+// (The b1 mma.sync form is emulated on sm_100a -- LOP3/MOVM.U4TO8 expansion
+// plus 8 IMMA per instruction, see DESIGN.md -- so int8 is the native path.)
+constexpr int kImWarps = 8;
+
+__device__ __forceinline__ void mma_s8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// Four fp32 values -> four +-1 bytes (element i in byte i); `valid` bytes past K are 0.
+__device__ __forceinline__ uint32_t sign_bytes(float x0, float x1, float x2, float x3) {
+  return (x0 >= 0.0f ? 0x00000001u : 0x000000FFu) | (x1 >= 0.0f ? 0x00000100u : 0x0000FF00u) |
+         (x2 >= 0.0f ? 0x00010000u : 0x00FF0000u) | (x3 >= 0.0f ? 0x01000000u : 0xFF000000u);
+}
+
+template <bool OUTB, int NT>
+__global__ void __launch_bounds__(kImWarps * 32)
+    k_bmm_imma(const float* __restrict__ a_f, const float* __restrict__ alpha,
+               const uint32_t* __restrict__ wt, const float* __restrict__ beta, int64_t rows, int k,
+               int kspw, int n, int ksteps, int ldw, int ospw, uint32_t* __restrict__ out_bits,
+               float* __restrict__ out_f) {
+  extern __shared__ uint4 smem4[];
+  uint8_t* w8 = reinterpret_cast<uint8_t*>(smem4);  // (8*NT) x ldw bytes
+  const int kpad = 32 * ksteps;
+  // weights: byte of (column o, position p) with p = 32*blk + 8*t + 4*half + i <-> k = 32*blk + 16*half + 4*t + i
+  for (int t = threadIdx.x; t < 8 * NT * (kpad / 4); t += blockDim.x) {
+    const int o = t / (kpad / 4), p4 = (t % (kpad / 4)) * 4;
+    const int blk = p4 >> 5, tt = (p4 >> 3) & 3, half = (p4 >> 2) & 1;
+    const int k0 = 32 * blk + 16 * half + 4 * tt;
+    uint32_t v = 0;
+    if (o < n) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int kk = k0 + i;
+        if (kk < k) {
+          const uint32_t bit = (__ldg(wt + static_cast<int64_t>(o) * kspw + (kk >> 5)) >> (31 - (kk & 31))) & 1u;
+          v |= (bit ? 0x01u : 0xFFu) << (8 * i);
+        }
+      }
+    }
+    *reinterpret_cast<uint32_t*>(w8 + o * ldw + p4) = v;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  const bool vec2 = (k & 1) == 0 && (reinterpret_cast<uintptr_t>(a_f) & 7) == 0;
+  for (int64_t tile = static_cast<int64_t>(blockIdx.x) * kImWarps + (threadIdx.x >> 5); tile * 16 < rows;
+       tile += static_cast<int64_t>(gridDim.x) * kImWarps) {
+    const int64_t r0 = tile * 16 + g, r1 = r0 + 8;
+    const float* x0 = a_f + (r0 < rows ? r0 : 0) * static_cast<int64_t>(k);
+    const float* x1 = a_f + (r1 < rows ? r1 : 0) * static_cast<int64_t>(k);
+    int acc[NT][4];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0;
+    for (int ks = 0; ks < ksteps; ++ks) {
+      const int ka = 32 * ks + 4 * t4, kb = ka + 16;  // element columns of a0/a1 and a2/a3
+      float v[16];
+      if (32 * ks + 32 <= k && vec2) {
+        const float2* p00 = reinterpret_cast<const float2*>(x0 + ka);
+        const float2* p01 = reinterpret_cast<const float2*>(x0 + kb);
+        const float2* p10 = reinterpret_cast<const float2*>(x1 + ka);
+        const float2* p11 = reinterpret_cast<const float2*>(x1 + kb);
+        float2 q[8] = {__ldg(p00), __ldg(p00 + 1), __ldg(p10), __ldg(p10 + 1),
+                       __ldg(p01), __ldg(p01 + 1), __ldg(p11), __ldg(p11 + 1)};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          v[2 * i] = q[i].x;
+          v[2 * i + 1] = q[i].y;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          v[i] = ka + i < k ? __ldg(x0 + ka + i) : 0.0f;
+          v[4 + i] = ka + i < k ? __ldg(x1 + ka + i) : 0.0f;
+          v[8 + i] = kb + i < k ? __ldg(x0 + kb + i) : 0.0f;
+          v[12 + i] = kb + i < k ? __ldg(x1 + kb + i) : 0.0f;
+        }
+      }
+      uint32_t a[4];
+#pragma unroll
+      for (int f = 0; f < 4; ++f) a[f] = sign_bytes(v[4 * f], v[4 * f + 1], v[4 * f + 2], v[4 * f + 3]);
+      if (32 * ks + 32 > k) {  // K tail: elements past K contribute 0
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (ka + i >= k) { a[0] &= ~(0xFFu << (8 * i)); a[1] &= ~(0xFFu << (8 * i)); }
+          if (kb + i >= k) { a[2] &= ~(0xFFu << (8 * i)); a[3] &= ~(0xFFu << (8 * i)); }
+        }
+      }
+      const uint8_t* wb = w8 + g * ldw + 32 * ks + 8 * t4;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const uint2 b = *reinterpret_cast<const uint2*>(wb + 8 * j * ldw);
+        mma_s8(acc[j], a, b.x, b.y);
+      }
+    }
+    // c0,c1: row r0, columns 8j+2t, 8j+2t+1; c2,c3: row r1, same columns
+    if (OUTB) {
+      // word w of a row = columns 32w..32w+31 = tiles 4w..4w+3; bit 31-c
+#pragma unroll
+      for (int w = 0; w < (NT + 3) / 4; ++w) {
+        uint32_t m0 = 0, m1 = 0;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = 4 * w + jj;
+          if (j < NT) {
+            const int c = 8 * jj + 2 * t4;
+            if (acc[j][0] >= 0) m0 |= 0x80000000u >> c;
+            if (acc[j][1] >= 0) m0 |= 0x40000000u >> c;
+            if (acc[j][2] >= 0) m1 |= 0x80000000u >> c;
+            if (acc[j][3] >= 0) m1 |= 0x40000000u >> c;
+          }
+        }
+        m0 |= __shfl_xor_sync(0xFFFFFFFFu, m0, 1);
+        m0 |= __shfl_xor_sync(0xFFFFFFFFu, m0, 2);
+        m1 |= __shfl_xor_sync(0xFFFFFFFFu, m1, 1);
+        m1 |= __shfl_xor_sync(0xFFFFFFFFu, m1, 2);
+        // columns >= n are zero padding (their weights are 0 so dot = 0 -> bit set): clear them
+        if (32 * w + 32 > n) {
+          const uint32_t keep = 32 * w >= n ? 0u : tail_mask32(n);
+          m0 &= keep;
+          m1 &= keep;
+        }
+        if (t4 == (w & 3)) {
+          if (r0 < rows) out_bits[r0 * ospw + w] = m0;
+          if (r1 < rows) out_bits[r1 * ospw + w] = m1;
+        }
+      }
+      if (t4 == 0)
+        for (int w = (n + 31) / 32; w < ospw; ++w) {  // storage padding of 64-bit rows
+          if (r0 < rows) out_bits[r0 * ospw + w] = 0;
+          if (r1 < rows) out_bits[r1 * ospw + w] = 0;
+        }
+    } else {
+      const double al0 = r0 < rows && alpha ? static_cast<double>(alpha[r0]) : 1.0;
+      const double al1 = r1 < rows && alpha ? static_cast<double>(alpha[r1]) : 1.0;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = 8 * j + 2 * t4 + e;
+          if (c < n) {
+            const double be = beta ? static_cast<double>(beta[c]) : 1.0;
+            if (r0 < rows)
+              out_f[r0 * n + c] = __double2float_rn(__dmul_rn(__dmul_rn(al0, static_cast<double>(acc[j][e])), be));
+            if (r1 < rows)
+              out_f[r1 * n + c] = __double2float_rn(__dmul_rn(__dmul_rn(al1, static_cast<double>(acc[j][2 + e])), be));
+          }
+        }
+      }
+    }
+  }
+}
+
+bool imma_ok(const BmmArgs& a) {
+  return a.a_f != nullptr && a.n <= 128 && a.k <= 8192 && std::getenv("BG_BMM_POPC") == nullptr;
+}
+
+template <bool OUTB>
+void launch_imma(const BmmArgs& a, cudaStream_t s) {
+  const int ksteps = static_cast<int>(cdiv(a.k, 32));
+  const int ldw = 32 * ksteps + 16;  // bytes; stride/4 = 8*ksteps + 4 -> conflict-free fragments
+  const int kspw = static_cast<int>(spw(a.k, a.wb));
+  const int ospw = static_cast<int>(spw(a.n, a.wb));
+  const int nt = static_cast<int>(cdiv(a.n, 8));
+  auto go = [&](auto kern, int NT) {
+    const size_t smem = static_cast<size_t>(8 * NT) * ldw;
+    BG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int per_sm = 0;
+    BG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kImWarps * 32, smem));
+    const int64_t blocks = std::max<int64_t>(
+        1, std::min<int64_t>(cdiv(a.rows, 16 * kImWarps), static_cast<int64_t>(sm_count()) * std::max(per_sm, 1)));
+    kern<<<static_cast<unsigned>(blocks), kImWarps * 32, smem, s>>>(
+        a.a_f, a.alpha, a.wt, a.beta, a.rows, static_cast<int>(a.k), kspw, static_cast<int>(a.n), ksteps, ldw,
+        ospw, a.out_bits, a.out_f);
+  };
+  if (nt <= 2) go(k_bmm_imma<OUTB, 2>, 2);
+  else if (nt <= 4) go(k_bmm_imma<OUTB, 4>, 4);
+  else if (nt <= 8) go(k_bmm_imma<OUTB, 8>, 8);
+  else go(k_bmm_imma<OUTB, 16>, 16);
+  BG_LAUNCH_CHECK();
+}
+
+// Row-per-lane B-output path: word count small enough for registers and the
+// weight table for shared memory.
+bool lanerow_ok(const BmmArgs& a) {
+  const int64_t kspw = spw(a.k, a.wb);
+  const int64_t npad = cdiv(a.n, 32) * 32;
+  const size_t smem = static_cast<size_t>(kspw * npad + kLrWarps * 32 * (kspw | 1)) * 4;
+  return a.out_bits != nullptr && kspw <= 32 && smem <= 160 * 1024 && std::getenv("BG_BMM_WARPROW") == nullptr;
+}
+
+template <bool AF>
+void launch_lanerow(const BmmArgs& a, cudaStream_t s) {
+  const int kspw = static_cast<int>(spw(a.k, a.wb));
+  const int npad = static_cast<int>(cdiv(a.n, 32) * 32);
+  const int ospw = static_cast<int>(spw(a.n, a.wb));
+  const size_t smem = static_cast<size_t>(kspw * npad + kLrWarps * 32 * (kspw | 1)) * 4;
+  const int64_t blocks = std::max<int64_t>(
+      1, std::min<int64_t>(cdiv(a.rows, kLrWarps * 32), static_cast<int64_t>(sm_count()) * 4));
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024)
+      BG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<static_cast<unsigned>(blocks), kLrWarps * 32, smem, s>>>(
+        a.a_bits, a.a_f, a.wt, a.rows, static_cast<int>(a.k), kspw, static_cast<int>(a.n), npad, ospw,
+        a.out_bits);
+  };
+  if (kspw <= 4) go(k_bmm_lanerow<AF, 4>);
+  else if (kspw <= 8) go(k_bmm_lanerow<AF, 8>);
+  else if (kspw <= 16) go(k_bmm_lanerow<AF, 16>);
+  else if (kspw <= 20) go(k_bmm_lanerow<AF, 20>);
+  else go(k_bmm_lanerow<AF, 32>);
+  BG_LAUNCH_CHECK();
+}
+
 template <bool AF, bool OUTB>
 void launch(const BmmArgs& a, cudaStream_t s) {
   auto pick = [](int64_t nc) {
@@ -125,6 +434,16 @@ void launch(const BmmArgs& a, cudaStream_t s) {
 void bmm(const BmmArgs& a, cudaStream_t s) {
   if (a.rows == 0 || a.n == 0) return;
   const bool af = a.a_f != nullptr, ob = a.out_bits != nullptr;
+  if (imma_ok(a)) {
+    if (ob) launch_imma<true>(a, s);
+    else launch_imma<false>(a, s);
+    return;
+  }
+  if (lanerow_ok(a)) {
+    if (af) launch_lanerow<true>(a, s);
+    else launch_lanerow<false>(a, s);
+    return;
+  }
   if (af && ob) launch<true, true>(a, s);
   else if (af) launch<true, false>(a, s);
   else if (ob) launch<false, true>(a, s);

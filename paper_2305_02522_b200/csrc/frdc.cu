@@ -129,7 +129,8 @@ __global__ void k_slot_max(const uint64_t* __restrict__ rp, const uint16_t* __re
   }
 }
 
-// Warp per tile row: nonzero nibbles per node row.
+// Warp per tile row: nonzero nibbles per node row, padded to a multiple of
+// kSliverPad entries (the aggregation kernels then need no bounds checks).
 __global__ void k_sliver_count(const uint64_t* __restrict__ rp, const uint16_t* __restrict__ tiles,
                                int64_t trows, int64_t rows, const int32_t* __restrict__ deg,
                                unsigned long long* __restrict__ cnt, int* __restrict__ maxima) {
@@ -146,14 +147,28 @@ __global__ void k_sliver_count(const uint64_t* __restrict__ rp, const uint16_t* 
   for (int r = 0; r < 4; ++r) {
     for (int o = 16; o; o >>= 1) c[r] += __shfl_xor_sync(0xFFFFFFFFu, c[r], o);
     if (lane == 0 && 4 * tr + r < rows) {
-      cnt[4 * tr + r] = static_cast<unsigned long long>(c[r]);
-      atomicMax(maxima, c[r]);
+      const int padded = (c[r] + kSliverPad - 1) / kSliverPad * kSliverPad;
+      cnt[4 * tr + r] = static_cast<unsigned long long>(padded);
+      atomicMax(maxima, padded);
       atomicMax(maxima + 1, deg[4 * tr + r] - c[r]);
     }
   }
 }
 
-// Warp per tile row: ballot-compact each row's nonzero nibbles in tile order.
+// Sliver entry of one nonzero nibble of tile column `col`: the node column of
+// its first set bit (bit 3-c of the nibble is local column c) and a 3-bit
+// mask of the following columns present (bit k-1 <-> first + k).
+__device__ __forceinline__ uint32_t sliver_entry(uint32_t col, uint32_t nib) {
+  const uint32_t c0 = __clz(nib) - 28;  // lowest local column present
+  uint32_t extra = 0;
+#pragma unroll
+  for (int k = 1; k < 4; ++k)
+    if (c0 + k < 4 && ((nib >> (3 - c0 - k)) & 1u)) extra |= 1u << (k - 1);
+  return ((4 * col + c0) << 3) | extra;
+}
+
+// Warp per tile row: ballot-compact each row's nonzero nibbles in tile order,
+// then the row's padding entries.
 __global__ void k_sliver_fill(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ ci,
                               const uint16_t* __restrict__ tiles, int64_t trows, int64_t rows,
                               const unsigned long long* __restrict__ srp,
@@ -177,10 +192,14 @@ __global__ void k_sliver_fill(const uint64_t* __restrict__ rp, const uint32_t* _
     for (int r = 0; r < 4; ++r) {
       const uint32_t nib = (t >> (12 - 4 * r)) & 0xFu;
       const uint32_t mask = __ballot_sync(0xFFFFFFFFu, nib != 0);
-      if (nib) out[pos[r] + __popc(mask & lt)] = (col << 4) | nib;
+      if (nib) out[pos[r] + __popc(mask & lt)] = sliver_entry(col, nib);
       pos[r] += __popc(mask);
     }
   }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+    if (4 * tr + r < rows)
+      for (unsigned long long k = pos[r] + lane; k < srp[4 * tr + r + 1]; k += 32) out[k] = kSliverSentinel;
 }
 
 __global__ void k_graph_scales(const int32_t* __restrict__ deg_loops,
@@ -231,7 +250,7 @@ void frdc_finalize(bg_frdc& m, cudaStream_t s) {
 
 void frdc_slivers(bg_frdc& m, cudaStream_t s) {
   if (m.nslivers >= 0) return;
-  if (m.tile_cols >= (int64_t{1} << 28)) fail("FRDC: too many tile columns for the sliver view");
+  if (4 * m.tile_cols >= (int64_t{1} << 29)) fail("FRDC: too many node columns for the sliver view");
   const size_t n1 = static_cast<size_t>(m.rows) + 1;
   DevBuf cnt(n1 * 8), maxima(8);
   m.sliver_ptr.alloc(n1 * 8);

@@ -7,6 +7,9 @@
 
 // Device-resident FRDC matrix (ref: FrdcMatrix, bitsparse.hpp:26-60) plus the
 // per-node-row degree the aggregation kernels use for thresholds.
+constexpr int kSliverPad = 8;
+constexpr uint32_t kSliverSentinel = 0xFFFFFFF8u;  // node column 2^29-1, no extra bits
+
 struct bg_frdc {
   int64_t rows = 0, cols = 0, tile_rows = 0, tile_cols = 0, nnz = 0, nnz_bits = 0;
   int64_t max_deg = 0;
@@ -19,13 +22,15 @@ struct bg_frdc {
   bg::DevBuf tiles;    // u16[nnz]
   bg::DevBuf degree;   // i32[rows]
   // Node-major view of the same bit tiles, built once on first use
-  // (frdc_slivers): for node row i, the nonzero 1x4 nibbles of its tiles as
-  // u32 (tile_col << 4 | nibble), ascending tile column (the reference's walk
-  // order, kernels.cpp:218-234).  Nibble bit 3-c is local column c.
+  // (frdc_slivers): for node row i, one u32 per nonzero 1x4 nibble of its
+  // tiles, ascending tile column (the reference's walk order,
+  // kernels.cpp:218-234): (node column of the nibble's first bit) << 3 | mask
+  // of the following columns present (bit k-1 <-> first + k).  Each row is
+  // padded to a multiple of kSliverPad entries with kSliverSentinel.
   bg::DevBuf sliver_ptr;  // u64[rows + 1]
   bg::DevBuf slivers;     // u32[nslivers]
   int64_t nslivers = -1;  // -1: not built
-  int64_t max_sl_row = 0;      // most slivers in one node row
+  int64_t max_sl_row = 0;      // most entries (padded) in one node row
   int64_t max_extra_bits = 0;  // most (bits - slivers) in one node row
   const uint64_t* srp() const { return sliver_ptr.as<uint64_t>(); }
   const uint32_t* sl() const { return slivers.as<uint32_t>(); }

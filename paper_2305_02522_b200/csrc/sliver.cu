@@ -24,8 +24,12 @@ namespace {
 
 constexpr int kSlWarps = 8;
 
-// Column of the lowest set bit of a nibble (bit 3 - c is local column c).
-__device__ __forceinline__ uint32_t nib_col(uint32_t low) { return 4u - __ffs(low); }
+// base + a * b with one IMAD.WIDE.U32 (gather address of node a, row stride b bytes).
+__device__ __forceinline__ uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t base) {
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(base));
+  return r;
+}
 
 template <int G, int NP, bool OUTB>
 __global__ void __launch_bounds__(kSlWarps * 32)
@@ -39,41 +43,46 @@ __global__ void __launch_bounds__(kSlWarps * 32)
   const int g = lane % G, slot = lane / G;
   const int64_t word = static_cast<int64_t>(blockIdx.y) * G + g;
   const bool word_ok = word < xspw;
-  const uint32_t* xw = x + (word_ok ? word : 0);
-  const uint32_t xs = static_cast<uint32_t>(xspw);
+  const uint64_t xbase = reinterpret_cast<uint64_t>(x + (word_ok ? word : 0));
+  const uint32_t xsb = static_cast<uint32_t>(xspw) * 4;  // row stride in bytes
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   for (int64_t i = row0 + wid; i < row1; i += nw) {
     uint32_t P[NP];
 #pragma unroll
     for (int q = 0; q < NP; ++q) P[q] = 0;
-    const uint64_t e0 = srp[i], e1 = srp[i + 1];
-    for (uint64_t base = e0; base < e1; base += B) {
-      uint32_t rest[8], xv[8];
+    const uint64_t e0 = srp[i];
+    const uint32_t len = static_cast<uint32_t>(srp[i + 1] - e0);  // multiple of kSliverPad
+    const uint32_t* rowp = sl + e0 + slot;
+    for (uint32_t off = 0; off < len; off += B) {
+      const uint32_t mcount = min(8u, (len - off) / S);  // warp-uniform (len % 8 == 0, S | 8)
+      uint32_t ent[8], xv[8], ex = 0;
 #pragma unroll
       for (int m = 0; m < 8; ++m) {
-        const uint64_t e = base + slot + S * m;
-        const uint32_t ent = e < e1 ? ld_nc_u32(sl + e) : 0u;
-        const uint32_t nib = ent & 0xFu, low = nib & (0u - nib);
-        rest[m] = nib ^ low;
-        xv[m] = low ? __ldg(xw + ((ent >> 4) * 4 + nib_col(low)) * xs) : 0u;
-        rest[m] |= ent & ~0xFu;  // keep the column for the rare extra rounds
+        ent[m] = m < mcount ? ld_nc_u32(rowp + off + S * m) : kSliverSentinel;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(mad_wide(ent[m] >> 3, xsb, xbase));
+        xv[m] = 0u;
+        if (ent[m] != kSliverSentinel) xv[m] = __ldg(src);
+        ex |= ent[m];
       }
       hs_add8<NP>(P, xv);
       // nibbles holding several bits: at most three further rounds (rare)
+      if (__any_sync(0xFFFFFFFFu, (ex & 7u) != 0)) {
 #pragma unroll 1
-      for (int round = 1; round < 4; ++round) {
-        const uint32_t any = __ballot_sync(
-            0xFFFFFFFFu, ((rest[0] | rest[1] | rest[2] | rest[3] | rest[4] | rest[5] | rest[6] |
-                           rest[7]) & 0xFu) != 0);
-        if (any == 0) break;
+        for (int round = 0; round < 3; ++round) {
+          uint32_t left = 0;
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const uint32_t nib = rest[m] & 0xFu, low = nib & (0u - nib);
-          xv[m] = low ? __ldg(xw + ((rest[m] >> 4) * 4 + nib_col(low)) * xs) : 0u;
-          rest[m] ^= low;
+          for (int m = 0; m < 8; ++m) {
+            const uint32_t more = ent[m] & 7u;
+            const uint32_t k = __ffs(more);  // column first + k
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(mad_wide((ent[m] >> 3) + k, xsb, xbase));
+            xv[m] = more ? __ldg(src) : 0u;
+            ent[m] &= ~(more & (0u - more));
+            left |= ent[m] & 7u;
+          }
+          hs_add8<NP>(P, xv);
+          if (!__any_sync(0xFFFFFFFFu, left != 0)) break;
         }
-        hs_add8<NP>(P, xv);
       }
     }
     __syncwarp();
@@ -116,7 +125,7 @@ __global__ void __launch_bounds__(kSlWarps * 32)
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane % G, slot = lane / G;
-  const uint4* rw = reinterpret_cast<const uint4*>(rec) + g;
+  const uint64_t rbase = reinterpret_cast<uint64_t>(reinterpret_cast<const uint4*>(rec) + g);
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   for (int64_t i = row0 + wid; i < row1; i += nw) {
@@ -138,34 +147,38 @@ __global__ void __launch_bounds__(kSlWarps * 32)
         hi[w] += ((a >> 8) & 0x00FF00FFu) + ((b >> 8) & 0x00FF00FFu) + ((c >> 8) & 0x00FF00FFu);
       }
     };
-    const uint64_t e0 = srp[i], e1 = srp[i + 1];
-    for (uint64_t base = e0; base < e1; base += B) {
-      uint32_t rest[8];
+    const uint64_t e0 = srp[i];
+    const uint32_t len = static_cast<uint32_t>(srp[i + 1] - e0);  // multiple of kSliverPad
+    const uint32_t* rowp = sl + e0 + slot;
+    for (uint32_t off = 0; off < len; off += B) {
+      const uint32_t mcount = min(8u, (len - off) / S);  // warp-uniform
+      uint32_t ent[8], ex = 0;
       uint4 v[8];
 #pragma unroll
       for (int m = 0; m < 8; ++m) {
-        const uint64_t e = base + slot + S * m;
-        const uint32_t ent = e < e1 ? ld_nc_u32(sl + e) : 0u;
-        const uint32_t nib = ent & 0xFu, low = nib & (0u - nib);
-        rest[m] = (nib ^ low) | (ent & ~0xFu);
-        v[m] = low ? __ldg(rw + static_cast<size_t>((ent >> 4) * 4 + nib_col(low)) * (kRec / 4))
-                   : make_uint4(0u, 0u, 0u, 0u);
+        ent[m] = m < mcount ? ld_nc_u32(rowp + off + S * m) : kSliverSentinel;
+        const uint4* src = reinterpret_cast<const uint4*>(mad_wide(ent[m] >> 3, kRec * 4, rbase));
+        v[m] = make_uint4(0u, 0u, 0u, 0u);
+        if (ent[m] != kSliverSentinel) v[m] = __ldg(src);
+        ex |= ent[m];
       }
       consume(v);
+      if (__any_sync(0xFFFFFFFFu, (ex & 7u) != 0)) {
 #pragma unroll 1
-      for (int round = 1; round < 4; ++round) {
-        const uint32_t any = __ballot_sync(
-            0xFFFFFFFFu, ((rest[0] | rest[1] | rest[2] | rest[3] | rest[4] | rest[5] | rest[6] |
-                           rest[7]) & 0xFu) != 0);
-        if (any == 0) break;
+        for (int round = 0; round < 3; ++round) {
+          uint32_t left = 0;
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const uint32_t nib = rest[m] & 0xFu, low = nib & (0u - nib);
-          v[m] = low ? __ldg(rw + static_cast<size_t>((rest[m] >> 4) * 4 + nib_col(low)) * (kRec / 4))
-                     : make_uint4(0u, 0u, 0u, 0u);
-          rest[m] ^= low;
+          for (int m = 0; m < 8; ++m) {
+            const uint32_t more = ent[m] & 7u;
+            const uint32_t k = __ffs(more);
+            const uint4* src = reinterpret_cast<const uint4*>(mad_wide((ent[m] >> 3) + k, kRec * 4, rbase));
+            v[m] = more ? __ldg(src) : make_uint4(0u, 0u, 0u, 0u);
+            ent[m] &= ~(more & (0u - more));
+            left |= ent[m] & 7u;
+          }
+          consume(v);
+          if (!__any_sync(0xFFFFFFFFu, left != 0)) break;
         }
-        consume(v);
       }
     }
     __syncwarp();
@@ -290,17 +303,18 @@ __global__ void __launch_bounds__(256)
   double d[M];
 #pragma unroll
   for (int m = 0; m < M; ++m) d[m] = 0.0;
-  const uint64_t e1 = srp[i + 1];
-  for (uint64_t base = srp[i]; base < e1; base += 32) {
-    const uint64_t e = base + lane;
-    const uint32_t mine = e < e1 ? ld_nc_u32(sl + e) : 0u;
-    const int cnt = static_cast<int>(e1 - base < 32 ? e1 - base : 32);
+  const uint64_t e0 = srp[i];
+  const uint32_t len = static_cast<uint32_t>(srp[i + 1] - e0);
+  for (uint32_t base = 0; base < len; base += 32) {
+    const uint32_t mine = base + lane < len ? ld_nc_u32(sl + e0 + base + lane) : kSliverSentinel;
+    const int cnt = static_cast<int>(min(32u, len - base));
     for (int L = 0; L < cnt; ++L) {  // slivers in order, then columns in order
       const uint32_t ent = __shfl_sync(0xFFFFFFFFu, mine, L);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (!(ent & (8u >> c))) continue;
-        const int64_t j = 4 * static_cast<int64_t>(ent >> 4) + c;
+      if (ent == kSliverSentinel) continue;  // row padding (warp-uniform)
+      const uint32_t first = ent >> 3;
+      uint32_t more = ent & 7u, col = first;
+      for (;;) {
+        const int64_t j = col;
         const double w = cs ? static_cast<double>(__ldg(cs + j)) : 1.0;
 #pragma unroll
         for (int m = 0; m < M; ++m) {
@@ -314,6 +328,9 @@ __global__ void __launch_bounds__(256)
             }
           }
         }
+        if (!more) break;
+        col = first + __ffs(more);
+        more &= more - 1;
       }
     }
   }
@@ -338,8 +355,8 @@ int64_t grid_warps(int64_t rows) {
   return std::max<int64_t>(1, std::min<int64_t>(cdiv(rows, kSlWarps), static_cast<int64_t>(sm_count()) * 32));
 }
 
-// Most bits a slot lane can count: its share of the row's slivers (batches
-// of 8 per slot) plus every extra bit of multi-bit nibbles.
+// Most bits a slot lane can count: its share of the row's (padded) entries
+// (batches of 8 per slot) plus every extra bit of multi-bit nibbles.
 int64_t lane_bound(const bg_frdc& A, int S) {
   return (A.max_sl_row + 8 * S - 1) / (8 * S) * 8 + A.max_extra_bits;
 }

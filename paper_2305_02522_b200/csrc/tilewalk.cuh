@@ -27,7 +27,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 
 __device__ __forceinline__ uint32_t ld_nc_u32(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));  // read-only data: no volatile
   return v;
 }
 

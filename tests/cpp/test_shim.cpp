@@ -215,6 +215,7 @@ static void test_gpu() {
                       std::make_shared<const b::DenseMatrix>(W2)});
   m.layers.push_back({b::LayerKind::Softmax, {}});
   CHECK(b::validate_model(m).empty());
+  CHECK(std::string(b::layer_kind_name(b::LayerKind::GcnConv)) == "gcn_conv");
   b::RunTrace trace;
   std::vector<b::KernelTiming> timings;
   b::DenseMatrix out = b::run_model(m, X, &trace, &timings);
@@ -241,9 +242,9 @@ static void test_gpu() {
   b::DenseMatrix o1 = model.forward(X, &lg1), o2 = model.forward(X, &lg2);
   CHECK(o1 == out && o2 == out && lg1 == trace.logits && lg2 == lg1);
 
-  // layer failures: std::runtime_error("layer i (Kind): ...") (graphops.cpp:476-479)
+  // layer failures: std::runtime_error("layer i (kind): ...") (graphops.cpp:476-479)
   b::DenseMatrix Xbad = random_dense(&r, n, 69);
-  CHECK(throws<std::runtime_error>([&] { b::run_model(m, Xbad); }, "layer 0 (GcnConv): "));
+  CHECK(throws<std::runtime_error>([&] { b::run_model(m, Xbad); }, "layer 0 (gcn_conv): "));
   og_graph_free(&og);
   og_frdc_free(&oA);
 }

@@ -154,7 +154,8 @@ BMM_VARIANTS = [f"BMM.{a}{b}{c}" for a in "FB" for b in "FB" for c in "FB" if (a
 
 @pytest.mark.parametrize("wb", [32, 64])
 @pytest.mark.parametrize("v", BMM_VARIANTS)
-@pytest.mark.parametrize("mkn", [(1, 1, 1), (7, 13, 5), (40, 33, 21), (33, 602, 128), (65, 128, 41), (9, 70, 300)])
+@pytest.mark.parametrize("mkn", [(1, 1, 1), (7, 13, 5), (40, 33, 21), (33, 602, 128), (65, 128, 41), (9, 70, 300),
+                                 (257, 602, 128), (48, 31, 127), (130, 100, 47), (64, 1433, 64), (35, 64, 16)])
 def test_bmm_every_variant(v, wb, mkn):
     m, k, n = mkn
     rng = po.Rng(1000 + m + k + n)
@@ -176,7 +177,8 @@ BSPMM_VARIANTS = [f"BSpMM.{a}{b}{c}" for a in "FB" for b in "FB" for c in "FB"]
 @pytest.mark.parametrize("wb", [32, 64])
 @pytest.mark.parametrize("v", BSPMM_VARIANTS)
 @pytest.mark.parametrize("nef", [(5, 9, 3), (37, 150, 31), (64, 400, 33), (200, 4000, 40), (17, 40, 1),
-                                 (300, 30000, 128), (150, 3000, 70), (90, 800, 520)])
+                                 (300, 30000, 128), (150, 3000, 70), (90, 800, 520), (120, 2500, 300),
+                                 (64, 900, 250), (200, 1500, 1000)])
 def test_bspmm_every_variant(v, wb, nef):
     n, e, f = nef
     rng = po.Rng(2000 + n + e + f)
