@@ -42,6 +42,17 @@ typedef void* bg_stream; /* cudaStream_t; NULL = legacy default stream */
 const char* bg_last_error(void);
 int bg_version(void);
 
+/* ---- aggregation layout (process-wide tuning, like the OpenMP thread count
+ * of the reference; every layout gives identical results) ------------------
+ * AUTO picks per call: column windows staged in shared memory for dense
+ * graphs (BBB/BBF, 4-word rows), node-major slivers otherwise.  window_nodes
+ * = 0 keeps the default window size (tests use small windows).  Initial
+ * values come from env BG_AGGREGATION=auto|slivers|tiles|window and
+ * BG_WINDOW_NODES. */
+enum { BG_AGG_AUTO = 0, BG_AGG_SLIVERS = 1, BG_AGG_TILES = 2, BG_AGG_WINDOW = 3 };
+int bg_set_aggregation(int mode, int window_nodes);
+int bg_get_aggregation(int* mode, int* window_nodes);
+
 /* ---- device memory (so C/C++ hosts need no CUDA headers) ---------------- */
 enum { BG_COPY_H2D = 0, BG_COPY_D2H = 1, BG_COPY_D2D = 2 };
 int bg_device_count(int* count);

@@ -61,6 +61,8 @@ class KernelTiming(C.Structure):
     _fields_ = [("label", C.c_char * 64), ("ms", C.c_double)]
 
 
+AGG_AUTO, AGG_SLIVERS, AGG_TILES, AGG_WINDOW = 0, 1, 2, 3
+
 P = C.c_void_p
 I64 = C.c_int64
 I32 = C.c_int
@@ -70,6 +72,8 @@ PI64 = C.POINTER(C.c_int64)
 PROTOTYPES = {
     "bg_last_error": (C.c_char_p, []),
     "bg_version": (I32, []),
+    "bg_set_aggregation": (I32, [I32, I32]),
+    "bg_get_aggregation": (I32, [C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "bg_device_count": (I32, [C.POINTER(C.c_int)]),
     "bg_device_alloc": (I32, [C.c_size_t, C.POINTER(C.c_void_p)]),
     "bg_device_free": (I32, [P]),

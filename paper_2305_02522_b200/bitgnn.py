@@ -35,6 +35,19 @@ def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+def set_aggregation(mode: int, window_nodes: int = 0) -> None:
+    """Process-wide aggregation layout (L.AGG_AUTO / AGG_SLIVERS / AGG_TILES /
+    AGG_WINDOW).  Every layout gives identical results; window_nodes > 0 sets
+    the shared-memory window size of the windowed BBB kernel (tests)."""
+    L.check(L.lib().bg_set_aggregation(int(mode), int(window_nodes)))
+
+
+def get_aggregation() -> Tuple[int, int]:
+    m, w = C.c_int(), C.c_int()
+    L.check(L.lib().bg_get_aggregation(C.byref(m), C.byref(w)))
+    return m.value, w.value
+
+
 def storage_words_per_row(cols: int, word_bits: int) -> int:
     return (cols + word_bits - 1) // word_bits * (word_bits // 32)
 

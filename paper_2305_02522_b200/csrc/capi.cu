@@ -57,6 +57,17 @@ extern "C" {
 const char* bg_last_error(void) { return bg::g_last_error.c_str(); }
 int bg_version(void) { return 100; }
 
+int bg_set_aggregation(int mode, int window_nodes) {
+  return guard([&] { set_aggregation(mode, window_nodes); });
+}
+
+int bg_get_aggregation(int* mode, int* window_nodes) {
+  return guard([&] {
+    if (mode) *mode = aggregation_mode();
+    if (window_nodes) *window_nodes = window_nodes_setting();
+  });
+}
+
 int bg_device_count(int* count) {
   return guard([&] {
     need(count, "output");
@@ -457,6 +468,7 @@ int bg_model_forward(bg_model* m, const bg_mat* x0, float* out, float* logits, b
     k.out = out;
     k.logits = logits;
     k.s = st;
+    k.agg_gen = aggregation_generation();
     if (m->exec && k == m->key) {
       BG_CUDA(cudaGraphLaunch(m->exec, st));
       return;

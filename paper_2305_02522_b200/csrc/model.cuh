@@ -69,9 +69,10 @@ struct bg_model {
     float* out = nullptr;
     float* logits = nullptr;
     cudaStream_t s = nullptr;
+    uint64_t agg_gen = 0;  // aggregation layout settings the graph was recorded with
     bool operator==(const Key& o) const {
       return x == o.x && rows == o.rows && cols == o.cols && prec == o.prec && wb == o.wb &&
-             out == o.out && logits == o.logits && s == o.s;
+             out == o.out && logits == o.logits && s == o.s && agg_gen == o.agg_gen;
     }
   } key;
   int key_runs = 0;

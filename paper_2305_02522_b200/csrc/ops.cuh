@@ -32,6 +32,17 @@ struct bg_frdc {
   int64_t nslivers = -1;  // -1: not built
   int64_t max_sl_row = 0;      // most entries (padded) in one node row
   int64_t max_extra_bits = 0;  // most (bits - slivers) in one node row
+  // Column-windowed view (window.cu), built once on first use: node rows in
+  // blocks of T (one CTA, one row per thread), node columns in windows of Wn
+  // (one shared-memory buffer).  Segment s = (block*nw + window)*(T/32) + warp
+  // holds the warp's entries of that window as ELL groups of 4 per lane:
+  // u16 index (column - window*Wn) at ell[(seg[s] + g)*128 + lane*4 + k],
+  // padded with Wn (a zero record after the window).
+  struct Windows {
+    int T = 0, Wn = 0, nw = 0, nb = 0;
+    bg::DevBuf seg;  // u32[nb*nw*(T/32) + 1], in 256-byte ELL groups
+    bg::DevBuf ell;  // u16
+  } win;
   const uint64_t* srp() const { return sliver_ptr.as<uint64_t>(); }
   const uint32_t* sl() const { return slivers.as<uint32_t>(); }
   const uint64_t* rp() const { return row_ptr.as<uint64_t>(); }
@@ -127,9 +138,22 @@ void sliver_gcn1_records(const uint32_t* h, int64_t n, int64_t K, int wb, const 
 void sliver_gcn1_aggregate(bg_frdc& A, const uint32_t* rec, int64_t K, int wb, const uint32_t* wt,
                            const float* beta, int64_t C, float* logits, float* probs,
                            cudaStream_t s, int64_t r0 = 0, int64_t r1 = -1);
-// Aggregation layout switch: true (default) = slivers, false = tile-row
-// walker (env BG_AGGREGATION=tiles); both produce identical results.
-bool use_slivers();
+// Aggregation layout (bg_set_aggregation; BG_AGG_* of bitgnn_b200.h).  All
+// layouts produce identical results.  aggregation_generation() changes on
+// every set, so captured CUDA graphs are re-recorded.
+int aggregation_mode();
+int window_nodes_setting();  // 0 = default window size
+uint64_t aggregation_generation();
+void set_aggregation(int mode, int window_nodes);
+inline bool use_slivers() { return aggregation_mode() != BG_AGG_TILES; }
+
+// ---- window.cu: BSpMM.BBB/BBF with the packed operand staged in shared
+// memory one column window at a time (bulk async copies), for graphs dense
+// enough that streaming the operand costs less than per-edge L2 gathers.
+// Returns false (nothing launched) when the shape is not eligible or the mode
+// is SLIVERS/TILES; mode WINDOW skips the cost model (tests).
+bool window_bb(bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* out_bits,
+               float* out_f, cudaStream_t s, int64_t r0, int64_t r1);
 
 // ---- elementwise.cu ------------------------------------------------------
 void add_bbb(const uint32_t* a, const uint32_t* b, int64_t words, uint32_t* out, cudaStream_t s);

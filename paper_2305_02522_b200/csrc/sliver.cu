@@ -13,6 +13,7 @@
 //   k_sl_f         real-valued walk in ascending column order (exact double
 //                  accumulation order of the reference).
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <string>
 
@@ -402,6 +403,7 @@ void sliver_bb(bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* out_b
   if (r1 < 0) r1 = A.rows;
   const int64_t xspw = spw(f, wb);
   if (r1 <= r0 || xspw == 0) return;
+  if (window_bb(A, x, f, wb, out_bits, out_f, s, r0, r1)) return;
   frdc_slivers(A, s);
   const bool ob = out_bits != nullptr;
   if (xspw <= 4) {
@@ -459,11 +461,30 @@ void sliver_gcn1_aggregate(bg_frdc& A, const uint32_t* rec, int64_t K, int wb, c
 }  // namespace bg
 
 namespace bg {
-bool use_slivers() {
-  static const bool v = [] {
-    const char* e = std::getenv("BG_AGGREGATION");
-    return !(e && std::string(e) == "tiles");
-  }();
-  return v;
+namespace {
+int env_mode() {
+  const char* e = std::getenv("BG_AGGREGATION");
+  if (!e) return BG_AGG_AUTO;
+  const std::string v(e);
+  return v == "tiles" ? BG_AGG_TILES : v == "slivers" ? BG_AGG_SLIVERS : v == "window" ? BG_AGG_WINDOW : BG_AGG_AUTO;
+}
+int env_window_nodes() {
+  const char* e = std::getenv("BG_WINDOW_NODES");
+  return e && *e ? std::max(0, std::atoi(e)) : 0;
+}
+std::atomic<int> g_mode{env_mode()};
+std::atomic<int> g_window_nodes{env_window_nodes()};
+std::atomic<uint64_t> g_generation{0};
+}  // namespace
+
+int aggregation_mode() { return g_mode.load(std::memory_order_relaxed); }
+int window_nodes_setting() { return g_window_nodes.load(std::memory_order_relaxed); }
+uint64_t aggregation_generation() { return g_generation.load(std::memory_order_relaxed); }
+void set_aggregation(int mode, int window_nodes) {
+  if (mode < BG_AGG_AUTO || mode > BG_AGG_WINDOW) fail("aggregation mode must be one of BG_AGG_*");
+  if (window_nodes < 0 || window_nodes > 65535) fail("window_nodes must be in [0, 65535]");
+  g_mode.store(mode);
+  g_window_nodes.store(window_nodes);
+  g_generation.fetch_add(1);
 }
 }  // namespace bg
