@@ -28,9 +28,12 @@
 namespace bg {
 namespace {
 
-// 2 x (6911+1) x 16 B = 221 KB of shared memory; Wn + 1 a multiple of 8 keeps
-// the bank group of a record the same in both buffers (k_win_bankorder).
-constexpr int kWinDefaultNodes = 6911;
+// Window buffers share 221 KB of shared memory (13824 records); Wn + 1 a
+// multiple of 8 keeps the bank group of a record the same in every buffer
+// (k_win_bankorder).  2 buffers -> Wn = 6911.
+constexpr int kWinSmemRecords = 13824;
+constexpr int kWinMaxBuf = 4;
+constexpr int kWinDefaultBuffers = 2;
 constexpr int kWinRec = 16;
 constexpr int kWinMaxThreads = 576;  // 18 warps: <= 112 registers per thread             // bytes per packed node row (4 u32 words)
 
@@ -234,42 +237,36 @@ __device__ __forceinline__ void ripple(uint32_t (&P)[NP], uint32_t c, int q0) {
 }
 
 template <int NP, bool OUTB>
-__global__ void __launch_bounds__(kWinMaxThreads, 1)
-    k_win_bb(const uint32_t* __restrict__ seg, const uint16_t* __restrict__ ell, int nw, int Wn,
+__global__ void __launch_bounds__(NP <= 10 ? kWinMaxThreads : 480, 1)
+    k_win_bb(const uint32_t* __restrict__ seg, const uint16_t* __restrict__ ell, int nw, int Wn, int nbuf,
              int64_t rows, int64_t row0, int64_t row1, int b0, int b1,
              const int32_t* __restrict__ degree, const uint4* __restrict__ x, int64_t f,
              uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
   static_assert(NP >= 5, "two-level Harley-Seal needs planes 0..4");
-  extern __shared__ __align__(16) uint4 sbuf[];  // 2 windows of (Wn + 1) records
-  __shared__ __align__(8) uint64_t full[2];
-  __shared__ uint32_t done[2];  // warps finished with each buffer (monotone)
+  extern __shared__ __align__(16) uint4 sbuf[];  // nbuf windows of (Wn + 1) records
+  __shared__ __align__(8) uint64_t full[kWinMaxBuf];
+  __shared__ uint32_t done[kWinMaxBuf];  // warps finished with each buffer (monotone)
   const int tid = threadIdx.x, T = blockDim.x, nwarps = T >> 5, warp = tid >> 5, lane = tid & 31;
   const int stride = Wn + 1;
-  if (tid < 2) {
+  if (tid < nbuf) {
     sbuf[tid * stride + Wn] = make_uint4(0u, 0u, 0u, 0u);  // padding target
     done[tid] = 0;
+    mbar_init(&full[tid], 1);
   }
-  if (tid == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
+  if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   const int mine = b1 - b0 - static_cast<int>(blockIdx.x);
   const int nblk = mine > 0 ? (mine + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x) : 0;
   const int nsteps = nblk * nw;
   auto issue = [&](int step) {
-    const int w = step % nw;
+    const int w = step % nw, buf = step % nbuf;
     const int64_t n0 = static_cast<int64_t>(w) * Wn;
     const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(Wn), rows - n0)) * kWinRec;
-    uint64_t* b = &full[step & 1];
-    mbar_expect_tx(b, bytes);
-    bulk_g2s(sbuf + (step & 1) * stride, x + n0, bytes, b);
+    mbar_expect_tx(&full[buf], bytes);
+    bulk_g2s(sbuf + buf * stride, x + n0, bytes, &full[buf]);
   };
-  if (tid == 0) {
-    if (nsteps > 0) issue(0);
-    if (nsteps > 1) issue(1);
-  }
+  if (tid == 0)
+    for (int k = 0; k < nbuf && k < nsteps; ++k) issue(k);
   auto seg_of = [&](int step) -> int64_t {
     const int bi = step / nw, w = step - bi * nw;
     const int b = b0 + static_cast<int>(blockIdx.x) + bi * static_cast<int>(gridDim.x);
@@ -279,110 +276,114 @@ __global__ void __launch_bounds__(kWinMaxThreads, 1)
   const uint2 sent2 = make_uint2(sent, sent);
   const uint2* ell2 = reinterpret_cast<const uint2*>(ell) + lane;
   const uint32_t sbase = smem_addr(sbuf);
-  uint32_t P[4][NP], pend[4];
-  bool have = false;  // pend holds a weight-8 carry (warp-uniform)
-  // entries of the current step's first group pair, prefetched a step ahead
+  auto ld_group = [&](uint32_t g, uint32_t g1) { return g < g1 ? ld_nc_v2(ell2 + static_cast<size_t>(g) * 32) : sent2; };
+  uint32_t P[4][NP];
+  // 8 entries (two ELL groups): 8 LDS.128, Harley-Seal into planes 0..2 of
+  // every word, weight-8 carries out
+  auto batch = [&](uint32_t wbase, uint2 a, uint2 c, uint32_t (&e)[4]) {
+    const uint32_t pk[4] = {a.x, a.y, c.x, c.y};
+    uint4 v[8];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const uint32_t lo = wbase + ((pk[m] & 0xFFFFu) << 4);
+      const uint32_t hi = wbase + ((pk[m] >> 16) << 4);
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v[2 * m].x), "=r"(v[2 * m].y), "=r"(v[2 * m].z), "=r"(v[2 * m].w)
+                   : "r"(lo));
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v[2 * m + 1].x), "=r"(v[2 * m + 1].y), "=r"(v[2 * m + 1].z), "=r"(v[2 * m + 1].w)
+                   : "r"(hi));
+    }
+    uint32_t xw[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) xw[m] = v[m].x;
+    e[0] = hs8_low<NP>(P[0], xw);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) xw[m] = v[m].y;
+    e[1] = hs8_low<NP>(P[1], xw);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) xw[m] = v[m].z;
+    e[2] = hs8_low<NP>(P[2], xw);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) xw[m] = v[m].w;
+    e[3] = hs8_low<NP>(P[3], xw);
+  };
+  // the current step's first four ELL groups, prefetched a step ahead
   uint32_t g0 = 0, g1 = 0;
-  uint2 a = sent2, c = sent2;
+  uint2 q0 = sent2, q1 = sent2, q2 = sent2, q3 = sent2;
   if (nsteps > 0) {
     const int64_t s0 = seg_of(0);
     g0 = __ldg(seg + s0);
     g1 = __ldg(seg + s0 + 1);
-    if (g0 < g1) a = ld_nc_v2(ell2 + static_cast<size_t>(g0) * 32);
-    if (g0 + 1 < g1) c = ld_nc_v2(ell2 + static_cast<size_t>(g0 + 1) * 32);
+    q0 = ld_group(g0, g1);
+    q1 = ld_group(g0 + 1, g1);
+    q2 = ld_group(g0 + 2, g1);
+    q3 = ld_group(g0 + 3, g1);
   }
   for (int step = 0; step < nsteps; ++step) {
-    const int w = step % nw;
+    const int w = step % nw, buf = step % nbuf;
     if (w == 0) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        pend[q] = 0u;
+      for (int q = 0; q < 4; ++q)
 #pragma unroll
         for (int p = 0; p < NP; ++p) P[q][p] = 0u;
-      }
-      have = false;
     }
-    // segment bounds of the next step (independent of this window)
-    uint32_t ng0 = 0, ng1 = 0;
+    uint32_t ng0 = 0, ng1 = 0;  // segment bounds of the next step
     if (step + 1 < nsteps) {
       const int64_t sn = seg_of(step + 1);
       ng0 = __ldg(seg + sn);
       ng1 = __ldg(seg + sn + 1);
     }
-    mbar_wait(&full[step & 1], (step >> 1) & 1);
-    const uint32_t wbase = sbase + static_cast<uint32_t>((step & 1) * stride) * kWinRec;
-    for (uint32_t g = g0; g < g1; g += 2) {
-      uint2 na = sent2, nc = sent2;
-      if (g + 2 < g1) na = ld_nc_v2(ell2 + static_cast<size_t>(g + 2) * 32);
-      if (g + 3 < g1) nc = ld_nc_v2(ell2 + static_cast<size_t>(g + 3) * 32);
-      const uint32_t pk[4] = {a.x, a.y, c.x, c.y};
-      uint4 v[8];
+    mbar_wait(&full[buf], static_cast<uint32_t>(step / nbuf) & 1u);
+    const uint32_t wbase = sbase + static_cast<uint32_t>(buf * stride) * kWinRec;
+    uint32_t g = g0;
+    for (; g + 4 <= g1; g += 4) {
+      const uint2 n0 = ld_group(g + 4, g1), n1 = ld_group(g + 5, g1);
+      const uint2 n2 = ld_group(g + 6, g1), n3 = ld_group(g + 7, g1);
+      uint32_t eA[4], eB[4];
+      batch(wbase, q0, q1, eA);
+      batch(wbase, q2, q3, eB);
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const uint32_t lo = wbase + ((pk[m] & 0xFFFFu) << 4);
-        const uint32_t hi = wbase + ((pk[m] >> 16) << 4);
-        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(v[2 * m].x), "=r"(v[2 * m].y), "=r"(v[2 * m].z), "=r"(v[2 * m].w)
-                     : "r"(lo));
-        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(v[2 * m + 1].x), "=r"(v[2 * m + 1].y), "=r"(v[2 * m + 1].z),
-                       "=r"(v[2 * m + 1].w)
-                     : "r"(hi));
+      for (int q = 0; q < 4; ++q) {  // two weight-8 carries: CSA into plane 3, ripple from 4
+        const uint32_t s3 = P[q][3] ^ eA[q] ^ eB[q];
+        const uint32_t cy = maj3(P[q][3], eA[q], eB[q]);
+        P[q][3] = s3;
+        ripple<NP>(P[q], cy, 4);
       }
-      uint32_t e[4];
-      {
-        uint32_t xw[8];
-#pragma unroll
-        for (int m = 0; m < 8; ++m) xw[m] = v[m].x;
-        e[0] = hs8_low<NP>(P[0], xw);
-#pragma unroll
-        for (int m = 0; m < 8; ++m) xw[m] = v[m].y;
-        e[1] = hs8_low<NP>(P[1], xw);
-#pragma unroll
-        for (int m = 0; m < 8; ++m) xw[m] = v[m].z;
-        e[2] = hs8_low<NP>(P[2], xw);
-#pragma unroll
-        for (int m = 0; m < 8; ++m) xw[m] = v[m].w;
-        e[3] = hs8_low<NP>(P[3], xw);
-      }
-      if (have) {  // two weight-8 carries: CSA into plane 3, ripple from plane 4
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t s3 = P[q][3] ^ pend[q] ^ e[q];
-          const uint32_t cy = maj3(P[q][3], pend[q], e[q]);
-          P[q][3] = s3;
-          ripple<NP>(P[q], cy, 4);
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) pend[q] = e[q];
-      }
-      have = !have;
-      a = na;
-      c = nc;
+      q0 = n0;
+      q1 = n1;
+      q2 = n2;
+      q3 = n3;
     }
-    // prefetch the next step's first pair, then release this buffer; the
-    // last warp out refills it with the window two steps ahead
-    a = sent2;
-    c = sent2;
-    if (ng0 < ng1) a = ld_nc_v2(ell2 + static_cast<size_t>(ng0) * 32);
-    if (ng0 + 1 < ng1) c = ld_nc_v2(ell2 + static_cast<size_t>(ng0 + 1) * 32);
+    if (g < g1) {  // 1..3 groups left (the rest of q0..q3 is padding)
+      uint32_t eA[4];
+      batch(wbase, q0, q1, eA);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ripple<NP>(P[q], eA[q], 3);
+      if (g + 2 < g1) {
+        batch(wbase, q2, q3, eA);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ripple<NP>(P[q], eA[q], 3);
+      }
+    }
+    // prefetch the next step's first groups, then release this buffer; the
+    // last warp out refills it with the window nbuf steps ahead
+    q0 = ld_group(ng0, ng1);
+    q1 = ld_group(ng0 + 1, ng1);
+    q2 = ld_group(ng0 + 2, ng1);
+    q3 = ld_group(ng0 + 3, ng1);
     g0 = ng0;
     g1 = ng1;
     __syncwarp();
     if (lane == 0) {
-      const uint32_t prev = atomicAdd(&done[step & 1], 1u);
-      if (prev + 1 == static_cast<uint32_t>(nwarps) * static_cast<uint32_t>((step >> 1) + 1) &&
-          step + 2 < nsteps) {
+      const uint32_t prev = atomicAdd(&done[buf], 1u);
+      if (prev + 1 == static_cast<uint32_t>(nwarps) * static_cast<uint32_t>(step / nbuf + 1) &&
+          step + nbuf < nsteps) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(step + 2);
+        issue(step + nbuf);
       }
     }
     if (w == nw - 1) {
-      if (have) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) ripple<NP>(P[q], pend[q], 3);
-      }
       const int bi = step / nw;
       const int b = b0 + static_cast<int>(blockIdx.x) + bi * static_cast<int>(gridDim.x);
       const int64_t i = static_cast<int64_t>(b) * T + tid;
@@ -416,7 +417,16 @@ __global__ void __launch_bounds__(kWinMaxThreads, 1)
 
 bool window_forced() { return aggregation_mode() == BG_AGG_WINDOW; }
 
-size_t win_smem_bytes(int Wn) { return 2 * static_cast<size_t>(Wn + 1) * kWinRec; }
+size_t win_smem_bytes(int Wn, int nbuf) { return static_cast<size_t>(nbuf) * static_cast<size_t>(Wn + 1) * kWinRec; }
+
+int win_buffers() {
+  static const int v = [] {
+    const char* e = std::getenv("BG_WINDOW_BUFFERS");
+    const int n = e && *e ? std::atoi(e) : kWinDefaultBuffers;
+    return std::max(1, std::min(n, kWinMaxBuf));
+  }();
+  return v;
+}
 
 // Largest block (multiple of 32 threads) the kernel instance can run with the
 // given dynamic shared memory, one CTA per SM.
@@ -487,9 +497,11 @@ bool launch_win(bg_frdc& A, const uint32_t* x, int64_t f, uint32_t* ob, float* o
                 int64_t r1, cudaStream_t s) {
   auto kern = k_win_bb<NP, OUTB>;
   const int sms = sm_count();
-  const int Wn = std::max(1, std::min<int>(window_nodes_setting() > 0 ? std::min(window_nodes_setting(), kWinDefaultNodes) : kWinDefaultNodes,
+  const int nbuf = win_buffers();
+  const int wmax = kWinSmemRecords / nbuf / 8 * 8 - 1;
+  const int Wn = std::max(1, std::min<int>(window_nodes_setting() > 0 ? std::min(window_nodes_setting(), wmax) : wmax,
                                            static_cast<int>(A.cols)));
-  static const int tmax = max_threads(kern, win_smem_bytes(kWinDefaultNodes));  // per instance
+  static const int tmax = max_threads(kern, static_cast<size_t>(kWinSmemRecords) * kWinRec);  // per instance
   const int64_t waves = std::max<int64_t>(1, cdiv(A.rows, static_cast<int64_t>(sms) * tmax));
   const int T = static_cast<int>(std::min<int64_t>(
       tmax, cdiv(cdiv(A.rows, static_cast<int64_t>(sms) * waves), 32) * 32));
@@ -503,7 +515,7 @@ bool launch_win(bg_frdc& A, const uint32_t* x, int64_t f, uint32_t* ob, float* o
   const auto& W = A.win;
   const int b0 = static_cast<int>(r0 / T), b1 = static_cast<int>(cdiv(r1, T));
   const int grid = std::min(sms, b1 - b0);
-  kern<<<grid, T, win_smem_bytes(Wn), s>>>(W.seg.as<uint32_t>(), W.ell.as<uint16_t>(), W.nw, W.Wn, A.rows,
+  kern<<<grid, T, win_smem_bytes(Wn, nbuf), s>>>(W.seg.as<uint32_t>(), W.ell.as<uint16_t>(), W.nw, W.Wn, nbuf, A.rows,
                                            r0, r1, b0, b1, A.deg(), reinterpret_cast<const uint4*>(x), f, ob,
                                            of);
   BG_LAUNCH_CHECK();
