@@ -223,6 +223,7 @@ unsigned grid1(int64_t n, int bs = 256) { return static_cast<unsigned>(cdiv(n, b
 void frdc_finalize(bg_frdc& m, cudaStream_t s) {
   m.nslivers = -1;  // derived views are rebuilt on next use
   m.win.T = 0;
+  m.nbits_view = -1;
   m.degree.alloc(static_cast<size_t>(std::max<int64_t>(m.rows, 1)) * 4);
   BG_CUDA(cudaMemsetAsync(m.degree.p, 0, m.degree.bytes, s));
   DevBuf stats(16);

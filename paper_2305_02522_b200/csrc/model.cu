@@ -306,7 +306,7 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
             // logits without materializing the N x C intermediate (gcn_fused.cu).
             if (h.trace) h.bits(prefix + "mm.bin_w", l.w1.bits.as<uint32_t>(), l.w1.rows, l.w1.cols, l.w1.wb);
             const bg_frdc& A = *m.graph->structure;
-            auto* recs = static_cast<uint32_t*>(m.pool.get(static_cast<size_t>(A.cols) * 64));
+            auto* recs = static_cast<uint32_t*>(m.pool.get(static_cast<size_t>(A.cols + 1) * 64));  // + zero record
             h.begin(prefix + "mm[" + variant_name(mm) + "]");
             gcn1_records(cur.bits, A.cols, cur.cols, cur.wb, l.w1.wt.as<uint32_t>(),
                          l.w1.scale.as<float>(), l.w1.cols, recs, s);

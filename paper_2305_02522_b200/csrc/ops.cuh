@@ -9,6 +9,7 @@
 // per-node-row degree the aggregation kernels use for thresholds.
 constexpr int kSliverPad = 8;
 constexpr uint32_t kSliverSentinel = 0xFFFFFFF8u;  // node column 2^29-1, no extra bits
+constexpr int kBitPad = 64;
 
 struct bg_frdc {
   int64_t rows = 0, cols = 0, tile_rows = 0, tile_cols = 0, nnz = 0, nnz_bits = 0;
@@ -38,6 +39,13 @@ struct bg_frdc {
   // holds the warp's entries of that window as ELL groups of 4 per lane:
   // u16 index (column - window*Wn) at ell[(seg[s] + g)*128 + lane*4 + k],
   // padded with Wn (a zero record after the window).
+  // Bit-entry view (frdc_bitview), built once on first use: for node row i,
+  // the node column of every adjacency bit in ascending order (the
+  // reference's walk order), padded to a multiple of kBitPad entries with the
+  // column count (the index of the zero record the consumers append).
+  bg::DevBuf bit_ptr;   // u64[rows + 1]
+  bg::DevBuf bit_cols;  // u32
+  int64_t nbits_view = -1;  // -1: not built
   struct Windows {
     int T = 0, Wn = 0, nw = 0, nb = 0;
     bg::DevBuf seg;  // u32[nb*nw*(T/32) + 1], in 256-byte ELL groups
@@ -78,6 +86,7 @@ std::unique_ptr<bg_frdc> frdc_from_host(int64_t rows, int64_t cols, const uint64
                                         cudaStream_t s);
 void frdc_finalize(bg_frdc& m, cudaStream_t s);  // degree, nnz_bits, max_deg
 void frdc_slivers(bg_frdc& m, cudaStream_t s);   // build the node-major sliver view once
+void frdc_bitview(bg_frdc& m, cudaStream_t s);   // build the bit-entry view once (from slivers)
 std::unique_ptr<bg_graph> prepare_graph(const int64_t* src, const int64_t* dst, int64_t e,
                                         int64_t n, cudaStream_t s);
 
@@ -121,6 +130,7 @@ void bspmm_f(const bg_frdc& A, const SpmmFArgs& a, cudaStream_t s, int64_t row0 
              int64_t row1 = -1);
 
 // ---- gcn_fused.cu: MM.BBF + BSpMM.FBF (+ softmax) without materializing Y ----
+// rec_buf holds n + 1 64-byte records (the last one zero, for padding entries).
 bool gcn1_fused_supported(const bg_frdc& A, int64_t K, int wb, int64_t C);
 void gcn1_records(const uint32_t* h, int64_t n, int64_t K, int wb, const uint32_t* wt,
                   const float* beta, int64_t C, uint32_t* rec_buf, cudaStream_t s);

@@ -253,7 +253,7 @@ void forward_sharded(bg_model& m, const Op& x0, const std::vector<int64_t>& boun
               sh.allgather(cur.bits, sh.row_bytes(cur));
               cur_full = true;
             }
-            auto* recs = static_cast<uint32_t*>(m.pool.get(static_cast<size_t>(n) * 64));
+            auto* recs = static_cast<uint32_t*>(m.pool.get(static_cast<size_t>(n + 1) * 64));  // + zero record
             gcn1_records(cur.bits, n, cur.cols, cur.wb, l.w1.wt.as<uint32_t>(), l.w1.scale.as<float>(),
                          l.w1.cols, recs, s);
             Op o = sh.alloc_like(BG_F, l.w1.cols, m.wb);

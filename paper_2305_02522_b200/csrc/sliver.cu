@@ -7,8 +7,9 @@
 //   k_sl_bb        BSpMM.BBB / BBF: lanes (word g, slot s) gather word g of the
 //                  neighbour rows of 8 slivers per slot and count them with
 //                  Harley-Seal planes; epilogue as in bspmm.cu.
-//   k_sl_gcn1      fused layer-1 GCN (gcn_fused.cu): 64-byte records laid out
-//                  so every lane owns one h word and three q words -- all lanes
+//   k_bv_gcn1      fused layer-1 GCN (gcn_fused.cu) over the bit-entry view
+//                  (one column per adjacency bit): 64-byte records laid out so
+//                  every lane owns one h word and three q words -- all lanes
 //                  run the same Harley-Seal + SWAR code, no divergence.
 //   k_sl_f         real-valued walk in ascending column order (exact double
 //                  accumulation order of the reference).
@@ -16,6 +17,8 @@
 #include <atomic>
 #include <cstdlib>
 #include <string>
+
+#include <cub/cub.cuh>
 
 #include "ops.cuh"
 #include "tilewalk.cuh"
@@ -107,22 +110,31 @@ __global__ void __launch_bounds__(kSlWarps * 32)
   }
 }
 
-// ---- fused layer-1 GCN over slivers ----------------------------------------
+// ---- fused layer-1 GCN over the bit-entry view -----------------------------
 // Record of node j (16 words): word 4g = h word g, words 4g+1..4g+3 = bytes
-// q_jk + 32 of classes 12g .. 12g+11 (4 per word, little-endian).
+// q_jk + 32 of classes 12g .. 12g+11 (4 per word, little-endian).  Record
+// `cols` (one past the last node) is all zero: the view's padding entries
+// point there, so every load is unconditional and adds nothing.
 constexpr int kRec = 16;
 
 template <int NP>
 __global__ void __launch_bounds__(kSlWarps * 32)
-    k_sl_gcn1(const uint64_t* __restrict__ srp, const uint32_t* __restrict__ sl, int64_t row0,
+    k_bv_gcn1(const uint64_t* __restrict__ bp, const uint32_t* __restrict__ bc, int64_t row0,
               int64_t row1, const int32_t* __restrict__ degree, const uint32_t* __restrict__ rec,
               const uint32_t* __restrict__ wt, int hspw, int K, const float* __restrict__ beta,
               int C, float* __restrict__ logits, float* __restrict__ probs) {
   constexpr int G = 4, S = 8, B = 8 * S, NQ = NP + 3;
-  __shared__ uint32_t planes_all[kSlWarps][4][NQ];
   __shared__ int qsum_all[kSlWarps][48];
+  __shared__ int sw_all[kSlWarps][48];
   __shared__ uint32_t wt_s[48 * 4];
-  for (int t = threadIdx.x; t < C * hspw; t += blockDim.x) wt_s[t] = wt[t];
+  __shared__ int wpop_s[48];
+  for (int t = threadIdx.x; t < 48 * 4; t += blockDim.x) {
+    const int k = t >> 2, w = t & 3;
+    wt_s[t] = (k < C && w < hspw) ? wt[k * hspw + w] : 0u;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 48; k += blockDim.x)
+    wpop_s[k] = __popc(wt_s[4 * k]) + __popc(wt_s[4 * k + 1]) + __popc(wt_s[4 * k + 2]) + __popc(wt_s[4 * k + 3]);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane % G, slot = lane / G;
@@ -134,7 +146,16 @@ __global__ void __launch_bounds__(kSlWarps * 32)
 #pragma unroll
     for (int q = 0; q < NP; ++q) P[q] = 0;
     uint32_t lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-    auto consume = [&](const uint4 (&v)[8]) {
+    const uint64_t e0 = bp[i];
+    const uint32_t len = static_cast<uint32_t>(bp[i + 1] - e0);  // multiple of kBitPad
+    const uint32_t* rowp = bc + e0 + slot;
+    for (uint32_t off = 0; off < len; off += B) {
+      uint4 v[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const uint32_t col = ld_nc_u32(rowp + off + S * m);
+        v[m] = __ldg(reinterpret_cast<const uint4*>(mad_wide(col, kRec * 4, rbase)));
+      }
       uint32_t h[8];
 #pragma unroll
       for (int m = 0; m < 8; ++m) h[m] = v[m].x;
@@ -147,43 +168,9 @@ __global__ void __launch_bounds__(kSlWarps * 32)
         lo[w] += (a & 0x00FF00FFu) + (b & 0x00FF00FFu) + (c & 0x00FF00FFu);
         hi[w] += ((a >> 8) & 0x00FF00FFu) + ((b >> 8) & 0x00FF00FFu) + ((c >> 8) & 0x00FF00FFu);
       }
-    };
-    const uint64_t e0 = srp[i];
-    const uint32_t len = static_cast<uint32_t>(srp[i + 1] - e0);  // multiple of kSliverPad
-    const uint32_t* rowp = sl + e0 + slot;
-    for (uint32_t off = 0; off < len; off += B) {
-      const uint32_t mcount = min(8u, (len - off) / S);  // warp-uniform
-      uint32_t ent[8], ex = 0;
-      uint4 v[8];
-#pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        ent[m] = m < mcount ? ld_nc_u32(rowp + off + S * m) : kSliverSentinel;
-        const uint4* src = reinterpret_cast<const uint4*>(mad_wide(ent[m] >> 3, kRec * 4, rbase));
-        v[m] = make_uint4(0u, 0u, 0u, 0u);
-        if (ent[m] != kSliverSentinel) v[m] = __ldg(src);
-        ex |= ent[m];
-      }
-      consume(v);
-      if (__any_sync(0xFFFFFFFFu, (ex & 7u) != 0)) {
-#pragma unroll 1
-        for (int round = 0; round < 3; ++round) {
-          uint32_t left = 0;
-#pragma unroll
-          for (int m = 0; m < 8; ++m) {
-            const uint32_t more = ent[m] & 7u;
-            const uint32_t k = __ffs(more);
-            const uint4* src = reinterpret_cast<const uint4*>(mad_wide((ent[m] >> 3) + k, kRec * 4, rbase));
-            v[m] = more ? __ldg(src) : make_uint4(0u, 0u, 0u, 0u);
-            ent[m] &= ~(more & (0u - more));
-            left |= ent[m] & 7u;
-          }
-          consume(v);
-          if (!__any_sync(0xFFFFFFFFu, left != 0)) break;
-        }
-      }
     }
-    __syncwarp();
-    // slot reductions: h planes (bit-sliced butterfly) and q sums (16-bit lanes)
+    // slot reductions: h planes (bit-sliced butterfly; every lane of word g
+    // ends with the row's planes of word g) and q sums (16-bit lanes)
     uint32_t Q[NQ];
     slot_reduce<G, NP, NQ>(P, Q);
 #pragma unroll
@@ -194,8 +181,6 @@ __global__ void __launch_bounds__(kSlWarps * 32)
       }
     const int deg = __ldg(degree + i);
     if (slot == 0) {
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) planes_all[warp][g][q] = Q[q];
       const int bias = 32 * deg;
 #pragma unroll
       for (int w = 0; w < 3; ++w) {
@@ -206,10 +191,27 @@ __global__ void __launch_bounds__(kSlWarps * 32)
         qsum_all[warp][k0 + 3] = static_cast<int>(hi[w] >> 16) - bias;
       }
     }
+    // sum_b cnt_b over this lane's word, then over the four words
+    int sall = 0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) sall += __popc(Q[q]) << q;
+    sall += __shfl_xor_sync(0xFFFFFFFFu, sall, 1);
+    sall += __shfl_xor_sync(0xFFFFFFFFu, sall, 2);
+    // sum_b [w_kb] cnt_b = sum_q 2^q popc(w_k & Q_q): (class, word) pairs over
+    // the lanes -- lane (k%8, g) of pass k/8 -- then a sum over the 4 words
+    for (int k0 = 0; k0 < C; k0 += 8) {
+      const int k = k0 + (lane >> 2);
+      const uint32_t wk = wt_s[4 * min(k, 47) + g];
+      int t = 0;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) t += __popc(wk & Q[q]) << q;
+      t += __shfl_xor_sync(0xFFFFFFFFu, t, 1);
+      t += __shfl_xor_sync(0xFFFFFFFFu, t, 2);
+      if (g == 0 && k < C) sw_all[warp][k] = t;
+    }
     __syncwarp();
-    // Per class: sum_j dot_jk = 2*(2*sum_b [w_bk] cnt_b - sum_b cnt_b) - deg*(2*popc(w_k) - K),
-    // with sum_b [mask_b] cnt_b = sum_q 2^q popc(mask & Q_q); then the exact
-    // combination of gcn_fused.cu and the fused softmax.
+    // Per class: sum_j dot_jk = 2*(2*sw - sall) - deg*(2*popc(w_k) - K); then
+    // the exact combination of gcn_fused.cu and the fused softmax.
     float lg[2];
     double mx = -INFINITY;
 #pragma unroll
@@ -217,19 +219,8 @@ __global__ void __launch_bounds__(kSlWarps * 32)
       const int k = lane + 32 * pass;
       lg[pass] = -INFINITY;
       if (k < C) {
-        int64_t sw = 0, sall = 0;
-        int wpop = 0;
-        for (int w = 0; w < hspw; ++w) {
-          const uint32_t wk = wt_s[k * hspw + w];
-          wpop += __popc(wk);
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) {
-            const uint32_t pl = planes_all[warp][w][q];
-            sw += static_cast<int64_t>(__popc(wk & pl)) << q;
-            sall += static_cast<int64_t>(__popc(pl)) << q;
-          }
-        }
-        const int64_t sdot = 2 * (2 * sw - sall) - static_cast<int64_t>(deg) * (2 * wpop - K);
+        const int64_t sdot = 2 * (2 * static_cast<int64_t>(sw_all[warp][k]) - sall) -
+                             static_cast<int64_t>(deg) * (2 * wpop_s[k] - K);
         const float bk = beta[k];
         const int ex = ((__float_as_int(bk) >> 23) & 0xFF) - 127;
         const double two_u = ldexp(1.0, ex - 22);
@@ -257,12 +248,32 @@ __global__ void __launch_bounds__(kSlWarps * 32)
   }
 }
 
-// Record producer for k_sl_gcn1 (layout above); thread per (node, word).
+// Bit-entry view construction (frdc_bitview).
+__global__ void k_bv_count(const int32_t* __restrict__ deg, int64_t rows, unsigned long long* __restrict__ cnt) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < rows) cnt[i] = (static_cast<unsigned long long>(deg[i]) + kBitPad - 1) / kBitPad * kBitPad;
+}
+
+__global__ void k_bv_fill(const uint64_t* __restrict__ srp, const uint32_t* __restrict__ sl, int64_t rows,
+                          uint32_t pad, const unsigned long long* __restrict__ bp, uint32_t* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  uint64_t p = bp[i];
+  for_each_col(srp, sl, i, [&](uint32_t col) { out[p++] = col; });
+  for (; p < bp[i + 1]; ++p) out[p] = pad;
+}
+
+// Record producer for k_bv_gcn1 (layout above); thread per (node, word),
+// plus the zero record after the last node.
 __global__ void k_sl_gcn1_records(const uint32_t* __restrict__ h, int64_t rows, int hspw, int K,
                                   const uint32_t* __restrict__ wt, const float* __restrict__ beta,
                                   int C, uint32_t* __restrict__ rec) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= rows * kRec) return;
+  if (t >= (rows + 1) * kRec) return;
+  if (t >= rows * kRec) {
+    rec[t] = 0u;
+    return;
+  }
   const int64_t j = t / kRec;
   const int w = static_cast<int>(t % kRec);
   uint32_t hw[4] = {0, 0, 0, 0};
@@ -434,7 +445,7 @@ void sliver_f(bg_frdc& A, const SpmmFArgs& a, cudaStream_t s, int64_t r0, int64_
 
 void sliver_gcn1_records(const uint32_t* h, int64_t n, int64_t K, int wb, const uint32_t* wt,
                          const float* beta, int64_t C, uint32_t* rec, cudaStream_t s) {
-  k_sl_gcn1_records<<<static_cast<unsigned>(cdiv(n * kRec, 256)), 256, 0, s>>>(
+  k_sl_gcn1_records<<<static_cast<unsigned>(cdiv((n + 1) * kRec, 256)), 256, 0, s>>>(
       h, n, static_cast<int>(spw(K, wb)), static_cast<int>(K), wt, beta, static_cast<int>(C), rec);
   BG_LAUNCH_CHECK();
 }
@@ -444,18 +455,52 @@ void sliver_gcn1_aggregate(bg_frdc& A, const uint32_t* rec, int64_t K, int wb, c
                            cudaStream_t s, int64_t r0, int64_t r1) {
   if (r1 < 0) r1 = A.rows;
   if (r1 <= r0) return;
-  frdc_slivers(A, s);
-  const int64_t per_lane = lane_bound(A, 8);
+  frdc_bitview(A, s);
+  // a slot lane counts <= ceil(max_deg / 64) * 8 bits of its word
+  const int64_t per_lane = (A.max_deg + kBitPad - 1) / kBitPad * 8;
   const int hspw = static_cast<int>(spw(K, wb));
   auto go = [&](auto kern) {
     kern<<<static_cast<unsigned>(grid_warps(r1 - r0)), kSlWarps * 32, 0, s>>>(
-        A.srp(), A.sl(), r0, r1, A.deg(), rec, wt, hspw, static_cast<int>(K), beta,
-        static_cast<int>(C), logits, probs);
+        A.bit_ptr.as<uint64_t>(), A.bit_cols.as<uint32_t>(), r0, r1, A.deg(), rec, wt, hspw,
+        static_cast<int>(K), beta, static_cast<int>(C), logits, probs);
   };
-  if (per_lane < (1 << 7)) go(k_sl_gcn1<7>);
-  else if (per_lane < (1 << 10)) go(k_sl_gcn1<10>);
-  else go(k_sl_gcn1<13>);
+  if (per_lane < (1 << 7)) go(k_bv_gcn1<7>);
+  else if (per_lane < (1 << 10)) go(k_bv_gcn1<10>);
+  else go(k_bv_gcn1<13>);
   BG_LAUNCH_CHECK();
+}
+
+void frdc_bitview(bg_frdc& m, cudaStream_t s) {
+  if (m.nbits_view >= 0) return;
+  frdc_slivers(m, s);
+  const size_t n1 = static_cast<size_t>(m.rows) + 1;
+  DevBuf cnt(n1 * 8);
+  m.bit_ptr.alloc(n1 * 8);
+  BG_CUDA(cudaMemsetAsync(cnt.p, 0, cnt.bytes, s));
+  BG_CUDA(cudaMemsetAsync(m.bit_ptr.p, 0, m.bit_ptr.bytes, s));
+  if (m.rows > 0)
+    k_bv_count<<<static_cast<unsigned>(cdiv(m.rows, 256)), 256, 0, s>>>(m.deg(), m.rows,
+                                                                        cnt.as<unsigned long long>());
+  BG_LAUNCH_CHECK();
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, cnt.as<unsigned long long>(),
+                                m.bit_ptr.as<unsigned long long>() + 1, static_cast<int>(m.rows), s);
+  DevBuf tmp(std::max<size_t>(tmp_bytes, 1));
+  if (m.rows > 0)
+    cub::DeviceScan::InclusiveSum(tmp.p, tmp_bytes, cnt.as<unsigned long long>(),
+                                  m.bit_ptr.as<unsigned long long>() + 1, static_cast<int>(m.rows), s);
+  BG_LAUNCH_CHECK();
+  unsigned long long total = 0;
+  BG_CUDA(cudaMemcpyAsync(&total, m.bit_ptr.as<unsigned long long>() + m.rows, 8, cudaMemcpyDeviceToHost, s));
+  BG_CUDA(cudaStreamSynchronize(s));
+  m.bit_cols.alloc(std::max<size_t>(static_cast<size_t>(total) * 4, 4));
+  if (m.rows > 0)
+    k_bv_fill<<<static_cast<unsigned>(cdiv(m.rows, 256)), 256, 0, s>>>(
+        m.srp(), m.sl(), m.rows, static_cast<uint32_t>(m.cols), m.bit_ptr.as<unsigned long long>(),
+        m.bit_cols.as<uint32_t>());
+  BG_LAUNCH_CHECK();
+  BG_CUDA(cudaStreamSynchronize(s));
+  m.nbits_view = static_cast<int64_t>(total);
 }
 
 }  // namespace bg

@@ -14,6 +14,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "ops.cuh"
 
 namespace bg {
 
@@ -175,6 +176,19 @@ __device__ __forceinline__ uint32_t plane_count(const uint32_t (&Q)[NQ], int b) 
 #pragma unroll
   for (int q = 0; q < NQ; ++q) cnt |= ((Q[q] >> (31 - b)) & 1u) << q;
   return cnt;
+}
+
+// Calls fn(col) for every adjacency bit of node row i in ascending column
+// order (sliver entries are sorted; padding sentinels close the row).
+template <class Fn>
+__device__ __forceinline__ void for_each_col(const uint64_t* srp, const uint32_t* sl, int64_t i, Fn&& fn) {
+  for (uint64_t e = srp[i]; e < srp[i + 1]; ++e) {
+    const uint32_t ent = sl[e];
+    if (ent == kSliverSentinel) break;
+    const uint32_t first = ent >> 3;
+    fn(first);
+    for (uint32_t more = ent & 7u; more; more &= more - 1) fn(first + __ffs(more));
+  }
 }
 
 }  // namespace bg

@@ -73,19 +73,6 @@ __device__ __forceinline__ uint2 ld_nc_v2(const uint2* p) {
 
 // ---- view construction (build once) -----------------------------------------
 
-// Calls fn(col) for every adjacency bit of node row i in ascending column
-// order (sliver entries are sorted; padding sentinels close the row).
-template <class Fn>
-__device__ __forceinline__ void for_each_col(const uint64_t* srp, const uint32_t* sl, int64_t i, Fn&& fn) {
-  for (uint64_t e = srp[i]; e < srp[i + 1]; ++e) {
-    const uint32_t ent = sl[e];
-    if (ent == kSliverSentinel) break;
-    const uint32_t first = ent >> 3;
-    fn(first);
-    for (uint32_t more = ent & 7u; more; more &= more - 1) fn(first + __ffs(more));
-  }
-}
-
 // Thread per node row: entries per window (u16, row-major rows x nw).
 __global__ void k_win_count(const uint64_t* __restrict__ srp, const uint32_t* __restrict__ sl,
                             int64_t rows, int Wn, int nw, uint16_t* __restrict__ cnt) {
