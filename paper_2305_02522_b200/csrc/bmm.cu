@@ -14,6 +14,7 @@
 #include <cstdlib>
 
 #include "ops.cuh"
+#include "async.cuh"
 
 namespace bg {
 namespace {
@@ -199,6 +200,14 @@ __device__ __forceinline__ void mma_s8(int (&c)[4], const uint32_t (&a)[4], uint
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// Four fp32 values -> four +-1 bytes (element i in byte i): the x >= 0 nibble
+// is spread to bytes by one multiply, then 1 -> 0x01, 0 -> 0xFF.
+__device__ __forceinline__ uint32_t sign_bytes4(float x0, float x1, float x2, float x3) {
+  const uint32_t m = static_cast<uint32_t>(x0 >= 0.0f) | (static_cast<uint32_t>(x1 >= 0.0f) << 1) |
+                     (static_cast<uint32_t>(x2 >= 0.0f) << 2) | (static_cast<uint32_t>(x3 >= 0.0f) << 3);
+  return 0xFFFFFFFFu - 0xFEu * ((m * 0x00204081u) & 0x01010101u);
+}
+
 // Four fp32 values -> four +-1 bytes (element i in byte i); `valid` bytes past K are 0.
 __device__ __forceinline__ uint32_t sign_bytes(float x0, float x1, float x2, float x3) {
   return (x0 >= 0.0f ? 0x00000001u : 0x000000FFu) | (x1 >= 0.0f ? 0x00000100u : 0x0000FF00u) |
@@ -342,6 +351,194 @@ __global__ void __launch_bounds__(kImWarps * 32)
   }
 }
 
+// ---- TMA-fed FBB: the fp32 activation stream at HBM speed -------------------
+// A CTA of two teams of four warps walks 16-row tiles of X.  Each tile (16 x K
+// fp32, contiguous) arrives by one bulk async copy into a 3-deep ring; the
+// team converts it once to +-1 bytes in shared memory (the fp32 slot is then
+// refilled with the tile three ahead), and warp w of the team runs the
+// m16n8k32 s8 MMAs for output word w (columns 32w..32w+31) and packs
+// dot >= 0 into the word (kernels.cpp:166-171).  Weights are +-1 bytes in
+// shared memory for the whole kernel.
+// One ring slot per team: slot j % kFbbStages is only ever waited on by team
+// j % kFbbTeams, so each slot's mbarrier phases are consumed in order by the
+// team that refills it (a parity wait cannot tell use u from use u-2).
+constexpr int kFbbTeams = 3;
+constexpr int kFbbStages = kFbbTeams;
+
+template <int NW>  // output words per row (N <= 32*NW); one warp per word
+__global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
+    k_fbb_tma(const float* __restrict__ a_f, const uint32_t* __restrict__ wt, int64_t tiles, int k,
+              int kspw, int n, int ksteps, int ospw, uint32_t qmagic,
+              uint32_t* __restrict__ out_bits) {
+  extern __shared__ __align__(16) uint8_t fbb_smem[];
+  __shared__ __align__(8) uint64_t full[kFbbStages];
+  const int kpad = 32 * ksteps;
+  const int lda = kpad + 16;  // bytes; (lda/4) % 32 == 28 -> conflict-free fragments
+  const uint32_t tile_bytes = static_cast<uint32_t>(16 * k) * 4u;
+  float* ring = reinterpret_cast<float*>(fbb_smem);                                  // stages x 16 x k fp32
+  uint8_t* a8 = fbb_smem + static_cast<size_t>(kFbbStages) * tile_bytes;            // teams x 16 x lda
+  uint8_t* w8 = a8 + static_cast<size_t>(kFbbTeams) * 16 * lda;                // 32*NW x lda
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int team = warp / NW, wq = warp % NW, ttid = tid - team * NW * 32;
+  const int g = lane >> 2, t4 = lane & 3;
+  // weights as +-1 bytes (0 past K and for columns >= n): 4 weight bits ->
+  // 4 bytes by spreading the nibble and mapping 1 -> 0x01, 0 -> 0xFF
+  for (int o = warp; o < 32 * NW; o += blockDim.x >> 5)
+    for (int p4 = 4 * lane; p4 < kpad; p4 += 128) {
+      uint32_t v = 0;
+      if (o < n && p4 < k) {
+        const uint32_t word = __ldg(wt + static_cast<int64_t>(o) * kspw + (p4 >> 5));
+        const uint32_t nib = (word >> (28 - (p4 & 31))) & 0xFu;  // bit 3 <-> element p4
+        const uint32_t spread = ((nib >> 3) & 1u) | (((nib >> 2) & 1u) << 8) | (((nib >> 1) & 1u) << 16) |
+                                ((nib & 1u) << 24);
+        v = 0xFFFFFFFFu - 0xFEu * spread;
+        if (p4 + 4 > k) v &= 0xFFFFFFFFu >> (8 * (p4 + 4 - k));
+      }
+      *reinterpret_cast<uint32_t*>(w8 + o * lda + p4) = v;
+    }
+  // the activation tiles' padding columns [K, kpad) stay zero
+  for (int t = tid; t < kFbbTeams * 16 * (lda / 4); t += blockDim.x) reinterpret_cast<uint32_t*>(a8)[t] = 0u;
+  const int64_t my = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (tid == 0) {
+    for (int s = 0; s < kFbbStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int64_t j = 0; j < kFbbStages && j < my; ++j) {
+      const int64_t tile = blockIdx.x + j * gridDim.x;
+      mbar_expect_tx(&full[j], tile_bytes);
+      bulk_g2s(ring + j * (tile_bytes / 4), a_f + tile * 16 * static_cast<int64_t>(k), tile_bytes, &full[j]);
+    }
+  }
+  __syncthreads();
+  uint8_t* mine = a8 + team * 16 * lda;
+  const int nthr = NW * 32;
+  const uint32_t q = (k + 7) / 8, items = 16 * q;  // 8-column groups per row, per tile
+  const bool keven = (k & 1) == 0;
+  for (int64_t j = team; j < my; j += kFbbTeams) {
+    const int slot = static_cast<int>(j % kFbbStages);
+    const int64_t tile = blockIdx.x + j * gridDim.x;
+    mbar_wait(&full[slot], static_cast<uint32_t>(j / kFbbStages) & 1u);
+    // fp32 -> +-1 bytes (x >= 0 -> +1, bitdense.cpp:83).  Item t = (row r,
+    // 8-column group) with r = t / q (magic multiply); groups past K are
+    // never written (zeroed once above); the last group of a row is masked.
+    {
+      const float* src = ring + static_cast<size_t>(slot) * (tile_bytes / 4);
+      for (uint32_t t = ttid; t < items; t += nthr) {
+        const uint32_t r = __umulhi(t, qmagic);
+        const uint32_t c = 8 * (t - r * q);
+        const float* x = src + r * k + c;
+        float e[8];
+        if (keven) {
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const float2 p2 = *reinterpret_cast<const float2*>(x + 2 * h);
+            e[2 * h] = p2.x;
+            e[2 * h + 1] = p2.y;
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < 8; ++h) e[h] = x[h];
+        }
+        uint2 v;
+        v.x = sign_bytes4(e[0], e[1], e[2], e[3]);
+        v.y = sign_bytes4(e[4], e[5], e[6], e[7]);
+        if (c + 8 > static_cast<uint32_t>(k)) {
+          const int rem = k - static_cast<int>(c);  // 1..7 valid columns
+          v.x &= rem >= 4 ? 0xFFFFFFFFu : 0xFFFFFFFFu >> (8 * (4 - rem));
+          v.y &= rem <= 4 ? 0u : 0xFFFFFFFFu >> (8 * (8 - rem));
+        }
+        *reinterpret_cast<uint2*>(mine + r * lda + c) = v;
+      }
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(nthr) : "memory");
+    if (ttid == 0 && j + kFbbStages < my) {  // the fp32 slot is free: refill it
+      const int64_t nt = blockIdx.x + (j + kFbbStages) * gridDim.x;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&full[slot], tile_bytes);
+      bulk_g2s(ring + static_cast<size_t>(slot) * (tile_bytes / 4), a_f + nt * 16 * static_cast<int64_t>(k),
+               tile_bytes, &full[slot]);
+    }
+    int acc[4][4];
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) acc[jj][0] = acc[jj][1] = acc[jj][2] = acc[jj][3] = 0;
+    const uint8_t* ab = mine + g * lda + 4 * t4;
+    const uint8_t* bb = w8 + (32 * wq + g) * lda + 4 * t4;
+    for (int ks = 0; ks < ksteps; ++ks) {
+      uint32_t a[4];
+      a[0] = *reinterpret_cast<const uint32_t*>(ab + 32 * ks);
+      a[1] = *reinterpret_cast<const uint32_t*>(ab + 8 * lda + 32 * ks);
+      a[2] = *reinterpret_cast<const uint32_t*>(ab + 32 * ks + 16);
+      a[3] = *reinterpret_cast<const uint32_t*>(ab + 8 * lda + 32 * ks + 16);
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const uint8_t* bp = bb + 8 * jj * lda + 32 * ks;
+        mma_s8(acc[jj], a, *reinterpret_cast<const uint32_t*>(bp), *reinterpret_cast<const uint32_t*>(bp + 16));
+      }
+    }
+    // c0,c1: row g, columns 8jj+2t4, +1; c2,c3: row g+8; bit 31-c of word wq
+    uint32_t m0 = 0, m1 = 0;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int c = 8 * jj + 2 * t4;
+      if (acc[jj][0] >= 0) m0 |= 0x80000000u >> c;
+      if (acc[jj][1] >= 0) m0 |= 0x40000000u >> c;
+      if (acc[jj][2] >= 0) m1 |= 0x80000000u >> c;
+      if (acc[jj][3] >= 0) m1 |= 0x40000000u >> c;
+    }
+    m0 |= __shfl_xor_sync(0xFFFFFFFFu, m0, 1);
+    m0 |= __shfl_xor_sync(0xFFFFFFFFu, m0, 2);
+    m1 |= __shfl_xor_sync(0xFFFFFFFFu, m1, 1);
+    m1 |= __shfl_xor_sync(0xFFFFFFFFu, m1, 2);
+    if (32 * wq + 32 > n) {  // columns >= n: zero weights give dot 0 -> clear
+      const uint32_t keep = 32 * wq >= n ? 0u : tail_mask32(n);
+      m0 &= keep;
+      m1 &= keep;
+    }
+    const int64_t r0 = tile * 16 + g;
+    if (t4 == 0 && wq < ospw) {
+      out_bits[r0 * ospw + wq] = m0;
+      out_bits[(r0 + 8) * ospw + wq] = m1;
+    }
+    if (t4 == 1 && wq == 0)  // storage padding words of 64-bit rows
+      for (int w = NW; w < ospw; ++w) {
+        out_bits[r0 * ospw + w] = 0u;
+        out_bits[(r0 + 8) * ospw + w] = 0u;
+      }
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(nthr) : "memory");  // int8 tile reusable
+  }
+}
+
+// FBB through k_fbb_tma for the whole 16-row tiles; returns the rows done.
+int64_t fbb_tma(const BmmArgs& a, cudaStream_t s) {
+  if (a.a_f == nullptr || a.out_bits == nullptr || a.n > 128 || a.k <= 8 || std::getenv("BG_BMM_POPC")) return 0;
+  if (reinterpret_cast<uintptr_t>(a.a_f) % 16 != 0) return 0;
+  const int ksteps = static_cast<int>(cdiv(a.k, 32));
+  const int lda = 32 * ksteps + 16;
+  const int nw = static_cast<int>(cdiv(a.n, 32));
+  const int NW = nw <= 1 ? 1 : nw <= 2 ? 2 : 4;
+  const size_t smem = static_cast<size_t>(kFbbStages) * 16 * a.k * 4 + static_cast<size_t>(kFbbTeams) * 16 * lda +
+                      static_cast<size_t>(32 * NW) * lda;
+  if (smem > 227 * 1024 - 128) return 0;  // opt-in shared memory per block, less the static part
+  const int64_t tiles = a.rows / 16;
+  if (tiles == 0) return 0;
+  const int kspw = static_cast<int>(spw(a.k, a.wb));
+  const int ospw = static_cast<int>(spw(a.n, a.wb));
+  // t / q == umulhi(t, ceil(2^32 / q)) for t < 16 q: the error term t*(M*q - 2^32) < 16 q^2 < 2^32
+  const uint32_t q = static_cast<uint32_t>((a.k + 7) / 8);
+  const uint32_t qmagic = static_cast<uint32_t>(((uint64_t{1} << 32) + q - 1) / q);
+  auto go = [&](auto kern) {
+    BG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    const int64_t blocks = std::min<int64_t>(tiles, sm_count());
+    kern<<<static_cast<unsigned>(blocks), kFbbTeams * NW * 32, smem, s>>>(
+        a.a_f, a.wt, tiles, static_cast<int>(a.k), kspw, static_cast<int>(a.n), ksteps, ospw, qmagic,
+        a.out_bits);
+  };
+  if (NW == 1) go(k_fbb_tma<1>);
+  else if (NW == 2) go(k_fbb_tma<2>);
+  else go(k_fbb_tma<4>);
+  BG_LAUNCH_CHECK();
+  return tiles * 16;
+}
+
 bool imma_ok(const BmmArgs& a) {
   return a.a_f != nullptr && a.n <= 128 && a.k <= 8192 && std::getenv("BG_BMM_POPC") == nullptr;
 }
@@ -435,8 +632,20 @@ void bmm(const BmmArgs& a, cudaStream_t s) {
   if (a.rows == 0 || a.n == 0) return;
   const bool af = a.a_f != nullptr, ob = a.out_bits != nullptr;
   if (imma_ok(a)) {
-    if (ob) launch_imma<true>(a, s);
-    else launch_imma<false>(a, s);
+    if (ob) {
+      // whole 16-row tiles on the TMA-fed kernel, the rest on the direct one
+      const int64_t done = fbb_tma(a, s);
+      if (done < a.rows) {
+        BmmArgs rest = a;
+        rest.rows = a.rows - done;
+        rest.a_f = a.a_f + done * a.k;
+        rest.alpha = a.alpha ? a.alpha + done : nullptr;
+        rest.out_bits = a.out_bits + done * spw(a.n, a.wb);
+        launch_imma<true>(rest, s);
+      }
+    } else {
+      launch_imma<false>(a, s);
+    }
     return;
   }
   if (lanerow_ok(a)) {

@@ -264,10 +264,21 @@ __global__ void k_bv_fill(const uint64_t* __restrict__ srp, const uint32_t* __re
 }
 
 // Record producer for k_bv_gcn1 (layout above); thread per (node, word),
-// plus the zero record after the last node.
-__global__ void k_sl_gcn1_records(const uint32_t* __restrict__ h, int64_t rows, int hspw, int K,
-                                  const uint32_t* __restrict__ wt, const float* __restrict__ beta,
-                                  int C, uint32_t* __restrict__ rec) {
+// plus the zero record after the last node.  The weight bits and scales are
+// staged in shared memory once per block; the node's h words are one 16-byte
+// load shared by its 16 threads.
+__global__ void __launch_bounds__(256)
+    k_sl_gcn1_records(const uint32_t* __restrict__ h, int64_t rows, int hspw, int K,
+                      const uint32_t* __restrict__ wt, const float* __restrict__ beta, int C,
+                      uint32_t* __restrict__ rec, bool h_v4) {
+  __shared__ uint32_t wt_s[48 * 4];
+  __shared__ float beta_s[48];
+  for (int t = threadIdx.x; t < 48 * 4; t += blockDim.x) {
+    const int k = t >> 2, w = t & 3;
+    wt_s[t] = (k < C && w < hspw) ? wt[k * hspw + w] : 0u;
+  }
+  for (int k = threadIdx.x; k < 48; k += blockDim.x) beta_s[k] = k < C ? beta[k] : 1.0f;
+  __syncthreads();
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= (rows + 1) * kRec) return;
   if (t >= rows * kRec) {
@@ -277,20 +288,26 @@ __global__ void k_sl_gcn1_records(const uint32_t* __restrict__ h, int64_t rows, 
   const int64_t j = t / kRec;
   const int w = static_cast<int>(t % kRec);
   uint32_t hw[4] = {0, 0, 0, 0};
-  for (int q = 0; q < hspw; ++q) hw[q] = __ldg(h + j * hspw + q);
+  if (h_v4) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(h) + j);
+    hw[0] = v.x, hw[1] = v.y, hw[2] = v.z, hw[3] = v.w;
+  } else {
+    for (int q = 0; q < hspw; ++q) hw[q] = __ldg(h + j * hspw + q);
+  }
   const int g = w >> 2, part = w & 3;
   if (part == 0) {
     rec[t] = hw[g];
     return;
   }
   uint32_t out = 0;
+#pragma unroll
   for (int b = 0; b < 4; ++b) {
     const int k = 12 * g + 4 * (part - 1) + b;
     if (k >= C) break;
-    int diff = 0;
-    for (int q = 0; q < hspw; ++q) diff += __popc(hw[q] ^ __ldg(wt + k * hspw + q));
+    const int diff = __popc(hw[0] ^ wt_s[4 * k]) + __popc(hw[1] ^ wt_s[4 * k + 1]) +
+                     __popc(hw[2] ^ wt_s[4 * k + 2]) + __popc(hw[3] ^ wt_s[4 * k + 3]);
     const float fd = static_cast<float>(K - 2 * diff);  // exact
-    const float bk = __ldg(beta + k);
+    const float bk = beta_s[k];
     const float x = __fmul_rn(fd, bk);
     const float e = __fmaf_rn(fd, bk, -x);  // exact rounding error of the product
     const int ex = ((__float_as_int(bk) >> 23) & 0xFF) - 127;
@@ -445,8 +462,10 @@ void sliver_f(bg_frdc& A, const SpmmFArgs& a, cudaStream_t s, int64_t r0, int64_
 
 void sliver_gcn1_records(const uint32_t* h, int64_t n, int64_t K, int wb, const uint32_t* wt,
                          const float* beta, int64_t C, uint32_t* rec, cudaStream_t s) {
+  const int hspw = static_cast<int>(spw(K, wb));
+  const bool v4 = hspw == 4 && reinterpret_cast<uintptr_t>(h) % 16 == 0;
   k_sl_gcn1_records<<<static_cast<unsigned>(cdiv((n + 1) * kRec, 256)), 256, 0, s>>>(
-      h, n, static_cast<int>(spw(K, wb)), static_cast<int>(K), wt, beta, static_cast<int>(C), rec);
+      h, n, hspw, static_cast<int>(K), wt, beta, static_cast<int>(C), rec, v4);
   BG_LAUNCH_CHECK();
 }
 
