@@ -107,4 +107,32 @@ __device__ __forceinline__ T ldg(const T* p) {
   return __ldg(p);
 }
 
+// exp(d) for d <= 0 in double: Cody-Waite reduction d = n ln2 + r, |r| <=
+// ln2/2, degree-13 Taylor polynomial (truncation < 5e-18 relative), scale by
+// 2^n.  Within an ulp of libm's exp, far below the float rounding of the
+// probabilities.
+__device__ __forceinline__ double exp_nonpos(double d) {
+  if (!(d > -745.2)) return 0.0;  // underflow, -inf (and NaN propagates below)
+  const double n = rint(d * 1.4426950408889634);
+  double r = fma(n, -6.93147180369123816490e-01, d);
+  r = fma(n, -1.90821492927058770002e-10, r);
+  double p = 1.0 / 6227020800.0;  // 1/13!
+  p = fma(p, r, 1.0 / 479001600.0);
+  p = fma(p, r, 1.0 / 39916800.0);
+  p = fma(p, r, 1.0 / 3628800.0);
+  p = fma(p, r, 1.0 / 362880.0);
+  p = fma(p, r, 1.0 / 40320.0);
+  p = fma(p, r, 1.0 / 5040.0);
+  p = fma(p, r, 1.0 / 720.0);
+  p = fma(p, r, 1.0 / 120.0);
+  p = fma(p, r, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int ni = static_cast<int>(n);
+  if (ni >= -1022) return p * __longlong_as_double(static_cast<long long>(ni + 1023) << 52);
+  return ldexp(p, ni);  // subnormal results
+}
+
 }  // namespace bg

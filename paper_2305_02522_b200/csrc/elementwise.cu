@@ -1,6 +1,8 @@
 // Small glue kernels of the layer chain: ADD variants, ReLU, softmax, SAGE
 // mean fix-up, BatchNorm, SCL, dense MM.FFF and CONCAT.
 // ref: kernels.cpp:193-212, :560-668; graphops.cpp:89-97, :304-314, :337-386.
+#include <algorithm>
+
 #include "ops.cuh"
 
 namespace bg {
@@ -41,6 +43,63 @@ __global__ void k_relu(float* __restrict__ x, int64_t n) {
 }
 
 // Row softmax in double, sequential column order (graphops.cpp:372-386).
+// A warp stages 32 rows (contiguous) through shared memory with coalesced
+// loads/stores.  The order-sensitive parts -- the row max and the sequential
+// double sum -- run lane per row; exp(x - max) (cached as double, the value
+// the reference recomputes identically) and the division run element-parallel.
+constexpr int kSmWarps = 2;
+constexpr int kSmMaxCols = 48;
+
+__global__ void __launch_bounds__(kSmWarps * 32)
+    k_softmax_staged(const float* __restrict__ x, int64_t rows, int cols, float* __restrict__ o) {
+  __shared__ float buf[kSmWarps][32 * (kSmMaxCols + 1)];
+  __shared__ double ex[kSmWarps][32 * kSmMaxCols];
+  __shared__ double rmx[kSmWarps][32], rsum[kSmWarps][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ld = cols | 1;
+  float* b = buf[warp];
+  double* e = ex[warp];
+  for (int64_t r0 = (static_cast<int64_t>(blockIdx.x) * kSmWarps + warp) * 32; r0 < rows;
+       r0 += static_cast<int64_t>(gridDim.x) * kSmWarps * 32) {
+    const int nr = static_cast<int>(rows - r0 < 32 ? rows - r0 : 32);
+    const int n = nr * cols;
+    const float* src = x + r0 * cols;
+    for (int t = lane, r = 0, c = lane; t < n; t += 32) {  // (r, c) = divmod(t, cols)
+      while (c >= cols) c -= cols, ++r;
+      b[r * ld + c] = src[t];
+      c += 32;
+    }
+    __syncwarp();
+    if (lane < nr) {
+      const float* xr = b + lane * ld;
+      double mx = -INFINITY;
+      for (int j = 0; j < cols; ++j) mx = fmax(mx, static_cast<double>(xr[j]));
+      rmx[warp][lane] = mx;
+    }
+    __syncwarp();
+    for (int t = lane, r = 0, c = lane; t < n; t += 32) {
+      while (c >= cols) c -= cols, ++r;
+      e[r * cols + c] = exp_nonpos(static_cast<double>(b[r * ld + c]) - rmx[warp][r]);
+      c += 32;
+    }
+    __syncwarp();
+    if (lane < nr) {
+      const double* er = e + lane * cols;
+      double sum = 0.0;
+      for (int j = 0; j < cols; ++j) sum = __dadd_rn(sum, er[j]);
+      rsum[warp][lane] = __drcp_rn(sum);
+    }
+    __syncwarp();
+    float* dst = o + r0 * cols;
+    for (int t = lane, r = 0, c = lane; t < n; t += 32) {
+      while (c >= cols) c -= cols, ++r;
+      dst[t] = __double2float_rn(__dmul_rn(e[r * cols + c], rsum[warp][r]));
+      c += 32;
+    }
+    __syncwarp();
+  }
+}
+
 __global__ void k_softmax(const float* __restrict__ x, int64_t rows, int64_t cols,
                           float* __restrict__ o) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -158,7 +217,12 @@ void relu(float* x, int64_t n, cudaStream_t s) {
 
 void softmax_rows(const float* x, int64_t rows, int64_t cols, float* out, cudaStream_t s) {
   if (rows == 0) return;
-  k_softmax<<<grid1(rows, 128), 128, 0, s>>>(x, rows, cols, out);
+  if (cols >= 1 && cols <= kSmMaxCols && x != out) {
+    const int64_t blocks = std::min<int64_t>(cdiv(rows, kSmWarps * 32), static_cast<int64_t>(sm_count()) * 32);
+    k_softmax_staged<<<static_cast<unsigned>(blocks), kSmWarps * 32, 0, s>>>(x, rows, static_cast<int>(cols), out);
+  } else {
+    k_softmax<<<grid1(rows, 128), 128, 0, s>>>(x, rows, cols, out);
+  }
   BG_LAUNCH_CHECK();
 }
 

@@ -111,6 +111,23 @@ __global__ void __launch_bounds__(kSlWarps * 32)
 }
 
 // ---- fused layer-1 GCN over the bit-entry view -----------------------------
+// float(beta*sdot - 2u*q) with 2u = 2^(exp(beta)-22) (gcn_fused.cu), exactly.
+__device__ __forceinline__ float logit_of(float beta, int64_t sdot, int qsum) {
+  const uint32_t bb = __float_as_uint(beta);
+  const int e = static_cast<int>((bb >> 23) & 0xFF);
+  if (e == 0 || e == 0xFF) {  // zero/subnormal/inf/nan scale: plain double path
+    const double two_u = ldexp(1.0, e - 127 - 22);
+    return __double2float_rn(__dsub_rn(__dmul_rn(static_cast<double>(beta), static_cast<double>(sdot)),
+                                       __dmul_rn(two_u, static_cast<double>(qsum))));
+  }
+  const int64_t m = static_cast<int64_t>((bb & 0x7FFFFFu) | 0x800000u) * ((bb >> 31) ? -1 : 1);
+  const int64_t X = m * sdot - 2 * static_cast<int64_t>(qsum);
+  // float(X) * 2^(e-150): exact scaling unless the result leaves the normal range
+  const int sc = e - 150;
+  if (sc >= -126 && sc <= 127) return __ll2float_rn(X) * __int_as_float((sc + 127) << 23);
+  return __double2float_rn(ldexp(static_cast<double>(X), sc));
+}
+
 // Record of node j (16 words): word 4g = h word g, words 4g+1..4g+3 = bytes
 // q_jk + 32 of classes 12g .. 12g+11 (4 per word, little-endian).  Record
 // `cols` (one past the last node) is all zero: the view's padding entries
@@ -221,26 +238,22 @@ __global__ void __launch_bounds__(kSlWarps * 32)
       if (k < C) {
         const int64_t sdot = 2 * (2 * static_cast<int64_t>(sw_all[warp][k]) - sall) -
                              static_cast<int64_t>(deg) * (2 * wpop_s[k] - K);
-        const float bk = beta[k];
-        const int ex = ((__float_as_int(bk) >> 23) & 0xFF) - 127;
-        const double two_u = ldexp(1.0, ex - 22);
-        const double val = __dsub_rn(__dmul_rn(static_cast<double>(bk), static_cast<double>(sdot)),
-                                     __dmul_rn(two_u, static_cast<double>(qsum_all[warp][k])));
-        lg[pass] = __double2float_rn(val);
+        // beta*sdot - 2u*qsum = 2^(e-23) * (m_beta*sdot - 2*qsum): an exact
+        // integer below 2^41 (the reference's double sum is exact too), so one
+        // int64 -> float rounding reproduces float(d); the scale is exact.
+        lg[pass] = logit_of(beta[k], sdot, qsum_all[warp][k]);
         if (logits) logits[i * C + k] = lg[pass];
         mx = fmax(mx, static_cast<double>(lg[pass]));
       }
     }
-    // warp reductions run unconditionally (uniform control flow); only the
-    // stores depend on probs
+    if (probs) {  // kernel parameter: warp-uniform (the model path runs softmax as a layer)
 #pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
-    const double x0 = lane < C ? exp(static_cast<double>(lg[0]) - mx) : 0.0;
-    const double x1 = lane + 32 < C ? exp(static_cast<double>(lg[1]) - mx) : 0.0;
-    double sum = x0 + x1;
+      for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+      const double x0 = lane < C ? exp_nonpos(static_cast<double>(lg[0]) - mx) : 0.0;
+      const double x1 = lane + 32 < C ? exp_nonpos(static_cast<double>(lg[1]) - mx) : 0.0;
+      double sum = x0 + x1;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
-    if (probs) {
+      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
       if (lane < C) probs[i * C + lane] = __double2float_rn(x0 / sum);
       if (lane + 32 < C) probs[i * C + lane + 32] = __double2float_rn(x1 / sum);
     }
