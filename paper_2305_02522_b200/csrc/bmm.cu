@@ -365,9 +365,48 @@ __global__ void __launch_bounds__(kImWarps * 32)
 constexpr int kFbbTeams = 3;
 constexpr int kFbbStages = kFbbTeams;
 
+// fp32 -> +-1 bytes (x >= 0 -> +1, bitdense.cpp:83) of one 16-row tile into
+// the team's int8 tile.  Item t = (row r, 8-column group) with r = t / q
+// (magic multiply); groups past K are never written (zeroed once); the last
+// group of a row is masked; rows >= valid become zero.  GLOBAL: the source is
+// the operand itself (partial last tile), else the shared-memory ring slot.
+template <bool GLOBAL>
+__device__ __forceinline__ void fbb_convert(const float* __restrict__ src, int valid, int k, bool keven,
+                                            uint32_t items, uint32_t q, uint32_t qmagic, int ttid, int nthr,
+                                            int lda, uint8_t* __restrict__ mine) {
+  for (uint32_t t = ttid; t < items; t += nthr) {
+    const uint32_t r = __umulhi(t, qmagic);
+    const uint32_t c = 8 * (t - r * q);
+    uint2 v = make_uint2(0u, 0u);
+    if (!GLOBAL || static_cast<int>(r) < valid) {
+      const float* x = src + r * k + c;
+      float e[8];
+      if (keven && (!GLOBAL || c + 8 <= static_cast<uint32_t>(k))) {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const float2 p2 = *reinterpret_cast<const float2*>(x + 2 * h);
+          e[2 * h] = p2.x;
+          e[2 * h + 1] = p2.y;
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 8; ++h) e[h] = (!GLOBAL || c + h < static_cast<uint32_t>(k)) ? x[h] : 0.0f;
+      }
+      v.x = sign_bytes4(e[0], e[1], e[2], e[3]);
+      v.y = sign_bytes4(e[4], e[5], e[6], e[7]);
+      if (c + 8 > static_cast<uint32_t>(k)) {
+        const int rem = k - static_cast<int>(c);  // 1..7 valid columns
+        v.x &= rem >= 4 ? 0xFFFFFFFFu : 0xFFFFFFFFu >> (8 * (4 - rem));
+        v.y &= rem <= 4 ? 0u : 0xFFFFFFFFu >> (8 * (8 - rem));
+      }
+    }
+    *reinterpret_cast<uint2*>(mine + r * lda + c) = v;
+  }
+}
+
 template <int NW>  // output words per row (N <= 32*NW); one warp per word
 __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
-    k_fbb_tma(const float* __restrict__ a_f, const uint32_t* __restrict__ wt, int64_t tiles, int k,
+    k_fbb_tma(const float* __restrict__ a_f, const uint32_t* __restrict__ wt, int64_t rows, int k,
               int kspw, int n, int ksteps, int ospw, uint32_t qmagic,
               uint32_t* __restrict__ out_bits) {
   extern __shared__ __align__(16) uint8_t fbb_smem[];
@@ -398,12 +437,18 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
     }
   // the activation tiles' padding columns [K, kpad) stay zero
   for (int t = tid; t < kFbbTeams * 16 * (lda / 4); t += blockDim.x) reinterpret_cast<uint32_t*>(a8)[t] = 0u;
+  // 16-row tiles; a partial last tile (rows % 16) is converted straight from
+  // global memory (a bulk copy must be a multiple of 16 bytes and must not
+  // read past the operand).  It is the last tile of its CTA, so skipping its
+  // copy leaves no later use of that ring slot out of phase.
+  const int64_t tiles = (rows + 15) / 16, full_tiles = rows / 16;
   const int64_t my = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   if (tid == 0) {
     for (int s = 0; s < kFbbStages; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int64_t j = 0; j < kFbbStages && j < my; ++j) {
       const int64_t tile = blockIdx.x + j * gridDim.x;
+      if (tile >= full_tiles) break;
       mbar_expect_tx(&full[j], tile_bytes);
       bulk_g2s(ring + j * (tile_bytes / 4), a_f + tile * 16 * static_cast<int64_t>(k), tile_bytes, &full[j]);
     }
@@ -416,42 +461,20 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
   for (int64_t j = team; j < my; j += kFbbTeams) {
     const int slot = static_cast<int>(j % kFbbStages);
     const int64_t tile = blockIdx.x + j * gridDim.x;
-    mbar_wait(&full[slot], static_cast<uint32_t>(j / kFbbStages) & 1u);
+    const bool partial = tile >= full_tiles;
+    if (!partial) mbar_wait(&full[slot], static_cast<uint32_t>(j / kFbbStages) & 1u);
     // fp32 -> +-1 bytes (x >= 0 -> +1, bitdense.cpp:83).  Item t = (row r,
     // 8-column group) with r = t / q (magic multiply); groups past K are
     // never written (zeroed once above); the last group of a row is masked.
-    {
-      const float* src = ring + static_cast<size_t>(slot) * (tile_bytes / 4);
-      for (uint32_t t = ttid; t < items; t += nthr) {
-        const uint32_t r = __umulhi(t, qmagic);
-        const uint32_t c = 8 * (t - r * q);
-        const float* x = src + r * k + c;
-        float e[8];
-        if (keven) {
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const float2 p2 = *reinterpret_cast<const float2*>(x + 2 * h);
-            e[2 * h] = p2.x;
-            e[2 * h + 1] = p2.y;
-          }
-        } else {
-#pragma unroll
-          for (int h = 0; h < 8; ++h) e[h] = x[h];
-        }
-        uint2 v;
-        v.x = sign_bytes4(e[0], e[1], e[2], e[3]);
-        v.y = sign_bytes4(e[4], e[5], e[6], e[7]);
-        if (c + 8 > static_cast<uint32_t>(k)) {
-          const int rem = k - static_cast<int>(c);  // 1..7 valid columns
-          v.x &= rem >= 4 ? 0xFFFFFFFFu : 0xFFFFFFFFu >> (8 * (4 - rem));
-          v.y &= rem <= 4 ? 0u : 0xFFFFFFFFu >> (8 * (8 - rem));
-        }
-        *reinterpret_cast<uint2*>(mine + r * lda + c) = v;
-      }
-    }
+    if (!partial)
+      fbb_convert<false>(ring + static_cast<size_t>(slot) * (tile_bytes / 4), 16, k, keven, items, q, qmagic,
+                         ttid, nthr, lda, mine);
+    else
+      fbb_convert<true>(a_f + tile * 16 * static_cast<int64_t>(k), static_cast<int>(rows - tile * 16), k, keven,
+                        items, q, qmagic, ttid, nthr, lda, mine);
     asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(nthr) : "memory");
-    if (ttid == 0 && j + kFbbStages < my) {  // the fp32 slot is free: refill it
-      const int64_t nt = blockIdx.x + (j + kFbbStages) * gridDim.x;
+    const int64_t nt = blockIdx.x + (j + kFbbStages) * gridDim.x;
+    if (ttid == 0 && j + kFbbStages < my && nt < full_tiles) {  // the fp32 slot is free: refill it
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&full[slot], tile_bytes);
       bulk_g2s(ring + static_cast<size_t>(slot) * (tile_bytes / 4), a_f + nt * 16 * static_cast<int64_t>(k),
@@ -495,19 +518,19 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
     }
     const int64_t r0 = tile * 16 + g;
     if (t4 == 0 && wq < ospw) {
-      out_bits[r0 * ospw + wq] = m0;
-      out_bits[(r0 + 8) * ospw + wq] = m1;
+      if (r0 < rows) out_bits[r0 * ospw + wq] = m0;
+      if (r0 + 8 < rows) out_bits[(r0 + 8) * ospw + wq] = m1;
     }
     if (t4 == 1 && wq == 0)  // storage padding words of 64-bit rows
       for (int w = NW; w < ospw; ++w) {
-        out_bits[r0 * ospw + w] = 0u;
-        out_bits[(r0 + 8) * ospw + w] = 0u;
+        if (r0 < rows) out_bits[r0 * ospw + w] = 0u;
+        if (r0 + 8 < rows) out_bits[(r0 + 8) * ospw + w] = 0u;
       }
     asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(nthr) : "memory");  // int8 tile reusable
   }
 }
 
-// FBB through k_fbb_tma for the whole 16-row tiles; returns the rows done.
+// FBB through k_fbb_tma (all rows; 0 = not eligible, use the direct kernel).
 int64_t fbb_tma(const BmmArgs& a, cudaStream_t s) {
   if (a.a_f == nullptr || a.out_bits == nullptr || a.n > 128 || a.k <= 8 || std::getenv("BG_BMM_POPC")) return 0;
   if (reinterpret_cast<uintptr_t>(a.a_f) % 16 != 0) return 0;
@@ -518,8 +541,7 @@ int64_t fbb_tma(const BmmArgs& a, cudaStream_t s) {
   const size_t smem = static_cast<size_t>(kFbbStages) * 16 * a.k * 4 + static_cast<size_t>(kFbbTeams) * 16 * lda +
                       static_cast<size_t>(32 * NW) * lda;
   if (smem > 227 * 1024 - 128) return 0;  // opt-in shared memory per block, less the static part
-  const int64_t tiles = a.rows / 16;
-  if (tiles == 0) return 0;
+  const int64_t tiles = (a.rows + 15) / 16;
   const int kspw = static_cast<int>(spw(a.k, a.wb));
   const int ospw = static_cast<int>(spw(a.n, a.wb));
   // t / q == umulhi(t, ceil(2^32 / q)) for t < 16 q: the error term t*(M*q - 2^32) < 16 q^2 < 2^32
@@ -529,14 +551,14 @@ int64_t fbb_tma(const BmmArgs& a, cudaStream_t s) {
     BG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     const int64_t blocks = std::min<int64_t>(tiles, sm_count());
     kern<<<static_cast<unsigned>(blocks), kFbbTeams * NW * 32, smem, s>>>(
-        a.a_f, a.wt, tiles, static_cast<int>(a.k), kspw, static_cast<int>(a.n), ksteps, ospw, qmagic,
+        a.a_f, a.wt, a.rows, static_cast<int>(a.k), kspw, static_cast<int>(a.n), ksteps, ospw, qmagic,
         a.out_bits);
   };
   if (NW == 1) go(k_fbb_tma<1>);
   else if (NW == 2) go(k_fbb_tma<2>);
   else go(k_fbb_tma<4>);
   BG_LAUNCH_CHECK();
-  return tiles * 16;
+  return a.rows;
 }
 
 bool imma_ok(const BmmArgs& a) {
