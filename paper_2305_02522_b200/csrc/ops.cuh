@@ -33,12 +33,6 @@ struct bg_frdc {
   int64_t nslivers = -1;  // -1: not built
   int64_t max_sl_row = 0;      // most entries (padded) in one node row
   int64_t max_extra_bits = 0;  // most (bits - slivers) in one node row
-  // Column-windowed view (window.cu), built once on first use: node rows in
-  // blocks of T (one CTA, one row per thread), node columns in windows of Wn
-  // (one shared-memory buffer).  Segment s = (block*nw + window)*(T/32) + warp
-  // holds the warp's entries of that window as ELL groups of 4 per lane:
-  // u16 index (column - window*Wn) at ell[(seg[s] + g)*128 + lane*4 + k],
-  // padded with Wn (a zero record after the window).
   // Bit-entry view (frdc_bitview), built once on first use: for node row i,
   // the node column of every adjacency bit in ascending order (the
   // reference's walk order), padded to a multiple of kBitPad entries with the
@@ -46,10 +40,16 @@ struct bg_frdc {
   bg::DevBuf bit_ptr;   // u64[rows + 1]
   bg::DevBuf bit_cols;  // u32
   int64_t nbits_view = -1;  // -1: not built
+  // Column-windowed view (window.cu), built once on first use: node rows in
+  // blocks of T (one CTA, one row per thread), node columns in half-windows of
+  // Wn (one shared-memory ring slot).  Each warp of each block owns one stream
+  // of ELL groups (4 u16 entries per lane per 256-byte group) covering all nw
+  // steps in order: stream base seg[b*(T/32)+v], step lengths steplen[.. *nw + k].
   struct Windows {
     int T = 0, Wn = 0, nw = 0, nb = 0;
-    bg::DevBuf seg;  // u32[nb*nw*(T/32) + 1], in 256-byte ELL groups
-    bg::DevBuf ell;  // u16
+    bg::DevBuf seg;      // u32[nb*(T/32) + 1] stream bases, in ELL groups
+    bg::DevBuf steplen;  // u16[nb*(T/32)*nw] groups per step
+    bg::DevBuf ell;      // u16 entries
   } win;
   const uint64_t* srp() const { return sliver_ptr.as<uint64_t>(); }
   const uint32_t* sl() const { return slivers.as<uint32_t>(); }

@@ -2,41 +2,46 @@
 // emit loop :438-465): out(i,k) = 2*#{j in N(i): x_jk = 1} - deg_i.
 //
 // Why: the per-edge gather of a 16-byte packed neighbour row from L2 costs one
-// L1TEX wavefront per edge (ncu: k_sl_bb runs at 87% of L1TEX throughput), so
-// a dense graph is bound at ~1 edge/clk/SM no matter how the loads are shaped.
-// Here the packed operand is streamed through shared memory instead, one
-// column window of Wn node rows at a time (cp.async.bulk + mbarrier, double
-// buffered), and each edge becomes one 16-byte LDS.  The CTA owns a block of
-// T node rows, one per thread, whose bit-sliced counters stay in registers
-// for the whole sweep over the windows.  Counting is order-free integer work,
-// so the result equals the reference's TwoAndMinusPopc/IfElse/AndAndNot
-// strategies bit for bit.
+// L1TEX wavefront per edge (ncu: the gather kernel k_sl_bb runs at 87% of
+// L1TEX throughput), so a dense graph is bound at ~1 edge/clk/SM however the
+// loads are shaped.  Here the packed operand streams through shared memory
+// instead, one half-window of Wh node rows at a time (cp.async.bulk +
+// mbarrier, a ring of three 64 KB slots), and each edge becomes one 16-byte
+// LDS.  The CTA owns a block of T node rows, one per thread, whose
+// bit-sliced counters stay in registers for the whole sweep.  Counting is
+// order-free integer work, so the result equals the reference's
+// TwoAndMinusPopc / IfElse / AndAndNot strategies bit for bit.
 //
-// Adjacency layout (bg_frdc::Windows, ops.cuh): per (row block, window,
-// warp) an ELL segment of u16 window-local columns, 4 per lane per group, so a
-// warp's loop count is uniform and every entry load is a coalesced 8-byte
-// load; padding entries point at a zero record stored after the window.
+// Two-choice schedule: at step k the ring holds half-windows k and k+1, so an
+// edge into half k may be counted at step k-1 or k.  A warp's 32 rows share
+// one loop count per step (ELL segment), which would otherwise be the maximum
+// of 32 Poisson counts; the build-time schedule finishes half k at step k and
+// tops every lane up to that step's length with edges of half k+1, which
+// evens the lanes out (simulated slot fill 56% -> ~80% on Reddit-like graphs).
+//
+// Entry encoding: u16 = slot << 12 | (column - half*Wh), slot = half % 3, so
+// the shared address is base + entry * 16 with the slots 64 KB apart; padding
+// is kWinPad (slot 0, record 4095: a zero record).
 #include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cstdlib>
 #include <string>
 
+#include "async.cuh"
 #include "ops.cuh"
 #include "tilewalk.cuh"
-#include "async.cuh"
 
 namespace bg {
 namespace {
 
-// Window buffers share 221 KB of shared memory (13824 records); Wn + 1 a
-// multiple of 8 keeps the bank group of a record the same in every buffer
-// (k_win_bankorder).  2 buffers -> Wn = 6911.
-constexpr int kWinSmemRecords = 13824;
-constexpr int kWinMaxBuf = 4;
-constexpr int kWinDefaultBuffers = 2;
-constexpr int kWinRec = 16;
-constexpr int kWinMaxThreads = 576;  // 18 warps: <= 112 registers per thread             // bytes per packed node row (4 u32 words)
+constexpr int kWinRec = 16;             // bytes per packed node row (4 u32 words)
+constexpr int kSlotRec = 4096;          // records per ring slot (64 KB)
+constexpr int kSlots = 3;               // ring slots; half h lives in slot h % 3
+constexpr int kWinHalf = kSlotRec - 1;  // node rows per half-window (record 4095 stays zero)
+constexpr uint16_t kWinPad = kWinHalf;  // slot 0, record 4095
+constexpr int kWinMaxThreads = 576;     // 18 warps: <= 112 registers per thread
+constexpr size_t kWinSmem = static_cast<size_t>(kSlots) * kSlotRec * kWinRec;  // 192 KB
 
 __device__ __forceinline__ uint2 ld_nc_v2(const uint2* p) {
   uint2 v;
@@ -44,21 +49,25 @@ __device__ __forceinline__ uint2 ld_nc_v2(const uint2* p) {
   return v;
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
 // ---- view construction (build once) -----------------------------------------
 
-// Thread per node row: entries per window (u16, row-major rows x nw).
+// Thread per node row: entries per half-window (u16, row-major rows x nh).
 __global__ void k_win_count(const uint64_t* __restrict__ srp, const uint32_t* __restrict__ sl,
-                            int64_t rows, int Wn, int nw, uint16_t* __restrict__ cnt) {
+                            int64_t rows, int Wh, int nh, uint16_t* __restrict__ cnt) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= rows) return;
-  uint16_t* c = cnt + i * nw;
+  uint16_t* c = cnt + i * nh;
   int cur = -1;
   uint32_t run = 0;
   for_each_col(srp, sl, i, [&](uint32_t col) {
-    const int w = static_cast<int>(col / static_cast<uint32_t>(Wn));
-    if (w != cur) {
+    const int h = static_cast<int>(col / static_cast<uint32_t>(Wh));
+    if (h != cur) {
       if (cur >= 0) c[cur] = static_cast<uint16_t>(run);
-      cur = w;
+      cur = h;
       run = 0;
     }
     ++run;
@@ -66,25 +75,37 @@ __global__ void k_win_count(const uint64_t* __restrict__ srp, const uint32_t* __
   if (cur >= 0) c[cur] = static_cast<uint16_t>(run);
 }
 
-// Thread per segment: ELL groups = ceil(max entries of the warp's rows / 4).
-__global__ void k_win_seglen(const uint16_t* __restrict__ cnt, int64_t rows, int T, int nw,
-                             int64_t nseg, uint32_t* __restrict__ len) {
-  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (s > nseg) return;
-  if (s == nseg) {
-    len[s] = 0;
-    return;
+// Warp per (row block, warp of the block), lane per row: the two-choice
+// schedule.  Step k must finish what is left of half k; its length K is the
+// lanes' maximum of that, rounded up to a batch of 8 entries (two ELL
+// groups), and every lane fills the rest of K with the first edges of half
+// k+1.  Writes the per-step entry counts of each row (u16, rows x nh), the
+// step lengths in groups (u16, warp-major: [b][v][k]) and each warp stream's
+// total (for the scan of stream bases).
+__global__ void k_win_sched(const uint16_t* __restrict__ cnt, int64_t rows, int T, int nh, int64_t nbv,
+                            uint16_t* __restrict__ nk, uint16_t* __restrict__ steplen,
+                            uint32_t* __restrict__ total) {
+  const int64_t wv = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (wv >= nbv) return;
+  const int lane = threadIdx.x & 31, nwarps = T / 32;
+  const int64_t b = wv / nwarps;
+  const int v = static_cast<int>(wv % nwarps);
+  const int64_t i = b * T + v * 32 + lane;
+  const bool ok = i < rows;
+  uint32_t q0 = ok ? cnt[i * nh] : 0u, sum = 0;
+  for (int k = 0; k < nh; ++k) {
+    uint32_t m = q0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+    const uint32_t K = (m + 7) & ~7u;
+    const uint32_t c1 = (ok && k + 1 < nh) ? cnt[i * nh + k + 1] : 0u;
+    const uint32_t take1 = min(K - q0, c1);
+    if (ok) nk[i * nh + k] = static_cast<uint16_t>(q0 + take1);
+    q0 = c1 - take1;
+    if (lane == 0) steplen[wv * nh + k] = static_cast<uint16_t>(K / 4);
+    sum += K / 4;
   }
-  const int nwarps = T / 32;
-  const int64_t b = s / (static_cast<int64_t>(nw) * nwarps);
-  const int64_t r = s % (static_cast<int64_t>(nw) * nwarps);
-  const int w = static_cast<int>(r / nwarps), v = static_cast<int>(r % nwarps);
-  uint32_t k = 0;
-  for (int l = 0; l < 32; ++l) {
-    const int64_t i = b * T + v * 32 + l;
-    if (i < rows) k = max(k, static_cast<uint32_t>(cnt[i * nw + w]));
-  }
-  len[s] = (k + 3) / 4;
+  if (lane == 0) total[wv] = sum;
 }
 
 __global__ void k_fill_u16(uint16_t* __restrict__ p, int64_t n, uint16_t v) {
@@ -93,62 +114,60 @@ __global__ void k_fill_u16(uint16_t* __restrict__ p, int64_t n, uint16_t v) {
     p[t] = v;
 }
 
-// Thread per node row: scatter its columns into the ELL slots of its lane.
+// Thread per node row: its columns in order, nk[k] of them into step k's
+// segment (the step's share of half k, then of half k+1).  A warp's segments
+// are consecutive in its stream: stream base + the lengths of earlier steps.
 __global__ void k_win_fill(const uint64_t* __restrict__ srp, const uint32_t* __restrict__ sl,
-                           int64_t rows, int T, int Wn, int nw, const uint32_t* __restrict__ seg,
+                           int64_t rows, int T, int Wh, int nh, const uint16_t* __restrict__ nk,
+                           const uint32_t* __restrict__ sbase, const uint16_t* __restrict__ steplen,
                            uint16_t* __restrict__ ell) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= rows) return;
-  const int nwarps = T / 32;
-  const int64_t b = i / T;
-  const int v = static_cast<int>((i % T) / 32), lane = static_cast<int>(i % 32);
-  int cur = -1;
-  uint32_t k = 0;
-  uint64_t base = 0;
+  const int64_t wv = i / 32;  // = b * (T/32) + v (T is a multiple of 32)
+  const int lane = static_cast<int>(i % 32);
+  const uint16_t* n = nk + i * nh;
+  const uint16_t* sll = steplen + wv * nh;
+  int k = -1;
+  uint32_t left = 0, pos = 0;
+  uint64_t g = sbase[wv], base = 0;
   for_each_col(srp, sl, i, [&](uint32_t col) {
-    const int w = static_cast<int>(col / static_cast<uint32_t>(Wn));
-    if (w != cur) {
-      cur = w;
-      k = 0;
-      base = static_cast<uint64_t>(seg[(b * nw + w) * nwarps + v]) * 128 + lane * 4;
+    while (left == 0) {
+      if (k >= 0) g += sll[k];
+      ++k;
+      left = n[k];
+      pos = 0;
+      base = g * 128 + lane * 4;
     }
-    ell[base + (k >> 2) * 128 + (k & 3)] = static_cast<uint16_t>(col - static_cast<uint32_t>(w) * Wn);
-    ++k;
+    const uint32_t h = col / static_cast<uint32_t>(Wh);
+    ell[base + (pos >> 2) * 128 + (pos & 3)] =
+        static_cast<uint16_t>(((h % kSlots) << 12) | (col - h * static_cast<uint32_t>(Wh)));
+    ++pos;
+    --left;
   });
 }
 
 // Bank-aware slot order (build once).  An LDS.128 is served per quarter warp
 // (8 lanes, 128 bytes): lanes of a quarter whose records sit in the same
-// 16-byte bank group (record index mod 8, the window stride being a multiple
-// of 8 records) and differ in address cost an extra wavefront each.  Counting
-// is order-free, so each lane's entries may be permuted freely: thread per
-// (segment, quarter) fills slot k greedily with, per lane, an entry of a bank
-// group no other lane of the quarter uses in that slot (looking a bounded
-// distance ahead in the lane's list).
-__global__ void k_win_bankorder(const uint32_t* __restrict__ seg, int64_t nseg, int Wn,
-                                uint16_t* __restrict__ ell) {
+// 16-byte bank group (entry mod 8, the slots being 64 KB apart) and differ in
+// address cost an extra wavefront each.  Counting is order-free, so each
+// lane's entries within a segment may be permuted freely: position k is
+// filled greedily with, per lane, an entry of a bank group no other lane of
+// the quarter uses there (bounded look-ahead).  K entries per lane; q quarter.
+__device__ void bank_order_segment(uint16_t* __restrict__ segp, uint32_t K, int q) {
   constexpr int kLook = 48;
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= nseg * 4) return;
-  const int64_t s = t >> 2;
-  const int q = static_cast<int>(t & 3);
-  const uint64_t base = static_cast<uint64_t>(seg[s]) * 128;
-  const uint32_t K = (seg[s + 1] - seg[s]) * 4;
   if (K == 0) return;
-  auto at = [&](int l, uint32_t k) -> uint16_t& {
-    return ell[base + (k >> 2) * 128 + (8 * q + l) * 4 + (k & 3)];
-  };
+  auto at = [&](int l, uint32_t k) -> uint16_t& { return segp[(k >> 2) * 128 + (8 * q + l) * 4 + (k & 3)]; };
   uint32_t cnt[8];
   for (int l = 0; l < 8; ++l) {
     uint32_t c = 0;
-    while (c < K && at(l, c) != Wn) ++c;
+    while (c < K && at(l, c) != kWinPad) ++c;
     cnt[l] = c;
   }
-  const uint32_t sent_bit = 1u << (Wn & 7);
+  const uint32_t pad_bit = 1u << (kWinPad & 7);
   for (uint32_t k = 0; k < K; ++k) {
     uint32_t used = 0;
     for (int l = 0; l < 8; ++l)
-      if (cnt[l] <= k) used |= sent_bit;
+      if (cnt[l] <= k) used |= pad_bit;
     for (int l = 0; l < 8; ++l) {
       if (cnt[l] <= k) continue;
       const uint32_t end = min(cnt[l], k + kLook);
@@ -168,6 +187,20 @@ __global__ void k_win_bankorder(const uint32_t* __restrict__ seg, int64_t nseg, 
   }
 }
 
+// Thread per (warp stream, quarter): every step segment of the stream in turn.
+__global__ void k_win_bankorder(const uint32_t* __restrict__ sbase, const uint16_t* __restrict__ steplen,
+                                int64_t nbv, int nh, uint16_t* __restrict__ ell) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nbv * 4) return;
+  const int64_t wv = t >> 2;
+  uint64_t g = sbase[wv];
+  for (int k = 0; k < nh; ++k) {
+    const uint32_t len = steplen[wv * nh + k];
+    bank_order_segment(ell + g * 128, len * 4, static_cast<int>(t & 3));
+    g += len;
+  }
+}
+
 // ---- the aggregation kernel ---------------------------------------------------
 
 // Harley-Seal over 8 words into planes P[0..2]; returns the weight-8 carry.
@@ -184,6 +217,16 @@ __device__ __forceinline__ uint32_t hs8_low(uint32_t (&P)[NP], const uint32_t (&
   return e;
 }
 
+// Harley-Seal over 4 words into planes P[0..1]; returns the weight-4 carry.
+template <int NP>
+__device__ __forceinline__ uint32_t hs4_low(uint32_t (&P)[NP], const uint32_t (&x)[4]) {
+  uint32_t t1, t2, f, s;
+  s = P[0] ^ x[0] ^ x[1]; t1 = maj3(P[0], x[0], x[1]); P[0] = s;
+  s = P[0] ^ x[2] ^ x[3]; t2 = maj3(P[0], x[2], x[3]); P[0] = s;
+  s = P[1] ^ t1 ^ t2;     f = maj3(P[1], t1, t2);      P[1] = s;
+  return f;
+}
+
 // Ripple a carry word of weight 2^q0 into planes q0.. (counts stay < 2^NP).
 template <int NP>
 __device__ __forceinline__ void ripple(uint32_t (&P)[NP], uint32_t c, int q0) {
@@ -196,20 +239,26 @@ __device__ __forceinline__ void ripple(uint32_t (&P)[NP], uint32_t c, int q0) {
   }
 }
 
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
 template <int NP, bool OUTB>
 __global__ void __launch_bounds__(NP <= 10 ? kWinMaxThreads : 480, 1)
-    k_win_bb(const uint32_t* __restrict__ seg, const uint16_t* __restrict__ ell, int nw, int Wn, int nbuf,
-             int64_t rows, int64_t row0, int64_t row1, int b0, int b1,
+    k_win_bb(const uint32_t* __restrict__ sbase, const uint16_t* __restrict__ steplen,
+             const uint16_t* __restrict__ ell, int nh, int Wh,
+             int64_t xrows, int64_t row0, int64_t row1, int b0, int b1,
              const int32_t* __restrict__ degree, const uint4* __restrict__ x, int64_t f,
              uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
   static_assert(NP >= 5, "two-level Harley-Seal needs planes 0..4");
-  extern __shared__ __align__(16) uint4 sbuf[];  // nbuf windows of (Wn + 1) records
-  __shared__ __align__(8) uint64_t full[kWinMaxBuf];
-  __shared__ uint32_t done[kWinMaxBuf];  // warps finished with each buffer (monotone)
+  extern __shared__ __align__(16) uint4 sbuf[];  // kSlots x kSlotRec records
+  __shared__ __align__(8) uint64_t full[kSlots];
+  __shared__ uint32_t done[kSlots];  // warps finished with each slot (monotone)
   const int tid = threadIdx.x, T = blockDim.x, nwarps = T >> 5, warp = tid >> 5, lane = tid & 31;
-  const int stride = Wn + 1;
-  if (tid < nbuf) {
-    sbuf[tid * stride + Wn] = make_uint4(0u, 0u, 0u, 0u);  // padding target
+  if (tid < kSlots) {
+    sbuf[tid * kSlotRec + kWinHalf] = make_uint4(0u, 0u, 0u, 0u);  // zero record (padding target)
     done[tid] = 0;
     mbar_init(&full[tid], 1);
   }
@@ -217,42 +266,41 @@ __global__ void __launch_bounds__(NP <= 10 ? kWinMaxThreads : 480, 1)
   __syncthreads();
   const int mine = b1 - b0 - static_cast<int>(blockIdx.x);
   const int nblk = mine > 0 ? (mine + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x) : 0;
-  const int nsteps = nblk * nw;
-  auto issue = [&](int step) {
-    const int w = step % nw, buf = step % nbuf;
-    const int64_t n0 = static_cast<int64_t>(w) * Wn;
-    const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(Wn), rows - n0)) * kWinRec;
-    mbar_expect_tx(&full[buf], bytes);
-    bulk_g2s(sbuf + buf * stride, x + n0, bytes, &full[buf]);
+  const int nsteps = nblk * nh;  // one half-window per step; nh % 3 == 0
+  auto issue = [&](int H) {      // half H of this CTA's sequence into slot H % 3
+    const int64_t n0 = static_cast<int64_t>(H % nh) * Wh;
+    const int64_t nodes = min(static_cast<int64_t>(Wh), xrows - n0);
+    uint64_t* bar = &full[H % kSlots];
+    if (nodes > 0) {
+      const uint32_t bytes = static_cast<uint32_t>(nodes) * kWinRec;
+      mbar_expect_tx(bar, bytes);
+      bulk_g2s(sbuf + (H % kSlots) * kSlotRec, x + n0, bytes, bar);
+    } else {
+      mbar_arrive(bar);  // padding half: nothing to load
+    }
   };
   if (tid == 0)
-    for (int k = 0; k < nbuf && k < nsteps; ++k) issue(k);
-  auto seg_of = [&](int step) -> int64_t {
-    const int bi = step / nw, w = step - bi * nw;
-    const int b = b0 + static_cast<int>(blockIdx.x) + bi * static_cast<int>(gridDim.x);
-    return (static_cast<int64_t>(b) * nw + w) * nwarps + warp;
-  };
-  const uint32_t sent = static_cast<uint32_t>(Wn) | (static_cast<uint32_t>(Wn) << 16);
-  const uint2 sent2 = make_uint2(sent, sent);
+    for (int H = 0; H < kSlots && H < nsteps; ++H) issue(H);
+  const uint32_t pad2 = static_cast<uint32_t>(kWinPad) * 0x10001u;
+  const uint2 sent2 = make_uint2(pad2, pad2);
   const uint2* ell2 = reinterpret_cast<const uint2*>(ell) + lane;
-  const uint32_t sbase = smem_addr(sbuf);
-  auto ld_group = [&](uint32_t g, uint32_t g1) { return g < g1 ? ld_nc_v2(ell2 + static_cast<size_t>(g) * 32) : sent2; };
-  uint32_t P[4][NP];
-  // 8 entries (two ELL groups): 8 LDS.128, Harley-Seal into planes 0..2 of
-  // every word, weight-8 carries out
-  auto batch = [&](uint32_t wbase, uint2 a, uint2 c, uint32_t (&e)[4]) {
+  const uint32_t sb = smem_addr(sbuf);
+  // This warp's groups of the current row block form one stream [gp, ge)
+  // across all steps; four groups are kept in flight ahead of use.
+  uint32_t gp = 0, ge = 0, lenreg = 0;
+  int64_t wv = 0;
+  auto fetch = [&](uint32_t g) { return g < ge ? ld_nc_v2(ell2 + static_cast<size_t>(g) * 32) : sent2; };
+  uint2 f0 = sent2, f1 = sent2, f2 = sent2, f3 = sent2;
+  uint32_t P[4][NP], pend[4];
+  bool have = false;  // pend holds a weight-8 carry per word (warp-uniform)
+  // 8 entries: 8 LDS.128, Harley-Seal into planes 0..2 of each word -> weight-8 carries
+  auto batch8 = [&](uint2 a, uint2 c, uint32_t (&e)[4]) {
     const uint32_t pk[4] = {a.x, a.y, c.x, c.y};
     uint4 v[8];
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-      const uint32_t lo = wbase + ((pk[m] & 0xFFFFu) << 4);
-      const uint32_t hi = wbase + ((pk[m] >> 16) << 4);
-      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(v[2 * m].x), "=r"(v[2 * m].y), "=r"(v[2 * m].z), "=r"(v[2 * m].w)
-                   : "r"(lo));
-      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(v[2 * m + 1].x), "=r"(v[2 * m + 1].y), "=r"(v[2 * m + 1].z), "=r"(v[2 * m + 1].w)
-                   : "r"(hi));
+      v[2 * m] = lds128(sb + ((pk[m] & 0xFFFFu) << 4));
+      v[2 * m + 1] = lds128(sb + ((pk[m] >> 16) << 4));
     }
     uint32_t xw[8];
 #pragma unroll
@@ -268,83 +316,69 @@ __global__ void __launch_bounds__(NP <= 10 ? kWinMaxThreads : 480, 1)
     for (int m = 0; m < 8; ++m) xw[m] = v[m].w;
     e[3] = hs8_low<NP>(P[3], xw);
   };
-  // the current step's first four ELL groups, prefetched a step ahead
-  uint32_t g0 = 0, g1 = 0;
-  uint2 q0 = sent2, q1 = sent2, q2 = sent2, q3 = sent2;
-  if (nsteps > 0) {
-    const int64_t s0 = seg_of(0);
-    g0 = __ldg(seg + s0);
-    g1 = __ldg(seg + s0 + 1);
-    q0 = ld_group(g0, g1);
-    q1 = ld_group(g0 + 1, g1);
-    q2 = ld_group(g0 + 2, g1);
-    q3 = ld_group(g0 + 3, g1);
-  }
-  for (int step = 0; step < nsteps; ++step) {
-    const int w = step % nw, buf = step % nbuf;
-    if (w == 0) {
+  for (int S = 0; S < nsteps; ++S) {
+    const int k = S % nh;
+    if (k == 0) {
 #pragma unroll
       for (int q = 0; q < 4; ++q)
 #pragma unroll
         for (int p = 0; p < NP; ++p) P[q][p] = 0u;
+      have = false;
+      const int b = b0 + static_cast<int>(blockIdx.x) + (S / nh) * static_cast<int>(gridDim.x);
+      wv = static_cast<int64_t>(b) * nwarps + warp;
+      gp = __ldg(sbase + wv);
+      ge = __ldg(sbase + wv + 1);
+      f0 = fetch(gp);
+      f1 = fetch(gp + 1);
+      f2 = fetch(gp + 2);
+      f3 = fetch(gp + 3);
     }
-    uint32_t ng0 = 0, ng1 = 0;  // segment bounds of the next step
-    if (step + 1 < nsteps) {
-      const int64_t sn = seg_of(step + 1);
-      ng0 = __ldg(seg + sn);
-      ng1 = __ldg(seg + sn + 1);
-    }
-    mbar_wait(&full[buf], static_cast<uint32_t>(step / nbuf) & 1u);
-    const uint32_t wbase = sbase + static_cast<uint32_t>(buf * stride) * kWinRec;
-    uint32_t g = g0;
-    for (; g + 4 <= g1; g += 4) {
-      const uint2 n0 = ld_group(g + 4, g1), n1 = ld_group(g + 5, g1);
-      const uint2 n2 = ld_group(g + 6, g1), n3 = ld_group(g + 7, g1);
-      uint32_t eA[4], eB[4];
-      batch(wbase, q0, q1, eA);
-      batch(wbase, q2, q3, eB);
+    if ((k & 31) == 0) lenreg = k + lane < nh ? __ldg(steplen + wv * nh + k + lane) : 0u;
+    const uint32_t K = __shfl_sync(0xFFFFFFFFu, lenreg, k & 31);  // groups this step (even)
+    // halves S and S+1 resident (re-waiting a completed phase is a no-op: the
+    // slot of S+1 cannot be refilled before every warp has finished S+1)
+    mbar_wait(&full[S % kSlots], static_cast<uint32_t>(S / kSlots) & 1u);
+    if (S + 1 < nsteps) mbar_wait(&full[(S + 1) % kSlots], static_cast<uint32_t>((S + 1) / kSlots) & 1u);
+    for (uint32_t t = 0; t < K; t += 2) {
+      const uint2 a = f0, c = f1;
+      f0 = f2;
+      f1 = f3;
+      f2 = fetch(gp + 4);
+      f3 = fetch(gp + 5);
+      gp += 2;
+      uint32_t e[4];
+      batch8(a, c, e);
+      if (have) {  // two weight-8 carries: CSA into plane 3, ripple from plane 4
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {  // two weight-8 carries: CSA into plane 3, ripple from 4
-        const uint32_t s3 = P[q][3] ^ eA[q] ^ eB[q];
-        const uint32_t cy = maj3(P[q][3], eA[q], eB[q]);
-        P[q][3] = s3;
-        ripple<NP>(P[q], cy, 4);
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t s3 = P[q][3] ^ pend[q] ^ e[q];
+          const uint32_t cy = maj3(P[q][3], pend[q], e[q]);
+          P[q][3] = s3;
+          ripple<NP>(P[q], cy, 4);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pend[q] = e[q];
       }
-      q0 = n0;
-      q1 = n1;
-      q2 = n2;
-      q3 = n3;
+      have = !have;
     }
-    if (g < g1) {  // 1..3 groups left (the rest of q0..q3 is padding)
-      uint32_t eA[4];
-      batch(wbase, q0, q1, eA);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) ripple<NP>(P[q], eA[q], 3);
-      if (g + 2 < g1) {
-        batch(wbase, q2, q3, eA);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) ripple<NP>(P[q], eA[q], 3);
-      }
-    }
-    // prefetch the next step's first groups, then release this buffer; the
-    // last warp out refills it with the window nbuf steps ahead
-    q0 = ld_group(ng0, ng1);
-    q1 = ld_group(ng0 + 1, ng1);
-    q2 = ld_group(ng0 + 2, ng1);
-    q3 = ld_group(ng0 + 3, ng1);
-    g0 = ng0;
-    g1 = ng1;
+    // release half S; the last warp out refills its slot with half S + 3
     __syncwarp();
     if (lane == 0) {
-      const uint32_t prev = atomicAdd(&done[buf], 1u);
-      if (prev + 1 == static_cast<uint32_t>(nwarps) * static_cast<uint32_t>(step / nbuf + 1) &&
-          step + nbuf < nsteps) {
+      const uint32_t prev = atomicAdd(&done[S % kSlots], 1u);
+      if (prev + 1 == static_cast<uint32_t>(nwarps) * static_cast<uint32_t>(S / kSlots + 1) &&
+          S + kSlots < nsteps) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(step + nbuf);
+        issue(S + kSlots);
       }
     }
-    if (w == nw - 1) {
-      const int bi = step / nw;
+    if (k == nh - 1) {
+      if (have) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ripple<NP>(P[q], pend[q], 3);
+        have = false;
+      }
+      const int bi = S / nh;
       const int b = b0 + static_cast<int>(blockIdx.x) + bi * static_cast<int>(gridDim.x);
       const int64_t i = static_cast<int64_t>(b) * T + tid;
       if (i >= row0 && i < row1) {
@@ -364,10 +398,10 @@ __global__ void __launch_bounds__(NP <= 10 ? kWinMaxThreads : 480, 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             for (int bb = 0; bb < 32; ++bb) {
-              const int64_t k = 32 * q + bb;
-              if (k >= f) break;
-              out_f[i * f + k] = static_cast<float>(2 * static_cast<int64_t>(plane_count<NP>(P[q], bb)) -
-                                                    static_cast<int64_t>(deg));
+              const int64_t kk = 32 * q + bb;
+              if (kk >= f) break;
+              out_f[i * f + kk] = static_cast<float>(2 * static_cast<int64_t>(plane_count<NP>(P[q], bb)) -
+                                                     static_cast<int64_t>(deg));
             }
         }
       }
@@ -376,17 +410,6 @@ __global__ void __launch_bounds__(NP <= 10 ? kWinMaxThreads : 480, 1)
 }
 
 bool window_forced() { return aggregation_mode() == BG_AGG_WINDOW; }
-
-size_t win_smem_bytes(int Wn, int nbuf) { return static_cast<size_t>(nbuf) * static_cast<size_t>(Wn + 1) * kWinRec; }
-
-int win_buffers() {
-  static const int v = [] {
-    const char* e = std::getenv("BG_WINDOW_BUFFERS");
-    const int n = e && *e ? std::atoi(e) : kWinDefaultBuffers;
-    return std::max(1, std::min(n, kWinMaxBuf));
-  }();
-  return v;
-}
 
 // Largest block (multiple of 32 threads) the kernel instance can run with the
 // given dynamic shared memory, one CTA per SM.
@@ -403,52 +426,57 @@ int max_threads(K kern, size_t smem) {
   return t;
 }
 
-void build_windows(bg_frdc& A, int T, int Wn, cudaStream_t s) {
+void build_windows(bg_frdc& A, int T, int Wh, cudaStream_t s) {
   auto& W = A.win;
-  if (W.T == T && W.Wn == Wn) return;
+  if (W.T == T && W.Wn == Wh) return;
   frdc_slivers(A, s);
   const int64_t rows = A.rows;
-  const int nw = static_cast<int>(cdiv(A.cols, Wn));
+  const int nh = static_cast<int>(cdiv(cdiv(A.cols, Wh), kSlots) * kSlots);
   const int nb = static_cast<int>(cdiv(rows, T));
-  const int64_t nseg = static_cast<int64_t>(nb) * nw * (T / 32);
-  DevBuf cnt(static_cast<size_t>(std::max<int64_t>(rows * nw, 1)) * 2);
-  DevBuf len(static_cast<size_t>(nseg + 1) * 4);
-  W.seg.alloc(static_cast<size_t>(nseg + 1) * 4);
+  const int64_t nbv = static_cast<int64_t>(nb) * (T / 32);  // warp streams
+  DevBuf cnt(static_cast<size_t>(std::max<int64_t>(rows * nh, 1)) * 2);
+  DevBuf nk(static_cast<size_t>(std::max<int64_t>(rows * nh, 1)) * 2);
+  DevBuf total(static_cast<size_t>(nbv + 1) * 4);
+  W.seg.alloc(static_cast<size_t>(nbv + 1) * 4);
+  W.steplen.alloc(static_cast<size_t>(std::max<int64_t>(nbv * nh, 1)) * 2);
   BG_CUDA(cudaMemsetAsync(cnt.p, 0, cnt.bytes, s));
+  BG_CUDA(cudaMemsetAsync(total.p, 0, total.bytes, s));
   if (rows > 0)
-    k_win_count<<<static_cast<unsigned>(cdiv(rows, 256)), 256, 0, s>>>(A.srp(), A.sl(), rows, Wn, nw,
+    k_win_count<<<static_cast<unsigned>(cdiv(rows, 256)), 256, 0, s>>>(A.srp(), A.sl(), rows, Wh, nh,
                                                                        cnt.as<uint16_t>());
   BG_LAUNCH_CHECK();
-  k_win_seglen<<<static_cast<unsigned>(cdiv(nseg + 1, 256)), 256, 0, s>>>(cnt.as<uint16_t>(), rows, T, nw,
-                                                                          nseg, len.as<uint32_t>());
+  if (nbv > 0)
+    k_win_sched<<<static_cast<unsigned>(cdiv(nbv * 32, 256)), 256, 0, s>>>(
+        cnt.as<uint16_t>(), rows, T, nh, nbv, nk.as<uint16_t>(), W.steplen.as<uint16_t>(), total.as<uint32_t>());
   BG_LAUNCH_CHECK();
   size_t tmp_bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, len.as<uint32_t>(), W.seg.as<uint32_t>(),
-                                static_cast<int>(nseg + 1), s);
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, total.as<uint32_t>(), W.seg.as<uint32_t>(),
+                                static_cast<int>(nbv + 1), s);
   DevBuf tmp(std::max<size_t>(tmp_bytes, 1));
-  cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, len.as<uint32_t>(), W.seg.as<uint32_t>(),
-                                static_cast<int>(nseg + 1), s);
+  cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, total.as<uint32_t>(), W.seg.as<uint32_t>(),
+                                static_cast<int>(nbv + 1), s);
   BG_LAUNCH_CHECK();
   uint32_t groups = 0;
-  BG_CUDA(cudaMemcpyAsync(&groups, W.seg.as<uint32_t>() + nseg, 4, cudaMemcpyDeviceToHost, s));
+  BG_CUDA(cudaMemcpyAsync(&groups, W.seg.as<uint32_t>() + nbv, 4, cudaMemcpyDeviceToHost, s));
   BG_CUDA(cudaStreamSynchronize(s));
   const int64_t n16 = static_cast<int64_t>(groups) * 128;
   W.ell.alloc(static_cast<size_t>(std::max<int64_t>(n16, 8)) * 2);
   k_fill_u16<<<static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cdiv(n16, 256), 65536))), 256, 0, s>>>(
-      W.ell.as<uint16_t>(), n16, static_cast<uint16_t>(Wn));
+      W.ell.as<uint16_t>(), n16, kWinPad);
   BG_LAUNCH_CHECK();
   if (rows > 0)
-    k_win_fill<<<static_cast<unsigned>(cdiv(rows, 256)), 256, 0, s>>>(A.srp(), A.sl(), rows, T, Wn, nw,
-                                                                      W.seg.as<uint32_t>(), W.ell.as<uint16_t>());
+    k_win_fill<<<static_cast<unsigned>(cdiv(rows, 256)), 256, 0, s>>>(
+        A.srp(), A.sl(), rows, T, Wh, nh, nk.as<uint16_t>(), W.seg.as<uint32_t>(), W.steplen.as<uint16_t>(),
+        W.ell.as<uint16_t>());
   BG_LAUNCH_CHECK();
-  if (nseg > 0)
-    k_win_bankorder<<<static_cast<unsigned>(cdiv(nseg * 4, 128)), 128, 0, s>>>(W.seg.as<uint32_t>(), nseg, Wn,
-                                                                              W.ell.as<uint16_t>());
+  if (nbv > 0)
+    k_win_bankorder<<<static_cast<unsigned>(cdiv(nbv * 4, 128)), 128, 0, s>>>(
+        W.seg.as<uint32_t>(), W.steplen.as<uint16_t>(), nbv, nh, W.ell.as<uint16_t>());
   BG_LAUNCH_CHECK();
   BG_CUDA(cudaStreamSynchronize(s));
   W.T = T;
-  W.Wn = Wn;
-  W.nw = nw;
+  W.Wn = Wh;
+  W.nw = nh;
   W.nb = nb;
 }
 
@@ -457,11 +485,10 @@ bool launch_win(bg_frdc& A, const uint32_t* x, int64_t f, uint32_t* ob, float* o
                 int64_t r1, cudaStream_t s) {
   auto kern = k_win_bb<NP, OUTB>;
   const int sms = sm_count();
-  const int nbuf = win_buffers();
-  const int wmax = kWinSmemRecords / nbuf / 8 * 8 - 1;
-  const int Wn = std::max(1, std::min<int>(window_nodes_setting() > 0 ? std::min(window_nodes_setting(), wmax) : wmax,
+  const int Wh = std::max(1, std::min<int>(window_nodes_setting() > 0 ? std::min(window_nodes_setting(), kWinHalf)
+                                                                       : kWinHalf,
                                            static_cast<int>(A.cols)));
-  static const int tmax = max_threads(kern, static_cast<size_t>(kWinSmemRecords) * kWinRec);  // per instance
+  static const int tmax = max_threads(kern, kWinSmem);  // per instance
   const int64_t waves = std::max<int64_t>(1, cdiv(A.rows, static_cast<int64_t>(sms) * tmax));
   const int T = static_cast<int>(std::min<int64_t>(
       tmax, cdiv(cdiv(A.rows, static_cast<int64_t>(sms) * waves), 32) * 32));
@@ -471,13 +498,13 @@ bool launch_win(bg_frdc& A, const uint32_t* x, int64_t f, uint32_t* ob, float* o
     const double streamed = static_cast<double>(waves) * sms * static_cast<double>(A.cols) * kWinRec;
     if (A.nnz_bits < (int64_t{1} << 22) || streamed > 20.0 * static_cast<double>(A.nnz_bits)) return false;
   }
-  build_windows(A, T, Wn, s);
+  build_windows(A, T, Wh, s);
   const auto& W = A.win;
   const int b0 = static_cast<int>(r0 / T), b1 = static_cast<int>(cdiv(r1, T));
   const int grid = std::min(sms, b1 - b0);
-  kern<<<grid, T, win_smem_bytes(Wn, nbuf), s>>>(W.seg.as<uint32_t>(), W.ell.as<uint16_t>(), W.nw, W.Wn, nbuf, A.rows,
-                                           r0, r1, b0, b1, A.deg(), reinterpret_cast<const uint4*>(x), f, ob,
-                                           of);
+  kern<<<grid, T, kWinSmem, s>>>(W.seg.as<uint32_t>(), W.steplen.as<uint16_t>(), W.ell.as<uint16_t>(), W.nw, W.Wn,
+                                 A.cols, r0, r1, b0, b1,
+                                 A.deg(), reinterpret_cast<const uint4*>(x), f, ob, of);
   BG_LAUNCH_CHECK();
   return true;
 }
