@@ -286,11 +286,13 @@ __global__ void __launch_bounds__(NP <= 10 ? kWinMaxThreads : 480, 1)
   const uint2* ell2 = reinterpret_cast<const uint2*>(ell) + lane;
   const uint32_t sb = smem_addr(sbuf);
   // This warp's groups of the current row block form one stream [gp, ge)
-  // across all steps; four groups are kept in flight ahead of use.
+  // across all steps; eight groups are kept in flight ahead of use.
   uint32_t gp = 0, ge = 0, lenreg = 0;
   int64_t wv = 0;
   auto fetch = [&](uint32_t g) { return g < ge ? ld_nc_v2(ell2 + static_cast<size_t>(g) * 32) : sent2; };
-  uint2 f0 = sent2, f1 = sent2, f2 = sent2, f3 = sent2;
+  uint2 fq[8];  // groups gp .. gp+7 in flight
+#pragma unroll
+  for (int u = 0; u < 8; ++u) fq[u] = sent2;
   uint32_t P[4][NP], pend[4];
   bool have = false;  // pend holds a weight-8 carry per word (warp-uniform)
   // 8 entries: 8 LDS.128, Harley-Seal into planes 0..2 of each word -> weight-8 carries
@@ -316,8 +318,9 @@ __global__ void __launch_bounds__(NP <= 10 ? kWinMaxThreads : 480, 1)
     for (int m = 0; m < 8; ++m) xw[m] = v[m].w;
     e[3] = hs8_low<NP>(P[3], xw);
   };
+  int k = 0, slot = 0;  // S % nh, S % kSlots
+  uint32_t use = 0;     // S / kSlots
   for (int S = 0; S < nsteps; ++S) {
-    const int k = S % nh;
     if (k == 0) {
 #pragma unroll
       for (int q = 0; q < 4; ++q)
@@ -328,23 +331,24 @@ __global__ void __launch_bounds__(NP <= 10 ? kWinMaxThreads : 480, 1)
       wv = static_cast<int64_t>(b) * nwarps + warp;
       gp = __ldg(sbase + wv);
       ge = __ldg(sbase + wv + 1);
-      f0 = fetch(gp);
-      f1 = fetch(gp + 1);
-      f2 = fetch(gp + 2);
-      f3 = fetch(gp + 3);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) fq[u] = fetch(gp + u);
     }
     if ((k & 31) == 0) lenreg = k + lane < nh ? __ldg(steplen + wv * nh + k + lane) : 0u;
     const uint32_t K = __shfl_sync(0xFFFFFFFFu, lenreg, k & 31);  // groups this step (even)
-    // halves S and S+1 resident (re-waiting a completed phase is a no-op: the
-    // slot of S+1 cannot be refilled before every warp has finished S+1)
-    mbar_wait(&full[S % kSlots], static_cast<uint32_t>(S / kSlots) & 1u);
-    if (S + 1 < nsteps) mbar_wait(&full[(S + 1) % kSlots], static_cast<uint32_t>((S + 1) / kSlots) & 1u);
+    // halves S and S+1 resident: S was waited for at step S-1 (its slot
+    // cannot be refilled before every warp has finished step S)
+    if (S == 0) mbar_wait(&full[0], 0u);
+    if (S + 1 < nsteps) {
+      const int s1 = slot == kSlots - 1 ? 0 : slot + 1;
+      mbar_wait(&full[s1], (use + (slot == kSlots - 1)) & 1u);
+    }
     for (uint32_t t = 0; t < K; t += 2) {
-      const uint2 a = f0, c = f1;
-      f0 = f2;
-      f1 = f3;
-      f2 = fetch(gp + 4);
-      f3 = fetch(gp + 5);
+      const uint2 a = fq[0], c = fq[1];
+#pragma unroll
+      for (int u = 0; u < 6; ++u) fq[u] = fq[u + 2];
+      fq[6] = fetch(gp + 8);
+      fq[7] = fetch(gp + 9);
       gp += 2;
       uint32_t e[4];
       batch8(a, c, e);
@@ -365,14 +369,16 @@ __global__ void __launch_bounds__(NP <= 10 ? kWinMaxThreads : 480, 1)
     // release half S; the last warp out refills its slot with half S + 3
     __syncwarp();
     if (lane == 0) {
-      const uint32_t prev = atomicAdd(&done[S % kSlots], 1u);
-      if (prev + 1 == static_cast<uint32_t>(nwarps) * static_cast<uint32_t>(S / kSlots + 1) &&
-          S + kSlots < nsteps) {
+      const uint32_t prev = atomicAdd(&done[slot], 1u);
+      if (prev + 1 == static_cast<uint32_t>(nwarps) * (use + 1) && S + kSlots < nsteps) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue(S + kSlots);
       }
     }
-    if (k == nh - 1) {
+    const bool last = k == nh - 1;
+    if (++k == nh) k = 0;
+    if (++slot == kSlots) slot = 0, ++use;
+    if (last) {
       if (have) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) ripple<NP>(P[q], pend[q], 3);
