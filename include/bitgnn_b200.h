@@ -147,6 +147,17 @@ int bg_frdc_from_host(int64_t node_rows, int64_t node_cols, const uint64_t* row_
 int bg_frdc_info_get(const bg_frdc* m, bg_frdc_info* info);
 /* Copy the three FRDC arrays to HOST buffers (row_ptr: tile_rows+1, others nnz). */
 int bg_frdc_download(const bg_frdc* m, uint64_t* row_ptr, uint32_t* col_ind, uint16_t* tiles);
+/* FRDC container (ref: write_frdc / read_frdc, bitsparse.cpp:171-222; layout
+ * bitsparse.hpp:92-96): little-endian bytes identical to the reference writer.
+ * Format and I/O faults are BG_RUNTIME_ERROR with the reference's messages
+ * ("FRDC: bad magic", "FRDC: truncated file", ...); a payload that fails the
+ * FrdcMatrix checks is BG_INVALID_ARGUMENT.  Reads stage through pinned host
+ * memory straight to the device. */
+int bg_frdc_serialized_size(const bg_frdc* m, size_t* bytes);
+int bg_frdc_serialize(const bg_frdc* m, int word_bits, void* buf, size_t buf_len);
+int bg_frdc_deserialize(const void* buf, size_t len, bg_frdc** out, int* word_bits, bg_stream stream);
+int bg_frdc_write_file(const bg_frdc* m, int word_bits, const char* path);
+int bg_frdc_read_file(const char* path, bg_frdc** out, int* word_bits, bg_stream stream);
 /* Fault hook (ref: runreport.cpp:55-63): flip bit 0 of stored tile k % nnz. */
 int bg_frdc_corrupt_tile(bg_frdc* m, int64_t k);
 void bg_frdc_destroy(bg_frdc* m);

@@ -285,6 +285,27 @@ inline FrdcMatrix download(const bg_frdc* h) {
   return FrdcMatrix(info.node_rows, info.node_cols, std::move(rp), std::move(ci), std::move(ti));
 }
 
+// ref: FrdcFile / write_frdc / read_frdc (bitsparse.hpp:92-106): the container
+// bytes are produced and parsed by the library (reads go straight to the
+// device); I/O and format faults rethrow as std::runtime_error.
+struct FrdcFile {
+  FrdcMatrix matrix;
+  int word_bits = 32;
+};
+
+inline void write_frdc(const std::string& path, const FrdcMatrix& m, int word_bits = 32) {
+  FrdcHandle h = upload(m);
+  check(bg_frdc_write_file(h.get(), word_bits, path.c_str()));
+}
+
+inline FrdcFile read_frdc(const std::string& path) {
+  bg_frdc* h = nullptr;
+  int wb = 32;
+  check(bg_frdc_read_file(path.c_str(), &h, &wb, nullptr));
+  FrdcHandle owned(h);
+  return {download(owned.get()), wb};
+}
+
 struct Edges {
   DeviceBuffer src, dst;
   int64_t n = 0, e = 0;

@@ -93,6 +93,11 @@ PROTOTYPES = {
     "bg_frdc_info_get": (I32, [P, C.POINTER(FrdcInfo)]),
     "bg_frdc_download": (I32, [P, P, P, P]),
     "bg_frdc_corrupt_tile": (I32, [P, I64]),
+    "bg_frdc_serialized_size": (I32, [P, C.POINTER(C.c_size_t)]),
+    "bg_frdc_serialize": (I32, [P, I32, P, C.c_size_t]),
+    "bg_frdc_deserialize": (I32, [P, C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(C.c_int), P]),
+    "bg_frdc_write_file": (I32, [P, I32, C.c_char_p]),
+    "bg_frdc_read_file": (I32, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int), P]),
     "bg_frdc_destroy": (None, [P]),
     "bg_prepare_graph": (I32, [P, P, I64, I64, C.POINTER(P), P]),
     "bg_graph_info_get": (I32, [P, C.POINTER(GraphInfo)]),

@@ -291,6 +291,29 @@ class FrdcMatrix:
         i = self.info()
         return device_view(i.degree, (i.node_rows,), "<i4")
 
+    # -- container I/O (ref: write_frdc / read_frdc, bitsparse.cpp:171-222) --
+    def to_bytes(self, word_bits: int = 32) -> bytes:
+        n = C.c_size_t()
+        check(lib().bg_frdc_serialized_size(self._h, C.byref(n)))
+        buf = (C.c_uint8 * n.value)()
+        check(lib().bg_frdc_serialize(self._h, word_bits, buf, n.value))
+        return bytes(buf)
+
+    @staticmethod
+    def from_bytes(data: bytes) -> Tuple["FrdcMatrix", int]:
+        h, wb = C.c_void_p(), C.c_int()
+        check(lib().bg_frdc_deserialize(data, len(data), C.byref(h), C.byref(wb), _stream()))
+        return FrdcMatrix(h.value), wb.value
+
+    def write(self, path: str, word_bits: int = 32) -> None:
+        check(lib().bg_frdc_write_file(self._h, word_bits, str(path).encode()))
+
+    @staticmethod
+    def read(path: str) -> Tuple["FrdcMatrix", int]:
+        h, wb = C.c_void_p(), C.c_int()
+        check(lib().bg_frdc_read_file(str(path).encode(), C.byref(h), C.byref(wb), _stream()))
+        return FrdcMatrix(h.value), wb.value
+
     def corrupt_tile(self, k: int) -> None:
         check(lib().bg_frdc_corrupt_tile(self._h, k))
 

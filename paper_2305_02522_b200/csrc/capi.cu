@@ -211,6 +211,45 @@ int bg_frdc_download(const bg_frdc* m, uint64_t* rp, uint32_t* ci, uint16_t* ti)
   });
 }
 
+int bg_frdc_serialized_size(const bg_frdc* m, size_t* bytes) {
+  return guard([&] {
+    need(m, "frdc");
+    need(bytes, "output");
+    *bytes = frdc_container_bytes(*m);
+  });
+}
+
+int bg_frdc_serialize(const bg_frdc* m, int word_bits, void* buf, size_t buf_len) {
+  return guard([&] {
+    need(m, "frdc");
+    need(buf, "buffer");
+    if (buf_len < frdc_container_bytes(*m)) fail("write_frdc: buffer too small");
+    frdc_serialize(*m, word_bits, buf);
+  });
+}
+
+int bg_frdc_deserialize(const void* buf, size_t len, bg_frdc** out, int* word_bits, bg_stream s) {
+  return guard([&] {
+    need(out, "output");
+    if (!buf && len) fail("null buffer");
+    *out = frdc_deserialize(buf, len, word_bits, S(s)).release();
+  });
+}
+
+int bg_frdc_write_file(const bg_frdc* m, int word_bits, const char* path) {
+  return guard([&] {
+    need(m, "frdc");
+    frdc_write_file(*m, word_bits, path);
+  });
+}
+
+int bg_frdc_read_file(const char* path, bg_frdc** out, int* word_bits, bg_stream s) {
+  return guard([&] {
+    need(out, "output");
+    *out = frdc_read_file(path, word_bits, S(s)).release();
+  });
+}
+
 int bg_frdc_corrupt_tile(bg_frdc* m, int64_t k) {
   return guard([&] {
     need(m, "frdc");

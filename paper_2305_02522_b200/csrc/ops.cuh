@@ -85,6 +85,12 @@ std::unique_ptr<bg_frdc> frdc_from_host(int64_t rows, int64_t cols, const uint64
                                         const uint32_t* ci, const uint16_t* ti, int64_t nnz,
                                         cudaStream_t s);
 void frdc_finalize(bg_frdc& m, cudaStream_t s);  // degree, nnz_bits, max_deg
+// ---- container.cu: FRDC container I/O (bitsparse.cpp:171-222) -----------
+size_t frdc_container_bytes(const bg_frdc& m);
+void frdc_serialize(const bg_frdc& m, int word_bits, void* buf);
+std::unique_ptr<bg_frdc> frdc_deserialize(const void* buf, size_t len, int* word_bits, cudaStream_t s);
+void frdc_write_file(const bg_frdc& m, int word_bits, const char* path);
+std::unique_ptr<bg_frdc> frdc_read_file(const char* path, int* word_bits, cudaStream_t s);
 void frdc_slivers(bg_frdc& m, cudaStream_t s);   // build the node-major sliver view once
 void frdc_bitview(bg_frdc& m, cudaStream_t s);   // build the bit-entry view once (from slivers)
 std::unique_ptr<bg_graph> prepare_graph(const int64_t* src, const int64_t* dst, int64_t e,
