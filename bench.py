@@ -352,7 +352,10 @@ def ncu_traffic(label):
     if not os.path.exists(p):
         return None
     with open(p) as fh:
-        return json.load(fh).get(label)
+        rec = json.load(fh).get(label)
+    # DRAM read + write bytes per launch of that kernel from the committed
+    # ncu --set full capture (profiles/r01_v4_ncu_summary.txt)
+    return rec.get("traffic_bytes") if isinstance(rec, dict) else rec
 
 
 def cpu_baseline(args, graph, out, model_name, n, f, h, c, plan):
