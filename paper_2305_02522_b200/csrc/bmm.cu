@@ -407,16 +407,17 @@ __device__ __forceinline__ void fbb_convert(const float* __restrict__ src, int v
 template <int NW>  // output words per row (N <= 32*NW); one warp per word
 __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
     k_fbb_tma(const float* __restrict__ a_f, const uint32_t* __restrict__ wt, int64_t rows, int k,
-              int kspw, int n, int ksteps, int ospw, uint32_t qmagic,
+              int kspw, int n, int ksteps, int ospw, uint32_t qmagic, int mb,
               uint32_t* __restrict__ out_bits) {
   extern __shared__ __align__(16) uint8_t fbb_smem[];
   __shared__ __align__(8) uint64_t full[kFbbStages];
   const int kpad = 32 * ksteps;
   const int lda = kpad + 16;  // bytes; (lda/4) % 32 == 28 -> conflict-free fragments
-  const uint32_t tile_bytes = static_cast<uint32_t>(16 * k) * 4u;
-  float* ring = reinterpret_cast<float*>(fbb_smem);                                  // stages x 16 x k fp32
-  uint8_t* a8 = fbb_smem + static_cast<size_t>(kFbbStages) * tile_bytes;            // teams x 16 x lda
-  uint8_t* w8 = a8 + static_cast<size_t>(kFbbTeams) * 16 * lda;                // 32*NW x lda
+  const int TR = 16 * mb;  // rows per tile: mb m16 blocks (small K: several, so per-tile costs amortize)
+  const uint32_t tile_bytes = static_cast<uint32_t>(TR * k) * 4u;
+  float* ring = reinterpret_cast<float*>(fbb_smem);                                  // stages x TR x k fp32
+  uint8_t* a8 = fbb_smem + static_cast<size_t>(kFbbStages) * tile_bytes;            // teams x TR x lda
+  uint8_t* w8 = a8 + static_cast<size_t>(kFbbTeams) * TR * lda;                     // 32*NW x lda
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int team = warp / NW, wq = warp % NW, ttid = tid - team * NW * 32;
   const int g = lane >> 2, t4 = lane & 3;
@@ -436,12 +437,12 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
       *reinterpret_cast<uint32_t*>(w8 + o * lda + p4) = v;
     }
   // the activation tiles' padding columns [K, kpad) stay zero
-  for (int t = tid; t < kFbbTeams * 16 * (lda / 4); t += blockDim.x) reinterpret_cast<uint32_t*>(a8)[t] = 0u;
-  // 16-row tiles; a partial last tile (rows % 16) is converted straight from
+  for (int t = tid; t < kFbbTeams * TR * (lda / 4); t += blockDim.x) reinterpret_cast<uint32_t*>(a8)[t] = 0u;
+  // TR-row tiles; a partial last tile (rows % TR) is converted straight from
   // global memory (a bulk copy must be a multiple of 16 bytes and must not
   // read past the operand).  It is the last tile of its CTA, so skipping its
   // copy leaves no later use of that ring slot out of phase.
-  const int64_t tiles = (rows + 15) / 16, full_tiles = rows / 16;
+  const int64_t tiles = (rows + TR - 1) / TR, full_tiles = rows / TR;
   const int64_t my = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   if (tid == 0) {
     for (int s = 0; s < kFbbStages; ++s) mbar_init(&full[s], 1);
@@ -450,13 +451,13 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
       const int64_t tile = blockIdx.x + j * gridDim.x;
       if (tile >= full_tiles) break;
       mbar_expect_tx(&full[j], tile_bytes);
-      bulk_g2s(ring + j * (tile_bytes / 4), a_f + tile * 16 * static_cast<int64_t>(k), tile_bytes, &full[j]);
+      bulk_g2s(ring + j * (tile_bytes / 4), a_f + tile * TR * static_cast<int64_t>(k), tile_bytes, &full[j]);
     }
   }
   __syncthreads();
-  uint8_t* mine = a8 + team * 16 * lda;
+  uint8_t* mine = a8 + team * TR * lda;
   const int nthr = NW * 32;
-  const uint32_t q = (k + 7) / 8, items = 16 * q;  // 8-column groups per row, per tile
+  const uint32_t q = (k + 7) / 8, items = TR * q;  // 8-column groups per row, per tile
   const bool keven = (k & 1) == 0;
   for (int64_t j = team; j < my; j += kFbbTeams) {
     const int slot = static_cast<int>(j % kFbbStages);
@@ -467,23 +468,24 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
     // 8-column group) with r = t / q (magic multiply); groups past K are
     // never written (zeroed once above); the last group of a row is masked.
     if (!partial)
-      fbb_convert<false>(ring + static_cast<size_t>(slot) * (tile_bytes / 4), 16, k, keven, items, q, qmagic,
+      fbb_convert<false>(ring + static_cast<size_t>(slot) * (tile_bytes / 4), TR, k, keven, items, q, qmagic,
                          ttid, nthr, lda, mine);
     else
-      fbb_convert<true>(a_f + tile * 16 * static_cast<int64_t>(k), static_cast<int>(rows - tile * 16), k, keven,
+      fbb_convert<true>(a_f + tile * TR * static_cast<int64_t>(k), static_cast<int>(rows - tile * TR), k, keven,
                         items, q, qmagic, ttid, nthr, lda, mine);
     asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(nthr) : "memory");
     const int64_t nt = blockIdx.x + (j + kFbbStages) * gridDim.x;
     if (ttid == 0 && j + kFbbStages < my && nt < full_tiles) {  // the fp32 slot is free: refill it
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&full[slot], tile_bytes);
-      bulk_g2s(ring + static_cast<size_t>(slot) * (tile_bytes / 4), a_f + nt * 16 * static_cast<int64_t>(k),
+      bulk_g2s(ring + static_cast<size_t>(slot) * (tile_bytes / 4), a_f + nt * TR * static_cast<int64_t>(k),
                tile_bytes, &full[slot]);
     }
+    for (int mblk = 0; mblk < mb; ++mblk) {
     int acc[4][4];
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj) acc[jj][0] = acc[jj][1] = acc[jj][2] = acc[jj][3] = 0;
-    const uint8_t* ab = mine + g * lda + 4 * t4;
+    const uint8_t* ab = mine + (16 * mblk + g) * lda + 4 * t4;
     const uint8_t* bb = w8 + (32 * wq + g) * lda + 4 * t4;
     for (int ks = 0; ks < ksteps; ++ks) {
       uint32_t a[4];
@@ -516,7 +518,7 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
       m0 &= keep;
       m1 &= keep;
     }
-    const int64_t r0 = tile * 16 + g;
+    const int64_t r0 = tile * TR + 16 * mblk + g;
     if (t4 == 0 && wq < ospw) {
       if (r0 < rows) out_bits[r0 * ospw + wq] = m0;
       if (r0 + 8 < rows) out_bits[(r0 + 8) * ospw + wq] = m1;
@@ -526,6 +528,7 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
         if (r0 < rows) out_bits[r0 * ospw + w] = 0u;
         if (r0 + 8 < rows) out_bits[(r0 + 8) * ospw + w] = 0u;
       }
+    }  // m16 block
     asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(nthr) : "memory");  // int8 tile reusable
   }
 }
@@ -538,20 +541,27 @@ int64_t fbb_tma(const BmmArgs& a, cudaStream_t s) {
   const int lda = 32 * ksteps + 16;
   const int nw = static_cast<int>(cdiv(a.n, 32));
   const int NW = nw <= 1 ? 1 : nw <= 2 ? 2 : 4;
-  const size_t smem = static_cast<size_t>(kFbbStages) * 16 * a.k * 4 + static_cast<size_t>(kFbbTeams) * 16 * lda +
-                      static_cast<size_t>(32 * NW) * lda;
+  // m16 blocks per tile: a slot of at most 16 x 602 fp32 (the Reddit tile),
+  // so small K batches several blocks per bulk copy and per barrier
+  int mb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, 38528 / (64 * a.k))));
+  auto smem_of = [&](int m) {
+    return static_cast<size_t>(kFbbStages) * 16 * m * a.k * 4 + static_cast<size_t>(kFbbTeams) * 16 * m * lda +
+           static_cast<size_t>(32 * NW) * lda;
+  };
+  while (mb > 1 && smem_of(mb) > 227 * 1024 - 128) --mb;
+  const size_t smem = smem_of(mb);
   if (smem > 227 * 1024 - 128) return 0;  // opt-in shared memory per block, less the static part
-  const int64_t tiles = (a.rows + 15) / 16;
+  const int64_t tiles = (a.rows + 16 * mb - 1) / (16 * mb);
   const int kspw = static_cast<int>(spw(a.k, a.wb));
   const int ospw = static_cast<int>(spw(a.n, a.wb));
-  // t / q == umulhi(t, ceil(2^32 / q)) for t < 16 q: the error term t*(M*q - 2^32) < 16 q^2 < 2^32
+  // t / q == umulhi(t, ceil(2^32 / q)) for t < 16 mb q: the error term t*(M*q - 2^32) < 128 q^2 < 2^32
   const uint32_t q = static_cast<uint32_t>((a.k + 7) / 8);
   const uint32_t qmagic = static_cast<uint32_t>(((uint64_t{1} << 32) + q - 1) / q);
   auto go = [&](auto kern) {
     BG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     const int64_t blocks = std::min<int64_t>(tiles, sm_count());
     kern<<<static_cast<unsigned>(blocks), kFbbTeams * NW * 32, smem, s>>>(
-        a.a_f, a.wt, a.rows, static_cast<int>(a.k), kspw, static_cast<int>(a.n), ksteps, ospw, qmagic,
+        a.a_f, a.wt, a.rows, static_cast<int>(a.k), kspw, static_cast<int>(a.n), ksteps, ospw, qmagic, mb,
         a.out_bits);
   };
   if (NW == 1) go(k_fbb_tma<1>);

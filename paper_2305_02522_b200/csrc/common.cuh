@@ -108,28 +108,24 @@ __device__ __forceinline__ T ldg(const T* p) {
 }
 
 // exp(d) for d <= 0 in double: Cody-Waite reduction d = n ln2 + r, |r| <=
-// ln2/2, degree-13 Taylor polynomial (truncation < 5e-18 relative), scale by
+// ln2/2, degree-13 Taylor polynomial (truncation < 5e-18 relative, Estrin
+// scheme), scale by
 // 2^n.  Within an ulp of libm's exp, far below the float rounding of the
 // probabilities.
 __device__ __forceinline__ double exp_nonpos(double d) {
-  if (!(d > -745.2)) return 0.0;  // underflow, -inf (and NaN propagates below)
+  if (!(d > -745.2)) return d != d ? d : 0.0;  // NaN propagates (as libm's exp); underflow, -inf -> 0
   const double n = rint(d * 1.4426950408889634);
   double r = fma(n, -6.93147180369123816490e-01, d);
   r = fma(n, -1.90821492927058770002e-10, r);
-  double p = 1.0 / 6227020800.0;  // 1/13!
-  p = fma(p, r, 1.0 / 479001600.0);
-  p = fma(p, r, 1.0 / 39916800.0);
-  p = fma(p, r, 1.0 / 3628800.0);
-  p = fma(p, r, 1.0 / 362880.0);
-  p = fma(p, r, 1.0 / 40320.0);
-  p = fma(p, r, 1.0 / 5040.0);
-  p = fma(p, r, 1.0 / 720.0);
-  p = fma(p, r, 1.0 / 120.0);
-  p = fma(p, r, 1.0 / 24.0);
-  p = fma(p, r, 1.0 / 6.0);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
+  // Estrin evaluation of sum_{i<=13} r^i / i!: dependency depth 5 instead of
+  // Horner's 14 (the kernels using it are FP64-latency-bound)
+  const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+  const double a0 = fma(r, 1.0, 1.0), a1 = fma(r, 1.0 / 6.0, 0.5), a2 = fma(r, 1.0 / 120.0, 1.0 / 24.0),
+               a3 = fma(r, 1.0 / 5040.0, 1.0 / 720.0), a4 = fma(r, 1.0 / 362880.0, 1.0 / 40320.0),
+               a5 = fma(r, 1.0 / 39916800.0, 1.0 / 3628800.0), a6 = fma(r, 1.0 / 6227020800.0, 1.0 / 479001600.0);
+  const double b0 = fma(a1, r2, a0), b1 = fma(a3, r2, a2), b2 = fma(a5, r2, a4);
+  const double d0 = fma(b1, r4, b0), d1 = fma(a6, r4, b2);
+  const double p = fma(d1, r8, d0);
   const int ni = static_cast<int>(n);
   if (ni >= -1022) return p * __longlong_as_double(static_cast<long long>(ni + 1023) << 52);
   return ldexp(p, ni);  // subnormal results

@@ -43,59 +43,52 @@ __global__ void k_relu(float* __restrict__ x, int64_t n) {
 }
 
 // Row softmax in double, sequential column order (graphops.cpp:372-386).
-// A warp stages 32 rows (contiguous) through shared memory with coalesced
-// loads/stores.  The order-sensitive parts -- the row max and the sequential
-// double sum -- run lane per row; exp(x - max) (cached as double, the value
-// the reference recomputes identically) and the division run element-parallel.
-constexpr int kSmWarps = 2;
-constexpr int kSmMaxCols = 48;
-
+// A warp owns 32 consecutive rows = one contiguous chunk of 32*cols floats:
+// it stages the chunk into shared memory with independent float4 loads, runs
+// the order-sensitive parts -- the row max and the sequential double sum --
+// lane per row, then recomputes exp(x - max) * (1/sum) element-parallel over
+// the chunk (row = element / cols by a magic multiply) and streams it back.
+constexpr int kSmWarps = 4;
+constexpr int kSmMaxCols = 64;
 __global__ void __launch_bounds__(kSmWarps * 32)
-    k_softmax_staged(const float* __restrict__ x, int64_t rows, int cols, float* __restrict__ o) {
-  __shared__ float buf[kSmWarps][32 * (kSmMaxCols + 1)];
-  __shared__ double ex[kSmWarps][32 * kSmMaxCols];
-  __shared__ double rmx[kSmWarps][32], rsum[kSmWarps][32];
+    k_softmax_staged(const float* __restrict__ x, int64_t rows, int cols, uint32_t cmagic, float* __restrict__ o) {
+  __shared__ __align__(16) float buf[kSmWarps][32 * kSmMaxCols];
+  __shared__ double rmx[kSmWarps][32], rinv[kSmWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ld = cols | 1;
   float* b = buf[warp];
-  double* e = ex[warp];
   for (int64_t r0 = (static_cast<int64_t>(blockIdx.x) * kSmWarps + warp) * 32; r0 < rows;
        r0 += static_cast<int64_t>(gridDim.x) * kSmWarps * 32) {
     const int nr = static_cast<int>(rows - r0 < 32 ? rows - r0 : 32);
-    const int n = nr * cols;
-    const float* src = x + r0 * cols;
-    for (int t = lane, r = 0, c = lane; t < n; t += 32) {  // (r, c) = divmod(t, cols)
-      while (c >= cols) c -= cols, ++r;
-      b[r * ld + c] = src[t];
-      c += 32;
-    }
+    const int n = nr * cols, n4 = n >> 2;
+    const float* src = x + r0 * cols;  // 16-byte aligned: r0*cols is a multiple of 4*32
+    const float4* src4 = reinterpret_cast<const float4*>(src);
+    float4* b4 = reinterpret_cast<float4*>(b);
+#pragma unroll 4
+    for (int t = lane; t < n4; t += 32) b4[t] = __ldg(src4 + t);
+    for (int t = 4 * n4 + lane; t < n; t += 32) b[t] = __ldg(src + t);
     __syncwarp();
     if (lane < nr) {
-      const float* xr = b + lane * ld;
+      const float* xr = b + lane * cols;
       double mx = -INFINITY;
       for (int j = 0; j < cols; ++j) mx = fmax(mx, static_cast<double>(xr[j]));
-      rmx[warp][lane] = mx;
-    }
-    __syncwarp();
-    for (int t = lane, r = 0, c = lane; t < n; t += 32) {
-      while (c >= cols) c -= cols, ++r;
-      e[r * cols + c] = exp_nonpos(static_cast<double>(b[r * ld + c]) - rmx[warp][r]);
-      c += 32;
-    }
-    __syncwarp();
-    if (lane < nr) {
-      const double* er = e + lane * cols;
       double sum = 0.0;
-      for (int j = 0; j < cols; ++j) sum = __dadd_rn(sum, er[j]);
-      rsum[warp][lane] = __drcp_rn(sum);
+#pragma unroll 4
+      for (int j = 0; j < cols; ++j) sum = __dadd_rn(sum, exp_nonpos(static_cast<double>(xr[j]) - mx));
+      rmx[warp][lane] = mx;
+      rinv[warp][lane] = __drcp_rn(sum);
+    }
+    __syncwarp();
+#pragma unroll 4
+    for (int t = lane; t < n; t += 32) {
+      const uint32_t r = __umulhi(static_cast<uint32_t>(t), cmagic);  // t / cols
+      b[t] = __double2float_rn(__dmul_rn(exp_nonpos(static_cast<double>(b[t]) - rmx[warp][r]), rinv[warp][r]));
     }
     __syncwarp();
     float* dst = o + r0 * cols;
-    for (int t = lane, r = 0, c = lane; t < n; t += 32) {
-      while (c >= cols) c -= cols, ++r;
-      dst[t] = __double2float_rn(__dmul_rn(e[r * cols + c], rsum[warp][r]));
-      c += 32;
-    }
+    float4* dst4 = reinterpret_cast<float4*>(dst);
+#pragma unroll 4
+    for (int t = lane; t < n4; t += 32) dst4[t] = b4[t];
+    for (int t = 4 * n4 + lane; t < n; t += 32) dst[t] = b[t];
     __syncwarp();
   }
 }
@@ -217,9 +210,13 @@ void relu(float* x, int64_t n, cudaStream_t s) {
 
 void softmax_rows(const float* x, int64_t rows, int64_t cols, float* out, cudaStream_t s) {
   if (rows == 0) return;
-  if (cols >= 1 && cols <= kSmMaxCols && x != out) {
-    const int64_t blocks = std::min<int64_t>(cdiv(rows, kSmWarps * 32), static_cast<int64_t>(sm_count()) * 32);
-    k_softmax_staged<<<static_cast<unsigned>(blocks), kSmWarps * 32, 0, s>>>(x, rows, static_cast<int>(cols), out);
+  if (cols >= 2 && cols <= kSmMaxCols && x != out && reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(out) % 16 == 0) {
+    // t / cols == umulhi(t, ceil(2^32 / cols)) for t < 32 cols (error 32 cols^2 < 2^32)
+    const uint32_t cmagic = static_cast<uint32_t>(((uint64_t{1} << 32) + cols - 1) / cols);
+    const int64_t blocks = std::min<int64_t>(cdiv(rows, kSmWarps * 32), static_cast<int64_t>(sm_count()) * 16);
+    k_softmax_staged<<<static_cast<unsigned>(blocks), kSmWarps * 32, 0, s>>>(x, rows, static_cast<int>(cols),
+                                                                            cmagic, out);
   } else {
     k_softmax<<<grid1(rows, 128), 128, 0, s>>>(x, rows, cols, out);
   }

@@ -170,6 +170,10 @@ inline bool use_slivers() { return aggregation_mode() != BG_AGG_TILES; }
 // is SLIVERS/TILES; mode WINDOW skips the cost model (tests).
 bool window_bb(bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* out_bits,
                float* out_f, cudaStream_t s, int64_t r0, int64_t r1);
+// sliver.cu: BBB/BBF for short rows (lane group per row over the bit-entry
+// view); false when not eligible (mode != AUTO, > 8 words, average degree >= 64).
+bool rowgroup_bb(bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uint32_t* out_bits, float* out_f,
+                 cudaStream_t s, int64_t r0, int64_t r1);
 
 // ---- elementwise.cu ------------------------------------------------------
 void add_bbb(const uint32_t* a, const uint32_t* b, int64_t words, uint32_t* out, cudaStream_t s);

@@ -110,6 +110,61 @@ __global__ void __launch_bounds__(kSlWarps * 32)
   }
 }
 
+// ---- BSpMM.BBB / BBF for low-degree graphs over the bit-entry view ----------
+// Lane (row r, word g): R = 32/G rows per warp, each lane walks its own row's
+// columns and counts word g of the neighbours with Harley-Seal planes; no
+// slot reduction, no padding beyond the warp's longest row.  The sliver
+// kernel's 8-slot split pays off for rows of hundreds of edges; for degrees
+// in the tens it mostly counts padding (ncu, products shape: 780 M
+// instructions, ALU 79 %).
+template <int G, int NP, bool OUTB>
+__global__ void __launch_bounds__(256)
+    k_bv_bb(const uint64_t* __restrict__ bp, const uint32_t* __restrict__ bc, int64_t row0, int64_t row1,
+            const int32_t* __restrict__ degree, const uint32_t* __restrict__ x, int64_t xspw, int64_t f,
+            uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
+  constexpr int R = 32 / G;
+  const int lane = threadIdx.x & 31, r = lane / G, g = lane % G;
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const bool word_ok = g < xspw;
+  const uint32_t* xg = x + (word_ok ? g : 0);
+  for (int64_t i0 = row0 + wid * R; i0 < row1; i0 += nw * R) {
+    const int64_t i = i0 + r;
+    const bool ok = i < row1;
+    const uint32_t deg = ok ? static_cast<uint32_t>(__ldg(degree + i)) : 0u;
+    uint32_t mx = deg;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    const uint32_t* cols = bc + (ok ? bp[i] : 0);
+    uint32_t P[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) P[q] = 0u;
+    for (uint32_t j = 0; j < mx; j += 8) {
+      uint32_t v[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        v[m] = 0u;
+        if (j + m < deg && word_ok) v[m] = __ldg(xg + static_cast<int64_t>(ld_nc_u32(cols + j + m)) * xspw);
+      }
+      hs_add8<NP>(P, v);
+    }
+    if (!ok || !word_ok) continue;
+    if (OUTB) {
+      // cnt >= ceil(deg/2)  <=>  2*cnt - deg >= 0   (kernels.cpp:440-454)
+      uint32_t ge = planes_ge<NP>(P, (deg + 1) >> 1);
+      if (32 * (g + 1) > f) ge &= (32 * g >= f) ? 0u : tail_mask32(f);
+      out_bits[i * xspw + g] = ge;
+    } else {
+      for (int b = 0; b < 32; ++b) {
+        const int64_t k = 32 * static_cast<int64_t>(g) + b;
+        if (k >= f) break;
+        out_f[i * f + k] = static_cast<float>(2 * static_cast<int64_t>(plane_count<NP>(P, b)) -
+                                              static_cast<int64_t>(deg));
+      }
+    }
+  }
+}
+
 // ---- fused layer-1 GCN over the bit-entry view -----------------------------
 // float(beta*sdot - 2u*q) with 2u = 2^(exp(beta)-22) (gcn_fused.cu), exactly.
 __device__ __forceinline__ float logit_of(float beta, int64_t sdot, int qsum) {
@@ -437,7 +492,47 @@ void launch_sl_f_m(const bg_frdc& A, const SpmmFArgs& a, int64_t r0, int64_t r1,
   else launch_sl_f<4, XBITS, OUTB>(A, a, r0, r1, s);
 }
 
+// Row-group path for graphs whose rows are short (average degree < 64): see k_bv_bb.
+template <int G, bool OUTB>
+bool launch_bv_bb(bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uint32_t* ob, float* of, int64_t r0,
+                  int64_t r1, cudaStream_t s) {
+  constexpr int R = 32 / G;
+  frdc_bitview(A, s);
+  const int64_t warps = std::max<int64_t>(
+      1, std::min<int64_t>(cdiv(r1 - r0, R), static_cast<int64_t>(sm_count()) * 64));
+  const unsigned blocks = static_cast<unsigned>(cdiv(warps * 32, 256));
+  auto go = [&](auto kern) {
+    kern<<<blocks, 256, 0, s>>>(A.bit_ptr.as<uint64_t>(), A.bit_cols.as<uint32_t>(), r0, r1, A.deg(), x, xspw,
+                                f, ob, of);
+  };
+  const int64_t d = A.max_deg;
+  if (d < (1 << 6)) go(k_bv_bb<G, 6, OUTB>);
+  else if (d < (1 << 9)) go(k_bv_bb<G, 9, OUTB>);
+  else if (d < (1 << 12)) go(k_bv_bb<G, 12, OUTB>);
+  else go(k_bv_bb<G, 16, OUTB>);
+  BG_LAUNCH_CHECK();
+  return true;
+}
+
 }  // namespace
+
+bool rowgroup_bb(bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uint32_t* out_bits, float* out_f,
+                 cudaStream_t s, int64_t r0, int64_t r1) {
+  // AUTO only: the SLIVERS / TILES / WINDOW modes keep their kernels (coverage)
+  if (aggregation_mode() != BG_AGG_AUTO) return false;
+  if (xspw > 8 || A.rows == 0 || A.max_deg >= (int64_t{1} << 16)) return false;
+  if (A.nnz_bits >= 64 * A.rows) return false;  // long rows: the 8-slot sliver split balances better
+  const bool ob = out_bits != nullptr;
+  auto run = [&](auto gtag) {
+    constexpr int G = decltype(gtag)::value;
+    return ob ? launch_bv_bb<G, true>(A, x, f, xspw, out_bits, out_f, r0, r1, s)
+              : launch_bv_bb<G, false>(A, x, f, xspw, out_bits, out_f, r0, r1, s);
+  };
+  if (xspw <= 1) return run(std::integral_constant<int, 1>{});
+  if (xspw <= 2) return run(std::integral_constant<int, 2>{});
+  if (xspw <= 4) return run(std::integral_constant<int, 4>{});
+  return run(std::integral_constant<int, 8>{});
+}
 
 void sliver_bb(bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* out_bits, float* out_f,
                cudaStream_t s, int64_t r0, int64_t r1) {
@@ -445,6 +540,7 @@ void sliver_bb(bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* out_b
   const int64_t xspw = spw(f, wb);
   if (r1 <= r0 || xspw == 0) return;
   if (window_bb(A, x, f, wb, out_bits, out_f, s, r0, r1)) return;
+  if (rowgroup_bb(A, x, f, xspw, out_bits, out_f, s, r0, r1)) return;
   frdc_slivers(A, s);
   const bool ob = out_bits != nullptr;
   if (xspw <= 4) {

@@ -133,3 +133,44 @@ def test_dense_graph_models_bit_exact_in_window_mode(window_mode, model, h):
     torch.cuda.synchronize()
     assert torch.equal(out2, out)
     assert np.allclose(out.cpu().numpy(), o_out, rtol=1e-6, atol=1e-7)
+
+
+# Every aggregation layout on the same operands: AUTO picks the row-group
+# kernel for short rows and the window/sliver kernels otherwise; SLIVERS and
+# TILES force the gather kernels.  All must agree with the oracle bit for bit.
+@pytest.mark.parametrize("mode", [L.AGG_AUTO, L.AGG_SLIVERS, L.AGG_TILES, L.AGG_WINDOW])
+@pytest.mark.parametrize("v", ["BSpMM.BBB", "BSpMM.BBF"])
+@pytest.mark.parametrize("nef", [(2000, 9000, 128), (1500, 30000, 64), (700, 2000, 250), (96, 3000, 31),
+                                 (5000, 20000, 100), (300, 60000, 128)])
+def test_every_layout_matches_oracle(mode, v, nef):
+    n, e, f = nef
+    rng = po.Rng(9100 + n + e + f)
+    s, d = rng.random_edges(n, e, True)
+    A = po.frdc_from_edges(n, s, d, True)
+    dA = bg.frdc_from_edges(n, s, d, True)
+    X = rng.random_dense(n, f)
+    dx, ox = _bits_operand(X, 32)
+    bg.set_aggregation(mode, 0)
+    try:
+        got = bg.bspmm(v, bg.AdjacencyOperand(dA), dx, None, 32)
+    finally:
+        bg.set_aggregation(L.AGG_AUTO, 0)
+    want = po.bspmm(v, A, ox, None, None, 32)
+    if want.prec == po.B:
+        assert bits_equal(got.bits.numpy(), want.bits)
+    else:
+        assert np.array_equal(got.cpu().numpy(), want.f)
+
+
+@pytest.mark.parametrize("cols", [1, 7, 41, 47, 48, 64, 65, 130])
+def test_softmax_rows_matches_oracle(cols):
+    rng = po.Rng(9300 + cols)
+    X = (rng.random_dense(1000, cols) * 30.0).astype(np.float32)
+    X[3, :] = -np.inf if cols > 1 else X[3, :]
+    X[5, 0] = 80.0
+    X[7, cols // 2] = np.nan
+    got = bg.softmax_rows(cuda(X)).cpu().numpy()
+    want = po.softmax_rows(X)
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    ok = np.isfinite(want)
+    assert np.allclose(got[ok], want[ok], rtol=1e-6, atol=1e-12)
