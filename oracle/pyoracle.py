@@ -501,6 +501,9 @@ def ref() -> C.CDLL:
             raise FileNotFoundError(REF_SO)
         L = C.CDLL(REF_SO)
         L.ref_error.restype = C.c_char_p
+        if hasattr(L, "ref_enumerate_plans"):
+            L.ref_enumerate_plans.restype = C.c_int64
+            L.ref_enumerate_plans.argtypes = [C.c_char_p, C.c_int, C.c_char_p, C.c_int64]
         L.ref_max_threads.restype = C.c_int
         L.ref_set_threads.argtypes = [C.c_int]
         L.ref_random_edges.restype = C.c_int64
@@ -655,3 +658,13 @@ class RefModel:
                 ref().ref_model_free(self.h)
         except Exception:
             pass
+
+
+def ref_enumerate_plans(model: str, layers: int):
+    """The real reference's enumerate_plans for a model skeleton (tune.cpp)."""
+    L = ref()
+    buf = C.create_string_buffer(1 << 22)
+    n = L.ref_enumerate_plans(model.encode(), layers, buf, len(buf))
+    if n < 0:
+        raise RuntimeError(L.ref_error().decode())
+    return [line.split("|") for line in buf.value.decode().splitlines()]

@@ -24,6 +24,7 @@
 #include "bitgnn/modelconfig.hpp"
 #include "bitgnn/rng.hpp"
 #include "bitgnn/runreport.hpp"
+#include "bitgnn/tune.hpp"
 
 using namespace bitgnn;
 
@@ -298,6 +299,36 @@ void ref_binarize(const float* x, int64_t rows, int64_t cols, int word_bits, uin
   for (int64_t i = 0; i < rows; ++i) {
     auto r = b.row_span(i);
     std::memcpy(out + i * b.storage_words_per_row(), r.data(), r.size() * 4);
+  }
+}
+
+// The reference's plan enumeration (tune.cpp:119-125) for a model skeleton
+// (skeleton_of, tune.cpp:84-96): writes the plans as lines of '|'-joined layer
+// chains into buf; returns the number of plans or -1 (error / buffer short).
+int64_t ref_enumerate_plans(const char* model, int layers, char* buf, int64_t cap) {
+  try {
+    std::vector<LayerKind> kinds;
+    const std::string m(model);
+    if (m == "gcn") {
+      kinds.assign(layers, LayerKind::GcnConv);
+    } else if (m == "sage") {
+      kinds.assign(layers, LayerKind::SageConv);
+    } else {
+      kinds.assign(layers - 1, LayerKind::GraphConv);
+      kinds.push_back(LayerKind::FullyConnected);
+    }
+    const auto plans = enumerate_plans(kinds, Precision::F);
+    std::string out;
+    for (const auto& p : plans) {
+      for (size_t i = 0; i < p.size(); ++i) out += (i ? "|" : "") + p[i];
+      out += "\n";
+    }
+    if (static_cast<int64_t>(out.size()) + 1 > cap) return -1;
+    std::memcpy(buf, out.c_str(), out.size() + 1);
+    return static_cast<int64_t>(plans.size());
+  } catch (const std::exception& e) {
+    guard(e);
+    return -1;
   }
 }
 
