@@ -46,7 +46,7 @@ struct bg_frdc {
   // of ELL groups (4 u16 entries per lane per 256-byte group) covering all nw
   // steps in order: stream base seg[b*(T/32)+v], step lengths steplen[.. *nw + k].
   struct Windows {
-    int T = 0, Wn = 0, nw = 0, nb = 0;
+    int T = 0, Wn = 0, nw = 0, nb = 0, rw = 0;  // T: rows per block; rw: rows per warp stream
     bg::DevBuf seg;      // u32[nb*(T/32) + 1] stream bases, in ELL groups
     bg::DevBuf steplen;  // u16[nb*(T/32)*nw] groups per step
     bg::DevBuf ell;      // u16 entries

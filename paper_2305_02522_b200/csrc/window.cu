@@ -82,16 +82,16 @@ __global__ void k_win_count(const uint64_t* __restrict__ srp, const uint32_t* __
 // k+1.  Writes the per-step entry counts of each row (u16, rows x nh), the
 // step lengths in groups (u16, warp-major: [b][v][k]) and each warp stream's
 // total (for the scan of stream bases).
-__global__ void k_win_sched(const uint16_t* __restrict__ cnt, int64_t rows, int T, int nh, int64_t nbv,
+__global__ void k_win_sched(const uint16_t* __restrict__ cnt, int64_t rows, int RB, int RW, int nh, int64_t nbv,
                             uint16_t* __restrict__ nk, uint16_t* __restrict__ steplen,
                             uint32_t* __restrict__ total) {
   const int64_t wv = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (wv >= nbv) return;
-  const int lane = threadIdx.x & 31, nwarps = T / 32;
-  const int64_t b = wv / nwarps;
-  const int v = static_cast<int>(wv % nwarps);
-  const int64_t i = b * T + v * 32 + lane;
-  const bool ok = i < rows;
+  const int lane = threadIdx.x & 31, streams = RB / RW;  // RW rows per warp stream
+  const int64_t b = wv / streams;
+  const int v = static_cast<int>(wv % streams);
+  const int64_t i = b * RB + v * RW + lane;
+  const bool ok = lane < RW && i < rows;
   uint32_t q0 = ok ? cnt[i * nh] : 0u, sum = 0;
   for (int k = 0; k < nh; ++k) {
     uint32_t m = q0;
@@ -118,13 +118,13 @@ __global__ void k_fill_u16(uint16_t* __restrict__ p, int64_t n, uint16_t v) {
 // segment (the step's share of half k, then of half k+1).  A warp's segments
 // are consecutive in its stream: stream base + the lengths of earlier steps.
 __global__ void k_win_fill(const uint64_t* __restrict__ srp, const uint32_t* __restrict__ sl,
-                           int64_t rows, int T, int Wh, int nh, const uint16_t* __restrict__ nk,
+                           int64_t rows, int RW, int Wh, int nh, const uint16_t* __restrict__ nk,
                            const uint32_t* __restrict__ sbase, const uint16_t* __restrict__ steplen,
                            uint16_t* __restrict__ ell) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= rows) return;
-  const int64_t wv = i / 32;  // = b * (T/32) + v (T is a multiple of 32)
-  const int lane = static_cast<int>(i % 32);
+  const int64_t wv = i / RW;  // = b * (RB/RW) + v (RB is a multiple of RW)
+  const int lane = static_cast<int>(i % RW);
   const uint16_t* n = nk + i * nh;
   const uint16_t* sll = steplen + wv * nh;
   int k = -1;
@@ -136,10 +136,10 @@ __global__ void k_win_fill(const uint64_t* __restrict__ srp, const uint32_t* __r
       ++k;
       left = n[k];
       pos = 0;
-      base = g * 128 + lane * 4;
+      base = g * (4 * RW) + lane * 4;
     }
     const uint32_t h = col / static_cast<uint32_t>(Wh);
-    ell[base + (pos >> 2) * 128 + (pos & 3)] =
+    ell[base + (pos >> 2) * (4 * RW) + (pos & 3)] =
         static_cast<uint16_t>(((h % kSlots) << 12) | (col - h * static_cast<uint32_t>(Wh)));
     ++pos;
     --left;
@@ -153,10 +153,10 @@ __global__ void k_win_fill(const uint64_t* __restrict__ srp, const uint32_t* __r
 // lane's entries within a segment may be permuted freely: position k is
 // filled greedily with, per lane, an entry of a bank group no other lane of
 // the quarter uses there (bounded look-ahead).  K entries per lane; q quarter.
-__device__ void bank_order_segment(uint16_t* __restrict__ segp, uint32_t K, int q) {
+__device__ void bank_order_segment(uint16_t* __restrict__ segp, uint32_t K, int q, int RW) {
   constexpr int kLook = 48;
   if (K == 0) return;
-  auto at = [&](int l, uint32_t k) -> uint16_t& { return segp[(k >> 2) * 128 + (8 * q + l) * 4 + (k & 3)]; };
+  auto at = [&](int l, uint32_t k) -> uint16_t& { return segp[(k >> 2) * (4 * RW) + (8 * q + l) * 4 + (k & 3)]; };
   uint32_t cnt[8];
   for (int l = 0; l < 8; ++l) {
     uint32_t c = 0;
@@ -187,16 +187,19 @@ __device__ void bank_order_segment(uint16_t* __restrict__ segp, uint32_t K, int 
   }
 }
 
-// Thread per (warp stream, quarter): every step segment of the stream in turn.
+// Thread per (warp stream, conflict group of 8 rows): every step segment of
+// the stream in turn.  (An LDS.128 is served per 8 lanes; with two threads
+// per row an LDS.64 is served per 16 lanes = 8 rows: a group is 8 rows either way.)
 __global__ void k_win_bankorder(const uint32_t* __restrict__ sbase, const uint16_t* __restrict__ steplen,
-                                int64_t nbv, int nh, uint16_t* __restrict__ ell) {
+                                int64_t nbv, int nh, int RW, uint16_t* __restrict__ ell) {
+  const int cg = RW / 8;
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= nbv * 4) return;
-  const int64_t wv = t >> 2;
+  if (t >= nbv * cg) return;
+  const int64_t wv = t / cg;
   uint64_t g = sbase[wv];
   for (int k = 0; k < nh; ++k) {
     const uint32_t len = steplen[wv * nh + k];
-    bank_order_segment(ell + g * 128, len * 4, static_cast<int>(t & 3));
+    bank_order_segment(ell + g * (4 * RW), len * 4, static_cast<int>(t % cg), RW);
     g += len;
   }
 }
@@ -239,20 +242,30 @@ __device__ __forceinline__ void ripple(uint32_t (&P)[NP], uint32_t c, int q0) {
   }
 }
 
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
 }
 
-template <int NP, bool OUTB>
-__global__ void __launch_bounds__(NP <= 10 ? kWinMaxThreads : 480, 1)
+// TPR threads per node row: each owns W = 4/TPR of the row's words (TPR = 2
+// halves the per-thread state, so ~1.5x the warps fit at the same register
+// file, and a warp stream covers 16 rows).
+template <int NP, bool OUTB, int TPR>
+__global__ void __launch_bounds__(TPR == 1 ? (NP <= 10 ? kWinMaxThreads : 480) : 800, 1)
     k_win_bb(const uint32_t* __restrict__ sbase, const uint16_t* __restrict__ steplen,
              const uint16_t* __restrict__ ell, int nh, int Wh,
              int64_t xrows, int64_t row0, int64_t row1, int b0, int b1,
              const int32_t* __restrict__ degree, const uint4* __restrict__ x, int64_t f,
              uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
   static_assert(NP >= 5, "two-level Harley-Seal needs planes 0..4");
+  constexpr int W = 4 / TPR, RW = 32 / TPR;  // words per thread, rows per warp stream
   extern __shared__ __align__(16) uint4 sbuf[];  // kSlots x kSlotRec records
   __shared__ __align__(8) uint64_t full[kSlots];
   __shared__ uint32_t done[kSlots];  // warps finished with each slot (monotone)
@@ -283,47 +296,54 @@ __global__ void __launch_bounds__(NP <= 10 ? kWinMaxThreads : 480, 1)
     for (int H = 0; H < kSlots && H < nsteps; ++H) issue(H);
   const uint32_t pad2 = static_cast<uint32_t>(kWinPad) * 0x10001u;
   const uint2 sent2 = make_uint2(pad2, pad2);
-  const uint2* ell2 = reinterpret_cast<const uint2*>(ell) + lane;
+  const int part = threadIdx.x % TPR;                              // which W words of the row
+  const uint2* ell2 = reinterpret_cast<const uint2*>(ell) + lane / TPR;  // this row's 4 entries
   const uint32_t sb = smem_addr(sbuf);
   // This warp's groups of the current row block form one stream [gp, ge)
   // across all steps; eight groups are kept in flight ahead of use.
   uint32_t gp = 0, ge = 0, lenreg = 0;
   int64_t wv = 0;
-  auto fetch = [&](uint32_t g) { return g < ge ? ld_nc_v2(ell2 + static_cast<size_t>(g) * 32) : sent2; };
+  auto fetch = [&](uint32_t g) { return g < ge ? ld_nc_v2(ell2 + static_cast<size_t>(g) * RW) : sent2; };
   uint2 fq[8];  // groups gp .. gp+7 in flight
 #pragma unroll
   for (int u = 0; u < 8; ++u) fq[u] = sent2;
-  uint32_t P[4][NP], pend[4];
+  uint32_t P[W][NP], pend[W];
   bool have = false;  // pend holds a weight-8 carry per word (warp-uniform)
-  // 8 entries: 8 LDS.128, Harley-Seal into planes 0..2 of each word -> weight-8 carries
-  auto batch8 = [&](uint2 a, uint2 c, uint32_t (&e)[4]) {
+  const uint32_t sbw = sb + part * (4 * W);  // this thread's words of each record
+  // 8 entries: 8 shared loads (W words each), Harley-Seal into planes 0..2 of
+  // each word -> weight-8 carries
+  auto batch8 = [&](uint2 a, uint2 c, uint32_t (&e)[W]) {
     const uint32_t pk[4] = {a.x, a.y, c.x, c.y};
-    uint4 v[8];
+    uint32_t v[8][W];
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-      v[2 * m] = lds128(sb + ((pk[m] & 0xFFFFu) << 4));
-      v[2 * m + 1] = lds128(sb + ((pk[m] >> 16) << 4));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t addr = sbw + ((h ? (pk[m] >> 16) : (pk[m] & 0xFFFFu)) << 4);
+        if (W == 4) {
+          const uint4 t = lds128(addr);
+          v[2 * m + h][0] = t.x, v[2 * m + h][1] = t.y, v[2 * m + h][W > 2 ? 2 : 0] = t.z,
+                       v[2 * m + h][W > 3 ? 3 : 0] = t.w;
+        } else {
+          const uint2 t = lds64(addr);
+          v[2 * m + h][0] = t.x, v[2 * m + h][1] = t.y;
+        }
+      }
     }
-    uint32_t xw[8];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) xw[m] = v[m].x;
-    e[0] = hs8_low<NP>(P[0], xw);
+    for (int q = 0; q < W; ++q) {
+      uint32_t xw[8];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) xw[m] = v[m].y;
-    e[1] = hs8_low<NP>(P[1], xw);
-#pragma unroll
-    for (int m = 0; m < 8; ++m) xw[m] = v[m].z;
-    e[2] = hs8_low<NP>(P[2], xw);
-#pragma unroll
-    for (int m = 0; m < 8; ++m) xw[m] = v[m].w;
-    e[3] = hs8_low<NP>(P[3], xw);
+      for (int m = 0; m < 8; ++m) xw[m] = v[m][q];
+      e[q] = hs8_low<NP>(P[q], xw);
+    }
   };
   int k = 0, slot = 0;  // S % nh, S % kSlots
   uint32_t use = 0;     // S / kSlots
   for (int S = 0; S < nsteps; ++S) {
     if (k == 0) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < W; ++q)
 #pragma unroll
         for (int p = 0; p < NP; ++p) P[q][p] = 0u;
       have = false;
@@ -350,11 +370,11 @@ __global__ void __launch_bounds__(NP <= 10 ? kWinMaxThreads : 480, 1)
       fq[6] = fetch(gp + 8);
       fq[7] = fetch(gp + 9);
       gp += 2;
-      uint32_t e[4];
+      uint32_t e[W];
       batch8(a, c, e);
       if (have) {  // two weight-8 carries: CSA into plane 3, ripple from plane 4
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < W; ++q) {
           const uint32_t s3 = P[q][3] ^ pend[q] ^ e[q];
           const uint32_t cy = maj3(P[q][3], pend[q], e[q]);
           P[q][3] = s3;
@@ -362,7 +382,7 @@ __global__ void __launch_bounds__(NP <= 10 ? kWinMaxThreads : 480, 1)
         }
       } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) pend[q] = e[q];
+        for (int q = 0; q < W; ++q) pend[q] = e[q];
       }
       have = !have;
     }
@@ -381,30 +401,28 @@ __global__ void __launch_bounds__(NP <= 10 ? kWinMaxThreads : 480, 1)
     if (last) {
       if (have) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) ripple<NP>(P[q], pend[q], 3);
+        for (int q = 0; q < W; ++q) ripple<NP>(P[q], pend[q], 3);
         have = false;
       }
       const int bi = S / nh;
       const int b = b0 + static_cast<int>(blockIdx.x) + bi * static_cast<int>(gridDim.x);
-      const int64_t i = static_cast<int64_t>(b) * T + tid;
+      const int64_t i = static_cast<int64_t>(b) * (T / TPR) + tid / TPR;
       if (i >= row0 && i < row1) {
         const uint32_t deg = static_cast<uint32_t>(__ldg(degree + i));
         if (OUTB) {
-          uint32_t o[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < W; ++q) {
+            const int wd = part * W + q;
             // cnt >= ceil(deg/2)  <=>  2*cnt - deg >= 0   (kernels.cpp:440-454)
             uint32_t ge = planes_ge<NP>(P[q], (deg + 1) >> 1);
-            if (32 * (q + 1) > f) ge &= (32 * q >= f) ? 0u : tail_mask32(f);
-            o[q] = ge;
+            if (32 * (wd + 1) > f) ge &= (32 * wd >= f) ? 0u : tail_mask32(f);
+            out_bits[i * 4 + wd] = ge;
           }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) out_bits[i * 4 + q] = o[q];
         } else {
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < W; ++q)
             for (int bb = 0; bb < 32; ++bb) {
-              const int64_t kk = 32 * q + bb;
+              const int64_t kk = 32 * (part * W + q) + bb;
               if (kk >= f) break;
               out_f[i * f + kk] = static_cast<float>(2 * static_cast<int64_t>(plane_count<NP>(P[q], bb)) -
                                                      static_cast<int64_t>(deg));
@@ -432,14 +450,15 @@ int max_threads(K kern, size_t smem) {
   return t;
 }
 
-void build_windows(bg_frdc& A, int T, int Wh, cudaStream_t s) {
+// RB node rows per block, RW rows per warp stream (32 / threads per row).
+void build_windows(bg_frdc& A, int RB, int RW, int Wh, cudaStream_t s) {
   auto& W = A.win;
-  if (W.T == T && W.Wn == Wh) return;
+  if (W.T == RB && W.Wn == Wh && W.rw == RW) return;
   frdc_slivers(A, s);
   const int64_t rows = A.rows;
   const int nh = static_cast<int>(cdiv(cdiv(A.cols, Wh), kSlots) * kSlots);
-  const int nb = static_cast<int>(cdiv(rows, T));
-  const int64_t nbv = static_cast<int64_t>(nb) * (T / 32);  // warp streams
+  const int nb = static_cast<int>(cdiv(rows, RB));
+  const int64_t nbv = static_cast<int64_t>(nb) * (RB / RW);  // warp streams
   DevBuf cnt(static_cast<size_t>(std::max<int64_t>(rows * nh, 1)) * 2);
   DevBuf nk(static_cast<size_t>(std::max<int64_t>(rows * nh, 1)) * 2);
   DevBuf total(static_cast<size_t>(nbv + 1) * 4);
@@ -453,7 +472,7 @@ void build_windows(bg_frdc& A, int T, int Wh, cudaStream_t s) {
   BG_LAUNCH_CHECK();
   if (nbv > 0)
     k_win_sched<<<static_cast<unsigned>(cdiv(nbv * 32, 256)), 256, 0, s>>>(
-        cnt.as<uint16_t>(), rows, T, nh, nbv, nk.as<uint16_t>(), W.steplen.as<uint16_t>(), total.as<uint32_t>());
+        cnt.as<uint16_t>(), rows, RB, RW, nh, nbv, nk.as<uint16_t>(), W.steplen.as<uint16_t>(), total.as<uint32_t>());
   BG_LAUNCH_CHECK();
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, total.as<uint32_t>(), W.seg.as<uint32_t>(),
@@ -465,52 +484,63 @@ void build_windows(bg_frdc& A, int T, int Wh, cudaStream_t s) {
   uint32_t groups = 0;
   BG_CUDA(cudaMemcpyAsync(&groups, W.seg.as<uint32_t>() + nbv, 4, cudaMemcpyDeviceToHost, s));
   BG_CUDA(cudaStreamSynchronize(s));
-  const int64_t n16 = static_cast<int64_t>(groups) * 128;
+  const int64_t n16 = static_cast<int64_t>(groups) * 4 * RW;
   W.ell.alloc(static_cast<size_t>(std::max<int64_t>(n16, 8)) * 2);
   k_fill_u16<<<static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cdiv(n16, 256), 65536))), 256, 0, s>>>(
       W.ell.as<uint16_t>(), n16, kWinPad);
   BG_LAUNCH_CHECK();
   if (rows > 0)
     k_win_fill<<<static_cast<unsigned>(cdiv(rows, 256)), 256, 0, s>>>(
-        A.srp(), A.sl(), rows, T, Wh, nh, nk.as<uint16_t>(), W.seg.as<uint32_t>(), W.steplen.as<uint16_t>(),
+        A.srp(), A.sl(), rows, RW, Wh, nh, nk.as<uint16_t>(), W.seg.as<uint32_t>(), W.steplen.as<uint16_t>(),
         W.ell.as<uint16_t>());
   BG_LAUNCH_CHECK();
   if (nbv > 0)
-    k_win_bankorder<<<static_cast<unsigned>(cdiv(nbv * 4, 128)), 128, 0, s>>>(
-        W.seg.as<uint32_t>(), W.steplen.as<uint16_t>(), nbv, nh, W.ell.as<uint16_t>());
+    k_win_bankorder<<<static_cast<unsigned>(cdiv(nbv * (RW / 8), 128)), 128, 0, s>>>(
+        W.seg.as<uint32_t>(), W.steplen.as<uint16_t>(), nbv, nh, RW, W.ell.as<uint16_t>());
   BG_LAUNCH_CHECK();
   BG_CUDA(cudaStreamSynchronize(s));
-  W.T = T;
+  W.T = RB;
+  W.rw = RW;
   W.Wn = Wh;
   W.nw = nh;
   W.nb = nb;
 }
 
-template <int NP, bool OUTB>
+// Threads per row: 1 (default; measured faster on Reddit: 0.235 vs 0.286 ms --
+// TPR 2 needs 4 waves of streaming instead of 3 and twice the shared loads,
+// which outweighs its ~1.5x resident warps).  BG_WINDOW_TPR=2 selects the other.
+int win_tpr() {
+  const char* e = std::getenv("BG_WINDOW_TPR");
+  return e && std::atoi(e) == 2 ? 2 : 1;
+}
+
+template <int NP, bool OUTB, int TPR>
 bool launch_win(bg_frdc& A, const uint32_t* x, int64_t f, uint32_t* ob, float* of, int64_t r0,
                 int64_t r1, cudaStream_t s) {
-  auto kern = k_win_bb<NP, OUTB>;
+  constexpr int RW = 32 / TPR;
+  auto kern = k_win_bb<NP, OUTB, TPR>;
   const int sms = sm_count();
   const int Wh = std::max(1, std::min<int>(window_nodes_setting() > 0 ? std::min(window_nodes_setting(), kWinHalf)
                                                                        : kWinHalf,
                                            static_cast<int>(A.cols)));
   static const int tmax = max_threads(kern, kWinSmem);  // per instance
-  const int64_t waves = std::max<int64_t>(1, cdiv(A.rows, static_cast<int64_t>(sms) * tmax));
-  const int T = static_cast<int>(std::min<int64_t>(
-      tmax, cdiv(cdiv(A.rows, static_cast<int64_t>(sms) * waves), 32) * 32));
+  const int64_t rmax = tmax / TPR;                      // rows per block at most
+  const int64_t waves = std::max<int64_t>(1, cdiv(A.rows, static_cast<int64_t>(sms) * rmax));
+  const int RB = static_cast<int>(std::min<int64_t>(
+      rmax / RW * RW, cdiv(cdiv(A.rows, static_cast<int64_t>(sms) * waves), RW) * RW));
   if (!window_forced()) {
     // cost model: bytes streamed into shared memory per adjacency bit vs the
     // ~32-byte L2 sector an edge gather costs
     const double streamed = static_cast<double>(waves) * sms * static_cast<double>(A.cols) * kWinRec;
     if (A.nnz_bits < (int64_t{1} << 22) || streamed > 20.0 * static_cast<double>(A.nnz_bits)) return false;
   }
-  build_windows(A, T, Wh, s);
+  build_windows(A, RB, RW, Wh, s);
   const auto& W = A.win;
-  const int b0 = static_cast<int>(r0 / T), b1 = static_cast<int>(cdiv(r1, T));
+  const int b0 = static_cast<int>(r0 / RB), b1 = static_cast<int>(cdiv(r1, RB));
   const int grid = std::min(sms, b1 - b0);
-  kern<<<grid, T, kWinSmem, s>>>(W.seg.as<uint32_t>(), W.steplen.as<uint16_t>(), W.ell.as<uint16_t>(), W.nw, W.Wn,
-                                 A.cols, r0, r1, b0, b1,
-                                 A.deg(), reinterpret_cast<const uint4*>(x), f, ob, of);
+  kern<<<grid, RB * TPR, kWinSmem, s>>>(W.seg.as<uint32_t>(), W.steplen.as<uint16_t>(), W.ell.as<uint16_t>(), W.nw,
+                                        W.Wn, A.cols, r0, r1, b0, b1, A.deg(), reinterpret_cast<const uint4*>(x), f,
+                                        ob, of);
   BG_LAUNCH_CHECK();
   return true;
 }
@@ -519,11 +549,15 @@ template <bool OUTB>
 bool launch_win_np(bg_frdc& A, const uint32_t* x, int64_t f, uint32_t* ob, float* of, int64_t r0,
                    int64_t r1, cudaStream_t s) {
   const int64_t d = A.max_deg;
-  if (d < (1 << 6)) return launch_win<6, OUTB>(A, x, f, ob, of, r0, r1, s);
-  if (d < (1 << 8)) return launch_win<8, OUTB>(A, x, f, ob, of, r0, r1, s);
-  if (d < (1 << 10)) return launch_win<10, OUTB>(A, x, f, ob, of, r0, r1, s);
-  if (d < (1 << 12)) return launch_win<12, OUTB>(A, x, f, ob, of, r0, r1, s);
-  return false;
+  auto go = [&](auto tpr) {
+    constexpr int TPR = decltype(tpr)::value;
+    if (d < (1 << 6)) return launch_win<6, OUTB, TPR>(A, x, f, ob, of, r0, r1, s);
+    if (d < (1 << 8)) return launch_win<8, OUTB, TPR>(A, x, f, ob, of, r0, r1, s);
+    if (d < (1 << 10)) return launch_win<10, OUTB, TPR>(A, x, f, ob, of, r0, r1, s);
+    if (d < (1 << 12)) return launch_win<12, OUTB, TPR>(A, x, f, ob, of, r0, r1, s);
+    return false;
+  };
+  return win_tpr() == 1 ? go(std::integral_constant<int, 1>{}) : go(std::integral_constant<int, 2>{});
 }
 
 }  // namespace

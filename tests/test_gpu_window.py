@@ -174,3 +174,23 @@ def test_softmax_rows_matches_oracle(cols):
     assert np.array_equal(np.isnan(got), np.isnan(want))
     ok = np.isfinite(want)
     assert np.allclose(got[ok], want[ok], rtol=1e-6, atol=1e-12)
+
+
+@pytest.mark.parametrize("tpr", ["1", "2"])
+@pytest.mark.parametrize("v", ["BSpMM.BBB", "BSpMM.BBF"])
+def test_window_threads_per_row_variants(window_mode, monkeypatch, tpr, v):
+    # both thread mappings of the windowed kernel (one or two threads per row)
+    monkeypatch.setenv("BG_WINDOW_TPR", tpr)
+    window_mode(97)
+    n, e, f = 3000, 200000, 128
+    rng = po.Rng(9500)
+    s, d = rng.random_edges(n, e, True)
+    A = po.frdc_from_edges(n, s, d, True)
+    dA = bg.frdc_from_edges(n, s, d, True)
+    dx, ox = _bits_operand(rng.random_dense(n, f), 32)
+    got = bg.bspmm(v, bg.AdjacencyOperand(dA), dx, None, 32)
+    want = po.bspmm(v, A, ox, None, None, 32)
+    if want.prec == po.B:
+        assert bits_equal(got.bits.numpy(), want.bits)
+    else:
+        assert np.array_equal(got.cpu().numpy(), want.f)
