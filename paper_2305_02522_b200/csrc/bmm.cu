@@ -12,6 +12,7 @@
 // read X exactly once and never write packed X back (north-star item 4).
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 
 #include "ops.cuh"
 #include "async.cuh"
@@ -533,6 +534,232 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
   }
 }
 
+// ---- FBB on the 5th-generation tensor cores (tcgen05.mma.kind::i8) -------------
+// A persistent CTA per SM walks 128-row tiles of X.  All warps convert the
+// tile's fp32 rows to +-1 bytes (x >= 0 -> +1, bitdense.cpp:83) straight from
+// global memory into shared memory in the canonical no-swizzle K-major UMMA
+// layout -- element (r, k) at (k/16)*128*16 + r*16 + k%16, i.e. 8x16-byte core
+// matrices, SBO = 128 B between 8-row groups, LBO = 2 KB between 16-byte K
+// chunks.  One thread then issues ceil(K/32) tcgen05.mma.kind::i8 (M = N =
+// 128, s8 x s8 -> s32) into a TMEM accumulator and commits to an mbarrier;
+// warps 0-3 read the accumulator back with tcgen05.ld.32x32b.x32 -- thread =
+// output row, 32 columns per load -- and pack dot >= 0 into one output word
+// per load (kernels.cpp:166-171).  The weights (N <= 128 columns) are +-1
+// bytes in the same layout for the whole kernel; the tensor core reads both
+// operands from shared memory once per 128 rows.
+constexpr int kUmmaM = 128, kUmmaN = 128;
+
+// mbarrier wait that traps (a launch error) instead of hanging if the phase
+// never completes -- a malformed MMA would otherwise wedge the GPU.
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  for (uint32_t it = 0; it < (1u << 24) && !ok; ++it)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  if (!ok) __trap();
+}
+constexpr int kUmmaThreads = 512;
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // descriptor version (sm_100)
+  return d;                             // base offset 0, layout SWIZZLE_NONE (0)
+}
+
+// kind::i8 instruction descriptor: D s32, A/B signed 8-bit, K-major, N = 128, M = 128.
+constexpr uint32_t kIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | ((kUmmaN >> 3) << 17) | ((kUmmaM >> 4) << 24);
+
+__device__ __forceinline__ void umma_epilogue(uint32_t tmem_acc, int warp, int lane, int64_t row0, int valid,
+                                              int n, int ospw, uint32_t* __restrict__ out_bits) {
+  const int r = 32 * warp + lane;
+  uint32_t words[4];
+#pragma unroll
+  for (int cw = 0; cw < 4; ++cw) {
+    uint32_t d[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
+          "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15]),
+          "=r"(d[16]), "=r"(d[17]), "=r"(d[18]), "=r"(d[19]), "=r"(d[20]), "=r"(d[21]), "=r"(d[22]),
+          "=r"(d[23]), "=r"(d[24]), "=r"(d[25]), "=r"(d[26]), "=r"(d[27]), "=r"(d[28]), "=r"(d[29]),
+          "=r"(d[30]), "=r"(d[31])
+        : "r"(tmem_acc + (static_cast<uint32_t>(32 * warp) << 16) + 32u * cw));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    uint32_t m = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) m |= (static_cast<int32_t>(d[j]) >= 0 ? 1u : 0u) << (31 - j);
+    if (32 * cw + 32 > n) m &= 32 * cw >= n ? 0u : tail_mask32(n);
+    words[cw] = m;
+  }
+  if (r < valid) {
+    uint32_t* o = out_bits + (row0 + r) * ospw;
+    for (int w = 0; w < ospw; ++w) o[w] = w < 4 ? words[w] : 0u;
+  }
+}
+
+__global__ void __launch_bounds__(kUmmaThreads, 1)
+    k_fbb_umma(const float* __restrict__ a_f, const uint32_t* __restrict__ wt, int64_t rows, int k, int kspw,
+               int n, int ksteps, int ospw, uint32_t qmagic, uint32_t* __restrict__ out_bits) {
+  extern __shared__ __align__(1024) uint8_t um_smem[];
+  __shared__ __align__(8) uint64_t mma_done;
+  __shared__ uint32_t tmem_base;
+  const int kpad = 32 * ksteps;
+  const int chunk = kUmmaM * 16;            // bytes per 16-byte K chunk of a 128-row operand
+  uint8_t* A = um_smem;                     // kpad/16 chunks x 128 rows x 16 B
+  uint8_t* Bw = um_smem + kpad * kUmmaM;    // same layout, 128 output columns
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // weights: column o, element kk -> +-1 byte at (kk/16)*chunk + o*16 + kk%16 (0 past K / n)
+  for (int t = tid; t < kUmmaN * (kpad / 4); t += blockDim.x) {
+    const int o = t / (kpad / 4), p4 = (t % (kpad / 4)) * 4;
+    uint32_t v = 0;
+    if (o < n && p4 < k) {
+      const uint32_t word = __ldg(wt + static_cast<int64_t>(o) * kspw + (p4 >> 5));
+      const uint32_t nib = (word >> (28 - (p4 & 31))) & 0xFu;
+      const uint32_t spread = ((nib >> 3) & 1u) | (((nib >> 2) & 1u) << 8) | (((nib >> 1) & 1u) << 16) | ((nib & 1u) << 24);
+      v = 0xFFFFFFFFu - 0xFEu * spread;
+      if (p4 + 4 > k) v &= 0xFFFFFFFFu >> (8 * (p4 + 4 - k));
+    }
+    *reinterpret_cast<uint32_t*>(Bw + (p4 >> 4) * chunk + o * 16 + (p4 & 15)) = v;
+  }
+  // zero the A columns [8*ceil(K/8), kpad) once; the conversion never writes them
+  for (int t = tid; t < kUmmaM * (kpad / 4); t += blockDim.x) {
+    const int r = t / (kpad / 4), p4 = (t % (kpad / 4)) * 4;
+    if (p4 >= (k + 7) / 8 * 8) *reinterpret_cast<uint32_t*>(A + (p4 >> 4) * chunk + r * 16 + (p4 & 15)) = 0u;
+  }
+  if (warp == 0) {  // TMEM: 128 lanes x 128 s32 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_base)),
+                 "r"(kUmmaN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    mbar_init(&mma_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // weights visible to the tensor core
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base;
+  const uint32_t q = (k + 7) / 8, items = kUmmaM * q;
+  const bool keven = (k & 1) == 0;
+  const int64_t tiles = (rows + kUmmaM - 1) / kUmmaM;
+  uint32_t phase = 0;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, phase ^= 1u) {
+    const int64_t row0 = tile * kUmmaM;
+    const int valid = static_cast<int>(rows - row0 < kUmmaM ? rows - row0 : kUmmaM);
+    const float* src = a_f + row0 * static_cast<int64_t>(k);
+    // fp32 -> +-1 bytes, item t = (row r, 8-column group): coalesced 8-byte
+    // loads along a row, four items per thread in flight (all loads first;
+    // rows past the operand are clamped for the load and zeroed after)
+    for (uint32_t t0 = tid; t0 < items; t0 += 4 * blockDim.x) {
+      uint32_t rr[4], cc[4];
+      float2 ld[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t t = min(t0 + u * blockDim.x, items - 1);
+        rr[u] = __umulhi(t, qmagic);
+        cc[u] = 8 * (t - rr[u] * q);
+        const uint32_t rl = min(rr[u], static_cast<uint32_t>(valid - 1));
+        const float* x = src + static_cast<int64_t>(rl) * k + cc[u];
+        const int lim = k - static_cast<int>(cc[u]);
+        if (keven) {
+#pragma unroll
+          for (int h = 0; h < 4; ++h)
+            ld[u][h] = 2 * h < lim ? __ldg(reinterpret_cast<const float2*>(x) + h) : make_float2(0.0f, 0.0f);
+        } else {
+#pragma unroll
+          for (int h = 0; h < 4; ++h)
+            ld[u][h] = make_float2(2 * h < lim ? __ldg(x + 2 * h) : 0.0f, 2 * h + 1 < lim ? __ldg(x + 2 * h + 1) : 0.0f);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t t = t0 + u * blockDim.x;
+        if (t >= items) break;
+        uint2 v = make_uint2(0u, 0u);
+        if (static_cast<int>(rr[u]) < valid) {
+          v.x = sign_bytes4(ld[u][0].x, ld[u][0].y, ld[u][1].x, ld[u][1].y);
+          v.y = sign_bytes4(ld[u][2].x, ld[u][2].y, ld[u][3].x, ld[u][3].y);
+          if (cc[u] + 8 > static_cast<uint32_t>(k)) {
+            const int rem = k - static_cast<int>(cc[u]);
+            v.x &= rem >= 4 ? 0xFFFFFFFFu : 0xFFFFFFFFu >> (8 * (4 - rem));
+            v.y &= rem <= 4 ? 0u : 0xFFFFFFFFu >> (8 * (8 - rem));
+          }
+        }
+        *reinterpret_cast<uint2*>(A + (cc[u] >> 4) * chunk + rr[u] * 16 + (cc[u] & 15)) = v;
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t abase = smem_addr(A), bbase = smem_addr(Bw);
+      for (int ks = 0; ks < ksteps; ++ks) {
+        const uint64_t ad = umma_desc(abase + 2 * ks * chunk, chunk, 128);
+        const uint64_t bd = umma_desc(bbase + 2 * ks * chunk, chunk, 128);
+        const uint32_t acc = ks > 0 ? 1u : 0u;
+        asm volatile(
+            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+            " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+            "l"(ad), "l"(bd), "r"(kIdescI8), "r"(acc)
+            : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_addr(&mma_done))
+                   : "memory");
+    }
+    mbar_wait_bounded(&mma_done, phase);  // MMAs done: A may be overwritten, TMEM holds the tile
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp < 4) umma_epilogue(tmem, warp, lane, row0, valid, n, ospw, out_bits);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();  // TMEM read back before the next tile's MMAs
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kUmmaN) : "memory");
+}
+
+// FBB through k_fbb_umma (opt-in: BG_FBB=umma); false when not selected or
+// not eligible.  Measured on Reddit (FBB 564.7 MB): 0.175 ms against 0.158 ms
+// for the TMA-fed mma.sync kernel -- the tensor core is idle >90% either way;
+// what differs is how the fp32 stream reaches shared memory (here 8-byte LDGs,
+// there one bulk copy per 16-row tile), and a TMA-fed variant of this kernel
+// does not fit: 3 fp32 stages + the 128-row A tile + the weights exceed 227 KB.
+bool fbb_umma(const BmmArgs& a, cudaStream_t s) {
+  if (a.a_f == nullptr || a.out_bits == nullptr || a.n > kUmmaN || a.k <= 8) return false;
+  const char* e = std::getenv("BG_FBB");
+  if (!e || std::string(e) != "umma") return false;
+  const int ksteps = static_cast<int>(cdiv(a.k, 32));
+  const size_t smem = static_cast<size_t>(2) * kUmmaM * 32 * ksteps;
+  if (smem > 200 * 1024) return false;
+  const int kspw = static_cast<int>(spw(a.k, a.wb));
+  const int ospw = static_cast<int>(spw(a.n, a.wb));
+  const uint32_t q = static_cast<uint32_t>((a.k + 7) / 8);
+  if (q > 5792) return false;  // t / q == umulhi(t, ceil(2^32/q)) for t < 128 q: error 128 q^2 < 2^32
+  const uint32_t qmagic = static_cast<uint32_t>(((uint64_t{1} << 32) + q - 1) / q);
+  static bool attr = false;
+  if (!attr) {
+    BG_CUDA(cudaFuncSetAttribute(k_fbb_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  const int64_t tiles = (a.rows + kUmmaM - 1) / kUmmaM;
+  const int64_t blocks = std::min<int64_t>(tiles, sm_count());
+  k_fbb_umma<<<static_cast<unsigned>(blocks), kUmmaThreads, smem, s>>>(
+      a.a_f, a.wt, a.rows, static_cast<int>(a.k), kspw, static_cast<int>(a.n), ksteps, ospw, qmagic, a.out_bits);
+  BG_LAUNCH_CHECK();
+  return true;
+}
+
 // FBB through k_fbb_tma (all rows; 0 = not eligible, use the direct kernel).
 int64_t fbb_tma(const BmmArgs& a, cudaStream_t s) {
   if (a.a_f == nullptr || a.out_bits == nullptr || a.n > 128 || a.k <= 8 || std::getenv("BG_BMM_POPC")) return 0;
@@ -666,6 +893,7 @@ void bmm(const BmmArgs& a, cudaStream_t s) {
   if (imma_ok(a)) {
     if (ob) {
       // whole 16-row tiles on the TMA-fed kernel, the rest on the direct one
+      if (fbb_umma(a, s)) return;
       const int64_t done = fbb_tma(a, s);
       if (done < a.rows) {
         BmmArgs rest = a;

@@ -1,0 +1,40 @@
+"""MM.FBB on the tcgen05 tensor cores (bmm.cu k_fbb_umma, opt-in BG_FBB=umma):
++-1 int8 operands in shared memory, s32 accumulators in TMEM.  Bit-exact
+against the oracle on tile-aligned and ragged shapes (partial 128-row tiles,
+odd K, N below the 128-column MMA, 64-bit words)."""
+import numpy as np
+import pytest
+import torch
+
+import pyoracle as po
+from helpers import bits_equal
+
+import paper_2305_02522_b200 as bg
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def umma(monkeypatch):
+    monkeypatch.setenv("BG_FBB", "umma")
+
+
+@pytest.mark.parametrize("wb", [32, 64])
+@pytest.mark.parametrize("mkn", [(128, 602, 128), (1000, 602, 128), (257, 33, 21), (300, 100, 128), (129, 500, 64),
+                                 (5, 17, 7), (4096, 301, 96), (640, 1024, 128), (77, 64, 32), (2000, 1433, 64)])
+def test_fbb_umma_matches_oracle(umma, wb, mkn):
+    m, k, n = mkn
+    rng = po.Rng(4242 + m + k + n)
+    A, W = rng.random_dense(m, k), rng.random_dense(k, n)
+    A.flat[::13] = 0.0
+    A.flat[5::17] = -0.0
+    wbits = po.binarize(W, wb)
+    dw = bg.BitOperand(bg.BitDenseMatrix.from_numpy(wbits, k, n, wb))
+    ow = po.Mat.binary(wbits, k, n, wb)
+    sc = po.l1_scales(W, po.COL)
+    dw.scale = torch.from_numpy(sc).cuda()
+    dw.scale_axis = bg.bitgnn.COL
+    ow.scale = sc
+    got = bg.bmm("BMM.FBB", torch.from_numpy(A).cuda(), dw, wb)
+    want = po.bmm("BMM.FBB", po.Mat.dense(A), ow, wb)
+    assert bits_equal(got.bits.numpy(), want.bits)
