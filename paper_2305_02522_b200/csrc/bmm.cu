@@ -729,6 +729,198 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kUmmaN) : "memory");
 }
 
+// TMA-fed variant: the fp32 rows arrive by bulk copies of 8-row sub-tiles
+// (contiguous, 16-byte multiples) into a 3-slot ring; team t of three
+// converts sub-tiles u = t (mod 3) -- slot t is only ever consumed and
+// refilled by team t, so its mbarrier phases are waited in order -- into the
+// 128-row A tile; after a tile's 16 sub-tiles one thread issues the MMAs and
+// warps 0-3 read the accumulator back.  Shared memory: weights + A + ring =
+// 2*128*kpad + 3*8*K*4 bytes (213 KB at K = 602).
+constexpr int kU2Teams = 3;
+
+__global__ void __launch_bounds__(kU2Teams * 128, 1)
+    k_fbb_umma2(const float* __restrict__ a_f, const uint32_t* __restrict__ wt, int64_t rows, int k, int kspw,
+                int n, int ksteps, int ospw, uint32_t qmagic, int sr, uint32_t* __restrict__ out_bits) {
+  extern __shared__ __align__(1024) uint8_t u2_smem[];
+  const int kU2Sub = sr;  // rows per sub-tile: 8..128, divides 128
+  __shared__ __align__(8) uint64_t full[kU2Teams], mma_done;
+  __shared__ uint32_t tmem_base;
+  const int kpad = 32 * ksteps;
+  const int chunk = kUmmaM * 16;
+  uint8_t* Bw = u2_smem;
+  uint8_t* A = u2_smem + kpad * kUmmaN;
+  float* ring = reinterpret_cast<float*>(u2_smem + 2 * kpad * kUmmaM);
+  const uint32_t slot_bytes = static_cast<uint32_t>(kU2Sub * k) * 4u;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int team = warp / 4, ttid = tid - team * 128;
+  for (int t = tid; t < kUmmaN * (kpad / 4); t += blockDim.x) {
+    const int o = t / (kpad / 4), p4 = (t % (kpad / 4)) * 4;
+    uint32_t v = 0;
+    if (o < n && p4 < k) {
+      const uint32_t word = __ldg(wt + static_cast<int64_t>(o) * kspw + (p4 >> 5));
+      const uint32_t nib = (word >> (28 - (p4 & 31))) & 0xFu;
+      const uint32_t spread = ((nib >> 3) & 1u) | (((nib >> 2) & 1u) << 8) | (((nib >> 1) & 1u) << 16) | ((nib & 1u) << 24);
+      v = 0xFFFFFFFFu - 0xFEu * spread;
+      if (p4 + 4 > k) v &= 0xFFFFFFFFu >> (8 * (p4 + 4 - k));
+    }
+    *reinterpret_cast<uint32_t*>(Bw + (p4 >> 4) * chunk + o * 16 + (p4 & 15)) = v;
+  }
+  for (int t = tid; t < kUmmaM * (kpad / 4); t += blockDim.x) {  // A columns past 8*ceil(K/8) stay zero
+    const int r = t / (kpad / 4), p4 = (t % (kpad / 4)) * 4;
+    if (p4 >= (k + 7) / 8 * 8) *reinterpret_cast<uint32_t*>(A + (p4 >> 4) * chunk + r * 16 + (p4 & 15)) = 0u;
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_base)),
+                 "r"(kUmmaN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  const int64_t tiles = (rows + kUmmaM - 1) / kUmmaM;
+  const int64_t my = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t nsub = my * (kUmmaM / kU2Sub);
+  // sub-tile u of this CTA: tile blockIdx.x + (u/16)*grid, rows +8*(u%16); rows past the operand -> no copy
+  // full sub-tiles arrive by bulk copy; a partial one (rows % sr) is read
+  // straight from global memory (a copy must be a 16-byte multiple and must
+  // not read past the operand), so its slot only gets a plain arrive
+  auto sub_rows = [&](int64_t u, int64_t* r0) {
+    const int64_t tile = blockIdx.x + (u / (kUmmaM / kU2Sub)) * gridDim.x;
+    *r0 = tile * kUmmaM + kU2Sub * (u % (kUmmaM / kU2Sub));
+    const int64_t left = rows - *r0;
+    return static_cast<int>(left <= 0 ? 0 : left < kU2Sub ? left : kU2Sub);
+  };
+  auto issue = [&](int64_t u) {
+    int64_t r0;
+    const int nr = sub_rows(u, &r0);
+    uint64_t* bar = &full[u % kU2Teams];
+    if (nr == kU2Sub) {
+      const uint32_t bytes = static_cast<uint32_t>(nr * k) * 4u;
+      mbar_expect_tx(bar, bytes);
+      bulk_g2s(ring + (u % kU2Teams) * (slot_bytes / 4), a_f + r0 * static_cast<int64_t>(k), bytes, bar);
+    } else {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+    }
+  };
+  if (tid == 0) {
+    for (int t = 0; t < kU2Teams; ++t) mbar_init(&full[t], 1);
+    mbar_init(&mma_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int64_t u = 0; u < kU2Teams && u < nsub; ++u) issue(u);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base;
+  const uint32_t q = (k + 7) / 8, items = static_cast<uint32_t>(kU2Sub) * q;
+  const bool keven = (k & 1) == 0;
+  for (int64_t ti = 0; ti < my; ++ti) {
+    const int64_t row0 = (blockIdx.x + ti * gridDim.x) * kUmmaM;
+    const int valid = static_cast<int>(rows - row0 < kUmmaM ? rows - row0 : kUmmaM);
+    // this team's sub-tiles of tile ti
+    for (int64_t u = ti * (kUmmaM / kU2Sub); u < (ti + 1) * (kUmmaM / kU2Sub); ++u) {
+      if (u % kU2Teams != team) continue;
+      mbar_wait_bounded(&full[team], static_cast<uint32_t>(u / kU2Teams) & 1u);
+      int64_t r0;
+      const int nr = sub_rows(u, &r0);
+      const int rbase = static_cast<int>(kU2Sub * (u % (kUmmaM / kU2Sub)));
+      const float* src = nr == kU2Sub ? ring + team * (slot_bytes / 4) : a_f + r0 * static_cast<int64_t>(k);
+      for (uint32_t t = ttid; t < items; t += 128) {
+        const uint32_t r = __umulhi(t, qmagic);
+        const uint32_t c = 8 * (t - r * q);
+        uint2 v = make_uint2(0u, 0u);
+        if (static_cast<int>(r) < nr) {
+          const float* x = src + r * k + c;
+          float e[8];
+          if (keven && c + 8 <= static_cast<uint32_t>(k)) {
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const float2 p2 = *reinterpret_cast<const float2*>(x + 2 * h);
+              e[2 * h] = p2.x;
+              e[2 * h + 1] = p2.y;
+            }
+          } else {
+#pragma unroll
+            for (int h = 0; h < 8; ++h) e[h] = c + h < static_cast<uint32_t>(k) ? x[h] : 0.0f;
+          }
+          v.x = sign_bytes4(e[0], e[1], e[2], e[3]);
+          v.y = sign_bytes4(e[4], e[5], e[6], e[7]);
+          if (c + 8 > static_cast<uint32_t>(k)) {
+            const int rem = k - static_cast<int>(c);
+            v.x &= rem >= 4 ? 0xFFFFFFFFu : 0xFFFFFFFFu >> (8 * (4 - rem));
+            v.y &= rem <= 4 ? 0u : 0xFFFFFFFFu >> (8 * (8 - rem));
+          }
+        }
+        *reinterpret_cast<uint2*>(A + (c >> 4) * chunk + (rbase + r) * 16 + (c & 15)) = v;
+      }
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + team) : "memory");  // the team is done with its slot
+      if (ttid == 0 && u + kU2Teams < nsub) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(u + kU2Teams);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // A (generic writes) -> tensor core
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t abase = smem_addr(A), bbase = smem_addr(Bw);
+      for (int ks = 0; ks < ksteps; ++ks) {
+        const uint64_t ad = umma_desc(abase + 2 * ks * chunk, chunk, 128);
+        const uint64_t bd = umma_desc(bbase + 2 * ks * chunk, chunk, 128);
+        const uint32_t acc = ks > 0 ? 1u : 0u;
+        asm volatile(
+            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+            " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+            "l"(ad), "l"(bd), "r"(kIdescI8), "r"(acc)
+            : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_addr(&mma_done))
+                   : "memory");
+    }
+    mbar_wait_bounded(&mma_done, static_cast<uint32_t>(ti & 1));
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp < 4) umma_epilogue(tmem, warp, lane, row0, valid, n, ospw, out_bits);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kUmmaN) : "memory");
+}
+
+bool fbb_umma2(const BmmArgs& a, cudaStream_t s) {
+  if (a.a_f == nullptr || a.out_bits == nullptr || a.n > kUmmaN || a.k <= 8) return false;
+  if (reinterpret_cast<uintptr_t>(a.a_f) % 16 != 0) return false;
+  const char* e = std::getenv("BG_FBB");  // opt-in: measured 0.246 ms on Reddit vs 0.158 ms default
+  if (!e || std::string(e) != "umma2") return false;
+  const int ksteps = static_cast<int>(cdiv(a.k, 32));
+  // rows per fp32 sub-tile: the largest of 128, 64, ..., 8 whose 3 ring slots fit
+  const size_t ab = static_cast<size_t>(2) * kUmmaM * 32 * ksteps;
+  int sr = 128;
+  while (sr > 8 && ab + static_cast<size_t>(kU2Teams) * sr * a.k * 4 > 226 * 1024) sr /= 2;
+  const size_t smem = ab + static_cast<size_t>(kU2Teams) * sr * a.k * 4;
+  if (smem > 226 * 1024) return false;
+  const int kspw = static_cast<int>(spw(a.k, a.wb));
+  const int ospw = static_cast<int>(spw(a.n, a.wb));
+  const uint32_t q = static_cast<uint32_t>((a.k + 7) / 8);
+  if (q > 5792) return false;  // t / q == umulhi(t, ceil(2^32/q)) for t < 128 q: error 128 q^2 < 2^32
+  const uint32_t qmagic = static_cast<uint32_t>(((uint64_t{1} << 32) + q - 1) / q);
+  static bool attr = false;
+  if (!attr) {
+    BG_CUDA(cudaFuncSetAttribute(k_fbb_umma2, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+    attr = true;
+  }
+  const int64_t tiles = (a.rows + kUmmaM - 1) / kUmmaM;
+  const int64_t blocks = std::min<int64_t>(tiles, sm_count());
+  k_fbb_umma2<<<static_cast<unsigned>(blocks), kU2Teams * 128, smem, s>>>(
+      a.a_f, a.wt, a.rows, static_cast<int>(a.k), kspw, static_cast<int>(a.n), ksteps, ospw, qmagic, sr,
+      a.out_bits);
+  BG_LAUNCH_CHECK();
+  return true;
+}
+
 // FBB through k_fbb_umma (opt-in: BG_FBB=umma); false when not selected or
 // not eligible.  Measured on Reddit (FBB 564.7 MB): 0.175 ms against 0.158 ms
 // for the TMA-fed mma.sync kernel -- the tensor core is idle >90% either way;
@@ -894,6 +1086,7 @@ void bmm(const BmmArgs& a, cudaStream_t s) {
     if (ob) {
       // whole 16-row tiles on the TMA-fed kernel, the rest on the direct one
       if (fbb_umma(a, s)) return;
+      if (fbb_umma2(a, s)) return;
       const int64_t done = fbb_tma(a, s);
       if (done < a.rows) {
         BmmArgs rest = a;

@@ -1,4 +1,4 @@
-"""MM.FBB on the tcgen05 tensor cores (bmm.cu k_fbb_umma, opt-in BG_FBB=umma):
+"""MM.FBB on the tcgen05 tensor cores (bmm.cu k_fbb_umma / k_fbb_umma2, opt-in BG_FBB=umma|umma2):
 +-1 int8 operands in shared memory, s32 accumulators in TMEM.  Bit-exact
 against the oracle on tile-aligned and ragged shapes (partial 128-row tiles,
 odd K, N below the 128-column MMA, 64-bit words)."""
@@ -14,9 +14,10 @@ import paper_2305_02522_b200 as bg
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture
-def umma(monkeypatch):
-    monkeypatch.setenv("BG_FBB", "umma")
+@pytest.fixture(params=["umma", "umma2"])
+def umma(monkeypatch, request):
+    # umma: LDG-fed conversion; umma2: bulk-copied fp32 sub-tiles (TMA ring)
+    monkeypatch.setenv("BG_FBB", request.param)
 
 
 @pytest.mark.parametrize("wb", [32, 64])
