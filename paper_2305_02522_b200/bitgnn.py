@@ -648,7 +648,9 @@ class Model:
         return out, [KernelTiming(arr[i].label.decode(), arr[i].ms) for i in range(n.value)]
 
     def forward_host(self, x: np.ndarray, logits: bool = False, stream: Optional[torch.cuda.Stream] = None):
-        """End-to-end call with host buffers (H2D + forward + D2H)."""
+        """End-to-end call with host buffers (H2D + forward + D2H).  The
+        returned host tensors are the model's pinned result buffers: they stay
+        valid until the next forward_host call (clone to keep them)."""
         if isinstance(x, torch.Tensor):
             xh = x.contiguous()
             rows, cols, xp = xh.shape[0], xh.shape[1], xh.data_ptr()
@@ -656,8 +658,14 @@ class Model:
             xh = np.ascontiguousarray(x, dtype=np.float32)
             rows, cols, xp = xh.shape[0], xh.shape[1], xh.ctypes.data
         oc = self.output_cols()
-        out = torch.empty((rows, oc), dtype=torch.float32, pin_memory=True)
-        lg = torch.empty((rows, oc), dtype=torch.float32, pin_memory=True) if logits else None
+        # pinned result buffers are reused across calls with the same shape
+        # (page-locking 10s of MB per call would cost more than the copy)
+        cache = getattr(self, "_host_out", None)
+        if cache is None or cache[0].shape != (rows, oc) or (logits and cache[1] is None):
+            cache = (torch.empty((rows, oc), dtype=torch.float32, pin_memory=True),
+                     torch.empty((rows, oc), dtype=torch.float32, pin_memory=True) if logits else None)
+            self._host_out = cache
+        out, lg = cache[0], (cache[1] if logits else None)
         s = (stream or torch.cuda.current_stream()).cuda_stream
         check(lib().bg_model_forward_host(self._h, xp, rows, cols, out.data_ptr(),
                                           lg.data_ptr() if lg is not None else None, s))

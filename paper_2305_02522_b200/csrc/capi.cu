@@ -539,31 +539,74 @@ int bg_model_forward(bg_model* m, const bg_mat* x0, float* out, float* logits, b
   });
 }
 
+// Host buffers in and out (the reference-facing call).  The fp32 input
+// streams in row chunks on an internal copy stream while layer 0's MM runs
+// on the chunks that have landed; the last layer produces its output per row
+// chunk and each chunk is copied out as soon as it is ready.  Results and
+// their order are those of bg_model_forward.
 int bg_model_forward_host(bg_model* m, const float* xh, int64_t rows, int64_t cols, float* outh,
                           float* logh, bg_stream s) {
   int64_t oc = 0;
   int rc = bg_model_output_cols(m, &oc);
   if (rc) return rc;
-  rc = guard([&] {
+  return guard([&] {
+    need(xh, "input");
+    need(outh, "output");
+    cudaStream_t st = S(s);
     const size_t xb = static_cast<size_t>(rows * cols) * 4, ob = static_cast<size_t>(rows * oc) * 4;
     if (m->hx.bytes < xb) m->hx.alloc(xb);
     if (m->hout.bytes < ob) m->hout.alloc(ob);
     if (logh && m->hlog.bytes < ob) m->hlog.alloc(ob);
-    BG_CUDA(cudaMemcpyAsync(m->hx.p, xh, xb, cudaMemcpyHostToDevice, S(s)));
-  });
-  if (rc) return rc;
-  bg_mat x{};
-  x.precision = BG_F;
-  x.rows = rows;
-  x.cols = cols;
-  x.data = m->hx.p;
-  rc = bg_model_forward(m, &x, m->hout.as<float>(), logh ? m->hlog.as<float>() : nullptr, s);
-  if (rc) return rc;
-  return guard([&] {
-    const size_t ob = static_cast<size_t>(rows * oc) * 4;
-    BG_CUDA(cudaMemcpyAsync(outh, m->hout.p, ob, cudaMemcpyDeviceToHost, S(s)));
-    if (logh) BG_CUDA(cudaMemcpyAsync(logh, m->hlog.p, ob, cudaMemcpyDeviceToHost, S(s)));
-    BG_CUDA(cudaStreamSynchronize(S(s)));
+    const int nc = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, rows / 4096)));
+    if (!m->copy_stream) BG_CUDA(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking));
+    while (m->chunk_events.size() < static_cast<size_t>(2 * nc + 1)) {
+      cudaEvent_t e;
+      BG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      m->chunk_events.push_back(e);
+    }
+    cudaStream_t cs = m->copy_stream;
+    cudaEvent_t* in_ev = m->chunk_events.data();
+    cudaEvent_t* out_ev = in_ev + nc;
+    cudaEvent_t done_ev = in_ev[2 * nc];
+    std::vector<int64_t> bounds(nc + 1);
+    for (int c = 0; c <= nc; ++c) bounds[c] = rows * c / nc / 16 * 16;
+    bounds[nc] = rows;
+    // the copy stream starts after everything already queued on the caller's stream
+    BG_CUDA(cudaEventRecord(done_ev, st));
+    BG_CUDA(cudaStreamWaitEvent(cs, done_ev, 0));
+    auto* hx = m->hx.as<float>();
+    for (int c = 0; c < nc; ++c) {
+      const size_t off = static_cast<size_t>(bounds[c] * cols), n = static_cast<size_t>((bounds[c + 1] - bounds[c]) * cols);
+      if (n) BG_CUDA(cudaMemcpyAsync(hx + off, xh + off, n * 4, cudaMemcpyHostToDevice, cs));
+      BG_CUDA(cudaEventRecord(in_ev[c], cs));
+    }
+    StreamChunks sc;
+    sc.in = RowChunks{nc, bounds.data(), in_ev};
+    sc.out = RowChunks{nc, bounds.data(), out_ev};
+    const Op x0 = [&] {
+      Op o;
+      o.prec = BG_F;
+      o.rows = rows;
+      o.cols = cols;
+      o.f = hx;
+      return o;
+    }();
+    if (x0.prec != m->input_prec) fail("model input tag does not match the provided operand");
+    forward_impl(*m, x0, m->hout.as<float>(), logh ? m->hlog.as<float>() : nullptr, nullptr, nullptr, st, &sc);
+    auto* ho = m->hout.as<float>();
+    if (sc.out_done) {
+      for (int c = 0; c < nc; ++c) {
+        const size_t off = static_cast<size_t>(bounds[c] * oc), n = static_cast<size_t>((bounds[c + 1] - bounds[c]) * oc);
+        BG_CUDA(cudaStreamWaitEvent(cs, out_ev[c], 0));
+        if (n) BG_CUDA(cudaMemcpyAsync(outh + off, ho + off, n * 4, cudaMemcpyDeviceToHost, cs));
+      }
+    }
+    BG_CUDA(cudaEventRecord(done_ev, st));
+    BG_CUDA(cudaStreamWaitEvent(cs, done_ev, 0));
+    if (!sc.out_done) BG_CUDA(cudaMemcpyAsync(outh, ho, ob, cudaMemcpyDeviceToHost, cs));
+    if (logh) BG_CUDA(cudaMemcpyAsync(logh, m->hlog.p, ob, cudaMemcpyDeviceToHost, cs));
+    BG_CUDA(cudaStreamSynchronize(cs));
+    BG_CUDA(cudaStreamSynchronize(st));
   });
 }
 

@@ -57,8 +57,17 @@ struct WeightCache {
   int64_t rows = 0, cols = 0;
   int wb = 32;
 };
+// Row chunks of an operand that arrives (or must leave) piecewise: chunk c
+// covers rows [bounds[c], bounds[c+1]); ready[c] is recorded when it is there.
+struct RowChunks {
+  int n = 0;
+  const int64_t* bounds = nullptr;
+  const cudaEvent_t* ready = nullptr;
+};
+// in_chunks: an fp32 activation still being copied in; the MM waits for each
+// chunk's event and runs on it (B outputs only: no row scales are needed).
 Op run_bmm(bg_variant v, const Op& a, const Op* w, const WeightCache* wc, int word_bits, Pool& pool,
-           cudaStream_t s);
+           cudaStream_t s, const RowChunks* in_chunks = nullptr);
 Op run_bspmm(bg_variant v, const bg_frdc* adj, const float* rs, const float* cs, const Op& x,
              int word_bits, Pool& pool, cudaStream_t s);
 Op run_add(bg_variant v, const Op& a, const Op& b, Pool& pool, cudaStream_t s);

@@ -207,10 +207,20 @@ struct Exec {
   bg_model& m;
   Hooks& h;
   cudaStream_t s;
+  const float* x0f = nullptr;           // the model input (fp32), when streamed in
+  const RowChunks* in_chunks = nullptr;  // its row chunks (host entry point)
 
   // ref: run_mm_slot (graphops.cpp:47-77)
+  // every chunk of a streamed input has landed (before any op that is not a
+  // chunk-aware MM reads it)
+  void wait_all_in() {
+    if (!in_chunks) return;
+    for (int c = 0; c < in_chunks->n; ++c) BG_CUDA(cudaStreamWaitEvent(s, in_chunks->ready[c], 0));
+  }
+
   Op mm_slot(bg_variant mm, const Op& x, const WeightDev& w, const std::string& label) {
     if (mm.op != BG_BMM) fail(label + ": plan slot expects an MM variant");
+    if (in_chunks && x.f == x0f && (is_dense_fff(mm) || h.trace)) wait_all_in();
     if (is_dense_fff(mm)) {
       if (x.prec != BG_F) fail(label + ": MM.FFF expects a full-precision input");
       if (x.cols != w.rows) fail("dense_mm: inner dimensions disagree");
@@ -234,7 +244,8 @@ struct Exec {
     }
     const WeightCache wc = w.cache();
     h.begin(label + "[" + variant_name(mm) + "]");
-    Op r = run_bmm(mm, x, nullptr, &wc, m.wb, m.pool, s);
+    const RowChunks* streamed = (in_chunks && x.prec == BG_F && x.f == x0f) ? in_chunks : nullptr;
+    Op r = run_bmm(mm, x, nullptr, &wc, m.wb, m.pool, s, streamed);
     h.end();
     if (mm.out == BG_B) h.bits(label + ".out", r.bits, r.rows, r.cols, r.wb);
     return r;
@@ -267,7 +278,7 @@ struct Exec {
 
 void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace* trace,
                   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>>* timing,
-                  cudaStream_t s) {
+                  cudaStream_t s, StreamChunks* chunks) {
   {
     std::vector<std::string> errors = validate_model(m.graph != nullptr, m.input_prec, m.infos);
     if (!errors.empty()) {
@@ -284,6 +295,18 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
   h.timing = timing;
   h.s = s;
   Exec ex{m, h, s};
+  if (chunks && chunks->in.n > 0 && x0.prec == BG_F) {
+    ex.x0f = x0.f;
+    ex.in_chunks = &chunks->in;
+  }
+  if (ex.in_chunks && !m.layers.empty()) {
+    const int k0 = m.layers[0].info.kind;  // only MM slots stream; anything else reads all of x0
+    if (k0 != BG_LAYER_GCN && k0 != BG_LAYER_SAGE && k0 != BG_LAYER_GRAPHCONV && k0 != BG_LAYER_FC) ex.wait_all_in();
+  }
+  // final output produced per row chunk (so its copy-out overlaps the rest)
+  auto chunked_out = [&](size_t layer_after) {
+    return chunks && chunks->out.n > 0 && layer_after == m.layers.size();
+  };
   Op cur = x0;
   bool logits_set = false;
   float* fused_probs = nullptr;   // softmax already produced by a fused epilogue
@@ -323,8 +346,19 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
               fused_logits = o.f;
             }
             h.begin(prefix + "spmm[" + variant_name(sp) + "]");
-            gcn1_aggregate(A, recs, cur.cols, cur.wb, l.w1.wt.as<uint32_t>(), l.w1.scale.as<float>(),
-                           l.w1.cols, o.f, probs, s);
+            if (probs == out && out && chunked_out(i + 2)) {
+              for (int c = 0; c < chunks->out.n; ++c) {
+                const int64_t r0 = chunks->out.bounds[c], r1 = chunks->out.bounds[c + 1];
+                if (r1 > r0)
+                  gcn1_aggregate(A, recs, cur.cols, cur.wb, l.w1.wt.as<uint32_t>(), l.w1.scale.as<float>(),
+                                 l.w1.cols, o.f, probs, s, r0, r1);
+                BG_CUDA(cudaEventRecord(chunks->out.ready[c], s));
+              }
+              chunks->out_done = true;
+            } else {
+              gcn1_aggregate(A, recs, cur.cols, cur.wb, l.w1.wt.as<uint32_t>(), l.w1.scale.as<float>(),
+                             l.w1.cols, o.f, probs, s);
+            }
             h.end();
             cur = o;
             break;
@@ -393,7 +427,16 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
           } else {
             o.f = (i + 1 == nl && out) ? out : static_cast<float*>(m.pool.get(cur.bytes()));
             h.begin(prefix + "softmax");
-            softmax_rows(cur.f, cur.rows, cur.cols, o.f, s);
+            if (o.f == out && chunked_out(i + 1)) {
+              for (int c = 0; c < chunks->out.n; ++c) {
+                const int64_t r0 = chunks->out.bounds[c], r1 = chunks->out.bounds[c + 1];
+                if (r1 > r0) softmax_rows(cur.f + r0 * cur.cols, r1 - r0, cur.cols, o.f + r0 * cur.cols, s);
+                BG_CUDA(cudaEventRecord(chunks->out.ready[c], s));
+              }
+              chunks->out_done = true;
+            } else {
+              softmax_rows(cur.f, cur.rows, cur.cols, o.f, s);
+            }
             h.end();
           }
           cur = o;

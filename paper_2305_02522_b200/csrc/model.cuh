@@ -79,13 +79,24 @@ struct bg_model {
   cudaGraphExec_t exec = nullptr;
   // Buffers of the host-pointer entry point.
   bg::DevBuf hx, hout, hlog;
+  cudaStream_t copy_stream = nullptr;    // H2D / D2H of the host entry point
+  std::vector<cudaEvent_t> chunk_events;  // 2 x chunks (input landed, output ready)
   ~bg_model() {
     if (exec) cudaGraphExecDestroy(exec);
+    for (cudaEvent_t e : chunk_events) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
   }
 };
 
 namespace bg {
+// Host-streaming context (bg_model_forward_host): the model input arrives in
+// row chunks (in.ready events) and the final output is produced per row chunk
+// (out.ready recorded; out_done set when the last layer did so).
+struct StreamChunks {
+  RowChunks in, out;
+  bool out_done = false;
+};
 void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace* trace,
                   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>>* timing,
-                  cudaStream_t s);
+                  cudaStream_t s, StreamChunks* chunks = nullptr);
 }

@@ -141,7 +141,12 @@ Op bmm_out_desc(bg_variant v, const Op& a, const Op& w, int word_bits) {
 }
 
 Op run_bmm(bg_variant v, const Op& a, const Op* w, const WeightCache* wc, int word_bits,
-           Pool& pool, cudaStream_t s) {
+           Pool& pool, cudaStream_t s, const RowChunks* in_chunks) {
+  // Only FBB-type products stream row chunks; every other variant reads the
+  // whole activation (row scales included), so it waits for all chunks first.
+  const bool stream_rows = in_chunks && in_chunks->n > 0 && v.in1 == BG_F && v.out == BG_B;
+  if (in_chunks && !stream_rows)
+    for (int c = 0; c < in_chunks->n; ++c) BG_CUDA(cudaStreamWaitEvent(s, in_chunks->ready[c], 0));
   Op wdesc;
   Op wtmp;
   if (wc && v.in2 == BG_F) {
@@ -221,6 +226,21 @@ Op run_bmm(bg_variant v, const Op& a, const Op* w, const WeightCache* wc, int wo
     out.f = static_cast<float*>(pool.get(out.bytes()));
     k.out_f = out.f;
     k.beta = beta;
+  }
+  if (stream_rows) {
+    // streamed input: each chunk of rows as soon as its copy has landed
+    const int64_t ospw = spw(out.cols, wb);
+    for (int c = 0; c < in_chunks->n; ++c) {
+      const int64_t r0 = in_chunks->bounds[c], r1 = in_chunks->bounds[c + 1];
+      BG_CUDA(cudaStreamWaitEvent(s, in_chunks->ready[c], 0));
+      if (r1 <= r0) continue;
+      BmmArgs kc = k;
+      kc.rows = r1 - r0;
+      kc.a_f = a.f + r0 * a.cols;
+      kc.out_bits = out.bits + r0 * ospw;
+      bmm(kc, s);
+    }
+    return out;
   }
   bmm(k, s);
   return out;

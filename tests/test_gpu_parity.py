@@ -352,3 +352,23 @@ def test_invalid_model_messages():
     with pytest.raises(bg.InvalidArgument) as e:
         bg.Model(layers + [bg.LayerSpec(bg._lib.LAYER_BINARIZE)], bg.prepare_graph(4, [0], [1]))
     assert str(e.value).startswith("invalid model:")
+
+
+@pytest.mark.parametrize("model,plan", [("gcn", None), ("sage", None), ("saint", None),
+                                        ("gcn", ["MM.FBB+BSpMM.BBB", "MM.BBB+BSpMM.BBB", "MM.BBF+BSpMM.FBF"]),
+                                        ("gcn", ["MM.FBF+BSpMM.FBF", "MM.FBF+BSpMM.FBF"])])
+def test_streamed_host_forward_matches_device_forward(model, plan):
+    # bg_model_forward_host streams X in row chunks (layer-0 MM per chunk) and
+    # copies the output out per chunk; results must equal the device forward
+    n, e = 19717, 88648
+    s, d = po.Rng(100).random_edges(n, e, False)
+    layers, X = po.build_model(model, 500, 64, 3, 99, n, plan)
+    m = bg.Model(to_layer_specs(bg, layers), bg.prepare_graph(n, s, d))
+    dev = m.forward(cuda(X)).cpu()
+    _, dev_log, _ = m.forward_traced(cuda(X))
+    for _ in range(2):  # repeated calls reuse the copy stream, events and buffers
+        host, lg = m.forward_host(torch.from_numpy(X).pin_memory(), logits=True)
+        assert torch.equal(host, dev)
+        assert torch.equal(lg, dev_log.cpu())
+    host2 = m.forward_host(X)  # pageable input
+    assert torch.equal(host2, dev)
