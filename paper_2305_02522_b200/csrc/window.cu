@@ -525,14 +525,20 @@ bool launch_win(bg_frdc& A, const uint32_t* x, int64_t f, uint32_t* ob, float* o
                                            static_cast<int>(A.cols)));
   static const int tmax = max_threads(kern, kWinSmem);  // per instance
   const int64_t rmax = tmax / TPR;                      // rows per block at most
-  const int64_t waves = std::max<int64_t>(1, cdiv(A.rows, static_cast<int64_t>(sms) * rmax));
-  const int RB = static_cast<int>(std::min<int64_t>(
-      rmax / RW * RW, cdiv(cdiv(A.rows, static_cast<int64_t>(sms) * waves), RW) * RW));
+  // blocks sized for the rows this call produces (a rank's shard under
+  // multi-GPU), so every SM gets a block
+  const int64_t nrows = r1 - r0;
+  const int64_t waves = std::max<int64_t>(1, cdiv(nrows, static_cast<int64_t>(sms) * rmax));
+  const int RB = static_cast<int>(std::max<int64_t>(RW, std::min<int64_t>(
+      rmax / RW * RW, cdiv(cdiv(nrows, static_cast<int64_t>(sms) * waves), RW) * RW)));
   if (!window_forced()) {
-    // cost model: bytes streamed into shared memory per adjacency bit vs the
-    // ~32-byte L2 sector an edge gather costs
-    const double streamed = static_cast<double>(waves) * sms * static_cast<double>(A.cols) * kWinRec;
-    if (A.nnz_bits < (int64_t{1} << 22) || streamed > 20.0 * static_cast<double>(A.nnz_bits)) return false;
+    // cost model: bytes streamed into shared memory per adjacency bit of the
+    // rows produced (every block streams the whole operand) vs the ~32-byte L2
+    // sector an edge gather costs; range bits estimated from the mean degree
+    const double bits = static_cast<double>(A.nnz_bits) * static_cast<double>(nrows) / static_cast<double>(A.rows);
+    const double streamed = static_cast<double>(waves) * std::min<int64_t>(sms, cdiv(nrows, RB)) *
+                            static_cast<double>(A.cols) * kWinRec;
+    if (bits < static_cast<double>(int64_t{1} << 22) || streamed > 20.0 * bits) return false;
   }
   build_windows(A, RB, RW, Wh, s);
   const auto& W = A.win;

@@ -49,3 +49,28 @@ def test_partition_is_balanced_by_tiles():
     tiles = [int(rp[b[k + 1] // 4] if b[k + 1] < 20000 else rp[-1]) - int(rp[b[k] // 4]) for k in range(8)]
     assert max(tiles) - min(tiles) <= 0.02 * sum(tiles) / 8 + 64
     assert [g.partition_rows(8, k) for k in range(8)] == [(b[k], b[k + 1]) for k in range(8)]
+
+
+@pytest.mark.parametrize("world", [1, 3, 8])
+def test_sharded_dense_graph_through_windowed_aggregation(world):
+    # a dense graph forced onto the column-windowed BBB kernel: each rank's
+    # row range gets its own row-block sizing; still bit-identical
+    from paper_2305_02522_b200 import _lib as L
+    n, e, f, h, c = 6000, 900000, 300, 128, 41
+    s, d = po.Rng(100).random_edges(n, e, False)
+    layers, X = po.build_model("gcn", f, h, c, 99, n)
+    g = bg.prepare_graph(n, s, d)
+    m = bg.Model(to_layer_specs(bg, layers), g)
+    x = torch.from_numpy(X).cuda()
+    bg.set_aggregation(L.AGG_WINDOW, 500)
+    try:
+        ref_out, ref_log, _ = m.forward_traced(x)
+        rp, _, _ = g.structure.download()
+        out, lg = forward_virtual_ranks(m, x, partition_bounds(rp, n, world), logits=True)
+        torch.cuda.synchronize()
+    finally:
+        bg.set_aggregation(L.AGG_AUTO, 0)
+    assert torch.equal(lg, ref_log)
+    assert torch.equal(out, ref_out)
+    o_out, o_log, _ = po.run_model(layers, po.Graph(n, s, d), X)
+    assert np.array_equal(lg.cpu().numpy(), o_log)
