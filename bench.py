@@ -354,7 +354,7 @@ def ncu_traffic(label):
     with open(p) as fh:
         rec = json.load(fh).get(label)
     # DRAM read + write bytes per launch of that kernel from the committed
-    # ncu --set full capture (profiles/r01_v4_ncu_summary.txt)
+    # ncu --set full capture (profiles/ncu_traffic.json, made by scripts/traffic_json.py)
     return rec.get("traffic_bytes") if isinstance(rec, dict) else rec
 
 
