@@ -49,7 +49,7 @@ struct bg_frdc {
     int T = 0, Wn = 0, nw = 0, nb = 0, rw = 0;  // T: rows per block; rw: rows per warp stream
     bg::DevBuf seg;      // u32[nb*(T/32) + 1] stream bases, in ELL groups
     bg::DevBuf steplen;  // u16[nb*(T/32)*nw] groups per step
-    bg::DevBuf ell;      // u16 entries
+    bg::DevBuf ell;      // u16 entries (ring record index)
   } win;
   const uint64_t* srp() const { return sliver_ptr.as<uint64_t>(); }
   const uint32_t* sl() const { return slivers.as<uint32_t>(); }

@@ -21,7 +21,8 @@
 //
 // Entry encoding: u16 = slot << 12 | (column - half*Wh), slot = half % 3, so
 // the shared address is base + entry * 16 with the slots 64 KB apart; padding
-// is kWinPad (slot 0, record 4095: a zero record).
+// is kWinPad (slot 0, record 4095: a zero record that no bulk copy ever
+// overwrites).
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -40,7 +41,9 @@ constexpr int kSlotRec = 4096;          // records per ring slot (64 KB)
 constexpr int kSlots = 3;               // ring slots; half h lives in slot h % 3
 constexpr int kWinHalf = kSlotRec - 1;  // node rows per half-window (record 4095 stays zero)
 constexpr uint16_t kWinPad = kWinHalf;  // slot 0, record 4095
-constexpr int kWinMaxThreads = 576;     // 18 warps: <= 112 registers per thread
+constexpr int kWinQ = 8;                // ELL groups in flight per lane (4 or 8)
+constexpr int kWinPrefetch = 24;        // groups ahead the stream is bulk-prefetched into L2
+constexpr int kWinMaxThreads = 576;     // 18 warps (5 per SMSP): <= 96 registers per thread
 constexpr size_t kWinSmem = static_cast<size_t>(kSlots) * kSlotRec * kWinRec;  // 192 KB
 
 __device__ __forceinline__ uint2 ld_nc_v2(const uint2* p) {
@@ -81,7 +84,8 @@ __global__ void k_win_count(const uint64_t* __restrict__ srp, const uint32_t* __
 // groups), and every lane fills the rest of K with the first edges of half
 // k+1.  Writes the per-step entry counts of each row (u16, rows x nh), the
 // step lengths in groups (u16, warp-major: [b][v][k]) and each warp stream's
-// total (for the scan of stream bases).
+// total (for the scan of stream bases), padded to a multiple of 8 groups: the
+// kernel consumes a stream 32 entries per lane at a time.
 __global__ void k_win_sched(const uint16_t* __restrict__ cnt, int64_t rows, int RB, int RW, int nh, int64_t nbv,
                             uint16_t* __restrict__ nk, uint16_t* __restrict__ steplen,
                             uint32_t* __restrict__ total) {
@@ -105,7 +109,7 @@ __global__ void k_win_sched(const uint16_t* __restrict__ cnt, int64_t rows, int 
     if (lane == 0) steplen[wv * nh + k] = static_cast<uint16_t>(K / 4);
     sum += K / 4;
   }
-  if (lane == 0) total[wv] = sum;
+  if (lane == 0) total[wv] = (sum + 7) & ~7u;
 }
 
 __global__ void k_fill_u16(uint16_t* __restrict__ p, int64_t n, uint16_t v) {
@@ -148,7 +152,7 @@ __global__ void k_win_fill(const uint64_t* __restrict__ srp, const uint32_t* __r
 
 // Bank-aware slot order (build once).  An LDS.128 is served per quarter warp
 // (8 lanes, 128 bytes): lanes of a quarter whose records sit in the same
-// 16-byte bank group (entry mod 8, the slots being 64 KB apart) and differ in
+// 16-byte bank group (record index mod 8, the slots being 64 KB apart) and differ in
 // address cost an extra wavefront each.  Counting is order-free, so each
 // lane's entries within a segment may be permuted freely: position k is
 // filled greedily with, per lane, an entry of a bank group no other lane of
@@ -156,6 +160,7 @@ __global__ void k_win_fill(const uint64_t* __restrict__ srp, const uint32_t* __r
 __device__ void bank_order_segment(uint16_t* __restrict__ segp, uint32_t K, int q, int RW) {
   constexpr int kLook = 48;
   if (K == 0) return;
+  auto bank = [](uint32_t e) { return e & 7u; };
   auto at = [&](int l, uint32_t k) -> uint16_t& { return segp[(k >> 2) * (4 * RW) + (8 * q + l) * 4 + (k & 3)]; };
   uint32_t cnt[8];
   for (int l = 0; l < 8; ++l) {
@@ -163,7 +168,7 @@ __device__ void bank_order_segment(uint16_t* __restrict__ segp, uint32_t K, int 
     while (c < K && at(l, c) != kWinPad) ++c;
     cnt[l] = c;
   }
-  const uint32_t pad_bit = 1u << (kWinPad & 7);
+  const uint32_t pad_bit = 1u << bank(kWinPad);
   for (uint32_t k = 0; k < K; ++k) {
     uint32_t used = 0;
     for (int l = 0; l < 8; ++l)
@@ -173,7 +178,7 @@ __device__ void bank_order_segment(uint16_t* __restrict__ segp, uint32_t K, int 
       const uint32_t end = min(cnt[l], k + kLook);
       uint32_t pick = k;
       for (uint32_t j = k; j < end; ++j)
-        if (!((used >> (at(l, j) & 7u)) & 1u)) {
+        if (!((used >> bank(at(l, j))) & 1u)) {
           pick = j;
           break;
         }
@@ -182,7 +187,7 @@ __device__ void bank_order_segment(uint16_t* __restrict__ segp, uint32_t K, int 
         at(l, pick) = at(l, k);
         at(l, k) = e;
       }
-      used |= 1u << (e & 7u);
+      used |= 1u << bank(e);
     }
   }
 }
@@ -257,6 +262,15 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 // TPR threads per node row: each owns W = 4/TPR of the row's words (TPR = 2
 // halves the per-thread state, so ~1.5x the warps fit at the same register
 // file, and a warp stream covers 16 rows).
+//
+// A warp walks its stream of the current row block as one sequence of
+// groups (4 entries per lane), 32 entries per lane per iteration: the step
+// boundaries (release half S, wait for half S+2) are checked between 8-entry
+// batches, so the ELL prefetch queue sits at fixed registers and the carry
+// tree is static -- four weight-8 carries per iteration fold through planes 3
+// and 4 and ripple from plane 5.  Streams are padded to whole iterations with
+// zero-record entries, and the ELL array is padded past its end, so the
+// prefetch needs no bounds checks.
 template <int NP, bool OUTB, int TPR>
 __global__ void __launch_bounds__(TPR == 1 ? (NP <= 10 ? kWinMaxThreads : 480) : 800, 1)
     k_win_bb(const uint32_t* __restrict__ sbase, const uint16_t* __restrict__ steplen,
@@ -264,7 +278,7 @@ __global__ void __launch_bounds__(TPR == 1 ? (NP <= 10 ? kWinMaxThreads : 480) :
              int64_t xrows, int64_t row0, int64_t row1, int b0, int b1,
              const int32_t* __restrict__ degree, const uint4* __restrict__ x, int64_t f,
              uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
-  static_assert(NP >= 5, "two-level Harley-Seal needs planes 0..4");
+  static_assert(NP >= 6, "three-level Harley-Seal needs planes 0..5");
   constexpr int W = 4 / TPR, RW = 32 / TPR;  // words per thread, rows per warp stream
   extern __shared__ __align__(16) uint4 sbuf[];  // kSlots x kSlotRec records
   __shared__ __align__(8) uint64_t full[kSlots];
@@ -294,40 +308,24 @@ __global__ void __launch_bounds__(TPR == 1 ? (NP <= 10 ? kWinMaxThreads : 480) :
   };
   if (tid == 0)
     for (int H = 0; H < kSlots && H < nsteps; ++H) issue(H);
-  const uint32_t pad2 = static_cast<uint32_t>(kWinPad) * 0x10001u;
-  const uint2 sent2 = make_uint2(pad2, pad2);
-  const int part = threadIdx.x % TPR;                              // which W words of the row
-  const uint2* ell2 = reinterpret_cast<const uint2*>(ell) + lane / TPR;  // this row's 4 entries
-  const uint32_t sb = smem_addr(sbuf);
-  // This warp's groups of the current row block form one stream [gp, ge)
-  // across all steps; eight groups are kept in flight ahead of use.
-  uint32_t gp = 0, ge = 0, lenreg = 0;
-  int64_t wv = 0;
-  auto fetch = [&](uint32_t g) { return g < ge ? ld_nc_v2(ell2 + static_cast<size_t>(g) * RW) : sent2; };
-  uint2 fq[8];  // groups gp .. gp+7 in flight
-#pragma unroll
-  for (int u = 0; u < 8; ++u) fq[u] = sent2;
-  uint32_t P[W][NP], pend[W];
-  bool have = false;  // pend holds a weight-8 carry per word (warp-uniform)
-  const uint32_t sbw = sb + part * (4 * W);  // this thread's words of each record
+  const int part = threadIdx.x % TPR;  // which W words of the row
+  const uint2* ell2 = reinterpret_cast<const uint2*>(ell) + lane / TPR;  // this row's 4 entries per group
+  const uint32_t sbw = smem_addr(sbuf) + part * (4 * W);  // + entry * 16 = this thread's words of a record
+  uint32_t P[W][NP];
   // 8 entries: 8 shared loads (W words each), Harley-Seal into planes 0..2 of
   // each word -> weight-8 carries
-  auto batch8 = [&](uint2 a, uint2 c, uint32_t (&e)[W]) {
+  auto batch8 = [&](const uint2& a, const uint2& c, uint32_t (&e)[W]) {
     const uint32_t pk[4] = {a.x, a.y, c.x, c.y};
     uint32_t v[8][W];
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t addr = sbw + ((h ? (pk[m] >> 16) : (pk[m] & 0xFFFFu)) << 4);
-        if (W == 4) {
-          const uint4 t = lds128(addr);
-          v[2 * m + h][0] = t.x, v[2 * m + h][1] = t.y, v[2 * m + h][W > 2 ? 2 : 0] = t.z,
-                       v[2 * m + h][W > 3 ? 3 : 0] = t.w;
-        } else {
-          const uint2 t = lds64(addr);
-          v[2 * m + h][0] = t.x, v[2 * m + h][1] = t.y;
-        }
+    for (int m = 0; m < 8; ++m) {
+      const uint32_t off = (m & 1) ? (pk[m >> 1] >> 12) & 0xFFFF0u : (pk[m >> 1] << 4) & 0xFFFF0u;
+      if (W == 4) {
+        const uint4 t = lds128(sbw + off);
+        v[m][0] = t.x, v[m][1] = t.y, v[m][W > 2 ? 2 : 0] = t.z, v[m][W > 3 ? 3 : 0] = t.w;
+      } else {
+        const uint2 t = lds64(sbw + off);
+        v[m][0] = t.x, v[m][1] = t.y;
       }
     }
 #pragma unroll
@@ -338,55 +336,10 @@ __global__ void __launch_bounds__(TPR == 1 ? (NP <= 10 ? kWinMaxThreads : 480) :
       e[q] = hs8_low<NP>(P[q], xw);
     }
   };
-  int k = 0, slot = 0;  // S % nh, S % kSlots
+  int S = 0, slot = 0;  // step (half-window) counter of this CTA, S % kSlots
   uint32_t use = 0;     // S / kSlots
-  for (int S = 0; S < nsteps; ++S) {
-    if (k == 0) {
-#pragma unroll
-      for (int q = 0; q < W; ++q)
-#pragma unroll
-        for (int p = 0; p < NP; ++p) P[q][p] = 0u;
-      have = false;
-      const int b = b0 + static_cast<int>(blockIdx.x) + (S / nh) * static_cast<int>(gridDim.x);
-      wv = static_cast<int64_t>(b) * nwarps + warp;
-      gp = __ldg(sbase + wv);
-      ge = __ldg(sbase + wv + 1);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) fq[u] = fetch(gp + u);
-    }
-    if ((k & 31) == 0) lenreg = k + lane < nh ? __ldg(steplen + wv * nh + k + lane) : 0u;
-    const uint32_t K = __shfl_sync(0xFFFFFFFFu, lenreg, k & 31);  // groups this step (even)
-    // halves S and S+1 resident: S was waited for at step S-1 (its slot
-    // cannot be refilled before every warp has finished step S)
-    if (S == 0) mbar_wait(&full[0], 0u);
-    if (S + 1 < nsteps) {
-      const int s1 = slot == kSlots - 1 ? 0 : slot + 1;
-      mbar_wait(&full[s1], (use + (slot == kSlots - 1)) & 1u);
-    }
-    for (uint32_t t = 0; t < K; t += 2) {
-      const uint2 a = fq[0], c = fq[1];
-#pragma unroll
-      for (int u = 0; u < 6; ++u) fq[u] = fq[u + 2];
-      fq[6] = fetch(gp + 8);
-      fq[7] = fetch(gp + 9);
-      gp += 2;
-      uint32_t e[W];
-      batch8(a, c, e);
-      if (have) {  // two weight-8 carries: CSA into plane 3, ripple from plane 4
-#pragma unroll
-        for (int q = 0; q < W; ++q) {
-          const uint32_t s3 = P[q][3] ^ pend[q] ^ e[q];
-          const uint32_t cy = maj3(P[q][3], pend[q], e[q]);
-          P[q][3] = s3;
-          ripple<NP>(P[q], cy, 4);
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < W; ++q) pend[q] = e[q];
-      }
-      have = !have;
-    }
-    // release half S; the last warp out refills its slot with half S + 3
+  // release half S; the last warp out refills its slot with half S + 3
+  auto finish = [&]() {
     __syncwarp();
     if (lane == 0) {
       const uint32_t prev = atomicAdd(&done[slot], 1u);
@@ -395,39 +348,110 @@ __global__ void __launch_bounds__(TPR == 1 ? (NP <= 10 ? kWinMaxThreads : 480) :
         issue(S + kSlots);
       }
     }
-    const bool last = k == nh - 1;
-    if (++k == nh) k = 0;
+    ++S;
     if (++slot == kSlots) slot = 0, ++use;
-    if (last) {
-      if (have) {
+  };
+  // step S may count entries of halves S and S+1: S was waited for at step
+  // S-1 (its slot cannot be refilled before every warp has finished step S)
+  auto wait_next = [&]() {
+    if (S + 1 < nsteps) {
+      const int s1 = slot == kSlots - 1 ? 0 : slot + 1;
+      mbar_wait(&full[s1], (use + (slot == kSlots - 1)) & 1u);
+    }
+  };
+  if (nsteps > 0) mbar_wait(&full[0], 0u);
+  for (int bi = 0; bi < nblk; ++bi) {
 #pragma unroll
-        for (int q = 0; q < W; ++q) ripple<NP>(P[q], pend[q], 3);
-        have = false;
-      }
-      const int bi = S / nh;
-      const int b = b0 + static_cast<int>(blockIdx.x) + bi * static_cast<int>(gridDim.x);
-      const int64_t i = static_cast<int64_t>(b) * (T / TPR) + tid / TPR;
-      if (i >= row0 && i < row1) {
-        const uint32_t deg = static_cast<uint32_t>(__ldg(degree + i));
-        if (OUTB) {
+    for (int q = 0; q < W; ++q)
 #pragma unroll
-          for (int q = 0; q < W; ++q) {
-            const int wd = part * W + q;
-            // cnt >= ceil(deg/2)  <=>  2*cnt - deg >= 0   (kernels.cpp:440-454)
-            uint32_t ge = planes_ge<NP>(P[q], (deg + 1) >> 1);
-            if (32 * (wd + 1) > f) ge &= (32 * wd >= f) ? 0u : tail_mask32(f);
-            out_bits[i * 4 + wd] = ge;
+      for (int p = 0; p < NP; ++p) P[q][p] = 0u;
+    const int b = b0 + static_cast<int>(blockIdx.x) + bi * static_cast<int>(gridDim.x);
+    const int64_t wv = static_cast<int64_t>(b) * nwarps + warp;
+    const uint32_t gp = __ldg(sbase + wv), total = __ldg(sbase + wv + 1) - gp;  // groups, multiple of 8
+    const uint2* es = ell2 + static_cast<size_t>(gp) * RW;
+    if (lane == 0 && total > kWinQ)
+      bulk_prefetch_l2(es + kWinQ * RW, min(static_cast<uint32_t>(kWinPrefetch - kWinQ), total - kWinQ) * RW *
+                                            static_cast<uint32_t>(sizeof(uint2)));
+    uint2 fq[kWinQ];  // groups g .. g+kWinQ-1 in flight
+#pragma unroll
+    for (int u = 0; u < kWinQ; ++u) fq[u] = ld_nc_v2(es + u * RW);
+    int kk = 0;  // step of this block
+    // step lengths, lane-parallel: lenA = steps 32c.., lenB = the next 32
+    // (loaded a whole chunk ahead of use)
+    const uint16_t* sl = steplen + wv * nh;
+    uint32_t lenA = lane < nh ? __ldg(sl + lane) : 0u;
+    uint32_t lenB = 32 + lane < nh ? __ldg(sl + 32 + lane) : 0u;
+    uint32_t step_end = __shfl_sync(0xFFFFFFFFu, lenA, 0);  // group index where step kk ends
+    wait_next();
+    auto boundary = [&](uint32_t at) {  // finish every step that ends at group `at`
+      while (at == step_end && kk < nh) {
+        finish();
+        if (++kk < nh) {
+          if ((kk & 31) == 0) {
+            lenA = lenB;
+            const int k2 = kk + 32 + lane;
+            lenB = k2 < nh ? __ldg(sl + k2) : 0u;
           }
-        } else {
-#pragma unroll
-          for (int q = 0; q < W; ++q)
-            for (int bb = 0; bb < 32; ++bb) {
-              const int64_t kk = 32 * (part * W + q) + bb;
-              if (kk >= f) break;
-              out_f[i * f + kk] = static_cast<float>(2 * static_cast<int64_t>(plane_count<NP>(P[q], bb)) -
-                                                     static_cast<int64_t>(deg));
-            }
+          step_end += __shfl_sync(0xFFFFFFFFu, lenA, kk & 31);
+          wait_next();
         }
+      }
+    };
+    for (uint32_t g = 0; g < total; g += 8) {
+      // the stream's groups g+24 .. g+31 into L2 (one bulk prefetch per 8
+      // groups), so the register queue only has to cover L2 latency
+      if (lane == 0 && g + kWinPrefetch < total)
+        bulk_prefetch_l2(es + static_cast<size_t>(g + kWinPrefetch) * RW,
+                         min(8u, total - g - kWinPrefetch) * RW * static_cast<uint32_t>(sizeof(uint2)));
+      uint32_t e0[W], c1[W];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        boundary(g + 2 * u);
+        const uint2 a = fq[(2 * u) % kWinQ], c = fq[(2 * u + 1) % kWinQ];
+        fq[(2 * u) % kWinQ] = ld_nc_v2(es + static_cast<size_t>(g + 2 * u + kWinQ) * RW);
+        fq[(2 * u + 1) % kWinQ] = ld_nc_v2(es + static_cast<size_t>(g + 2 * u + kWinQ + 1) * RW);
+        uint32_t e[W];
+        batch8(a, c, e);
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+          if (u == 0 || u == 2) {
+            e0[q] = e[q];
+          } else {  // two weight-8 carries: CSA into plane 3 -> weight-16 carry
+            const uint32_t s3 = P[q][3] ^ e0[q] ^ e[q], cy = maj3(P[q][3], e0[q], e[q]);
+            P[q][3] = s3;
+            if (u == 1) {
+              c1[q] = cy;
+            } else {  // two weight-16 carries: CSA into plane 4, ripple from plane 5
+              const uint32_t s4 = P[q][4] ^ c1[q] ^ cy, d = maj3(P[q][4], c1[q], cy);
+              P[q][4] = s4;
+              ripple<NP>(P[q], d, 5);
+            }
+          }
+        }
+      }
+    }
+    boundary(total);
+    const int64_t i = static_cast<int64_t>(b) * (T / TPR) + tid / TPR;
+    if (i >= row0 && i < row1) {
+      const uint32_t deg = static_cast<uint32_t>(__ldg(degree + i));
+      if (OUTB) {
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+          const int wd = part * W + q;
+          // cnt >= ceil(deg/2)  <=>  2*cnt - deg >= 0   (kernels.cpp:440-454)
+          uint32_t ge = planes_ge<NP>(P[q], (deg + 1) >> 1);
+          if (32 * (wd + 1) > f) ge &= (32 * wd >= f) ? 0u : tail_mask32(f);
+          out_bits[i * 4 + wd] = ge;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < W; ++q)
+          for (int bb = 0; bb < 32; ++bb) {
+            const int64_t kk2 = 32 * (part * W + q) + bb;
+            if (kk2 >= f) break;
+            out_f[i * f + kk2] = static_cast<float>(2 * static_cast<int64_t>(plane_count<NP>(P[q], bb)) -
+                                                    static_cast<int64_t>(deg));
+          }
       }
     }
   }
@@ -484,8 +508,9 @@ void build_windows(bg_frdc& A, int RB, int RW, int Wh, cudaStream_t s) {
   uint32_t groups = 0;
   BG_CUDA(cudaMemcpyAsync(&groups, W.seg.as<uint32_t>() + nbv, 4, cudaMemcpyDeviceToHost, s));
   BG_CUDA(cudaStreamSynchronize(s));
-  const int64_t n16 = static_cast<int64_t>(groups) * 4 * RW;
-  W.ell.alloc(static_cast<size_t>(std::max<int64_t>(n16, 8)) * 2);
+  // + 8 groups past the end: the kernel's prefetch runs up to 8 groups ahead
+  const int64_t n16 = (static_cast<int64_t>(groups) + 8) * 4 * RW;
+  W.ell.alloc(static_cast<size_t>(n16) * 2);
   k_fill_u16<<<static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cdiv(n16, 256), 65536))), 256, 0, s>>>(
       W.ell.as<uint16_t>(), n16, kWinPad);
   BG_LAUNCH_CHECK();
