@@ -728,6 +728,21 @@ inline std::vector<std::string> validate_model(const ModelSpec& m) {
   return out;
 }
 
+// ref: rewrite_eliminate_scl (graphops.cpp:357-368): a Scale node directly
+// ahead of a Binarize is dropped (positive factors move no value across the
+// sign threshold); every other layer is kept in order.
+inline ModelSpec rewrite_eliminate_scl(const ModelSpec& m) {
+  ModelSpec out = m;
+  out.layers.clear();
+  for (size_t i = 0; i < m.layers.size(); ++i) {
+    if (m.layers[i].kind == LayerKind::Scale && i + 1 < m.layers.size() &&
+        m.layers[i + 1].kind == LayerKind::Binarize)
+      continue;
+    out.layers.push_back(m.layers[i]);
+  }
+  return out;
+}
+
 // A device-resident model: weights binarized once, forward captured as one
 // CUDA graph after its first run.  The serving entry point.
 class Model {

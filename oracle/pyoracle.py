@@ -546,6 +546,82 @@ def ref_random_edges(seed: int, nodes: int, m: int, allow_self: bool = False):
     return src[:k].copy(), dst[:k].copy()
 
 
+class _RefLayer(C.Structure):
+    _fields_ = [("kind", C.c_int), ("plan", C.c_char_p),
+                ("w1", C.c_void_p), ("w1_rows", C.c_int64), ("w1_cols", C.c_int64),
+                ("w2", C.c_void_p), ("w2_rows", C.c_int64), ("w2_cols", C.c_int64),
+                ("relu", C.c_int),
+                ("bn_gamma", C.c_void_p), ("bn_beta", C.c_void_p), ("bn_mean", C.c_void_p),
+                ("bn_sigma", C.c_void_p), ("bn_len", C.c_int64),
+                ("scale_row", C.c_void_p), ("scale_row_len", C.c_int64),
+                ("scale_col", C.c_void_p), ("scale_col_len", C.c_int64)]
+
+
+def ref_spec_run(layers, graph: Optional["RefGraph"], x: np.ndarray, word_bits: int = 32):
+    """Any layer list through the real reference's run_model (graphops.cpp:
+    390-484).  `layers`: objects with kind (LayerKind order), plan (variant
+    names), w1, w2, relu, bn (gamma, beta, mean, sigma), scale_row, scale_col.
+    Returns (out, logits, trace points)."""
+    arr = (_RefLayer * max(len(layers), 1))()
+    keep = []
+
+    def host(a):
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        keep.append(a)
+        return a
+
+    for i, l in enumerate(layers):
+        d = arr[i]
+        d.kind = int(l.kind)
+        plan = "+".join(str(p) if isinstance(p, str) else p.name() for p in (l.plan or []))
+        keep.append(plan.encode())
+        d.plan = keep[-1]
+        for name in ("w1", "w2"):
+            w = getattr(l, name, None)
+            if w is not None:
+                w = host(w)
+                setattr(d, name, w.ctypes.data)
+                setattr(d, name + "_rows", w.shape[0])
+                setattr(d, name + "_cols", w.shape[1])
+        d.relu = int(bool(getattr(l, "relu", False)))
+        bn = getattr(l, "bn", None)
+        if bn is not None:
+            g, b, m, sg = (host(v) for v in bn)
+            d.bn_gamma, d.bn_beta, d.bn_mean, d.bn_sigma = g.ctypes.data, b.ctypes.data, m.ctypes.data, sg.ctypes.data
+            d.bn_len = g.shape[0]
+        for name in ("scale_row", "scale_col"):
+            v = getattr(l, name, None)
+            if v is not None:
+                v = host(v)
+                setattr(d, name, v.ctypes.data)
+                setattr(d, name + "_len", v.shape[0])
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    points: List[TracePoint] = []
+
+    def sink(_ctx, label, bits, r, c, wb):
+        n = r * spw(c, wb)
+        a = np.ctypeslib.as_array(bits, shape=(n,)).reshape(r, -1).copy() if n else \
+            np.zeros((r, spw(c, wb)), np.uint32)
+        points.append(TracePoint(label.decode(), a, r, c, wb))
+
+    cb = _TRACE_FN(sink)
+    out_p, log_p, oc = C.POINTER(C.c_float)(), C.POINTER(C.c_float)(), C.c_int64(0)
+    L = ref()
+    L.ref_spec_run.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int64,
+                               C.c_void_p, C.c_void_p, C.c_void_p, _TRACE_FN, C.c_void_p]
+    L.ref_free.argtypes = [C.c_void_p]
+    rc = L.ref_spec_run(graph.h if graph is not None else None, arr, len(layers), word_bits, _ptr(x),
+                        x.shape[0], x.shape[1], C.byref(out_p), C.byref(log_p), C.byref(oc), cb, None)
+    if rc:
+        raise ValueError(L.ref_error().decode())
+    rows = x.shape[0]
+    out = np.ctypeslib.as_array(out_p, shape=(max(rows * oc.value, 1),))[:rows * oc.value].reshape(rows, -1).copy()
+    lg = np.ctypeslib.as_array(log_p, shape=(max(rows * oc.value, 1),))[:rows * oc.value].reshape(rows, -1).copy()
+    L.ref_free(C.cast(out_p, C.c_void_p))
+    L.ref_free(C.cast(log_p, C.c_void_p))
+    return out, lg, points
+
+
 class RefGraph:
     @staticmethod
     def from_frdc(n: int, loops: "Frdc", raw: "Frdc") -> "RefGraph":

@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -331,5 +332,82 @@ int64_t ref_enumerate_plans(const char* model, int layers, char* buf, int64_t ca
     return -1;
   }
 }
+
+// An arbitrary layer list through the reference's run_model (graphops.cpp:
+// 390-484): layer kinds in LayerKind order (graphops.hpp:42-53), plan as a
+// '+'-joined chain (parse_plan_chain), optional weights / BatchNorm / Scale
+// parameters, graph optional.  Output and logits are malloc'd (free with
+// ref_free); the trace callback sees every BIN point.
+typedef struct {
+  int kind;
+  const char* plan;
+  const float* w1;
+  int64_t w1_rows, w1_cols;
+  const float* w2;
+  int64_t w2_rows, w2_cols;
+  int relu;
+  const float *bn_gamma, *bn_beta, *bn_mean, *bn_sigma;
+  int64_t bn_len;
+  const float* scale_row;
+  int64_t scale_row_len;
+  const float* scale_col;
+  int64_t scale_col_len;
+} ref_layer;
+
+int ref_spec_run(void* graph, const ref_layer* layers, int n, int word_bits, const float* x, int64_t rows,
+                 int64_t cols, float** out, float** logits, int64_t* out_cols, ref_trace_fn trace, void* ctx) {
+  try {
+    ModelSpec spec;
+    spec.word_bits = word_bits;
+    if (graph) spec.graph = static_cast<RefGraph*>(graph)->g;
+    auto dense = [](const float* p, int64_t r, int64_t c) {
+      auto d = std::make_shared<DenseMatrix>(r, c);
+      if (r * c) std::memcpy(d->row(0), p, static_cast<size_t>(r * c) * sizeof(float));
+      return d;
+    };
+    auto vec = [](const float* p, int64_t len) { return std::vector<Real>(p, p + len); };
+    for (int i = 0; i < n; ++i) {
+      const ref_layer& d = layers[i];
+      LayerSpec l;
+      l.kind = static_cast<LayerKind>(d.kind);
+      if (d.plan && *d.plan) l.plan = parse_plan_chain(d.plan);
+      if (d.w1) l.w1 = dense(d.w1, d.w1_rows, d.w1_cols);
+      if (d.w2) l.w2 = dense(d.w2, d.w2_rows, d.w2_cols);
+      l.relu = d.relu != 0;
+      if (d.bn_gamma)
+        l.bn = BatchNormParams{vec(d.bn_gamma, d.bn_len), vec(d.bn_beta, d.bn_len), vec(d.bn_mean, d.bn_len),
+                               vec(d.bn_sigma, d.bn_len)};
+      if (d.scale_row) l.scale_row = ScaleVector(Axis::Row, vec(d.scale_row, d.scale_row_len));
+      if (d.scale_col) l.scale_col = ScaleVector(Axis::Col, vec(d.scale_col, d.scale_col_len));
+      spec.layers.push_back(std::move(l));
+    }
+    DenseMatrix x0(rows, cols);
+    if (rows * cols) std::memcpy(x0.row(0), x, static_cast<size_t>(rows * cols) * sizeof(float));
+    RunTrace tr;
+    DenseMatrix o = run_model(spec, MatOperand(x0), &tr);
+    if (trace)
+      for (const auto& p : tr.points) {
+        std::vector<uint32_t> words(static_cast<size_t>(p.bits.rows() * p.bits.storage_words_per_row()));
+        for (int64_t r = 0; r < p.bits.rows(); ++r) {
+          auto sp = p.bits.row_span(r);
+          std::memcpy(words.data() + r * p.bits.storage_words_per_row(), sp.data(), sp.size() * 4);
+        }
+        trace(ctx, p.label.c_str(), words.data(), p.bits.rows(), p.bits.cols(), p.bits.word_bits());
+      }
+    *out_cols = o.cols();
+    const size_t nb = static_cast<size_t>(o.rows() * o.cols()) * sizeof(float);
+    *out = static_cast<float*>(std::malloc(std::max<size_t>(nb, 4)));
+    *logits = static_cast<float*>(std::malloc(std::max<size_t>(nb, 4)));
+    if (nb) std::memcpy(*out, o.row(0), nb);
+    const bool has_logits = tr.logits.rows() * tr.logits.cols() == o.rows() * o.cols() && nb;
+    if (has_logits) std::memcpy(*logits, tr.logits.row(0), nb);
+    else if (nb) std::memcpy(*logits, o.row(0), nb);
+    return 0;
+  } catch (const std::exception& ex) {
+    return guard(ex);
+  }
+}
+
+void ref_free(void* p) { std::free(p); }
 
 }  // extern "C"

@@ -13,5 +13,5 @@ from .bitgnn import *  # noqa: E402,F401,F403
 from .bitgnn import (AdjacencyOperand, BitDenseMatrix, BitOperand, FrdcMatrix,  # noqa: E402,F401
                      GraphBundle, KernelVariant, LayerSpec, Model, Rng, add, binarize,
                      binarize_with_scale, bmm, bspmm, build_model_spec, concat, frdc_from_edges,
-                     prepare_graph, run_model, transpose, unpack, validate_model)
+                     prepare_graph, rewrite_eliminate_scl, run_model, transpose, unpack, validate_model)
 from ._lib import (B, F, CudaError, InvalidArgument, LogicError, RuntimeFailure)  # noqa: E402,F401

@@ -574,6 +574,13 @@ def validate_model(layers: Sequence[LayerSpec], has_graph: bool = True,
     return buf.value.decode().split("\n") if n else []
 
 
+def rewrite_eliminate_scl(layers: Sequence[LayerSpec]) -> List[LayerSpec]:
+    """graphops.cpp:357-368 -- drop every Scale layer directly ahead of a
+    Binarize (positive factors move no value across the sign threshold)."""
+    return [l for i, l in enumerate(layers)
+            if not (l.kind == L.LAYER_SCALE and i + 1 < len(layers) and layers[i + 1].kind == L.LAYER_BINARIZE)]
+
+
 @dataclass
 class TracePoint:
     label: str
