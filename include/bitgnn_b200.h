@@ -158,6 +158,24 @@ int bg_frdc_serialize(const bg_frdc* m, int word_bits, void* buf, size_t buf_len
 int bg_frdc_deserialize(const void* buf, size_t len, bg_frdc** out, int* word_bits, bg_stream stream);
 int bg_frdc_write_file(const bg_frdc* m, int word_bits, const char* path);
 int bg_frdc_read_file(const char* path, bg_frdc** out, int* word_bits, bg_stream stream);
+
+/* ---- graph file readers (ref: graphio.hpp:11-24, graphio.cpp:72-176) -------
+ * Host edge lists: "src dst [weight]" lines ('#'/'%' comments), MatrixMarket
+ * coordinate (pattern/real/integer, general/symmetric; 1-based, mirrored when
+ * symmetric or undirected), and load_graph's sniffing of a file (FRDC
+ * container -> its edges, "%%MatrixMarket" -> MM, else an edge list).
+ * forced_nodes = -1 infers the node count.  Errors: BG_RUNTIME_ERROR with the
+ * reference's "name:line: message" text.  The result is a host-side handle:
+ * read its arrays with bg_edges_info (valid until bg_edges_destroy), then
+ * build the device graph with bg_frdc_from_edges / bg_prepare_graph. */
+typedef struct bg_edges bg_edges;
+int bg_read_edge_list(const char* text, size_t len, const char* name, int64_t forced_nodes, int undirected,
+                      bg_edges** out);
+int bg_read_matrix_market(const char* text, size_t len, const char* name, int undirected, bg_edges** out);
+int bg_load_graph(const char* path, int64_t forced_nodes, int undirected, bg_edges** out);
+int bg_edges_info(const bg_edges* e, int64_t* node_count, int64_t* n_edges, const int64_t** src,
+                  const int64_t** dst, const double** weights, int64_t* n_weights);
+void bg_edges_destroy(bg_edges* e);
 /* Fault hook (ref: runreport.cpp:55-63): flip bit 0 of stored tile k % nnz. */
 int bg_frdc_corrupt_tile(bg_frdc* m, int64_t k);
 void bg_frdc_destroy(bg_frdc* m);

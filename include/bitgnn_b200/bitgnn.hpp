@@ -20,6 +20,8 @@
 #include <memory>
 #include <optional>
 #include <stdexcept>
+#include <istream>
+#include <iterator>
 #include <string>
 #include <string_view>
 #include <utility>
@@ -741,6 +743,50 @@ inline ModelSpec rewrite_eliminate_scl(const ModelSpec& m) {
     out.layers.push_back(m.layers[i]);
   }
   return out;
+}
+
+// ---- graph readers (ref: graphio.hpp:11-24) ----------------------------------
+namespace detail {
+inline EdgeList take_edges(bg_edges* h) {
+  struct Guard {
+    bg_edges* h;
+    ~Guard() { bg_edges_destroy(h); }
+  } g{h};
+  int64_t n = 0, m = 0, nw = 0;
+  const int64_t *src = nullptr, *dst = nullptr;
+  const double* w = nullptr;
+  check(bg_edges_info(h, &n, &m, &src, &dst, &w, &nw));
+  EdgeList e;
+  e.node_count = n;
+  e.edges.reserve(static_cast<size_t>(m));
+  for (int64_t k = 0; k < m; ++k) e.edges.emplace_back(src[k], dst[k]);
+  e.weights.assign(w, w + nw);
+  return e;
+}
+}  // namespace detail
+
+// Whitespace "src dst [weight]" pairs, 0-based; '#'/'%' comments.
+inline EdgeList read_edge_list(std::istream& in, const std::string& name, int64_t forced_nodes = -1,
+                               bool undirected = false) {
+  const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  bg_edges* h = nullptr;
+  detail::check(bg_read_edge_list(text.data(), text.size(), name.c_str(), forced_nodes, undirected ? 1 : 0, &h));
+  return detail::take_edges(h);
+}
+
+// MatrixMarket coordinate (pattern/real/integer, general/symmetric).
+inline EdgeList read_matrix_market(std::istream& in, const std::string& name, bool undirected = false) {
+  const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  bg_edges* h = nullptr;
+  detail::check(bg_read_matrix_market(text.data(), text.size(), name.c_str(), undirected ? 1 : 0, &h));
+  return detail::take_edges(h);
+}
+
+// Sniffs the file: FRDC container, MatrixMarket, else an edge list.
+inline EdgeList load_graph(const std::string& path, int64_t forced_nodes = -1, bool undirected = false) {
+  bg_edges* h = nullptr;
+  detail::check(bg_load_graph(path.c_str(), forced_nodes, undirected ? 1 : 0, &h));
+  return detail::take_edges(h);
 }
 
 // A device-resident model: weights binarized once, forward captured as one

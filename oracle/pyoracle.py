@@ -622,6 +622,33 @@ def ref_spec_run(layers, graph: Optional["RefGraph"], x: np.ndarray, word_bits: 
     return out, lg, points
 
 
+def ref_read_graph(kind: int, text, name: str = "<stream>", forced_nodes: int = -1, undirected: bool = False):
+    """The reference's graphio readers (kind 0 read_edge_list, 1
+    read_matrix_market, 2 load_graph(path=text)).  Returns (node_count, src,
+    dst, weights) or raises ValueError with the reference's message."""
+    b = text.encode() if isinstance(text, str) else bytes(text)
+    L = ref()
+    L.ref_read_graph.argtypes = [C.c_int, C.c_char_p, C.c_size_t, C.c_char_p, C.c_int64, C.c_int,
+                                 C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.POINTER(C.c_int64)),
+                                 C.POINTER(C.POINTER(C.c_int64)), C.POINTER(C.c_int64),
+                                 C.POINTER(C.POINTER(C.c_double))]
+    L.ref_free.argtypes = [C.c_void_p]
+    n, m, nw = C.c_int64(), C.c_int64(), C.c_int64()
+    sp, dp, wp = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)(), C.POINTER(C.c_double)()
+    rc = L.ref_read_graph(kind, b, len(b), name.encode(), forced_nodes, int(undirected), C.byref(n), C.byref(m),
+                          C.byref(sp), C.byref(dp), C.byref(nw), C.byref(wp))
+    if rc:
+        raise ValueError(L.ref_error().decode())
+    try:
+        src = np.ctypeslib.as_array(sp, shape=(max(m.value, 1),))[:m.value].copy()
+        dst = np.ctypeslib.as_array(dp, shape=(max(m.value, 1),))[:m.value].copy()
+        w = np.ctypeslib.as_array(wp, shape=(max(nw.value, 1),))[:nw.value].copy()
+    finally:
+        for p in (sp, dp, wp):
+            L.ref_free(C.cast(p, C.c_void_p))
+    return n.value, src, dst, w
+
+
 class RefGraph:
     @staticmethod
     def from_frdc(n: int, loops: "Frdc", raw: "Frdc") -> "RefGraph":

@@ -16,10 +16,12 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <sstream>
 #include <string>
 #include <vector>
 
 #include "bitgnn/bitsparse.hpp"
+#include "bitgnn/graphio.hpp"
 #include "bitgnn/graphops.hpp"
 #include "bitgnn/kernels.hpp"
 #include "bitgnn/modelconfig.hpp"
@@ -409,5 +411,33 @@ int ref_spec_run(void* graph, const ref_layer* layers, int n, int word_bits, con
 }
 
 void ref_free(void* p) { std::free(p); }
+
+// graphio.cpp readers.  kind 0: read_edge_list(text), 1: read_matrix_market
+// (text), 2: load_graph(path = text).  Arrays are malloc'd (ref_free).
+int ref_read_graph(int kind, const char* text, size_t len, const char* name, int64_t forced, int undirected,
+                   int64_t* node_count, int64_t* n_edges, int64_t** src, int64_t** dst, int64_t* n_weights,
+                   double** weights) {
+  try {
+    EdgeList e;
+    if (kind == 2) {
+      e = load_graph(std::string(text, len), forced, undirected != 0);
+    } else {
+      std::istringstream in(std::string(text, len));
+      e = kind == 0 ? read_edge_list(in, name, forced, undirected != 0)
+                    : read_matrix_market(in, name, undirected != 0);
+    }
+    *node_count = e.node_count;
+    *n_edges = static_cast<int64_t>(e.edges.size());
+    *src = static_cast<int64_t*>(std::malloc(std::max<size_t>(e.edges.size(), 1) * 8));
+    *dst = static_cast<int64_t*>(std::malloc(std::max<size_t>(e.edges.size(), 1) * 8));
+    for (size_t k = 0; k < e.edges.size(); ++k) (*src)[k] = e.edges[k].first, (*dst)[k] = e.edges[k].second;
+    *n_weights = static_cast<int64_t>(e.weights.size());
+    *weights = static_cast<double*>(std::malloc(std::max<size_t>(e.weights.size(), 1) * 8));
+    for (size_t k = 0; k < e.weights.size(); ++k) (*weights)[k] = e.weights[k];
+    return 0;
+  } catch (const std::exception& ex) {
+    return guard(ex);
+  }
+}
 
 }  // extern "C"

@@ -12,6 +12,7 @@ _load()
 from .bitgnn import *  # noqa: E402,F401,F403
 from .bitgnn import (AdjacencyOperand, BitDenseMatrix, BitOperand, FrdcMatrix,  # noqa: E402,F401
                      GraphBundle, KernelVariant, LayerSpec, Model, Rng, add, binarize,
-                     binarize_with_scale, bmm, bspmm, build_model_spec, concat, frdc_from_edges,
+                     binarize_with_scale, bmm, bspmm, build_model_spec, concat, EdgeList, frdc_from_edges,
+                     load_graph, read_edge_list, read_matrix_market,
                      prepare_graph, rewrite_eliminate_scl, run_model, transpose, unpack, validate_model)
 from ._lib import (B, F, CudaError, InvalidArgument, LogicError, RuntimeFailure)  # noqa: E402,F401

@@ -99,6 +99,12 @@ PROTOTYPES = {
     "bg_frdc_write_file": (I32, [P, I32, C.c_char_p]),
     "bg_frdc_read_file": (I32, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int), P]),
     "bg_frdc_destroy": (None, [P]),
+    "bg_read_edge_list": (I32, [C.c_char_p, C.c_size_t, C.c_char_p, I64, I32, C.POINTER(P)]),
+    "bg_read_matrix_market": (I32, [C.c_char_p, C.c_size_t, C.c_char_p, I32, C.POINTER(P)]),
+    "bg_load_graph": (I32, [C.c_char_p, I64, I32, C.POINTER(P)]),
+    "bg_edges_info": (I32, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(P), C.POINTER(P), C.POINTER(P),
+                            C.POINTER(I64)]),
+    "bg_edges_destroy": (None, [P]),
     "bg_prepare_graph": (I32, [P, P, I64, I64, C.POINTER(P), P]),
     "bg_graph_info_get": (I32, [P, C.POINTER(GraphInfo)]),
     "bg_graph_corrupt_tile": (I32, [P, I64]),

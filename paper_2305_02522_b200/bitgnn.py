@@ -325,6 +325,59 @@ class FrdcMatrix:
             pass
 
 
+@dataclass
+class EdgeList:
+    """ref: EdgeList (bitsparse.hpp) -- node count, (src, dst) pairs and the
+    optional weight column (possibly shorter than the edges, as in the
+    reference: it is padded with 1.0 only up to the last weighted line)."""
+    node_count: int
+    src: np.ndarray
+    dst: np.ndarray
+    weights: np.ndarray
+
+
+def _take_edges(h: C.c_void_p) -> EdgeList:
+    try:
+        n, m, nw = C.c_int64(), C.c_int64(), C.c_int64()
+        sp, dp, wp = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(lib().bg_edges_info(h, C.byref(n), C.byref(m), C.byref(sp), C.byref(dp), C.byref(wp), C.byref(nw)))
+
+        def arr(p, k, t):
+            return np.ctypeslib.as_array(C.cast(p, C.POINTER(t)), shape=(k,)).copy() if k else \
+                np.zeros(0, np.int64 if t is C.c_int64 else np.float64)
+        return EdgeList(n.value, arr(sp.value, m.value, C.c_int64), arr(dp.value, m.value, C.c_int64),
+                        arr(wp.value, nw.value, C.c_double))
+    finally:
+        lib().bg_edges_destroy(h)
+
+
+def _text(t) -> bytes:
+    return t.encode() if isinstance(t, str) else bytes(t)
+
+
+def read_edge_list(text, name: str = "<stream>", forced_nodes: int = -1, undirected: bool = False) -> EdgeList:
+    """graphio.cpp:72-99: whitespace 'src dst [weight]' lines, 0-based."""
+    b = _text(text)
+    h = C.c_void_p()
+    check(lib().bg_read_edge_list(b, len(b), name.encode(), forced_nodes, int(undirected), C.byref(h)))
+    return _take_edges(h)
+
+
+def read_matrix_market(text, name: str = "<stream>", undirected: bool = False) -> EdgeList:
+    """graphio.cpp:101-155: MatrixMarket coordinate, weights dropped."""
+    b = _text(text)
+    h = C.c_void_p()
+    check(lib().bg_read_matrix_market(b, len(b), name.encode(), int(undirected), C.byref(h)))
+    return _take_edges(h)
+
+
+def load_graph(path: str, forced_nodes: int = -1, undirected: bool = False) -> EdgeList:
+    """graphio.cpp:157-176: FRDC container, MatrixMarket or edge list by sniffing."""
+    h = C.c_void_p()
+    check(lib().bg_load_graph(str(path).encode(), forced_nodes, int(undirected), C.byref(h)))
+    return _take_edges(h)
+
+
 def _edges(src, dst) -> Tuple[torch.Tensor, torch.Tensor]:
     s = torch.as_tensor(np.asarray(src, dtype=np.int64) if not isinstance(src, torch.Tensor) else src)
     d = torch.as_tensor(np.asarray(dst, dtype=np.int64) if not isinstance(dst, torch.Tensor) else dst)

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -84,6 +85,28 @@ static void test_cpu() {
   m.layers[1].plan[1] = b::KernelVariant::parse("BSpMM.BBB");  // chain ends at B
   errs = b::validate_model(m);
   CHECK(errs.size() >= 2);
+
+  // SCL elimination (graphops.cpp:357-368)
+  b::ModelSpec sm;
+  b::LayerSpec scale;
+  scale.kind = b::LayerKind::Scale;
+  b::LayerSpec binz;
+  binz.kind = b::LayerKind::Binarize;
+  sm.layers = {m.layers[0], scale, binz, scale, m.layers[2]};
+  const b::ModelSpec r = b::rewrite_eliminate_scl(sm);
+  CHECK(r.layers.size() == 4 && r.layers[1].kind == b::LayerKind::Binarize && r.layers[2].kind == b::LayerKind::Scale);
+
+  // graph readers (graphio.cpp:72-176): host parsing, no device needed
+  std::istringstream el("# a comment\n1 2 0.5\n0 5\n");
+  const b::EdgeList e = b::read_edge_list(el, "two.txt", -1, true);
+  CHECK(e.node_count == 6 && e.edges.size() == 4 && e.edges[2].first == 2 && e.edges[2].second == 1 &&
+        e.weights.size() == 1 && e.weights[0] == 0.5);
+  std::istringstream bad("0 1\nfoo bar\n");
+  CHECK(throws<std::runtime_error>([&] { b::read_edge_list(bad, "broken.txt"); }, "broken.txt:2: expected \"src dst\""));
+  std::istringstream mm("%%MatrixMarket matrix coordinate real symmetric\n3 3 2\n2 1 0.5\n3 3 1.0\n");
+  const b::EdgeList me = b::read_matrix_market(mm, "mm.mtx");
+  CHECK(me.node_count == 3 && me.edges.size() == 3);
+  CHECK(throws<std::runtime_error>([&] { b::load_graph("/nonexistent/x.txt"); }, "/nonexistent/x.txt: cannot open"));
 }
 
 // Without a device every op fails loudly (no CPU fallback).

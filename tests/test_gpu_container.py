@@ -108,3 +108,30 @@ def test_missing_file_names_the_path(tmp_path):
     m = bg.frdc_from_edges(4, [0], [1], False)
     with pytest.raises(bg.RuntimeFailure, match="write_frdc: cannot open"):
         m.write(tmp_path / "no_dir" / "x.frdc")
+
+
+@pytest.mark.skipif(not po.ref_available(), reason="oracle/_ref (reference library) not built")
+@pytest.mark.parametrize("forced,undirected", [(-1, False), (-1, True), (5000, False), (10, False)])
+def test_load_graph_decodes_a_container_like_the_reference(tmp_path, forced, undirected):
+    # graphio.cpp:46-70: tiles -> edges in storage order, node count from the
+    # header (trailing isolated nodes kept), the forced count checked
+    n = 3001  # not a multiple of 4; node 3000 is isolated
+    s, d = po.Rng(78).random_edges(3000, 20000, False)
+    m = bg.frdc_from_edges(n, s, d, False)
+    path = tmp_path / "g.frdc"
+    m.write(path)
+    try:
+        want = po.ref_read_graph(2, str(path), "", forced, undirected)
+    except ValueError as e:
+        with pytest.raises(bg.RuntimeFailure) as got:
+            bg.load_graph(str(path), forced, undirected)
+        assert str(got.value) == str(e)
+        return
+    e = bg.load_graph(str(path), forced, undirected)
+    assert e.node_count == want[0]
+    assert np.array_equal(e.src, want[1]) and np.array_equal(e.dst, want[2])
+    # and the edges rebuild the same adjacency on the device
+    back = bg.frdc_from_edges(e.node_count, e.src, e.dst, False)
+    if not undirected and forced < 0:
+        for a, b in zip(back.download(), m.download()):
+            assert np.array_equal(a, b)
