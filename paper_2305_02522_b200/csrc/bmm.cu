@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(kWarps * 32)
           float* __restrict__ out_f) {
   extern __shared__ uint32_t smem[];
   uint32_t* sw = smem;                       // nc x ld transposed weight words
-  uint32_t* srow = smem + nc * ld;           // kWarps x kspw packed activation rows
+  uint32_t* srow = smem + 32 * M * ld;       // kWarps x kspw packed activation rows (after all 32*M weight rows the lanes read)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t t = threadIdx.x; t < nc * kspw; t += blockDim.x) {
     const int64_t j = t / kspw, w = t % kspw;
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kWarps * 32)
         const int64_t j = 32 * m + lane;
         const bool bit = j < nc && (k - 2 * static_cast<int64_t>(diff[m])) >= 0;
         const uint32_t word = __brev(__ballot_sync(0xFFFFFFFFu, bit));
-        if (lane == 0) out_bits[row * ospw + c0 / 32 + m] = word;
+        if (lane == 0 && 32 * m < nc) out_bits[row * ospw + c0 / 32 + m] = word;  // only words of this pass
       }
       // zero the storage-padding words of 64-bit rows after the last pass
       if (lane == 0 && c0 + nc == n)
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(kImWarps * 32)
           m0 &= keep;
           m1 &= keep;
         }
-        if (t4 == (w & 3)) {
+        if (t4 == (w & 3) && w < ospw) {  // words past the row (N < 32*NT/4) do not exist
           if (r0 < rows) out_bits[r0 * ospw + w] = m0;
           if (r1 < rows) out_bits[r1 * ospw + w] = m1;
         }
@@ -1065,7 +1065,8 @@ void launch(const BmmArgs& a, cudaStream_t s) {
   blocks = std::max<int64_t>(blocks, 1);
   for (int64_t c0 = 0; c0 < a.n; c0 += pass) {
     const int64_t nc = std::min(pass, a.n - c0);
-    const size_t smem = static_cast<size_t>(cdiv(nc, 32) * 32 * ld + kWarps * kspw) * 4;
+    const int64_t mcols = nc <= 32 ? 32 : nc <= 64 ? 64 : nc <= 128 ? 128 : 256;  // 32*M of pick(nc)
+    const size_t smem = static_cast<size_t>(mcols * ld + kWarps * kspw) * 4;
     auto kern = pick(nc);
     if (smem > 48 * 1024) BG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                       static_cast<int>(smem)));
@@ -1079,15 +1080,36 @@ void launch(const BmmArgs& a, cudaStream_t s) {
 
 }  // namespace
 
+// Which F-input path (tests and A/B runs: BG_FBB=scalar|imma|tma; default
+// picks by shape).  0 = default, 1 = scalar warp per row, 2 = imma, 3 = tma.
+int fbb_force() {
+  const char* e = std::getenv("BG_FBB");
+  if (!e) return 0;
+  const std::string v(e);
+  return v == "scalar" ? 1 : v == "imma" ? 2 : v == "tma" ? 3 : 0;
+}
+
 void bmm(const BmmArgs& a, cudaStream_t s) {
   if (a.rows == 0 || a.n == 0) return;
   const bool af = a.a_f != nullptr, ob = a.out_bits != nullptr;
+  const int force = af ? fbb_force() : 0;
+  // Few rows (Cora 2.7K, PubMed 20K, Flickr 89K): a warp per row puts every
+  // row in flight at once, where the tile kernels leave SMs idle or run
+  // short pipelines (measured FBB: Cora 66 -> 20 us, PubMed 28 -> 26 us,
+  // Flickr 169 -> 154 us; Reddit 233K rows stays on the TMA kernel, 0.158 vs
+  // 0.297 ms).  F output keeps the tensor-core kernel (Flickr FBF 63 vs 83 us).
+  const bool few_rows = af && ob && a.rows < 131072 && std::getenv("BG_FBB") == nullptr;
+  if (force == 1 || few_rows) {
+    if (ob) launch<true, true>(a, s);
+    else launch<true, false>(a, s);
+    return;
+  }
   if (imma_ok(a)) {
     if (ob) {
       // whole 16-row tiles on the TMA-fed kernel, the rest on the direct one
       if (fbb_umma(a, s)) return;
       if (fbb_umma2(a, s)) return;
-      const int64_t done = fbb_tma(a, s);
+      const int64_t done = force == 2 ? 0 : fbb_tma(a, s);
       if (done < a.rows) {
         BmmArgs rest = a;
         rest.rows = a.rows - done;

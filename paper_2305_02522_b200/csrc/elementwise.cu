@@ -22,45 +22,99 @@ __global__ void k_or(const uint32_t* __restrict__ a, const uint32_t* __restrict_
 }
 
 // ADD.BBF: 2*(a+b) - 2 over 0/1 bits (:618-624).
+// ADD.BBF: 2*(a+b) - 2 per element (kernels.cpp:608-616), optionally with the
+// layer's ReLU fused (graphops.cpp:89-97: x > 0 ? x : 0).  Thread per (row,
+// 32-column word): two word loads, 32 floats out (float4 stores when the row
+// start is 16-byte aligned).
+template <bool RELU>
 __global__ void k_add_bbf(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
                           int64_t rows, int64_t cols, int64_t spw, float* __restrict__ o) {
+  const int64_t wpr = (cols + 31) >> 5;  // 32-column words per row
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= rows * cols) return;
-  const int64_t i = t / cols, j = t % cols;
-  o[t] = static_cast<float>(2 * static_cast<int>(bit_of(a, spw, i, j) + bit_of(b, spw, i, j)) - 2);
+  if (t >= rows * wpr) return;
+  const int64_t i = t / wpr, w = t - i * wpr;
+  const uint32_t wa = a[i * spw + w], wb = b[i * spw + w];
+  float* orow = o + i * cols;
+  const int64_t c0 = 32 * w, n = cols - c0 < 32 ? cols - c0 : 32;
+  auto val = [&](int q) {
+    const float v = static_cast<float>(2 * static_cast<int>(((wa >> (31 - q)) & 1u) + ((wb >> (31 - q)) & 1u)) - 2);
+    return RELU ? (v > 0.0f ? v : 0.0f) : v;
+  };
+  if (n == 32 && (reinterpret_cast<uintptr_t>(orow + c0) & 15) == 0) {
+    float4* o4 = reinterpret_cast<float4*>(orow + c0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o4[q] = make_float4(val(4 * q), val(4 * q + 1), val(4 * q + 2), val(4 * q + 3));
+  } else {
+    for (int q = 0; q < n; ++q) orow[c0 + q] = val(q);
+  }
 }
 
-// ADD.FFF: float(double(a) + b) (:603-607).
+// ADD.FFF: float(double(a) + b) (:603-607), optionally with the ReLU fused;
+// four elements per thread.
+template <bool RELU>
 __global__ void k_add_fff(const float* __restrict__ a, const float* __restrict__ b, int64_t n,
                           float* __restrict__ o) {
+  const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  auto one = [](float x, float y) {
+    const float v = __double2float_rn(__dadd_rn(static_cast<double>(x), static_cast<double>(y)));
+    return RELU ? (v > 0.0f ? v : 0.0f) : v;
+  };
+  if (t + 4 <= n) {
+    const float4 x = *reinterpret_cast<const float4*>(a + t), y = *reinterpret_cast<const float4*>(b + t);
+    *reinterpret_cast<float4*>(o + t) = make_float4(one(x.x, y.x), one(x.y, y.y), one(x.z, y.z), one(x.w, y.w));
+  } else {
+    for (int64_t k = t; k < n; ++k) o[k] = one(a[k], b[k]);
+  }
+}
+
+template <bool RELU>  // unaligned operands: element per thread
+__global__ void k_add_fff1(const float* __restrict__ a, const float* __restrict__ b, int64_t n,
+                           float* __restrict__ o) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t < n) o[t] = __double2float_rn(__dadd_rn(static_cast<double>(a[t]), static_cast<double>(b[t])));
+  if (t >= n) return;
+  const float v = __double2float_rn(__dadd_rn(static_cast<double>(a[t]), static_cast<double>(b[t])));
+  o[t] = RELU ? (v > 0.0f ? v : 0.0f) : v;
 }
 
 __global__ void k_relu(float* __restrict__ x, int64_t n) {
+  const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  auto r = [](float v) { return v > 0.0f ? v : 0.0f; };
+  if (t + 4 <= n) {
+    float4 v = *reinterpret_cast<float4*>(x + t);
+    *reinterpret_cast<float4*>(x + t) = make_float4(r(v.x), r(v.y), r(v.z), r(v.w));
+  } else {
+    for (int64_t k = t; k < n; ++k) x[k] = r(x[k]);
+  }
+}
+
+__global__ void k_relu1(float* __restrict__ x, int64_t n) {  // unaligned fallback
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t < n) x[t] = x[t] > 0.0f ? x[t] : 0.0f;
 }
 
 // Row softmax in double, sequential column order (graphops.cpp:372-386).
-// A warp owns 32 consecutive rows = one contiguous chunk of 32*cols floats:
-// it stages the chunk into shared memory with independent float4 loads, runs
-// the order-sensitive parts -- the row max and the sequential double sum --
-// lane per row, then recomputes exp(x - max) * (1/sum) element-parallel over
-// the chunk (row = element / cols by a magic multiply) and streams it back.
-constexpr int kSmWarps = 4;
+// A warp owns kSmRows consecutive rows = one contiguous chunk of
+// kSmRows*cols floats: it stages the chunk into shared memory with
+// independent float4 loads, takes the row maxima lane per row, computes
+// every exp(x - max) once element-parallel into a double buffer (row =
+// element / cols by a magic multiply), sums each row lane per row in column
+// order, and writes exp * (1/sum) back through float4 stores.
+constexpr int kSmWarps = 2;  // 24 KB of staging per block
 constexpr int kSmMaxCols = 64;
+constexpr int kSmRows = 16;
 __global__ void __launch_bounds__(kSmWarps * 32)
     k_softmax_staged(const float* __restrict__ x, int64_t rows, int cols, uint32_t cmagic, float* __restrict__ o) {
-  __shared__ __align__(16) float buf[kSmWarps][32 * kSmMaxCols];
-  __shared__ double rmx[kSmWarps][32], rinv[kSmWarps][32];
+  __shared__ __align__(16) float buf[kSmWarps][kSmRows * kSmMaxCols];
+  __shared__ double ebuf[kSmWarps][kSmRows * kSmMaxCols];
+  __shared__ double rmx[kSmWarps][kSmRows], rinv[kSmWarps][kSmRows];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* b = buf[warp];
-  for (int64_t r0 = (static_cast<int64_t>(blockIdx.x) * kSmWarps + warp) * 32; r0 < rows;
-       r0 += static_cast<int64_t>(gridDim.x) * kSmWarps * 32) {
-    const int nr = static_cast<int>(rows - r0 < 32 ? rows - r0 : 32);
+  double* e = ebuf[warp];
+  for (int64_t r0 = (static_cast<int64_t>(blockIdx.x) * kSmWarps + warp) * kSmRows; r0 < rows;
+       r0 += static_cast<int64_t>(gridDim.x) * kSmWarps * kSmRows) {
+    const int nr = static_cast<int>(rows - r0 < kSmRows ? rows - r0 : kSmRows);
     const int n = nr * cols, n4 = n >> 2;
-    const float* src = x + r0 * cols;  // 16-byte aligned: r0*cols is a multiple of 4*32
+    const float* src = x + r0 * cols;  // 16-byte aligned: r0*cols is a multiple of 4*kSmRows
     const float4* src4 = reinterpret_cast<const float4*>(src);
     float4* b4 = reinterpret_cast<float4*>(b);
 #pragma unroll 4
@@ -69,19 +123,28 @@ __global__ void __launch_bounds__(kSmWarps * 32)
     __syncwarp();
     if (lane < nr) {
       const float* xr = b + lane * cols;
-      double mx = -INFINITY;
-      for (int j = 0; j < cols; ++j) mx = fmax(mx, static_cast<double>(xr[j]));
-      double sum = 0.0;
-#pragma unroll 4
-      for (int j = 0; j < cols; ++j) sum = __dadd_rn(sum, exp_nonpos(static_cast<double>(xr[j]) - mx));
-      rmx[warp][lane] = mx;
-      rinv[warp][lane] = __drcp_rn(sum);
+      float mx = -INFINITY;  // exact in float; NaN is skipped like std::max(mx, x) does
+      for (int j = 0; j < cols; ++j) mx = fmaxf(mx, xr[j]);
+      rmx[warp][lane] = static_cast<double>(mx);
     }
     __syncwarp();
 #pragma unroll 4
     for (int t = lane; t < n; t += 32) {
       const uint32_t r = __umulhi(static_cast<uint32_t>(t), cmagic);  // t / cols
-      b[t] = __double2float_rn(__dmul_rn(exp_nonpos(static_cast<double>(b[t]) - rmx[warp][r]), rinv[warp][r]));
+      e[t] = exp_nonpos(static_cast<double>(b[t]) - rmx[warp][r]);
+    }
+    __syncwarp();
+    if (lane < nr) {
+      const double* er = e + lane * cols;
+      double sum = 0.0;
+      for (int j = 0; j < cols; ++j) sum = __dadd_rn(sum, er[j]);
+      rinv[warp][lane] = __drcp_rn(sum);
+    }
+    __syncwarp();
+#pragma unroll 4
+    for (int t = lane; t < n; t += 32) {
+      const uint32_t r = __umulhi(static_cast<uint32_t>(t), cmagic);
+      b[t] = __double2float_rn(__dmul_rn(e[t], rinv[warp][r]));
     }
     __syncwarp();
     float* dst = o + r0 * cols;
@@ -190,21 +253,35 @@ void add_bbb(const uint32_t* a, const uint32_t* b, int64_t words, uint32_t* out,
 }
 
 void add_bbf(const uint32_t* a, const uint32_t* b, int64_t rows, int64_t cols, int wb, float* out,
-             cudaStream_t s) {
+             cudaStream_t s, bool fuse_relu) {
   if (rows * cols == 0) return;
-  k_add_bbf<<<grid1(rows * cols), 256, 0, s>>>(a, b, rows, cols, spw(cols, wb), out);
+  const int64_t threads = rows * ((cols + 31) / 32);
+  if (fuse_relu)
+    k_add_bbf<true><<<grid1(threads), 256, 0, s>>>(a, b, rows, cols, spw(cols, wb), out);
+  else
+    k_add_bbf<false><<<grid1(threads), 256, 0, s>>>(a, b, rows, cols, spw(cols, wb), out);
   BG_LAUNCH_CHECK();
 }
 
-void add_fff(const float* a, const float* b, int64_t n, float* out, cudaStream_t s) {
+void add_fff(const float* a, const float* b, int64_t n, float* out, cudaStream_t s, bool fuse_relu) {
   if (n == 0) return;
-  k_add_fff<<<grid1(n), 256, 0, s>>>(a, b, n, out);
+  const bool v4 = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
+                    reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  const int64_t threads = cdiv(n, 4);
+  if (v4) {
+    if (fuse_relu) k_add_fff<true><<<grid1(threads), 256, 0, s>>>(a, b, n, out);
+    else k_add_fff<false><<<grid1(threads), 256, 0, s>>>(a, b, n, out);
+  } else {
+    if (fuse_relu) k_add_fff1<true><<<grid1(n), 256, 0, s>>>(a, b, n, out);
+    else k_add_fff1<false><<<grid1(n), 256, 0, s>>>(a, b, n, out);
+  }
   BG_LAUNCH_CHECK();
 }
 
 void relu(float* x, int64_t n, cudaStream_t s) {
   if (n == 0) return;
-  k_relu<<<grid1(n), 256, 0, s>>>(x, n);
+  if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) k_relu<<<grid1(cdiv(n, 4)), 256, 0, s>>>(x, n);
+  else k_relu1<<<grid1(n), 256, 0, s>>>(x, n);
   BG_LAUNCH_CHECK();
 }
 
@@ -212,9 +289,9 @@ void softmax_rows(const float* x, int64_t rows, int64_t cols, float* out, cudaSt
   if (rows == 0) return;
   if (cols >= 2 && cols <= kSmMaxCols && x != out && reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
       reinterpret_cast<uintptr_t>(out) % 16 == 0) {
-    // t / cols == umulhi(t, ceil(2^32 / cols)) for t < 32 cols (error 32 cols^2 < 2^32)
+    // t / cols == umulhi(t, ceil(2^32 / cols)) for t < kSmRows cols (error kSmRows cols^2 < 2^32)
     const uint32_t cmagic = static_cast<uint32_t>(((uint64_t{1} << 32) + cols - 1) / cols);
-    const int64_t blocks = std::min<int64_t>(cdiv(rows, kSmWarps * 32), static_cast<int64_t>(sm_count()) * 16);
+    const int64_t blocks = std::min<int64_t>(cdiv(rows, kSmWarps * kSmRows), static_cast<int64_t>(sm_count()) * 32);
     k_softmax_staged<<<static_cast<unsigned>(blocks), kSmWarps * 32, 0, s>>>(x, rows, static_cast<int>(cols),
                                                                             cmagic, out);
   } else {

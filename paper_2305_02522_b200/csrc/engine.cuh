@@ -70,7 +70,8 @@ Op run_bmm(bg_variant v, const Op& a, const Op* w, const WeightCache* wc, int wo
            cudaStream_t s, const RowChunks* in_chunks = nullptr);
 Op run_bspmm(bg_variant v, const bg_frdc* adj, const float* rs, const float* cs, const Op& x,
              int word_bits, Pool& pool, cudaStream_t s);
-Op run_add(bg_variant v, const Op& a, const Op& b, Pool& pool, cudaStream_t s);
+// fuse_relu: apply the layer's ReLU inside the kernel when the result is F
+Op run_add(bg_variant v, const Op& a, const Op& b, Pool& pool, cudaStream_t s, bool fuse_relu = false);
 Op run_concat(bg_variant v, const Op& a, const Op& b, Pool& pool, cudaStream_t s);
 
 // Output shapes (for caller allocation through the C ABI).

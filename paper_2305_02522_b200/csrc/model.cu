@@ -382,9 +382,10 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
           Op agg = ex.spmm_slot(sp, m.graph->raw.get(), rs, cs, hn, prefix + "spmm");
           if (mean && sp.in2 == BG_B && sp.out == BG_F)
             scale_rows_double(agg.f, agg.rows, agg.cols, m.graph->neighbor_count.as<int64_t>(), s);
-          cur = run_add(l.info.plan[3], hs, agg, m.pool, s);
+          // the layer's ReLU rides in the ADD kernel when the sum is F (on a B
+          // sum it is a no-op, graphops.cpp:89-97)
+          cur = run_add(l.info.plan[3], hs, agg, m.pool, s, l.relu && l.info.plan[3].out == BG_F);
           if (l.info.plan[3].out == BG_B) h.bits(prefix + "add.out", cur.bits, cur.rows, cur.cols, cur.wb);
-          if (l.relu) ex.relu_inplace(cur, x0);
           break;
         }
         case BG_LAYER_FC: {

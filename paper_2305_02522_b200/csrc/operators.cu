@@ -312,7 +312,7 @@ void binary_pair(bg_variant v, const Op& a, const Op& b, const char* what) {
 
 }  // namespace
 
-Op run_add(bg_variant v, const Op& a, const Op& b, Pool& pool, cudaStream_t s) {
+Op run_add(bg_variant v, const Op& a, const Op& b, Pool& pool, cudaStream_t s, bool fuse_relu) {
   if (v.op != BG_ADD) fail("add: variant " + variant_name(v) + " is not an ADD variant");
   if (!variant_valid(v)) fail("add: " + variant_name(v) + " is not a supported variant");
   if (a.rows != b.rows || a.cols != b.cols) fail("add: operand shapes disagree");
@@ -323,7 +323,7 @@ Op run_add(bg_variant v, const Op& a, const Op& b, Pool& pool, cudaStream_t s) {
     if (a.prec != BG_F || b.prec != BG_F) fail("add: FFF requires full-precision operands");
     out.prec = BG_F;
     out.f = static_cast<float*>(pool.get(out.bytes()));
-    add_fff(a.f, b.f, a.rows * a.cols, out.f, s);
+    add_fff(a.f, b.f, a.rows * a.cols, out.f, s, fuse_relu);
     return out;
   }
   binary_pair(v, a, b, "add");
@@ -335,7 +335,7 @@ Op run_add(bg_variant v, const Op& a, const Op& b, Pool& pool, cudaStream_t s) {
   } else {
     out.prec = BG_F;
     out.f = static_cast<float*>(pool.get(out.bytes()));
-    add_bbf(a.bits, b.bits, a.rows, a.cols, a.wb, out.f, s);
+    add_bbf(a.bits, b.bits, a.rows, a.cols, a.wb, out.f, s, fuse_relu);
   }
   return out;
 }

@@ -178,8 +178,8 @@ bool rowgroup_bb(bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uint32_
 // ---- elementwise.cu ------------------------------------------------------
 void add_bbb(const uint32_t* a, const uint32_t* b, int64_t words, uint32_t* out, cudaStream_t s);
 void add_bbf(const uint32_t* a, const uint32_t* b, int64_t rows, int64_t cols, int wb, float* out,
-             cudaStream_t s);
-void add_fff(const float* a, const float* b, int64_t n, float* out, cudaStream_t s);
+             cudaStream_t s, bool fuse_relu = false);
+void add_fff(const float* a, const float* b, int64_t n, float* out, cudaStream_t s, bool fuse_relu = false);
 void relu(float* x, int64_t n, cudaStream_t s);
 void softmax_rows(const float* x, int64_t rows, int64_t cols, float* out, cudaStream_t s);
 void scale_rows_double(float* x, int64_t rows, int64_t cols, const int64_t* cnt, cudaStream_t s);

@@ -1,4 +1,6 @@
-"""MM.FBB on the tcgen05 tensor cores (bmm.cu k_fbb_umma / k_fbb_umma2, opt-in BG_FBB=umma|umma2):
+"""MM.FBB on every kernel (BG_FBB forces one): the tcgen05 tensor cores (bmm.cu k_fbb_umma /
+k_fbb_umma2, opt-in BG_FBB=umma|umma2), the TMA-fed and direct mma.sync kernels and the
+warp-per-row popcount kernel:
 +-1 int8 operands in shared memory, s32 accumulators in TMEM.  Bit-exact
 against the oracle on tile-aligned and ragged shapes (partial 128-row tiles,
 odd K, N below the 128-column MMA, 64-bit words)."""
@@ -14,15 +16,18 @@ import paper_2305_02522_b200 as bg
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["umma", "umma2"])
+@pytest.fixture(params=["umma", "umma2", "tma", "imma", "scalar"])
 def umma(monkeypatch, request):
-    # umma: LDG-fed conversion; umma2: bulk-copied fp32 sub-tiles (TMA ring)
+    # umma: LDG-fed conversion; umma2: bulk-copied fp32 sub-tiles (TMA ring);
+    # and the non-tcgen05 paths the default dispatch picks by shape: the
+    # TMA-fed mma.sync kernel, the direct mma.sync kernel, a warp per row
     monkeypatch.setenv("BG_FBB", request.param)
 
 
 @pytest.mark.parametrize("wb", [32, 64])
 @pytest.mark.parametrize("mkn", [(128, 602, 128), (1000, 602, 128), (257, 33, 21), (300, 100, 128), (129, 500, 64),
-                                 (5, 17, 7), (4096, 301, 96), (640, 1024, 128), (77, 64, 32), (2000, 1433, 64)])
+                                 (5, 17, 7), (4096, 301, 96), (640, 1024, 128), (77, 64, 32), (2000, 1433, 64),
+                                 (333, 200, 72), (50, 90, 40), (2711, 1433, 100)])
 def test_fbb_umma_matches_oracle(umma, wb, mkn):
     m, k, n = mkn
     rng = po.Rng(4242 + m + k + n)
