@@ -300,9 +300,14 @@ def main():
             for k in tl:
                 per.setdefault(k.label, []).append(k.ms)
         kernels = []
+        # N > 1: each rank moves its rows' share of every row-local array
+        # (tile-balanced bounds); the fused GCN records are replicated
+        frac = (runner.row1 - runner.row0) / n if world > 1 else 1.0
         for lab, v in per.items():
             kms = float(np.mean(v))
             b = kernel_bytes(lab, shapes)
+            if world > 1 and not (model_name == "gcn" and "mm[BMM.BBF]" in lab):
+                b = int(b * frac)
             kernels.append({"label": lab, "ms": round(kms, 4), "alg_bytes": b,
                             "gb_s": round(b / (kms * 1e-3) / 1e9, 1) if kms > 0 else None})
         launches_per_step = len(per)
@@ -316,6 +321,10 @@ def main():
         for _ in range(e2e_steps):
             runner.forward_host(xh)
         e2e_ms = (time.perf_counter() - t) * 1e3 / e2e_steps
+        if dist:  # the job's end-to-end time is its slowest rank's
+            tt = torch.tensor([e2e_ms], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = float(tt.item())
 
     peak, peak_kind = peaks()
     dom = max(kernels, key=lambda k: k["ms"])

@@ -331,6 +331,11 @@ void bg_comm_destroy(bg_comm* c);
 int bg_model_forward_sharded(bg_model* m, bg_comm* comm, const bg_mat* x, const int64_t* bounds,
                              int world_size, int rank, float* out, float* logits,
                              bg_stream stream);
+/* The same forward with per-op CUDA-event times (labels as bg_model_forward_timed,
+ * plus "layerI.allgather" for each exchange); synchronizes the stream. */
+int bg_model_forward_sharded_timed(bg_model* m, bg_comm* comm, const bg_mat* x, const int64_t* bounds,
+                                   int world_size, int rank, float* out, bg_kernel_timing* timings, int cap,
+                                   int* n, bg_stream stream);
 
 /* ---- deterministic synthetic inputs (ref: rng.hpp:16-80) --------------- */
 typedef struct bg_rng bg_rng;

@@ -143,6 +143,8 @@ PROTOTYPES = {
     "bg_comm_create": (I32, [I32, I32, P, C.c_size_t, C.POINTER(P)]),
     "bg_comm_destroy": (None, [P]),
     "bg_model_forward_sharded": (I32, [P, P, C.POINTER(Mat), P, I32, I32, P, P, P]),
+    "bg_model_forward_sharded_timed": (I32, [P, P, C.POINTER(Mat), P, I32, I32, P, C.POINTER(KernelTiming), I32,
+                                             C.POINTER(I32), P]),
     "bg_rng_create": (I32, [C.c_uint64, C.POINTER(P)]),
     "bg_rng_destroy": (None, [P]),
     "bg_rng_dense": (I32, [P, I64, I64, P]),

@@ -83,16 +83,38 @@ namespace {
                              " at " __FILE__ ":" + std::to_string(__LINE__));               \
   } while (0)
 
+// Per-op CUDA-event timing of the sharded forward (bench.py's kernel table at
+// N > 1); labels follow the single-GPU forward, plus "layerI.allgather".
+using EventList = std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>>;
+struct Timer {
+  EventList* ev = nullptr;
+  cudaStream_t s = nullptr;
+  void begin(const std::string& label) {
+    if (!ev) return;
+    cudaEvent_t a, b;
+    BG_CUDA(cudaEventCreate(&a));
+    BG_CUDA(cudaEventCreate(&b));
+    BG_CUDA(cudaEventRecord(a, s));
+    ev->push_back({label, {a, b}});
+  }
+  void end() {
+    if (ev) BG_CUDA(cudaEventRecord(ev->back().second.second, s));
+  }
+};
+
 struct Shard {
   bg_model& m;
   const std::vector<int64_t>& bounds;  // world + 1 node-row boundaries
   std::vector<std::pair<int64_t, int64_t>> ranges;  // ranges computed by this process
   bg_comm* comm;                       // null: virtual ranks in one process
   cudaStream_t s;
+  Timer tm;
+  std::string prefix;  // "layerI." of the layer being run
 
   // Make rows [bounds[q], bounds[q+1]) of a full-size buffer valid on every rank.
   void allgather(void* buf, int64_t row_bytes) {
     if (!comm || comm->world == 1) return;
+    tm.begin(prefix + "allgather");
     BG_NCCL(nccl().group_start());
     for (int q = 0; q < comm->world; ++q) {
       const int64_t r0 = bounds[q], r1 = bounds[q + 1];
@@ -102,6 +124,7 @@ struct Shard {
                             comm->comm, s));
     }
     BG_NCCL(nccl().group_end());
+    tm.end();
   }
 
   int64_t row_bytes(const Op& o) const {
@@ -120,7 +143,13 @@ struct Shard {
   }
 
   // ref: run_mm_slot on rows [r0, r1) (row-local).
-  Op mm(bg_variant v, const Op& x, const WeightDev& w) {
+  Op mm(bg_variant v, const Op& x, const WeightDev& w, const std::string& label) {
+    tm.begin(prefix + label + "[" + variant_name(v) + "]");
+    Op o = mm_impl(v, x, w);
+    tm.end();
+    return o;
+  }
+  Op mm_impl(bg_variant v, const Op& x, const WeightDev& w) {
     if (v.in1 == BG_F && v.in2 == BG_F && v.out == BG_F) fail("sharded forward: MM.FFF not supported");
     if (v.in1 == BG_B && x.wb != w.wb) fail("bmm: operand word widths disagree");
     if (x.cols != w.rows) fail("bmm: inner dimensions disagree");
@@ -164,6 +193,7 @@ struct Shard {
       allgather(x.prec == BG_F ? static_cast<void*>(x.f) : static_cast<void*>(x.bits), row_bytes(x));
       x_full = true;
     }
+    tm.begin(prefix + "spmm[" + variant_name(v) + "]");
     Op out = alloc_like(v.out, x.cols, v.in1 == BG_B ? x.wb : m.wb);
     for (auto [r0, r1] : ranges) {
       if (r1 <= r0) continue;
@@ -186,35 +216,42 @@ struct Shard {
         bspmm_f(*A, a, s, r0, r1);
       }
     }
+    tm.end();
     return out;
   }
 
-  Op add(bg_variant v, const Op& a, const Op& b) {
+  // fuse_relu: the layer's ReLU inside the F-output ADD kernel
+  Op add(bg_variant v, const Op& a, const Op& b, bool fuse_relu) {
+    tm.begin(prefix + "add[" + variant_name(v) + "]");
     Op out = alloc_like(v.out, a.cols, a.wb);
     for (auto [r0, r1] : ranges) {
       if (r1 <= r0) continue;
       if (v.in1 == BG_F) {
-        add_fff(a.f + r0 * a.cols, b.f + r0 * b.cols, (r1 - r0) * a.cols, out.f + r0 * a.cols, s);
+        add_fff(a.f + r0 * a.cols, b.f + r0 * b.cols, (r1 - r0) * a.cols, out.f + r0 * a.cols, s, fuse_relu);
       } else if (v.out == BG_B) {
         const int64_t w = spw(a.cols, a.wb);
         add_bbb(a.bits + r0 * w, b.bits + r0 * w, (r1 - r0) * w, out.bits + r0 * w, s);
       } else {
         const int64_t w = spw(a.cols, a.wb);
-        add_bbf(a.bits + r0 * w, b.bits + r0 * w, r1 - r0, a.cols, a.wb, out.f + r0 * a.cols, s);
+        add_bbf(a.bits + r0 * w, b.bits + r0 * w, r1 - r0, a.cols, a.wb, out.f + r0 * a.cols, s, fuse_relu);
       }
     }
+    tm.end();
     return out;
   }
 
   void relu_rows(Op& x) {
     if (x.prec != BG_F) return;
+    tm.begin(prefix + "relu");
     for (auto [r0, r1] : ranges)
       if (r1 > r0) relu(x.f + r0 * x.cols, (r1 - r0) * x.cols, s);
+    tm.end();
   }
 };
 
 void forward_sharded(bg_model& m, const Op& x0, const std::vector<int64_t>& bounds, int world,
-                     int rank, bg_comm* comm, float* out_base, float* logits_base, cudaStream_t s) {
+                     int rank, bg_comm* comm, float* out_base, float* logits_base, cudaStream_t s,
+                     EventList* timing = nullptr) {
   if (!m.graph) fail("sharded forward: model carries no graph");
   const int64_t n = m.graph->n;
   if (static_cast<int>(bounds.size()) != world + 1 || bounds.front() != 0 || bounds.back() != n)
@@ -228,7 +265,7 @@ void forward_sharded(bg_model& m, const Op& x0, const std::vector<int64_t>& boun
     if (!errors.empty()) fail("invalid model: " + errors.front());
   }
   m.pool.reset();
-  Shard sh{m, bounds, {}, comm, s};
+  Shard sh{m, bounds, {}, comm, s, Timer{timing, s}, ""};
   if (comm) sh.ranges.push_back({bounds[rank], bounds[rank + 1]});
   else
     for (int q = 0; q < world; ++q) sh.ranges.push_back({bounds[q], bounds[q + 1]});
@@ -239,6 +276,7 @@ void forward_sharded(bg_model& m, const Op& x0, const std::vector<int64_t>& boun
   float* probs_done = nullptr;
   for (size_t i = 0; i < nl; ++i) {
     ModelLayer& l = m.layers[i];
+    sh.prefix = "layer" + std::to_string(i) + ".";
     try {
       switch (l.info.kind) {
         case BG_LAYER_GCN: {
@@ -254,22 +292,26 @@ void forward_sharded(bg_model& m, const Op& x0, const std::vector<int64_t>& boun
               cur_full = true;
             }
             auto* recs = static_cast<uint32_t*>(m.pool.get(static_cast<size_t>(n + 1) * 64));  // + zero record
+            sh.tm.begin(sh.prefix + "mm[" + variant_name(mm) + "]");
             gcn1_records(cur.bits, n, cur.cols, cur.wb, l.w1.wt.as<uint32_t>(), l.w1.scale.as<float>(),
                          l.w1.cols, recs, s);
+            sh.tm.end();
             Op o = sh.alloc_like(BG_F, l.w1.cols, m.wb);
             float* probs = nullptr;
             if (i + 1 < nl && m.layers[i + 1].info.kind == BG_LAYER_SOFTMAX)
               probs = (i + 2 == nl && out_base) ? out_base : static_cast<float*>(m.pool.get(o.bytes()));
+            sh.tm.begin(sh.prefix + "spmm[" + variant_name(sp) + "]");
             for (auto [r0, r1] : sh.ranges)
               if (r1 > r0)
                 gcn1_aggregate(A, recs, cur.cols, cur.wb, l.w1.wt.as<uint32_t>(), l.w1.scale.as<float>(),
                                l.w1.cols, o.f, probs, s, r0, r1);
+            sh.tm.end();
             probs_done = probs;
             cur = o;
             cur_full = comm == nullptr;
             break;
           }
-          Op h = sh.mm(mm, cur, l.w1);
+          Op h = sh.mm(mm, cur, l.w1, "mm");
           bool h_full = comm == nullptr;
           const bool fac = sp.in2 == BG_F;
           cur = sh.spmm(sp, &A, fac ? m.graph->norm.as<float>() : nullptr,
@@ -281,8 +323,8 @@ void forward_sharded(bg_model& m, const Op& x0, const std::vector<int64_t>& boun
         case BG_LAYER_SAGE:
         case BG_LAYER_GRAPHCONV: {
           const bool mean = l.info.kind == BG_LAYER_SAGE;
-          Op hs = sh.mm(l.info.plan[0], cur, l.w1);
-          Op hn = sh.mm(l.info.plan[1], cur, l.w2);
+          Op hs = sh.mm(l.info.plan[0], cur, l.w1, "mm_self");
+          Op hn = sh.mm(l.info.plan[1], cur, l.w2, "mm_neigh");
           bool hn_full = comm == nullptr;
           const bg_variant sp = l.info.plan[2];
           const bool fac = sp.in2 == BG_F;
@@ -294,13 +336,12 @@ void forward_sharded(bg_model& m, const Op& x0, const std::vector<int64_t>& boun
               if (r1 > r0)
                 scale_rows_double(agg.f + r0 * agg.cols, r1 - r0, agg.cols,
                                   m.graph->neighbor_count.as<int64_t>() + r0, s);
-          cur = sh.add(l.info.plan[3], hs, agg);
+          cur = sh.add(l.info.plan[3], hs, agg, l.relu && l.info.plan[3].out == BG_F);
           cur_full = comm == nullptr;
-          if (l.relu) sh.relu_rows(cur);
           break;
         }
         case BG_LAYER_FC:
-          cur = sh.mm(l.info.plan[0], cur, l.w1);
+          cur = sh.mm(l.info.plan[0], cur, l.w1, "mm");
           cur_full = comm == nullptr;
           if (l.relu) sh.relu_rows(cur);
           break;
@@ -317,10 +358,15 @@ void forward_sharded(bg_model& m, const Op& x0, const std::vector<int64_t>& boun
                                         cudaMemcpyDeviceToDevice, s));
           float* dst = (i + 1 == nl && out_base) ? out_base : static_cast<float*>(m.pool.get(cur.bytes()));
           if (probs_done && i == nl - 1 && probs_done == out_base) {
-            // already produced by the fused aggregation epilogue
+            // already produced by the fused aggregation epilogue (an empty
+            // timed span keeps the label list of the 1-GPU forward)
+            sh.tm.begin(sh.prefix + "softmax");
+            sh.tm.end();
           } else {
+            sh.tm.begin(sh.prefix + "softmax");
             for (auto [r0, r1] : sh.ranges)
               if (r1 > r0) softmax_rows(cur.f + r0 * cur.cols, r1 - r0, cur.cols, dst + r0 * cur.cols, s);
+            sh.tm.end();
           }
           cur.f = dst;
           break;
@@ -350,6 +396,38 @@ void forward_sharded(bg_model& m, const Op& x0, const std::vector<int64_t>& boun
   }
 }
 
+}  // namespace
+}  // namespace bg
+
+namespace bg {
+namespace {
+void sharded_entry(bg_model* m, bg_comm* comm, const bg_mat* x, const int64_t* bounds, int world, int rank,
+                   float* out, float* logits, bg_stream stream, EventList* timing) {
+  {
+    if (!m || !x || !bounds) fail("sharded forward: null argument");
+    if (comm && (comm->world != world || comm->rank != rank))
+      fail("sharded forward: communicator does not match world/rank");
+    if (rank < 0 || rank >= world) fail("sharded forward: bad rank");
+    std::vector<int64_t> b(bounds, bounds + world + 1);
+    Op x0 = op_from_mat(x);
+    const int64_t r0 = b[rank], r1 = b[rank + 1];
+    int64_t oc = 0;
+    for (const auto& l : m->layers)
+      if (l.info.has_w1) oc = l.w1.cols;
+    float* out_base = out;
+    float* log_base = logits;
+    if (comm) {
+      // x and out hold this rank's rows only: index them through shifted bases
+      if (x0.rows != r1 - r0) fail("sharded forward: x must hold this rank's rows");
+      if (x0.prec == BG_F) x0.f -= r0 * x0.cols;
+      else x0.bits -= r0 * spw(x0.cols, x0.wb);
+      x0.rows = m->graph ? m->graph->n : x0.rows;
+      if (out) out_base = out - r0 * oc;
+      if (logits) log_base = logits - r0 * oc;
+    }
+    forward_sharded(*m, x0, b, world, rank, comm, out_base, log_base, S(stream), timing);
+  }
+}
 }  // namespace
 }  // namespace bg
 
@@ -401,30 +479,34 @@ void bg_comm_destroy(bg_comm* c) { delete c; }
 
 int bg_model_forward_sharded(bg_model* m, bg_comm* comm, const bg_mat* x, const int64_t* bounds,
                              int world, int rank, float* out, float* logits, bg_stream stream) {
-  return guard([&] {
-    if (!m || !x || !bounds) fail("sharded forward: null argument");
-    if (comm && (comm->world != world || comm->rank != rank))
-      fail("sharded forward: communicator does not match world/rank");
-    if (rank < 0 || rank >= world) fail("sharded forward: bad rank");
-    std::vector<int64_t> b(bounds, bounds + world + 1);
-    Op x0 = op_from_mat(x);
-    const int64_t r0 = b[rank], r1 = b[rank + 1];
-    int64_t oc = 0;
-    for (const auto& l : m->layers)
-      if (l.info.has_w1) oc = l.w1.cols;
-    float* out_base = out;
-    float* log_base = logits;
-    if (comm) {
-      // x and out hold this rank's rows only: index them through shifted bases
-      if (x0.rows != r1 - r0) fail("sharded forward: x must hold this rank's rows");
-      if (x0.prec == BG_F) x0.f -= r0 * x0.cols;
-      else x0.bits -= r0 * spw(x0.cols, x0.wb);
-      x0.rows = m->graph ? m->graph->n : x0.rows;
-      if (out) out_base = out - r0 * oc;
-      if (logits) log_base = logits - r0 * oc;
+  return guard([&] { sharded_entry(m, comm, x, bounds, world, rank, out, logits, stream, nullptr); });
+}
+
+int bg_model_forward_sharded_timed(bg_model* m, bg_comm* comm, const bg_mat* x, const int64_t* bounds,
+                                   int world, int rank, float* out, bg_kernel_timing* timings, int cap, int* n,
+                                   bg_stream stream) {
+  EventList ev;
+  const int rc = guard([&] {
+    sharded_entry(m, comm, x, bounds, world, rank, out, nullptr, stream, &ev);
+    BG_CUDA(cudaStreamSynchronize(S(stream)));
+    int k = 0;
+    for (const auto& e : ev) {
+      if (k >= cap) break;
+      float ms = 0.0f;
+      BG_CUDA(cudaEventElapsedTime(&ms, e.second.first, e.second.second));
+      std::memset(timings[k].label, 0, sizeof timings[k].label);
+      std::strncpy(timings[k].label, e.first.c_str(), sizeof timings[k].label - 1);
+      timings[k].ms = ms;
+      ++k;
     }
-    forward_sharded(*m, x0, b, world, rank, comm, out_base, log_base, S(stream));
+    if (n) *n = k;
   });
+  for (auto& e : ev) {
+    cudaEventDestroy(e.second.first);
+    cudaEventDestroy(e.second.second);
+  }
+  return rc;
 }
 
 }  // extern "C"
+

@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from .bitgnn import Model, _mat, _stream, storage_words_per_row
+from .bitgnn import KernelTiming, Model, _mat, _stream, storage_words_per_row
 from ._lib import check, lib
 
 
@@ -93,11 +93,28 @@ class ShardedModel:
         return out
 
     def forward_timed(self, x):
-        return self.model.forward_timed(x)
+        """The sharded forward with per-op CUDA-event times on this rank
+        (same labels as Model.forward_timed, plus 'layerI.allgather')."""
+        xl = self._local(x).contiguous()
+        rows = self.row1 - self.row0
+        out = torch.empty((rows, self.model.output_cols()), dtype=torch.float32, device="cuda")
+        cx = _mat(xl)
+        cap = 256
+        arr = (L.KernelTiming * cap)()
+        n = C.c_int()
+        check(lib().bg_model_forward_sharded_timed(
+            self.model._h, self.comm._h if self.comm else None, C.byref(cx), self.b.ctypes.data, self.world,
+            self.rank, out.data_ptr(), arr, cap, C.byref(n), _stream()))
+        return out, [KernelTiming(arr[i].label.decode(), arr[i].ms) for i in range(n.value)]
 
     def forward_host(self, xh):
-        xl = torch.from_numpy(np.ascontiguousarray(xh[self.row0:self.row1].numpy())).cuda() \
-            if isinstance(xh, torch.Tensor) else torch.from_numpy(xh[self.row0:self.row1]).cuda()
+        """End to end on this rank: its rows of the host X in (a pinned tensor's
+        row slice stays pinned, so the copy is a DMA), the sharded forward,
+        its output rows back to the host."""
+        if isinstance(xh, torch.Tensor):
+            xl = xh[self.row0:self.row1].to("cuda", non_blocking=True)
+        else:
+            xl = torch.from_numpy(np.ascontiguousarray(xh[self.row0:self.row1])).cuda()
         out = self.forward(xl)
         return out.cpu()
 

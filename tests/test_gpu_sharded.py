@@ -10,6 +10,7 @@ import pyoracle as po
 from helpers import to_layer_specs
 
 import paper_2305_02522_b200 as bg
+from paper_2305_02522_b200 import sharded
 from paper_2305_02522_b200.sharded import forward_virtual_ranks, partition_bounds
 
 pytestmark = pytest.mark.gpu
@@ -74,3 +75,35 @@ def test_sharded_dense_graph_through_windowed_aggregation(world):
     assert torch.equal(out, ref_out)
     o_out, o_log, _ = po.run_model(layers, po.Graph(n, s, d), X)
     assert np.array_equal(lg.cpu().numpy(), o_log)
+
+
+def test_sharded_model_host_entry_point_single_rank():
+    # bench.py's e2e path under torchrun: this rank's pinned host rows in,
+    # its output rows out; with one rank it is the whole forward
+    n, e, f, h, c = 3000, 60000, 300, 128, 41
+    s, d = po.Rng(100).random_edges(n, e, False)
+    layers, X = po.build_model("gcn", f, h, c, 99, n)
+    g = bg.prepare_graph(n, s, d)
+    specs = to_layer_specs(bg, layers)
+    want = bg.Model(specs, g).forward(torch.from_numpy(X).cuda()).cpu()
+    sm = sharded.ShardedModel(specs, g, None, 1, 0)
+    got = sm.forward_host(torch.from_numpy(X).pin_memory())
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+
+
+def test_sharded_timed_forward_single_rank_labels_and_output():
+    # bench.py's per-op table under torchrun: same labels as the 1-GPU forward
+    n, e, f, h, c = 3000, 60000, 300, 128, 41
+    s, d = po.Rng(100).random_edges(n, e, False)
+    layers, X = po.build_model("gcn", f, h, c, 99, n)
+    g = bg.prepare_graph(n, s, d)
+    specs = to_layer_specs(bg, layers)
+    m = bg.Model(specs, g)
+    x = torch.from_numpy(X).cuda()
+    want, t1 = m.forward_timed(x)
+    sm = sharded.ShardedModel(specs, g, None, 1, 0)
+    got, t2 = sm.forward_timed(x)
+    assert torch.equal(got, want)
+    assert [k.label for k in t2] == [k.label for k in t1]
+    assert all(k.ms >= 0 for k in t2) and t2[0].ms > 0
