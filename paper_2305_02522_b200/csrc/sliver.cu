@@ -139,12 +139,22 @@ __global__ void __launch_bounds__(256)
     uint32_t P[NP];
 #pragma unroll
     for (int q = 0; q < NP; ++q) P[q] = 0u;
+    const uint32_t padded = (deg + kBitPad - 1) / kBitPad * kBitPad;  // this row's view length
     for (uint32_t j = 0; j < mx; j += 8) {
+      // the row's next 8 column indices as two 16-byte loads (the 4 lanes of
+      // a row read the same address: one request), not 8 scalar loads per
+      // lane that re-fetch the same sector from L2
+      uint4 c0 = make_uint4(0u, 0u, 0u, 0u), c1 = c0;
+      if (j < padded) {
+        c0 = __ldg(reinterpret_cast<const uint4*>(cols + j));
+        c1 = __ldg(reinterpret_cast<const uint4*>(cols + j + 4));
+      }
+      const uint32_t cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
       uint32_t v[8];
 #pragma unroll
       for (int m = 0; m < 8; ++m) {
         v[m] = 0u;
-        if (j + m < deg && word_ok) v[m] = __ldg(xg + static_cast<int64_t>(ld_nc_u32(cols + j + m)) * xspw);
+        if (j + m < deg && word_ok) v[m] = __ldg(xg + static_cast<int64_t>(cc[m]) * xspw);
       }
       hs_add8<NP>(P, v);
     }
