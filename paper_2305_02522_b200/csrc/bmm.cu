@@ -405,10 +405,32 @@ __device__ __forceinline__ void fbb_convert(const float* __restrict__ src, int v
   }
 }
 
+// Even K, full tile in the ring slot: the tile is TR*K contiguous fp32 in
+// shared memory (16-byte aligned), so it is read as 16-byte chunks of the
+// flattened tile -- one LDS.128 per lane, consecutive lanes consecutive
+// chunks (4 wavefronts per warp instruction, where fbb_convert's per-row
+// 8-column items cost 8 per LDS.64).  A chunk's elements (2p, 2p+1) never
+// straddle a row (K even), so it lands as two 2-byte stores.
+__device__ __forceinline__ void fbb_convert4(const float* __restrict__ src, int tr, int k, uint32_t kmagic,
+                                             int ttid, int nthr, int lda, uint8_t* __restrict__ mine) {
+  const uint32_t nch = static_cast<uint32_t>(tr * k) >> 2;
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  for (uint32_t i = ttid; i < nch; i += nthr) {
+    const float4 v = s4[i];
+    const uint32_t b = sign_bytes4(v.x, v.y, v.z, v.w);
+    const uint32_t f = 4 * i;
+    const uint32_t r = __umulhi(f, kmagic);  // f / k (f * k < 2^32)
+    const uint32_t c = f - r * static_cast<uint32_t>(k);
+    *reinterpret_cast<uint16_t*>(mine + r * lda + c) = static_cast<uint16_t>(b);
+    const bool wrap = c + 2 >= static_cast<uint32_t>(k);
+    *reinterpret_cast<uint16_t*>(mine + (wrap ? (r + 1) * lda : r * lda + c + 2)) = static_cast<uint16_t>(b >> 16);
+  }
+}
+
 template <int NW>  // output words per row (N <= 32*NW); one warp per word
 __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
     k_fbb_tma(const float* __restrict__ a_f, const uint32_t* __restrict__ wt, int64_t rows, int k,
-              int kspw, int n, int ksteps, int ospw, uint32_t qmagic, int mb,
+              int kspw, int n, int ksteps, int ospw, uint32_t qmagic, uint32_t kmagic, int mb,
               uint32_t* __restrict__ out_bits) {
   extern __shared__ __align__(16) uint8_t fbb_smem[];
   __shared__ __align__(8) uint64_t full[kFbbStages];
@@ -468,7 +490,9 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
     // fp32 -> +-1 bytes (x >= 0 -> +1, bitdense.cpp:83).  Item t = (row r,
     // 8-column group) with r = t / q (magic multiply); groups past K are
     // never written (zeroed once above); the last group of a row is masked.
-    if (!partial)
+    if (!partial && keven)
+      fbb_convert4(ring + static_cast<size_t>(slot) * (tile_bytes / 4), TR, k, kmagic, ttid, nthr, lda, mine);
+    else if (!partial)
       fbb_convert<false>(ring + static_cast<size_t>(slot) * (tile_bytes / 4), TR, k, keven, items, q, qmagic,
                          ttid, nthr, lda, mine);
     else
@@ -976,11 +1000,13 @@ int64_t fbb_tma(const BmmArgs& a, cudaStream_t s) {
   // t / q == umulhi(t, ceil(2^32 / q)) for t < 16 mb q: the error term t*(M*q - 2^32) < 128 q^2 < 2^32
   const uint32_t q = static_cast<uint32_t>((a.k + 7) / 8);
   const uint32_t qmagic = static_cast<uint32_t>(((uint64_t{1} << 32) + q - 1) / q);
+  // f / k == umulhi(f, ceil(2^32 / k)) for flat tile offsets f < 16 mb k (f k < 2^32)
+  const uint32_t kmagic = static_cast<uint32_t>(((uint64_t{1} << 32) + a.k - 1) / a.k);
   auto go = [&](auto kern) {
     BG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     const int64_t blocks = std::min<int64_t>(tiles, sm_count());
     kern<<<static_cast<unsigned>(blocks), kFbbTeams * NW * 32, smem, s>>>(
-        a.a_f, a.wt, a.rows, static_cast<int>(a.k), kspw, static_cast<int>(a.n), ksteps, ospw, qmagic, mb,
+        a.a_f, a.wt, a.rows, static_cast<int>(a.k), kspw, static_cast<int>(a.n), ksteps, ospw, qmagic, kmagic, mb,
         a.out_bits);
   };
   if (NW == 1) go(k_fbb_tma<1>);
