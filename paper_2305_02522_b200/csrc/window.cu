@@ -19,10 +19,13 @@
 // tops every lane up to that step's length with edges of half k+1, which
 // evens the lanes out (simulated slot fill 56% -> ~80% on Reddit-like graphs).
 //
-// Entry encoding: u16 = slot << 12 | (column - half*Wh), slot = half % 3, so
-// the shared address is base + entry * 16 with the slots 64 KB apart; padding
-// is kWinPad (slot 0, record 4095: a zero record that no bulk copy ever
-// overwrites).
+// Entry encoding: u16 = slot * kSlotRec + (column - half*Wh), slot = half %
+// kSlots, so the shared address is base + entry * 16 with the slots
+// contiguous; padding is kWinPad (slot 0's last record: a zero record that no
+// bulk copy ever overwrites).  BG_WIN_SLOTS=4 (4 x 56 KB: a refill may land
+// while the slowest warp is two steps behind) measured slower on Reddit,
+// 0.244 vs 0.228 ms: 68 smaller steps instead of 57 cost more in per-step
+// work and padding than the extra slack saves.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -37,14 +40,18 @@ namespace bg {
 namespace {
 
 constexpr int kWinRec = 16;             // bytes per packed node row (4 u32 words)
-constexpr int kSlotRec = 4096;          // records per ring slot (64 KB)
-constexpr int kSlots = 3;               // ring slots; half h lives in slot h % 3
-constexpr int kWinHalf = kSlotRec - 1;  // node rows per half-window (record 4095 stays zero)
-constexpr uint16_t kWinPad = kWinHalf;  // slot 0, record 4095
+#ifndef BG_WIN_SLOTS
+#define BG_WIN_SLOTS 3
+#endif
+constexpr int kSlots = BG_WIN_SLOTS;    // ring slots; half h lives in slot h % kSlots
+// records per ring slot: 4 x 56 KB (or 3 x 64 KB) of shared memory
+constexpr int kSlotRec = kSlots == 4 ? 3584 : 4096;  // 64 KB slots by default
+constexpr int kWinHalf = kSlotRec - 1;  // node rows per half-window (the last record stays zero)
+constexpr uint16_t kWinPad = kWinHalf;  // slot 0's zero record
 constexpr int kWinQ = 8;                // ELL groups in flight per lane (4 or 8)
 constexpr int kWinPrefetch = 24;        // groups ahead the stream is bulk-prefetched into L2
 constexpr int kWinMaxThreads = 576;     // 18 warps (5 per SMSP): <= 96 registers per thread
-constexpr size_t kWinSmem = static_cast<size_t>(kSlots) * kSlotRec * kWinRec;  // 192 KB
+constexpr size_t kWinSmem = static_cast<size_t>(kSlots) * kSlotRec * kWinRec;  // 192 KB (224 KB with 4 slots)
 
 __device__ __forceinline__ uint2 ld_nc_v2(const uint2* p) {
   uint2 v;
@@ -144,7 +151,7 @@ __global__ void k_win_fill(const uint64_t* __restrict__ srp, const uint32_t* __r
     }
     const uint32_t h = col / static_cast<uint32_t>(Wh);
     ell[base + (pos >> 2) * (4 * RW) + (pos & 3)] =
-        static_cast<uint16_t>(((h % kSlots) << 12) | (col - h * static_cast<uint32_t>(Wh)));
+        static_cast<uint16_t>((h % kSlots) * kSlotRec + (col - h * static_cast<uint32_t>(Wh)));
     ++pos;
     --left;
   });
