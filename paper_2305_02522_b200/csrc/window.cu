@@ -199,6 +199,148 @@ __device__ void bank_order_segment(uint16_t* __restrict__ segp, uint32_t K, int 
   }
 }
 
+// Matching-based order for segments of at most kMatchK entries per lane.
+// Per position, the lanes of the group are matched to distinct bank groups by
+// augmenting paths (Kuhn), lanes with the most real entries left first and
+// bank groups with the most entries left tried first (the max-degree rule of
+// bipartite edge colouring, under which K positions suffice whenever no bank
+// group holds more than K of the group's entries).  Padding entries all
+// address the same zero record (bank group 7): any number of them at one
+// position is one wavefront, but they block bank group 7 for real entries.
+constexpr int kMatchK = 48;
+__device__ void bank_match_segment(uint16_t* __restrict__ segp, uint32_t K, int q, int RW) {
+  auto at = [&](int l, uint32_t k) -> uint16_t& { return segp[(k >> 2) * (4 * RW) + (8 * q + l) * 4 + (k & 3)]; };
+  uint16_t ent[8][kMatchK];
+  uint8_t cnt[8][8];
+  int real[8], pads[8], bank_left[8];
+  for (int b = 0; b < 8; ++b) bank_left[b] = 0;
+  for (int l = 0; l < 8; ++l) {
+    real[l] = pads[l] = 0;
+    for (int b = 0; b < 8; ++b) cnt[l][b] = 0;
+    for (uint32_t k = 0; k < K; ++k) {
+      const uint16_t e = at(l, k);
+      ent[l][k] = e;
+      if (e == kWinPad) {
+        ++pads[l];
+      } else {
+        ++real[l];
+        ++cnt[l][e & 7];
+        ++bank_left[e & 7];
+      }
+    }
+  }
+  for (uint32_t k = 0; k < K; ++k) {
+    int order[8], n = 0;
+    for (int l = 0; l < 8; ++l)
+      if (real[l] > 0) order[n++] = l;
+    for (int a = 1; a < n; ++a)  // most real entries left first
+      for (int c = a; c > 0 && real[order[c]] > real[order[c - 1]]; --c) {
+        const int t = order[c];
+        order[c] = order[c - 1];
+        order[c - 1] = t;
+      }
+    int border[8];
+    for (int b = 0; b < 8; ++b) border[b] = b;
+    for (int a = 1; a < 8; ++a)
+      for (int c = a; c > 0 && bank_left[border[c]] > bank_left[border[c - 1]]; --c) {
+        const int t = border[c];
+        border[c] = border[c - 1];
+        border[c - 1] = t;
+      }
+    bool pad_forced = false;  // a lane with only padding left places it here
+    for (int l = 0; l < 8; ++l)
+      if (real[l] == 0 && pads[l] > 0) pad_forced = true;
+    int lane_bank[8], bank_lane[8];
+    auto match = [&](bool allow7) {
+      for (int b = 0; b < 8; ++b) bank_lane[b] = -1;
+      for (int l = 0; l < 8; ++l) lane_bank[l] = -1;
+      for (int a = 0; a < n; ++a) {
+        // iterative augmenting-path search from lane order[a]
+        int prev_bank[8], via_lane[8];
+        bool seen[8] = {false, false, false, false, false, false, false, false};
+        int queue[8], qh = 0, qt = 0, found = -1;
+        queue[qt++] = order[a];
+        int from_bank_of_lane[8];
+        for (int l = 0; l < 8; ++l) from_bank_of_lane[l] = -1;
+        while (qh < qt && found < 0) {
+          const int l = queue[qh++];
+          for (int bi = 0; bi < 8 && found < 0; ++bi) {
+            const int b = border[bi];
+            if (seen[b] || cnt[l][b] == 0 || (b == 7 && !allow7)) continue;
+            seen[b] = true;
+            via_lane[b] = l;
+            prev_bank[b] = from_bank_of_lane[l];
+            if (bank_lane[b] < 0) {
+              found = b;
+            } else {
+              const int l2 = bank_lane[b];
+              from_bank_of_lane[l2] = b;
+              queue[qt++] = l2;
+            }
+          }
+        }
+        for (int b = found; b >= 0;) {  // flip the path
+          const int l = via_lane[b], pb = prev_bank[b];
+          bank_lane[b] = l;
+          lane_bank[l] = b;
+          b = pb;
+        }
+      }
+    };
+    match(!pad_forced);
+    bool any_pad = pad_forced;
+    for (int a = 0; a < n; ++a)
+      if (lane_bank[order[a]] < 0 && pads[order[a]] > 0) any_pad = true;
+    if (any_pad && !pad_forced && bank_lane[7] >= 0) {
+      // padding will be placed: see whether giving up bank group 7 costs a lane
+      int lb[8], bl[8];
+      for (int i = 0; i < 8; ++i) lb[i] = lane_bank[i], bl[i] = bank_lane[i];
+      int m1 = 0;
+      for (int l = 0; l < 8; ++l) m1 += lane_bank[l] >= 0;
+      match(false);
+      int m2 = 0;
+      for (int l = 0; l < 8; ++l) m2 += lane_bank[l] >= 0;
+      // a real entry in bank group 7 next to padding costs one wavefront, as
+      // does one lane fewer matched: keep bank 7 only if that saves more
+      if (m2 + 1 < m1)
+        for (int i = 0; i < 8; ++i) lane_bank[i] = lb[i], bank_lane[i] = bl[i];
+    }
+    // place: matched lanes an entry of their bank group, the rest padding if
+    // they have any, else any real entry (a conflict)
+    for (int l = 0; l < 8; ++l) {
+      int want = lane_bank[l];
+      bool pad = false;
+      if (want < 0) {
+        if (pads[l] > 0) pad = true;
+        else
+          for (int b = 0; b < 8 && want < 0; ++b)
+            if (cnt[l][b]) want = b;
+      }
+      // find a remaining entry at positions >= k and swap it to k
+      uint32_t pick = k;
+      for (uint32_t j = k; j < K; ++j) {
+        const uint16_t e = ent[l][j];
+        if (pad ? e == kWinPad : (e != kWinPad && (e & 7) == static_cast<uint32_t>(want))) {
+          pick = j;
+          break;
+        }
+      }
+      const uint16_t e = ent[l][pick];
+      ent[l][pick] = ent[l][k];
+      ent[l][k] = e;
+      if (e == kWinPad) {
+        --pads[l];
+      } else {
+        --real[l];
+        --cnt[l][e & 7];
+        --bank_left[e & 7];
+      }
+    }
+  }
+  for (int l = 0; l < 8; ++l)
+    for (uint32_t k = 0; k < K; ++k) at(l, k) = ent[l][k];
+}
+
 // Thread per (warp stream, conflict group of 8 rows): every step segment of
 // the stream in turn.  (An LDS.128 is served per 8 lanes; with two threads
 // per row an LDS.64 is served per 16 lanes = 8 rows: a group is 8 rows either way.)
@@ -211,7 +353,8 @@ __global__ void k_win_bankorder(const uint32_t* __restrict__ sbase, const uint16
   uint64_t g = sbase[wv];
   for (int k = 0; k < nh; ++k) {
     const uint32_t len = steplen[wv * nh + k];
-    bank_order_segment(ell + g * (4 * RW), len * 4, static_cast<int>(t % cg), RW);
+    if (len * 4 <= kMatchK) bank_match_segment(ell + g * (4 * RW), len * 4, static_cast<int>(t % cg), RW);
+    else bank_order_segment(ell + g * (4 * RW), len * 4, static_cast<int>(t % cg), RW);
     g += len;
   }
 }
