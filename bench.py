@@ -143,7 +143,8 @@ def kernel_bytes(label: str, shapes: dict) -> int:
     if v.startswith("BMM"):
         a = 4 * n * fin if tags[0] == "F" else 4 * n * spw(fin)
         o = 4 * n * spw(fout) if tags[2] == "B" else 4 * n * fout
-        return a + 4 * fout * spw(fin) + 4 * fout + o
+        pair = 2 if "mm_pair" in label else 1  # two weights and two results, the input once
+        return a + pair * (4 * fout * spw(fin) + 4 * fout + o)
     if v.startswith("BSpMM"):
         which = "loops" if shapes["model"] == "gcn" else "raw"
         x = 4 * n * spw(fout) if tags[0] == "B" else 4 * n * fout

@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(kWarps * 32)
           const float* __restrict__ alpha, const uint32_t* __restrict__ wt,
           const float* __restrict__ beta, int64_t rows, int64_t k, int64_t n, int64_t kspw,
           int64_t ld, int64_t c0, int64_t nc, int64_t ospw, uint32_t* __restrict__ out_bits,
-          float* __restrict__ out_f) {
+          float* __restrict__ out_f, uint32_t* __restrict__ out_bits2, int64_t n2, int64_t ntot) {
   extern __shared__ uint32_t smem[];
   uint32_t* sw = smem;                       // nc x ld transposed weight words
   uint32_t* srow = smem + 32 * M * ld;       // kWarps x kspw packed activation rows (after all 32*M weight rows the lanes read)
@@ -72,16 +72,28 @@ __global__ void __launch_bounds__(kWarps * 32)
     }
     __syncwarp();
     if (OUTB) {
+      // combined column jg = c0 + j: words below nw1 belong to the first
+      // result (n valid columns), the rest to out_bits2 (n2 valid columns)
+      const int64_t nw1 = (n + 31) / 32, nw2 = (n2 + 31) / 32;
+      const int64_t ospw2 = out_bits2 ? ospw : 0;  // paired results share the word width and column count class
 #pragma unroll
       for (int m = 0; m < M; ++m) {
-        const int64_t j = 32 * m + lane;
-        const bool bit = j < nc && (k - 2 * static_cast<int64_t>(diff[m])) >= 0;
+        const int64_t j = 32 * m + lane, gw = c0 / 32 + m;
+        const bool second = gw >= nw1;
+        const int64_t col = second ? c0 + j - 32 * nw1 : c0 + j;
+        const bool bit = j < nc && col < (second ? n2 : n) && (k - 2 * static_cast<int64_t>(diff[m])) >= 0;
         const uint32_t word = __brev(__ballot_sync(0xFFFFFFFFu, bit));
-        if (lane == 0 && 32 * m < nc) out_bits[row * ospw + c0 / 32 + m] = word;  // only words of this pass
+        if (lane == 0 && 32 * m < nc) {  // only words of this pass
+          if (second) out_bits2[row * ospw2 + (gw - nw1)] = word;
+          else out_bits[row * ospw + gw] = word;
+        }
       }
       // zero the storage-padding words of 64-bit rows after the last pass
-      if (lane == 0 && c0 + nc == n)
-        for (int64_t w = (n + 31) / 32; w < ospw; ++w) out_bits[row * ospw + w] = 0;
+      if (lane == 0 && c0 + nc == ntot) {
+        for (int64_t w = nw1; w < ospw; ++w) out_bits[row * ospw + w] = 0;
+        if (out_bits2)
+          for (int64_t w = nw2; w < ospw2; ++w) out_bits2[row * ospw2 + w] = 0;
+      }
     } else {
       const double al = alpha ? static_cast<double>(alpha[row]) : 1.0;
 #pragma unroll
@@ -431,7 +443,11 @@ template <int NW>  // output words per row (N <= 32*NW); one warp per word
 __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
     k_fbb_tma(const float* __restrict__ a_f, const uint32_t* __restrict__ wt, int64_t rows, int k,
               int kspw, int n, int ksteps, int ospw, uint32_t qmagic, uint32_t kmagic, int mb,
-              uint32_t* __restrict__ out_bits) {
+              uint32_t* __restrict__ out_bits, uint32_t* __restrict__ out_bits2) {
+  // out_bits2: paired product -- weight columns [32*NW, 64*NW) of wt are a
+  // second matrix (same n) whose result goes there; each warp then runs its
+  // MMAs twice on the same converted tile
+  const int halves = out_bits2 ? 2 : 1;
   extern __shared__ __align__(16) uint8_t fbb_smem[];
   __shared__ __align__(8) uint64_t full[kFbbStages];
   const int kpad = 32 * ksteps;
@@ -440,16 +456,16 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
   const uint32_t tile_bytes = static_cast<uint32_t>(TR * k) * 4u;
   float* ring = reinterpret_cast<float*>(fbb_smem);                                  // stages x TR x k fp32
   uint8_t* a8 = fbb_smem + static_cast<size_t>(kFbbStages) * tile_bytes;            // teams x TR x lda
-  uint8_t* w8 = a8 + static_cast<size_t>(kFbbTeams) * TR * lda;                     // 32*NW x lda
+  uint8_t* w8 = a8 + static_cast<size_t>(kFbbTeams) * TR * lda;                     // halves*32*NW x lda
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int team = warp / NW, wq = warp % NW, ttid = tid - team * NW * 32;
   const int g = lane >> 2, t4 = lane & 3;
   // weights as +-1 bytes (0 past K and for columns >= n): 4 weight bits ->
   // 4 bytes by spreading the nibble and mapping 1 -> 0x01, 0 -> 0xFF
-  for (int o = warp; o < 32 * NW; o += blockDim.x >> 5)
+  for (int o = warp; o < 32 * NW * halves; o += blockDim.x >> 5)
     for (int p4 = 4 * lane; p4 < kpad; p4 += 128) {
       uint32_t v = 0;
-      if (o < n && p4 < k) {
+      if ((o & (32 * NW - 1)) < n && p4 < k) {
         const uint32_t word = __ldg(wt + static_cast<int64_t>(o) * kspw + (p4 >> 5));
         const uint32_t nib = (word >> (28 - (p4 & 31))) & 0xFu;  // bit 3 <-> element p4
         const uint32_t spread = ((nib >> 3) & 1u) | (((nib >> 2) & 1u) << 8) | (((nib >> 1) & 1u) << 16) |
@@ -506,12 +522,14 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
       bulk_g2s(ring + static_cast<size_t>(slot) * (tile_bytes / 4), a_f + nt * TR * static_cast<int64_t>(k),
                tile_bytes, &full[slot]);
     }
-    for (int mblk = 0; mblk < mb; ++mblk) {
+    for (int hm = 0; hm < halves * mb; ++hm) {
+    const int mblk = hm % mb, half = hm / mb;
+    uint32_t* const ob = half ? out_bits2 : out_bits;
     int acc[4][4];
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj) acc[jj][0] = acc[jj][1] = acc[jj][2] = acc[jj][3] = 0;
     const uint8_t* ab = mine + (16 * mblk + g) * lda + 4 * t4;
-    const uint8_t* bb = w8 + (32 * wq + g) * lda + 4 * t4;
+    const uint8_t* bb = w8 + (32 * (wq + NW * half) + g) * lda + 4 * t4;
     for (int ks = 0; ks < ksteps; ++ks) {
       uint32_t a[4];
       a[0] = *reinterpret_cast<const uint32_t*>(ab + 32 * ks);
@@ -545,13 +563,13 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
     }
     const int64_t r0 = tile * TR + 16 * mblk + g;
     if (t4 == 0 && wq < ospw) {
-      if (r0 < rows) out_bits[r0 * ospw + wq] = m0;
-      if (r0 + 8 < rows) out_bits[(r0 + 8) * ospw + wq] = m1;
+      if (r0 < rows) ob[r0 * ospw + wq] = m0;
+      if (r0 + 8 < rows) ob[(r0 + 8) * ospw + wq] = m1;
     }
     if (t4 == 1 && wq == 0)  // storage padding words of 64-bit rows
       for (int w = NW; w < ospw; ++w) {
-        if (r0 < rows) out_bits[r0 * ospw + w] = 0u;
-        if (r0 + 8 < rows) out_bits[(r0 + 8) * ospw + w] = 0u;
+        if (r0 < rows) ob[r0 * ospw + w] = 0u;
+        if (r0 + 8 < rows) ob[(r0 + 8) * ospw + w] = 0u;
       }
     }  // m16 block
     asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(nthr) : "memory");  // int8 tile reusable
@@ -984,12 +1002,15 @@ int64_t fbb_tma(const BmmArgs& a, cudaStream_t s) {
   const int lda = 32 * ksteps + 16;
   const int nw = static_cast<int>(cdiv(a.n, 32));
   const int NW = nw <= 1 ? 1 : nw <= 2 ? 2 : 4;
+  const int halves = a.out_bits2 ? 2 : 1;
+  // a paired product needs W2 to start at word NW of the combined weights
+  if (a.out_bits2 && (a.n2 != a.n || NW != nw)) return 0;
   // m16 blocks per tile: a slot of at most 16 x 602 fp32 (the Reddit tile),
   // so small K batches several blocks per bulk copy and per barrier
   int mb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, 38528 / (64 * a.k))));
   auto smem_of = [&](int m) {
     return static_cast<size_t>(kFbbStages) * 16 * m * a.k * 4 + static_cast<size_t>(kFbbTeams) * 16 * m * lda +
-           static_cast<size_t>(32 * NW) * lda;
+           static_cast<size_t>(32 * NW * halves) * lda;
   };
   while (mb > 1 && smem_of(mb) > 227 * 1024 - 128) --mb;
   const size_t smem = smem_of(mb);
@@ -1007,7 +1028,7 @@ int64_t fbb_tma(const BmmArgs& a, cudaStream_t s) {
     const int64_t blocks = std::min<int64_t>(tiles, sm_count());
     kern<<<static_cast<unsigned>(blocks), kFbbTeams * NW * 32, smem, s>>>(
         a.a_f, a.wt, a.rows, static_cast<int>(a.k), kspw, static_cast<int>(a.n), ksteps, ospw, qmagic, kmagic, mb,
-        a.out_bits);
+        a.out_bits, a.out_bits2);
   };
   if (NW == 1) go(k_fbb_tma<1>);
   else if (NW == 2) go(k_fbb_tma<2>);
@@ -1079,19 +1100,23 @@ void launch_lanerow(const BmmArgs& a, cudaStream_t s) {
 
 template <bool AF, bool OUTB>
 void launch(const BmmArgs& a, cudaStream_t s) {
+  // F->B products may take 512 columns per pass (a paired product of two
+  // 256-column weights reads its input once)
+  constexpr bool wide = AF && OUTB;
   auto pick = [](int64_t nc) {
     return nc <= 32 ? k_bmm<AF, OUTB, 1> : nc <= 64 ? k_bmm<AF, OUTB, 2>
-         : nc <= 128 ? k_bmm<AF, OUTB, 4> : k_bmm<AF, OUTB, 8>;
+         : nc <= 128 ? k_bmm<AF, OUTB, 4> : nc <= 256 || !wide ? k_bmm<AF, OUTB, 8> : k_bmm<AF, OUTB, wide ? 16 : 8>;
   };
   const int64_t kspw = spw(a.k, a.wb);
   const int64_t ld = kspw | 1;
   const int64_t ospw = spw(a.n, a.wb);
-  const int64_t pass = 32 * kMaxOutPerLane;
+  const int64_t ntot = a.out_bits2 ? 32 * cdiv(a.n, 32) + a.n2 : a.n;  // combined columns
+  const int64_t pass = 32 * (wide ? 2 * kMaxOutPerLane : kMaxOutPerLane);
   int64_t blocks = std::min<int64_t>(cdiv(a.rows, kWarps), static_cast<int64_t>(sm_count()) * 8);
   blocks = std::max<int64_t>(blocks, 1);
-  for (int64_t c0 = 0; c0 < a.n; c0 += pass) {
-    const int64_t nc = std::min(pass, a.n - c0);
-    const int64_t mcols = nc <= 32 ? 32 : nc <= 64 ? 64 : nc <= 128 ? 128 : 256;  // 32*M of pick(nc)
+  for (int64_t c0 = 0; c0 < ntot; c0 += pass) {
+    const int64_t nc = std::min(pass, ntot - c0);
+    const int64_t mcols = nc <= 32 ? 32 : nc <= 64 ? 64 : nc <= 128 ? 128 : nc <= 256 ? 256 : 512;  // 32*M of pick(nc)
     const size_t smem = static_cast<size_t>(mcols * ld + kWarps * kspw) * 4;
     auto kern = pick(nc);
     if (smem > 48 * 1024) BG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1099,7 +1124,7 @@ void launch(const BmmArgs& a, cudaStream_t s) {
     if (smem > 200 * 1024) fail("bmm: inner dimension too large for one pass");
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
         a.a_bits, a.a_f, a.alpha, a.wt, a.beta, a.rows, a.k, a.n, kspw, ld, c0, nc, ospw,
-        a.out_bits, a.out_f);
+        a.out_bits, a.out_f, a.out_bits2, a.n2, ntot);
     BG_LAUNCH_CHECK();
   }
 }
@@ -1113,6 +1138,23 @@ int fbb_force() {
   if (!e) return 0;
   const std::string v(e);
   return v == "scalar" ? 1 : v == "imma" ? 2 : v == "tma" ? 3 : 0;
+}
+
+bool bmm_pair(const BmmArgs& a, cudaStream_t s) {
+  if (!a.a_f || !a.out_bits || !a.out_bits2 || a.n2 != a.n || a.n == 0) return false;
+  if (a.rows == 0) return true;
+  const int force = fbb_force();
+  const bool few_rows = a.rows < 131072 && std::getenv("BG_FBB") == nullptr;
+  if (force == 1 || few_rows) {
+    // warp per row: pairs up to 256 combined columns (8 per lane); wider
+    // pairs measured slower than two products (Flickr, 2 x 256 columns:
+    // 0.35 ms paired vs 2 x 0.154 ms)
+    if (32 * cdiv(a.n, 32) + a.n2 > 32 * kMaxOutPerLane) return false;
+    launch<true, true>(a, s);
+    return true;
+  }
+  if (force == 0 || force == 3) return imma_ok(a) && fbb_tma(a, s) == a.rows;
+  return false;  // other forced kernels take the products one at a time
 }
 
 void bmm(const BmmArgs& a, cudaStream_t s) {

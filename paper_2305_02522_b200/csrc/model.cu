@@ -203,6 +203,26 @@ struct Hooks {
   }
 };
 
+}  // namespace
+
+// W1 | zero rows to a 32-column boundary | W2 as one transposed weight array
+// (the paired product's layout, ops.cuh BmmArgs), built on first use.
+const uint32_t* paired_weights(ModelLayer& l, int wb, cudaStream_t s) {
+  const WeightDev &w1 = l.w1, &w2 = l.w2;
+  const int64_t kspw = spw(w1.rows, wb), n = w1.cols, n1pad = 32 * cdiv(n, 32);
+  if (!l.wt_pair.p) {
+    const size_t bytes = static_cast<size_t>((n1pad + n) * kspw) * 4;
+    l.wt_pair.alloc(bytes);
+    BG_CUDA(cudaMemsetAsync(l.wt_pair.p, 0, bytes, s));
+    BG_CUDA(cudaMemcpyAsync(l.wt_pair.p, w1.wt.p, static_cast<size_t>(n * kspw) * 4, cudaMemcpyDeviceToDevice, s));
+    BG_CUDA(cudaMemcpyAsync(l.wt_pair.as<uint32_t>() + n1pad * kspw, w2.wt.p, static_cast<size_t>(n * kspw) * 4,
+                            cudaMemcpyDeviceToDevice, s));
+  }
+  return l.wt_pair.as<uint32_t>();
+}
+
+namespace {
+
 struct Exec {
   bg_model& m;
   Hooks& h;
@@ -249,6 +269,73 @@ struct Exec {
     h.end();
     if (mm.out == BG_B) h.bits(label + ".out", r.bits, r.rows, r.cols, r.wb);
     return r;
+  }
+
+  // The two MMs of a SAGE / GraphConv layer when both are F -> B on the same
+  // fp32 input (MM.FBB / MM.FFB): one paired product reads the input once
+  // (bmm_pair).  Untraced forwards only (the traced one keeps the per-slot
+  // BIN points); false when the shapes do not pair.
+  bool mm_pair(const ModelLayer& lc, const Op& x, const std::string& prefix, Op& hs, Op& hn) {
+    auto& l = const_cast<ModelLayer&>(lc);
+    const bg_variant p0 = l.info.plan[0], p1 = l.info.plan[1];
+    auto fb = [](bg_variant v) { return v.op == BG_BMM && v.in1 == BG_F && v.out == BG_B; };
+    if (h.trace || !fb(p0) || !fb(p1) || x.prec != BG_F || x.scale) return false;
+    const WeightDev &w1 = l.w1, &w2 = l.w2;
+    if (w1.rows != w2.rows || w1.cols != w2.cols || w1.wb != m.wb || w2.wb != m.wb || x.cols != w1.rows)
+      return false;
+    const int64_t n = w1.cols;
+    const uint32_t* wtp = paired_weights(l, m.wb, s);
+    Op a, b;
+    a.prec = b.prec = BG_B;
+    a.rows = b.rows = x.rows;
+    a.cols = b.cols = n;
+    a.wb = b.wb = m.wb;
+    a.bits = static_cast<uint32_t*>(m.pool.get(a.bytes()));
+    b.bits = static_cast<uint32_t*>(m.pool.get(b.bytes()));
+    BmmArgs k;
+    k.k = x.cols;
+    k.n = n;
+    k.n2 = n;
+    k.wb = m.wb;
+    k.wt = wtp;
+    const int64_t ospw = spw(n, m.wb);
+    h.begin(prefix + "mm_pair[" + variant_name(p0) + "]");
+    const bool streamed = in_chunks && x.f == x0f;
+    const int nc = streamed ? in_chunks->n : 1;
+    bool ok = true;
+    for (int c = 0; c < nc && ok; ++c) {
+      const int64_t r0 = streamed ? in_chunks->bounds[c] : 0, r1 = streamed ? in_chunks->bounds[c + 1] : x.rows;
+      if (streamed) BG_CUDA(cudaStreamWaitEvent(s, in_chunks->ready[c], 0));
+      k.rows = r1 - r0;
+      k.a_f = x.f + r0 * x.cols;
+      k.out_bits = a.bits + r0 * ospw;
+      k.out_bits2 = b.bits + r0 * ospw;
+      const bool paired = bmm_pair(k, s);
+      if (!paired && c == 0) {
+        ok = false;
+      } else if (!paired) {  // a later chunk the pair kernels do not take: one product at a time
+        BmmArgs one = k;
+        one.out_bits2 = nullptr;
+        one.n2 = 0;
+        one.wt = w1.wt.as<uint32_t>();
+        bmm(one, s);
+        one.wt = w2.wt.as<uint32_t>();
+        one.out_bits = k.out_bits2;
+        bmm(one, s);
+      }
+    }
+    h.end();
+    if (!ok) {
+      if (h.timing) {  // drop the empty span
+        cudaEventDestroy(h.timing->back().second.first);
+        cudaEventDestroy(h.timing->back().second.second);
+        h.timing->pop_back();
+      }
+      return false;
+    }
+    hs = a;
+    hn = b;
+    return true;
   }
 
   Op spmm_slot(bg_variant sp, const bg_frdc* adj, const float* rs, const float* cs, const Op& x,
@@ -373,8 +460,11 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
         case BG_LAYER_SAGE:
         case BG_LAYER_GRAPHCONV: {  // ref: neighborhood_layer, graphops.cpp:289-321
           const bool mean = l.info.kind == BG_LAYER_SAGE;
-          Op hs = ex.mm_slot(l.info.plan[0], cur, l.w1, prefix + "mm_self");
-          Op hn = ex.mm_slot(l.info.plan[1], cur, l.w2, prefix + "mm_neigh");
+          Op hs, hn;
+          if (!ex.mm_pair(l, cur, prefix, hs, hn)) {
+            hs = ex.mm_slot(l.info.plan[0], cur, l.w1, prefix + "mm_self");
+            hn = ex.mm_slot(l.info.plan[1], cur, l.w2, prefix + "mm_neigh");
+          }
           const bg_variant sp = l.info.plan[2];
           const bool fac = sp.in2 == BG_F;
           const float* rs = fac ? (mean ? m.graph->mean_row.as<float>() : m.graph->ones.as<float>()) : nullptr;

@@ -27,6 +27,7 @@ struct ModelLayer {
   LayerInfo info;
   bool relu = false;
   WeightDev w1, w2;
+  DevBuf wt_pair;  // W1 | zero pad to a 32-column boundary | W2, transposed bits (paired FBB)
   DevBuf bn_g, bn_b, bn_m, bn_s;
   int64_t bn_len = 0;
   DevBuf sr, sc;
@@ -44,6 +45,9 @@ int layer_output_precision(const LayerInfo& l, int in, std::vector<std::string>*
 std::vector<std::string> validate_model(bool has_graph, int input_prec,
                                         const std::vector<LayerInfo>& layers);
 LayerInfo layer_info(const bg_layer_desc& d);
+
+// The paired-product weight layout of a SAGE / GraphConv layer (W1 | pad | W2).
+const uint32_t* paired_weights(ModelLayer& l, int wb, cudaStream_t s);
 
 }  // namespace bg
 

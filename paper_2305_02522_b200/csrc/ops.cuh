@@ -111,8 +111,16 @@ struct BmmArgs {
   int wb = 32;
   uint32_t* out_bits = nullptr;
   float* out_f = nullptr;
+  // Paired F->B product (two weight matrices on one fp32 input, the input
+  // read once): wt holds W1's n columns, zero rows up to n1pad = 32*ceil(n/32),
+  // then W2's n2 columns; the second result goes to out_bits2.
+  uint32_t* out_bits2 = nullptr;
+  int64_t n2 = 0;
 };
 void bmm(const BmmArgs& a, cudaStream_t s);
+// Both products of a paired BmmArgs; false (nothing launched) when no kernel
+// takes the pair, so the caller runs the two products separately.
+bool bmm_pair(const BmmArgs& a, cudaStream_t s);
 
 // ---- bspmm.cu ------------------------------------------------------------
 // Integer path (BBB / BBF): out(i,k) = 2*#{j in N(i): x_jk = 1} - deg_i.

@@ -142,6 +142,58 @@ struct Shard {
     return o;
   }
 
+  // Both MMs of a SAGE / GraphConv layer as one paired F->B product on this
+  // process's rows (the input read once); false when they do not pair.
+  bool mm_pair(ModelLayer& l, const Op& x, Op& hs, Op& hn) {
+    const bg_variant p0 = l.info.plan[0], p1 = l.info.plan[1];
+    auto fb = [](bg_variant v) { return v.op == BG_BMM && v.in1 == BG_F && v.out == BG_B; };
+    if (!fb(p0) || !fb(p1) || x.prec != BG_F || x.scale) return false;
+    if (l.w1.rows != l.w2.rows || l.w1.cols != l.w2.cols || l.w1.wb != m.wb || l.w2.wb != m.wb ||
+        x.cols != l.w1.rows)
+      return false;
+    const int64_t n = l.w1.cols, ospw = spw(n, m.wb);
+    const uint32_t* wtp = paired_weights(l, m.wb, s);
+    Op a = alloc_like(BG_B, n, m.wb), b = alloc_like(BG_B, n, m.wb);
+    tm.begin(prefix + "mm_pair[" + variant_name(p0) + "]");
+    bool first = true;
+    for (auto [r0, r1] : ranges) {
+      if (r1 <= r0) continue;
+      BmmArgs k;
+      k.rows = r1 - r0;
+      k.k = x.cols;
+      k.n = k.n2 = n;
+      k.wb = m.wb;
+      k.wt = wtp;
+      k.a_f = x.f + r0 * x.cols;
+      k.out_bits = a.bits + r0 * ospw;
+      k.out_bits2 = b.bits + r0 * ospw;
+      if (!bmm_pair(k, s)) {
+        if (first) {  // nothing launched: the caller runs the two products
+          tm.end();
+          if (tm.ev) {
+            cudaEventDestroy(tm.ev->back().second.first);
+            cudaEventDestroy(tm.ev->back().second.second);
+            tm.ev->pop_back();
+          }
+          return false;
+        }
+        BmmArgs one = k;  // a later range the pair kernels do not take
+        one.out_bits2 = nullptr;
+        one.n2 = 0;
+        one.wt = l.w1.wt.as<uint32_t>();
+        bmm(one, s);
+        one.wt = l.w2.wt.as<uint32_t>();
+        one.out_bits = k.out_bits2;
+        bmm(one, s);
+      }
+      first = false;
+    }
+    tm.end();
+    hs = a;
+    hn = b;
+    return true;
+  }
+
   // ref: run_mm_slot on rows [r0, r1) (row-local).
   Op mm(bg_variant v, const Op& x, const WeightDev& w, const std::string& label) {
     tm.begin(prefix + label + "[" + variant_name(v) + "]");
@@ -323,8 +375,11 @@ void forward_sharded(bg_model& m, const Op& x0, const std::vector<int64_t>& boun
         case BG_LAYER_SAGE:
         case BG_LAYER_GRAPHCONV: {
           const bool mean = l.info.kind == BG_LAYER_SAGE;
-          Op hs = sh.mm(l.info.plan[0], cur, l.w1, "mm_self");
-          Op hn = sh.mm(l.info.plan[1], cur, l.w2, "mm_neigh");
+          Op hs, hn;
+          if (!sh.mm_pair(l, cur, hs, hn)) {
+            hs = sh.mm(l.info.plan[0], cur, l.w1, "mm_self");
+            hn = sh.mm(l.info.plan[1], cur, l.w2, "mm_neigh");
+          }
           bool hn_full = comm == nullptr;
           const bg_variant sp = l.info.plan[2];
           const bool fac = sp.in2 == BG_F;
