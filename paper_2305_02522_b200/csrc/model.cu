@@ -275,8 +275,7 @@ struct Exec {
   // fp32 input (MM.FBB / MM.FFB): one paired product reads the input once
   // (bmm_pair).  Untraced forwards only (the traced one keeps the per-slot
   // BIN points); false when the shapes do not pair.
-  bool mm_pair(const ModelLayer& lc, const Op& x, const std::string& prefix, Op& hs, Op& hn) {
-    auto& l = const_cast<ModelLayer&>(lc);
+  bool mm_pair(ModelLayer& l, const Op& x, const std::string& prefix, Op& hs, Op& hn) {
     const bg_variant p0 = l.info.plan[0], p1 = l.info.plan[1];
     auto fb = [](bg_variant v) { return v.op == BG_BMM && v.in1 == BG_F && v.out == BG_B; };
     if (h.trace || !fb(p0) || !fb(p1) || x.prec != BG_F || x.scale) return false;
