@@ -38,7 +38,7 @@ void copy_out(const Op& r, bg_mat* out, cudaStream_t s) {
   if (out->precision != r.prec || out->rows != r.rows || out->cols != r.cols ||
       (r.prec == BG_B && out->word_bits != r.wb))
     fail("output operand shape/precision does not match the result");
-  need(out->data, "output data");
+  if (r.bytes()) need(out->data, "output data");  // an empty result needs no buffer
   const void* src = r.prec == BG_F ? static_cast<const void*>(r.f) : static_cast<const void*>(r.bits);
   if (r.bytes()) BG_CUDA(cudaMemcpyAsync(out->data, src, r.bytes(), cudaMemcpyDeviceToDevice, s));
   out->semantics = BG_PLUS_MINUS;
