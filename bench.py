@@ -339,9 +339,7 @@ def main():
         "data": "synthetic (reference generators: random_edges seed 100, build_model seed 99)",
         "config": workload_config(args.workload, nnz_bits),
         "bit_spmm_gteps": round(gteps, 1) if gteps else None,
-        "roofline": {"bound": "hbm", "kernel": dom["label"], "achieved": round(achieved, 1),
-                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dom["label"])},
+        "roofline": roofline_obj(dom, achieved, peak, peak_kind),
         "kernels": kernels,
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms",
                 "h2d_bytes_per_step": int(X.nbytes), "d2h_bytes_per_step": int(n * c * 4)},
@@ -357,15 +355,32 @@ def main():
         dist.destroy_process_group()
 
 
-def ncu_traffic(label):
+def ncu_record(label):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
-        return None
+        return {}
     with open(p) as fh:
         rec = json.load(fh).get(label)
+    return rec if isinstance(rec, dict) else {}
+
+
+def ncu_traffic(label):
     # DRAM read + write bytes per launch of that kernel from the committed
     # ncu --set full capture (profiles/ncu_traffic.json, made by scripts/traffic_json.py)
-    return rec.get("traffic_bytes") if isinstance(rec, dict) else rec
+    return ncu_record(label).get("traffic_bytes")
+
+
+def roofline_obj(dom, achieved, peak, peak_kind):
+    r = {"bound": "hbm", "kernel": dom["label"], "achieved": round(achieved, 1), "peak": peak,
+         "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+         "traffic": ncu_traffic(dom["label"])}
+    l2 = ncu_record(dom["label"]).get("l2_to_l1_bytes")
+    if l2 and dom["ms"] > 0:
+        # a gather kernel's real limiter: L2 -> SM bytes of the same ncu capture
+        # per launch, over this run's measured launch time
+        r["l2_to_sm_bytes"] = l2
+        r["l2_to_sm_gbs"] = round(l2 / (dom["ms"] * 1e-3) / 1e9, 1)
+    return r
 
 
 def cpu_baseline(args, graph, out, model_name, n, f, h, c, plan):

@@ -16,9 +16,12 @@ for line in open(src):
         elif cur:
             cur = None  # first launch of each kernel only
         continue
-    m = re.match(r"\s*dram (read|write)\s+([\d.]+) Mbyte", line)
+    m = re.match(r"\s*dram (read|write)\s+([\d.]+) (Mbyte|Gbyte)", line)
     if m and cur:
-        out[cur]["dram_" + m.group(1)] = int(round(float(m.group(2)) * 1e6))
+        out[cur]["dram_" + m.group(1)] = int(round(float(m.group(2)) * (1e9 if m.group(3) == "Gbyte" else 1e6)))
+    m = re.match(r"\s*L2->L1 bytes\s+([\d.]+) (Mbyte|Gbyte)", line)
+    if m and cur:
+        out[cur]["l2_to_l1_bytes"] = int(round(float(m.group(1)) * (1e9 if m.group(2) == "Gbyte" else 1e6)))
 for rec in out.values():
     rec["traffic_bytes"] = rec.get("dram_read", 0) + rec.get("dram_write", 0)
 json.dump(out, open("profiles/ncu_traffic.json", "w"), indent=1)
