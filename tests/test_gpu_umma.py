@@ -44,3 +44,25 @@ def test_fbb_umma_matches_oracle(umma, wb, mkn):
     got = bg.bmm("BMM.FBB", torch.from_numpy(A).cuda(), dw, wb)
     want = po.bmm("BMM.FBB", po.Mat.dense(A), ow, wb)
     assert bits_equal(got.bits.numpy(), want.bits)
+
+
+@pytest.mark.parametrize("wb", [32, 64])
+@pytest.mark.parametrize("mkn", [(128, 602, 41), (1000, 128, 47), (257, 33, 21), (300, 100, 128), (5, 17, 7),
+                                 (4096, 301, 96), (77, 64, 32), (2000, 1433, 64), (333, 200, 72)])
+def test_fbf_matches_oracle(umma, wb, mkn):
+    # MM.FBF: float((alpha_r * dot) * beta_c) in double with row scales of X
+    # and column scales of W (kernels.cpp:179-190) -- exact
+    m, k, n = mkn
+    rng = po.Rng(5151 + m + k + n)
+    A, W = rng.random_dense(m, k), rng.random_dense(k, n)
+    A.flat[::11] = 0.0
+    wbits = po.binarize(W, wb)
+    dw = bg.BitOperand(bg.BitDenseMatrix.from_numpy(wbits, k, n, wb))
+    ow = po.Mat.binary(wbits, k, n, wb)
+    sc = po.l1_scales(W, po.COL)
+    dw.scale = torch.from_numpy(sc).cuda()
+    dw.scale_axis = bg.bitgnn.COL
+    ow.scale = sc
+    got = bg.bmm("BMM.FBF", torch.from_numpy(A).cuda(), dw, wb)
+    want = po.bmm("BMM.FBF", po.Mat.dense(A), ow, wb)
+    assert np.array_equal(got.cpu().numpy(), want.f)
