@@ -1,0 +1,53 @@
+"""bench.py's algorithmic-byte accounting against SURVEY.md §8(d)'s per-kernel
+budget for the Reddit shape (FBB 564.7 MB, BBB 684.5 MB, BBF 41.9 MB, FBF
+753.4 MB, softmax 76.4 MB), the roofline object, and the workload metadata."""
+import importlib.util
+import os
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+bench = importlib.util.module_from_spec(spec)
+spec.loader.exec_module(bench)
+
+# Reddit FRDC sizes (112,757,282 tiles over ceil(N/4) tile rows)
+N = 232_965
+SHAPES = {"nodes": N, "features": 602, "hidden": 128, "classes": 41, "model": "gcn", "last_conv": 1,
+          "loops_tile_rows": (N + 3) // 4, "loops_nnz_tiles": 112_757_282,
+          "raw_tile_rows": (N + 3) // 4, "raw_nnz_tiles": 0}
+
+
+@pytest.mark.parametrize("label,mb", [("layer0.mm[BMM.FBB]", 564.7), ("layer0.spmm[BSpMM.BBB]", 684.5),
+                                      ("layer1.mm[BMM.BBF]", 41.9), ("layer1.spmm[BSpMM.FBF]", 753.4),
+                                      ("layer2.softmax", 76.4)])
+def test_reddit_bytes_match_the_survey_budget(label, mb):
+    assert bench.kernel_bytes(label, SHAPES) / 1e6 == pytest.approx(mb, abs=0.05)
+
+
+def test_paired_product_counts_two_weights_and_results_one_input():
+    one = bench.kernel_bytes("layer0.mm_self[BMM.FBB]", SHAPES)
+    pair = bench.kernel_bytes("layer0.mm_pair[BMM.FBB]", SHAPES)
+    x = 4 * N * 602
+    assert pair - x == 2 * (one - x)
+
+
+def test_non_kernel_labels_count_nothing():
+    assert bench.kernel_bytes("layer0.allgather", SHAPES) == 0
+    assert bench.kernel_bytes("layer1.relu", SHAPES) == 0
+
+
+def test_roofline_object_fields():
+    dom = {"label": "layer1.spmm[BSpMM.FBF]", "ms": 0.66, "alg_bytes": 753_422_156}
+    r = bench.roofline_obj(dom, 1141.5, 6545.9, "measured")
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["frac"] == pytest.approx(1141.5 / 6545.9, abs=1e-4)
+    if "l2_to_sm_bytes" in r:  # from the committed ncu capture
+        assert r["l2_to_sm_gbs"] == pytest.approx(r["l2_to_sm_bytes"] / 0.66e-3 / 1e9, rel=1e-3)
+
+
+def test_workload_config_names_the_baseline_shapes():
+    c = bench.workload_config("reddit", 114_727_589)
+    assert c["nodes"] == N and c["features"] == 602 and c["classes"] == 41 and c["model_family"] == "gcn"
+    for wl in bench.WORKLOADS:
+        assert bench.workload_config(wl)["workload"]
+    assert bench.peaks()[0] > 1000
