@@ -34,22 +34,38 @@ __global__ void __launch_bounds__(kWarps * 32)
   uint32_t* sw = smem;                       // nc x ld transposed weight words
   uint32_t* srow = smem + 32 * M * ld;       // kWarps x kspw packed activation rows (after all 32*M weight rows the lanes read)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // fp32 input: the first batch of this warp's first row goes out before the
+  // weight staging, so the two latencies overlap (few-row shapes such as
+  // Cora run one row per warp: staging and loads were the whole kernel)
+  float pre[8];
+  const int64_t row_first = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+  if (AF && row_first < rows) {
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const int64_t j = 32 * m + lane;
+      pre[m] = j < k ? __ldg(a_f + row_first * k + j) : -1.0f;
+    }
+  }
   for (int64_t t = threadIdx.x; t < nc * kspw; t += blockDim.x) {
     const int64_t j = t / kspw, w = t % kspw;
     sw[j * ld + w] = __ldg(wt + (c0 + j) * kspw + w);
   }
   __syncthreads();
   uint32_t* arow = srow + warp * kspw;
-  for (int64_t row = static_cast<int64_t>(blockIdx.x) * kWarps + warp; row < rows;
-       row += static_cast<int64_t>(gridDim.x) * kWarps) {
+  for (int64_t row = row_first; row < rows; row += static_cast<int64_t>(gridDim.x) * kWarps) {
     if (AF) {
       const float* xr = a_f + row * k;
       for (int64_t w0 = 0; w0 < kspw; w0 += 8) {
         float v[8];
+        if (w0 == 0 && row == row_first) {
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const int64_t j = 32 * (w0 + m) + lane;
-          v[m] = j < k ? __ldg(xr + j) : -1.0f;
+          for (int m = 0; m < 8; ++m) v[m] = pre[m];
+        } else {
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            const int64_t j = 32 * (w0 + m) + lane;
+            v[m] = j < k ? __ldg(xr + j) : -1.0f;
+          }
         }
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
