@@ -50,7 +50,6 @@ struct Cursor {
   void skip() {
     while (p < e && is_space(*p)) ++p;
   }
-  bool at_end() const { return p == e; }
   // istream >> int64_t: optional sign, at least one digit, no overflow.
   bool int64(int64_t& v) {
     skip();
