@@ -341,30 +341,32 @@ __global__ void k_bv_fill(const uint64_t* __restrict__ srp, const uint32_t* __re
   for (; p < bp[i + 1]; ++p) out[p] = pad;
 }
 
-// Record producer for k_bv_gcn1 (layout above); thread per (node, word),
-// plus the zero record after the last node.  The weight bits and scales are
-// staged in shared memory once per block; the node's h words are one 16-byte
-// load shared by its 16 threads.
+// Record producer for k_bv_gcn1 (layout above): thread per (node, word group
+// g), which holds the node's h words and writes its 16-byte quarter -- h word
+// g and the q bytes of classes 12g .. 12g+11 -- with one store; plus the zero
+// record after the last node.  The weight bits and scales are staged in
+// shared memory once per block.
 __global__ void __launch_bounds__(256)
     k_sl_gcn1_records(const uint32_t* __restrict__ h, int64_t rows, int hspw, int K,
                       const uint32_t* __restrict__ wt, const float* __restrict__ beta, int C,
                       uint32_t* __restrict__ rec, bool h_v4) {
-  __shared__ uint32_t wt_s[48 * 4];
+  __shared__ uint4 wt_s[48];
   __shared__ float beta_s[48];
   for (int t = threadIdx.x; t < 48 * 4; t += blockDim.x) {
     const int k = t >> 2, w = t & 3;
-    wt_s[t] = (k < C && w < hspw) ? wt[k * hspw + w] : 0u;
+    reinterpret_cast<uint32_t*>(wt_s)[t] = (k < C && w < hspw) ? wt[k * hspw + w] : 0u;
   }
   for (int k = threadIdx.x; k < 48; k += blockDim.x) beta_s[k] = k < C ? beta[k] : 1.0f;
   __syncthreads();
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= (rows + 1) * kRec) return;
-  if (t >= rows * kRec) {
-    rec[t] = 0u;
+  if (t >= (rows + 1) * 4) return;
+  uint4* rec4 = reinterpret_cast<uint4*>(rec);
+  if (t >= rows * 4) {
+    rec4[t] = make_uint4(0u, 0u, 0u, 0u);
     return;
   }
-  const int64_t j = t / kRec;
-  const int w = static_cast<int>(t % kRec);
+  const int64_t j = t >> 2;
+  const int g = static_cast<int>(t & 3);
   uint32_t hw[4] = {0, 0, 0, 0};
   if (h_v4) {
     const uint4 v = __ldg(reinterpret_cast<const uint4*>(h) + j);
@@ -372,28 +374,25 @@ __global__ void __launch_bounds__(256)
   } else {
     for (int q = 0; q < hspw; ++q) hw[q] = __ldg(h + j * hspw + q);
   }
-  const int g = w >> 2, part = w & 3;
-  if (part == 0) {
-    rec[t] = hw[g];
-    return;
-  }
-  uint32_t out = 0;
+  uint32_t out[3] = {0u, 0u, 0u};
 #pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    const int k = 12 * g + 4 * (part - 1) + b;
-    if (k >= C) break;
-    const int diff = __popc(hw[0] ^ wt_s[4 * k]) + __popc(hw[1] ^ wt_s[4 * k + 1]) +
-                     __popc(hw[2] ^ wt_s[4 * k + 2]) + __popc(hw[3] ^ wt_s[4 * k + 3]);
-    const float fd = static_cast<float>(K - 2 * diff);  // exact
-    const float bk = beta_s[k];
-    const float x = __fmul_rn(fd, bk);
-    const float e = __fmaf_rn(fd, bk, -x);  // exact rounding error of the product
-    const int ex = ((__float_as_int(bk) >> 23) & 0xFF) - 127;
-    const float inv2u = __int_as_float((127 + 22 - ex) << 23);
-    const int q = __float2int_rn(e * inv2u);  // in [-32, 32]
-    out |= static_cast<uint32_t>(q + 32) << (8 * b);
-  }
-  rec[t] = out;
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int k = 12 * g + 4 * p + b;
+      if (k >= C) continue;
+      const uint4 wk = wt_s[k];
+      const int diff = __popc(hw[0] ^ wk.x) + __popc(hw[1] ^ wk.y) + __popc(hw[2] ^ wk.z) + __popc(hw[3] ^ wk.w);
+      const float fd = static_cast<float>(K - 2 * diff);  // exact
+      const float bk = beta_s[k];
+      const float x = __fmul_rn(fd, bk);
+      const float e = __fmaf_rn(fd, bk, -x);  // exact rounding error of the product
+      const int ex = ((__float_as_int(bk) >> 23) & 0xFF) - 127;
+      const float inv2u = __int_as_float((127 + 22 - ex) << 23);
+      const int q = __float2int_rn(e * inv2u);  // in [-32, 32]
+      out[p] |= static_cast<uint32_t>(q + 32) << (8 * b);
+    }
+  rec4[t] = make_uint4(hw[g], out[0], out[1], out[2]);
 }
 
 // ---- real-valued walk in ascending column order ------------------------------
@@ -583,7 +582,7 @@ void sliver_gcn1_records(const uint32_t* h, int64_t n, int64_t K, int wb, const 
                          const float* beta, int64_t C, uint32_t* rec, cudaStream_t s) {
   const int hspw = static_cast<int>(spw(K, wb));
   const bool v4 = hspw == 4 && reinterpret_cast<uintptr_t>(h) % 16 == 0;
-  k_sl_gcn1_records<<<static_cast<unsigned>(cdiv((n + 1) * kRec, 256)), 256, 0, s>>>(
+  k_sl_gcn1_records<<<static_cast<unsigned>(cdiv((n + 1) * 4, 256)), 256, 0, s>>>(
       h, n, hspw, static_cast<int>(K), wt, beta, static_cast<int>(C), rec, v4);
   BG_LAUNCH_CHECK();
 }
