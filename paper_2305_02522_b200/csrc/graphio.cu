@@ -235,9 +235,10 @@ std::unique_ptr<bg_edges> matrix_market(const char* text, size_t len, const std:
 
 // ref: read_frdc_edges (graphio.cpp:46-70): tiles in storage order, the set
 // bits of a tile from bit 0 up (row-major position 15 down to 0).
-std::unique_ptr<bg_edges> frdc_edges(const std::string& path, int64_t forced, bool undirected) {
+std::unique_ptr<bg_edges> frdc_edges(const std::string& path, const std::string& bytes, int64_t forced,
+                                     bool undirected) {
   int wb = 0;
-  auto m = frdc_read_file(path.c_str(), &wb, nullptr);
+  auto m = frdc_deserialize(bytes.data(), bytes.size(), &wb, nullptr);  // the bytes load_graph read
   const int64_t tr = (m->rows + 3) / 4;
   std::vector<uint64_t> rp(static_cast<size_t>(tr + 1));
   std::vector<uint32_t> ci(static_cast<size_t>(m->nnz));
@@ -307,7 +308,7 @@ int bg_load_graph(const char* path, int64_t forced_nodes, int undirected, bg_edg
     const std::string p(path);
     std::string text = slurp(p);
     if (text.size() >= 4 && std::memcmp(text.data(), "FRDC", 4) == 0) {
-      *out = frdc_edges(p, forced_nodes, undirected != 0).release();
+      *out = frdc_edges(p, text, forced_nodes, undirected != 0).release();
       return;
     }
     if (text.rfind("%%MatrixMarket", 0) == 0) {
