@@ -120,3 +120,19 @@ def test_operand_validation_is_host_side():
         bg.BitDenseMatrix.empty(2, 2, word_bits=48)
     buf = ctypes.create_string_buffer(8)
     assert L.lib().bg_variant_name(L.Variant(0, 0, 1, 1), buf, 8) == 0 and buf.value == b"BMM.FBB"
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_device_work_fails_loudly_without_a_gpu():
+    # no CPU fallback anywhere: device entry points report a CUDA error and
+    # host tensors are rejected instead of being computed on the host
+    import numpy as np
+    import torch
+    src = np.array([0, 1], np.int64)
+    dst = np.array([1, 2], np.int64)
+    g = ctypes.c_void_p()
+    rc = L.lib().bg_prepare_graph(src.ctypes.data, dst.ctypes.data, 2, 4, ctypes.byref(g), None)
+    assert rc == L.BG_CUDA_ERROR
+    assert L.lib().bg_last_error()
+    with pytest.raises(bg.InvalidArgument, match="CUDA tensors"):
+        bg.binarize(torch.zeros(2, 3))
