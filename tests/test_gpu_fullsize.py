@@ -71,3 +71,23 @@ def test_flickr_frdc_equals_reference_prepare_graph():
         ref = rg.frdc(which)
         rp, ci, ti = mine.download()
         assert np.array_equal(rp, ref.row_ptr) and np.array_equal(ci, ref.col_ind) and np.array_equal(ti, ref.tiles)
+
+
+@pytest.mark.parametrize("wl,world", [("reddit", 8), ("products", 8), ("reddit", 3)])
+def test_full_size_sharded_ranges_equal_single_gpu(wl, world):
+    # the 8-GPU configuration's per-rank work (every rank's row range through
+    # the sharded engine in one process) is bit-identical to the 1-GPU forward
+    from paper_2305_02522_b200.sharded import forward_virtual_ranks, partition_bounds
+    model, n, e, f, h, c, plan = SHAPES[wl]
+    src, dst = bg.Rng(100).random_edges(n, e, False)
+    layers, X = bg.build_model_spec(model, f, h, c, 99, n, plan)
+    g = bg.prepare_graph(n, src, dst)
+    m = bg.Model(layers, g)
+    x = torch.from_numpy(X).cuda()
+    out1, log1, _ = m.forward_traced(x)
+    rp, _, _ = g.structure.download()
+    b = partition_bounds(rp, n, world)
+    out, lg = forward_virtual_ranks(m, x, b, logits=True)
+    torch.cuda.synchronize()
+    assert torch.equal(lg, log1)
+    assert torch.equal(out, out1)
