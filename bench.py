@@ -407,12 +407,18 @@ def cpu_baseline(args, graph, out, model_name, n, f, h, c, plan):
         # parity of this run: GPU logits-side output vs the reference output
         rout, _, _ = rm.run(c, trace=False)
         got = out.cpu().numpy()
+        # the reference's own per-kernel record_ns breakdown (runreport.cpp:241-277)
+        kt = rm.kernel_times()
+        bbb = [v for lab, v in kt if "BSpMM.BBB" in lab]
         return {"value": round(ms, 2), "unit": "ms", "cores": threads, "kind": "reference",
                 "sample": f"{len(times)} full-graph forwards of the same workload (median) after 1 "
                           f"warm-up; bitgnn::run_model built from /root/reference/proj/src, "
                           f"{threads} OpenMP threads; setup {setup:.1f}s",
                 "speedup_vs_value": None,
-                "output_max_abs_diff": float(np.max(np.abs(got - rout)))}
+                "output_max_abs_diff": float(np.max(np.abs(got - rout))),
+                "kernels": [{"label": lab, "ms": round(v, 3)} for lab, v in kt],
+                "bit_spmm_gteps": round(graph.structure.nnz_bits / (bbb[0] * 1e-3) / 1e9, 3)
+                if bbb and model_name == "gcn" else None}
     except Exception as ex:  # the baseline is reported, never required
         log("cpu baseline failed:", ex)
         return None
