@@ -340,6 +340,8 @@ def main():
         "config": workload_config(args.workload, nnz_bits),
         "bit_spmm_gteps": round(gteps, 1) if gteps else None,
         "roofline": roofline_obj(dom, achieved, peak, peak_kind),
+        # the north star's bit-SpMM target (>= 60 % of HBM) is about this kernel
+        "roofline_bit_spmm": (roofline_obj(spmm[0], spmm[0]["gb_s"], peak, peak_kind) if spmm else None),
         "kernels": kernels,
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms",
                 "h2d_bytes_per_step": int(X.nbytes), "d2h_bytes_per_step": int(n * c * 4)},
