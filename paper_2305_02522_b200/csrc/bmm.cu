@@ -1160,7 +1160,7 @@ bool bmm_pair(const BmmArgs& a, cudaStream_t s) {
   if (!a.a_f || !a.out_bits || !a.out_bits2 || a.n2 != a.n || a.n == 0) return false;
   if (a.rows == 0) return true;
   const int force = fbb_force();
-  const bool few_rows = a.rows < 131072 && std::getenv("BG_FBB") == nullptr;
+  const bool few_rows = a.rows < 24576 && std::getenv("BG_FBB") == nullptr;  // as bmm()
   if (force == 1 || few_rows) {
     // warp per row: pairs up to 256 combined columns (8 per lane); wider
     // pairs measured slower than two products (Flickr, 2 x 256 columns:
@@ -1177,12 +1177,15 @@ void bmm(const BmmArgs& a, cudaStream_t s) {
   if (a.rows == 0 || a.n == 0) return;
   const bool af = a.a_f != nullptr, ob = a.out_bits != nullptr;
   const int force = af ? fbb_force() : 0;
-  // Few rows (Cora 2.7K, PubMed 20K, Flickr 89K): a warp per row puts every
-  // row in flight at once, where the tile kernels leave SMs idle or run
-  // short pipelines (measured FBB: Cora 66 -> 20 us, PubMed 28 -> 26 us,
-  // Flickr 169 -> 154 us; Reddit 233K rows stays on the TMA kernel, 0.158 vs
-  // 0.297 ms).  F output keeps the tensor-core kernel (Flickr FBF 63 vs 83 us).
-  const bool few_rows = af && ob && a.rows < 131072 && std::getenv("BG_FBB") == nullptr;
+  // Few rows (Cora 2.7K, PubMed 20K): a warp per row puts every row in
+  // flight at once, where the tile kernel leaves SMs idle or runs short
+  // pipelines (measured FBB: Cora 66 -> 20 us, PubMed 28 -> 26 us).  From
+  // ~25K rows the TMA kernel wins (K = 602, scripts/fbb_rows_probe.py: 29K
+  // rows -- a Reddit shard of 8 -- 81 vs 99 us; 233K rows 0.14 vs 0.30 ms);
+  // N > 128 (Flickr's 256 columns, 89K rows: 154 vs 169 us on the lane-per-
+  // row kernel) stays on the warp-per-row kernel at any row count.
+  // F output keeps the tensor-core kernel (Flickr FBF 63 vs 83 us).
+  const bool few_rows = af && ob && (a.rows < 24576 || a.n > 128) && std::getenv("BG_FBB") == nullptr;
   if (force == 1 || few_rows) {
     if (ob) launch<true, true>(a, s);
     else launch<true, false>(a, s);
