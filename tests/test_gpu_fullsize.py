@@ -91,3 +91,24 @@ def test_full_size_sharded_ranges_equal_single_gpu(wl, world):
     torch.cuda.synchronize()
     assert torch.equal(lg, log1)
     assert torch.equal(out, out1)
+
+
+@pytest.mark.parametrize("wl", ["pubmed", "flickr"])
+def test_full_size_64_bit_words_match_reference_engine(wl):
+    # the same models packed in 64-bit words (big-endian u32 pairs,
+    # bitdense.hpp:61-107) on both sides
+    model, n, e, f, h, c, plan = SHAPES[wl]
+    src, dst = bg.Rng(100).random_edges(n, e, False)
+    layers, X = bg.build_model_spec(model, f, h, c, 99, n, plan)
+    g = bg.prepare_graph(n, src, dst)
+    m = bg.Model(layers, g, word_bits=64)
+    out, logits, pts = m.forward_traced(torch.from_numpy(X).cuda())
+    torch.cuda.synchronize()
+    a, r = g.structure.download(), g.raw.download()
+    rg = po.RefGraph.from_frdc(n, po.Frdc(n, n, *a), po.Frdc(n, n, *r))
+    rm = po.RefModel(rg, model, f, h, c, 99, n, 64, plan)
+    r_out, r_log, r_pts = rm.run(c)
+    assert [p.label for p in pts] == [p.label for p in r_pts]
+    for p, q in zip(pts, r_pts):
+        assert p.bits.word_bits == 64 and bits_equal(p.bits.numpy(), q.bits), p.label
+    assert np.array_equal(logits.cpu().numpy(), r_log)
