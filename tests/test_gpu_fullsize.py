@@ -93,7 +93,7 @@ def test_full_size_sharded_ranges_equal_single_gpu(wl, world):
     assert torch.equal(out, out1)
 
 
-@pytest.mark.parametrize("wl", ["pubmed", "flickr"])
+@pytest.mark.parametrize("wl", ["pubmed", "flickr", "reddit"])
 def test_full_size_64_bit_words_match_reference_engine(wl):
     # the same models packed in 64-bit words (big-endian u32 pairs,
     # bitdense.hpp:61-107) on both sides
