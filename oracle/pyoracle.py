@@ -763,6 +763,25 @@ class RefModel:
             pass
 
 
+def ref_bench_bspmm_bbb(nodes: int = 65536, density: float = 0.001, cols: int = 128, seed: int = 7,
+                        word_bits: int = 32) -> dict:
+    """The reference's own single-thread kernelbench (kernelbench.cpp:110-186):
+    BSpMM.BBB vs a naive CSR SpMM.  GTEPS = adjacency bits / engine time."""
+    L = ref()
+    em, bm = C.c_double(), C.c_double()
+    edges, match = C.c_int64(), C.c_int()
+    L.ref_bench_bspmm_bbb.argtypes = [C.c_int64, C.c_double, C.c_int64, C.c_uint64, C.c_int,
+                                      C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_int64), C.POINTER(C.c_int)]
+    if L.ref_bench_bspmm_bbb(nodes, density, cols, seed, word_bits, C.byref(em), C.byref(bm),
+                             C.byref(edges), C.byref(match)):
+        raise RuntimeError(L.ref_error().decode())
+    return {"nodes": nodes, "density": density, "features": cols, "edges": edges.value,
+            "engine_ms": em.value, "naive_csr_ms": bm.value, "values_match": bool(match.value),
+            "gteps": edges.value / (em.value * 1e-3) / 1e9 if em.value > 0 else None,
+            "threads": 1}
+
+
 def ref_enumerate_plans(model: str, layers: int):
     """The real reference's enumerate_plans for a model skeleton (tune.cpp)."""
     L = ref()

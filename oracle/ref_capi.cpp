@@ -23,6 +23,7 @@
 #include "bitgnn/bitsparse.hpp"
 #include "bitgnn/graphio.hpp"
 #include "bitgnn/graphops.hpp"
+#include "bitgnn/kernelbench.hpp"
 #include "bitgnn/kernels.hpp"
 #include "bitgnn/modelconfig.hpp"
 #include "bitgnn/rng.hpp"
@@ -291,6 +292,25 @@ int ref_model_kernel_times(void* h, int cap, char* labels, int label_len, double
   } catch (const std::exception& ex) {
     guard(ex);
     return -1;
+  }
+}
+
+// The reference's own single-thread kernel benchmark (kernelbench.cpp:110-186):
+// BSpMM.BBB over a random graph vs a naive CSR SpMM.  edges = adjacency bits
+// the tiled kernel walked (kernelbench.cpp:143/179), parsed from its result name.
+int ref_bench_bspmm_bbb(int64_t nodes, double density, int64_t cols, uint64_t seed, int word_bits,
+                        double* engine_ms, double* baseline_ms, int64_t* edges, int* match) {
+  try {
+    KernelBenchResult r = bench_bspmm_bbb(nodes, density, cols, seed, word_bits);
+    *engine_ms = r.engine_ms;
+    *baseline_ms = r.baseline_ms;
+    *match = r.values_match ? 1 : 0;
+    const std::string key = " nodes, ";
+    size_t p = r.name.find(key);
+    *edges = p == std::string::npos ? -1 : std::strtoll(r.name.c_str() + p + key.size(), nullptr, 10);
+    return 0;
+  } catch (const std::exception& ex) {
+    return guard(ex);
   }
 }
 

@@ -165,9 +165,12 @@ def _mat(m: MatOperand, scale_axis: int = ROW) -> L.Mat:
         c.word_bits = m.bits.word_bits
         c.semantics = m.bits.semantics
         c.rows, c.cols = m.bits.rows, m.bits.cols
-        c.data = m.bits.words.data_ptr()
-        c.scale = m.scale.data_ptr() if m.scale is not None else None
+        words = m.bits.words.contiguous()
+        sc = _vec(m.scale)
+        c.data = words.data_ptr()
+        c.scale = sc.data_ptr() if sc is not None else None
         c.scale_axis = m.scale_axis
+        c._keep = (words, sc)  # alive as long as the descriptor (the C call reads them)
     elif isinstance(m, BitDenseMatrix):
         return _mat(BitOperand(m))
     else:
@@ -176,7 +179,21 @@ def _mat(m: MatOperand, scale_axis: int = ROW) -> L.Mat:
         c.word_bits = 32
         c.rows, c.cols = t.shape
         c.data = t.data_ptr()
+        c._keep = (t,)  # a non-contiguous input's contiguous copy must outlive the call
     return c
+
+
+def _vec(t: Optional[torch.Tensor]) -> Optional[torch.Tensor]:
+    """A scale vector as the C ABI reads it: contiguous float32 on the device."""
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float32 or not t.is_cuda:
+        raise InvalidArgument("scale vectors are float32 CUDA tensors")
+    return t.contiguous()
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else t.data_ptr()
 
 
 def _dense(t: torch.Tensor) -> torch.Tensor:
@@ -461,10 +478,6 @@ def bmm(v, a: MatOperand, w: MatOperand, word_bits: int = 32) -> MatOperand:
     return out
 
 
-def _scale_ptr(t: Optional[torch.Tensor]):
-    return None if t is None else t.contiguous().data_ptr()
-
-
 def bspmm(v, adj: AdjacencyOperand, x: MatOperand, strategy: Optional[int] = None,
           word_bits: int = 32) -> MatOperand:
     v = _v(v)
@@ -475,7 +488,8 @@ def bspmm(v, adj: AdjacencyOperand, x: MatOperand, strategy: Optional[int] = Non
     check(lib().bg_bspmm_out_desc(v._c(), adj.structure._h, C.byref(cx), word_bits, C.byref(desc)))
     out, desc = _alloc(desc)
     st = -1 if strategy is None else int(strategy)
-    check(lib().bg_bspmm(v._c(), adj.structure._h, _scale_ptr(adj.row_scale), _scale_ptr(adj.col_scale),
+    rs, cs = _vec(adj.row_scale), _vec(adj.col_scale)  # kept alive until the call returns
+    check(lib().bg_bspmm(v._c(), adj.structure._h, _ptr(rs), _ptr(cs),
                          C.byref(cx), st, word_bits, C.byref(desc), _stream()))
     return out
 
@@ -521,8 +535,9 @@ def fused_mm_spmm(mm, spmm, x: MatOperand, w: MatOperand, adj: AdjacencyOperand,
     check(lib().bg_bspmm_out_desc(spmm._c(), adj.structure._h, C.byref(hdesc), 32, C.byref(desc)))
     out, desc = _alloc(desc)
     st = -1 if strategy is None else int(strategy)
+    rs, cs = _vec(adj.row_scale), _vec(adj.col_scale)
     check(lib().bg_fused_mm_spmm(mm._c(), spmm._c(), C.byref(cx), C.byref(cw), adj.structure._h,
-                                 _scale_ptr(adj.row_scale), _scale_ptr(adj.col_scale), st,
+                                 _ptr(rs), _ptr(cs), st,
                                  C.byref(desc), _stream()))
     return out
 
@@ -540,9 +555,10 @@ def scl(x: torch.Tensor, row: torch.Tensor, col: torch.Tensor) -> torch.Tensor:
     x = _dense(x)
     if row.numel() != x.shape[0] or col.numel() != x.shape[1]:
         raise InvalidArgument("scl: scale length mismatch")
+    row, col = _vec(row), _vec(col)
     out = torch.empty_like(x)
-    check(lib().bg_scl(x.data_ptr(), x.shape[0], x.shape[1], row.contiguous().data_ptr(),
-                       col.contiguous().data_ptr(), out.data_ptr(), _stream()))
+    check(lib().bg_scl(x.data_ptr(), x.shape[0], x.shape[1], row.data_ptr(),
+                       col.data_ptr(), out.data_ptr(), _stream()))
     return out
 
 

@@ -508,6 +508,10 @@ int bg_model_forward(bg_model* m, const bg_mat* x0, float* out, float* logits, b
     k.logits = logits;
     k.s = st;
     k.agg_gen = aggregation_generation();
+    // Any other entry point sharing the pool (traced, timed, host, sharded)
+    // may have grown a slot since the capture: pool_gen then differs and the
+    // graph, which holds the old pointers, is re-recorded.
+    k.pool_gen = m->pool.gen;
     if (m->exec && k == m->key) {
       BG_CUDA(cudaGraphLaunch(m->exec, st));
       return;
@@ -518,8 +522,9 @@ int bg_model_forward(bg_model* m, const bg_mat* x0, float* out, float* logits, b
         cudaGraphExecDestroy(m->exec);
         m->exec = nullptr;
       }
-      m->key = k;
       forward_impl(*m, x, out, logits, nullptr, nullptr, st);
+      m->key = k;
+      m->key.pool_gen = m->pool.gen;
       return;
     }
     // Second run with the same binding: capture and replay from now on.

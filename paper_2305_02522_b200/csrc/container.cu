@@ -36,6 +36,15 @@ struct Source {
     std::memcpy(dst, buf + pos, n);
     pos += n;
   }
+  // Bytes left in the source (a non-seekable file reports "unbounded").
+  uint64_t remaining() {
+    if (!f) return len - pos;
+    const long here = std::ftell(f);
+    if (here < 0 || std::fseek(f, 0, SEEK_END) != 0) return UINT64_MAX;
+    const long end = std::ftell(f);
+    std::fseek(f, here, SEEK_SET);
+    return end >= here ? static_cast<uint64_t>(end - here) : 0;
+  }
   uint64_t get(int n) {
     uint8_t b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     read(b, static_cast<size_t>(n));
@@ -75,9 +84,15 @@ std::unique_ptr<bg_frdc> read_container(Source& in, int* word_bits, cudaStream_t
   const auto node_cols = static_cast<int64_t>(in.get(8));
   const uint64_t nnz = in.get(8);
   if (node_rows < 0 || node_cols < 0) fail("FRDC: negative dimension");
-  const int64_t tile_rows = (node_rows + 3) / 4;
+  const int64_t tile_rows = node_rows / 4 + (node_rows % 4 != 0);
+  // The header's sizes are untrusted: the arrays they declare must fit in
+  // what is left of the source before anything is allocated (checked without
+  // overflow; the reference's reader runs out of bytes there too).
+  const uint64_t left = in.remaining();
+  const uint64_t rp_words = static_cast<uint64_t>(tile_rows) + 1;
+  if (rp_words > left / 8 || nnz > (left - rp_words * 8) / 6) throw std::runtime_error("FRDC: truncated file");
   // x86-64 and the GPU are little-endian: the arrays are read as-is
-  const size_t rp_bytes = static_cast<size_t>(tile_rows + 1) * 8, ci_bytes = static_cast<size_t>(nnz) * 4,
+  const size_t rp_bytes = static_cast<size_t>(rp_words) * 8, ci_bytes = static_cast<size_t>(nnz) * 4,
                ti_bytes = static_cast<size_t>(nnz) * 2;
   Pinned rp(rp_bytes), ci(ci_bytes), ti(ti_bytes);
   in.read(rp.p, rp_bytes);

@@ -34,9 +34,12 @@ void op_to_mat(const Op& o, bg_mat* m);
 
 // Deterministic bump pool: the same call sequence gets the same buffers, so a
 // forward can be captured once and replayed as a CUDA graph.
+// gen changes whenever a slot is (re)allocated: a CUDA graph captured over the
+// pool's pointers is only valid while gen is unchanged.
 struct Pool {
   std::vector<DevBuf> bufs;
   size_t next = 0;
+  uint64_t gen = 0;
   void reset() { next = 0; }
   void* get(size_t bytes);
 };

@@ -9,10 +9,14 @@ namespace bg {
 void* Pool::get(size_t bytes) {
   bytes = bytes ? (bytes + 255) / 256 * 256 : 256;
   if (next < bufs.size()) {
-    if (bufs[next].bytes < bytes) bufs[next].alloc(bytes);
+    if (bufs[next].bytes < bytes) {
+      bufs[next].alloc(bytes);
+      ++gen;
+    }
     return bufs[next++].p;
   }
   bufs.emplace_back(bytes);
+  ++gen;
   return bufs[next++].p;
 }
 

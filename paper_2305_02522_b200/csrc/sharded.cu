@@ -336,9 +336,23 @@ void forward_sharded(bg_model& m, const Op& x0, const std::vector<int64_t>& boun
           const bg_frdc& A = *m.graph->structure;
           const bool fused = mm.in1 == BG_B && mm.in2 == BG_B && mm.out == BG_F &&
                              sp.in1 == BG_F && sp.in2 == BG_B && sp.out == BG_F && !l.relu &&
-                             cur.prec == BG_B && !cur.scale && cur.wb == m.wb &&
+                             cur.prec == BG_B && cur.sem == BG_PLUS_MINUS && !cur.scale && cur.wb == m.wb &&
+                             cur.cols == l.w1.rows && cur.rows == A.cols &&
                              gcn1_fused_supported(A, cur.cols, cur.wb, l.w1.cols);
           if (fused) {
+            if (comm && cur.bits == x0.bits) {
+              // the caller's rank-local input (read through a shifted base):
+              // gather into a full-size buffer, never into the caller's memory
+              Op full = sh.alloc_like(BG_B, cur.cols, cur.wb);
+              const int64_t rb = sh.row_bytes(cur), r0 = bounds[rank], r1 = bounds[rank + 1];
+              if (r1 > r0)
+                BG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(full.bits) + r0 * rb,
+                                        reinterpret_cast<const char*>(cur.bits) + r0 * rb,
+                                        static_cast<size_t>((r1 - r0) * rb), cudaMemcpyDeviceToDevice, s));
+              full.sem = cur.sem;
+              cur = full;
+              cur_full = false;
+            }
             if (!cur_full) {
               sh.allgather(cur.bits, sh.row_bytes(cur));
               cur_full = true;

@@ -51,3 +51,33 @@ def test_workload_config_names_the_baseline_shapes():
     for wl in bench.WORKLOADS:
         assert bench.workload_config(wl)["workload"]
     assert bench.peaks()[0] > 1000
+
+
+def _ref_available():
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    return po.ref_available()
+
+
+@pytest.mark.skipif(not _ref_available(), reason="oracle/_ref (reference library) not built")
+def test_reference_arm_never_maps_the_product_library():
+    # The reference arm runs the unmodified reference only: its process must
+    # not map libbitgnn_b200.so (the driver voids the ratio if it does).
+    import json
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--workload", "cora", "--steps", "2", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference"
+    libs = line["native_so_loaded"]
+    assert "oracle/_ref/libbitgnn_ref.so" in libs
+    assert not any("libbitgnn_b200" in x for x in libs), libs
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "reference" and cb["cores"] >= 1
+    assert cb["host_cpu"]["logical_cpus"] >= 1
+    kb = cb["kernelbench_bspmm_bbb_1thread"]
+    assert kb["values_match"] and kb["edges"] > 0 and kb["gteps"] > 0

@@ -49,6 +49,21 @@ def test_reader_rejects_foreign_and_damaged_headers():
             bg.FrdcMatrix.from_bytes(data)
 
 
+@pytest.mark.parametrize("rows,nnz", [(8, 1 << 63), (8, (1 << 64) - 1), (8, 1 << 40),
+                                      ((1 << 62), 0), (8, 3)])
+def test_reader_rejects_untrusted_sizes_before_allocating(rows, nnz, tmp_path):
+    # crafted headers whose declared arrays overflow size arithmetic or exceed
+    # the bytes present: "truncated", never a wrapped size or a huge allocation
+    body = struct.pack("<QQQ", 0, 0, 1 << 63) + struct.pack("<I", 0) + struct.pack("<H", 0x8000)
+    data = b"FRDC" + struct.pack("<IBBHQQQ", 1, 4, 32, 0, rows, 8, nnz) + body
+    with pytest.raises(bg.RuntimeFailure, match="FRDC: truncated file"):
+        bg.FrdcMatrix.from_bytes(data)
+    p = tmp_path / "crafted.frdc"
+    p.write_bytes(data)
+    with pytest.raises(bg.RuntimeFailure, match="FRDC: truncated file"):
+        bg.FrdcMatrix.read(str(p))
+
+
 def test_reader_rejects_payload_that_fails_validation():
     # a container whose tiles break the FrdcMatrix invariants (all-zero tile)
     m = bg.frdc_from_edges(8, [1, 0], [2, 5], False)

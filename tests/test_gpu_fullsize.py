@@ -112,3 +112,34 @@ def test_full_size_64_bit_words_match_reference_engine(wl):
     for p, q in zip(pts, r_pts):
         assert p.bits.word_bits == 64 and bits_equal(p.bits.numpy(), q.bits), p.label
     assert np.array_equal(logits.cpu().numpy(), r_log)
+
+
+def _sha(a):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("wl", ["reddit", "products"])
+def test_full_size_frdc_equals_reference_prepare_graph_digests(wl):
+    # The device FRDC build at the full BASELINE shapes against the REAL
+    # reference's own prepare_graph (frdc_from_edges x2 + scales,
+    # graphops.cpp:146-170), recorded once in the dev container by
+    # tests/golden/make_fullsize_frdc.py: every array byte-identical.
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "fullsize_frdc.json")) as fh:
+        want = json.load(fh)["shapes"][wl]
+    model, n, e, *_ = SHAPES[wl]
+    src, dst = bg.Rng(100).random_edges(n, e, False)
+    assert (_sha(src), _sha(dst)) == (want["sha_src"], want["sha_dst"])
+    g = bg.prepare_graph(n, src, dst)
+    for key, mine in (("loops", g.structure), ("raw", g.raw)):
+        rp, ci, ti = mine.download()
+        w = want[key]
+        assert ti.shape[0] == w["nnz_tiles"] and mine.nnz_bits == w["nnz_bits"], key
+        assert _sha(rp) == w["sha_row_ptr"], key
+        assert _sha(ci) == w["sha_col_ind"], key
+        assert _sha(ti) == w["sha_tiles"], key
+    assert _sha(g.norm_row.cpu().numpy()) == want["sha_norm"]
+    assert _sha(g.mean_row.cpu().numpy()) == want["sha_mean_row"]
+    assert _sha(g.neighbor_count.cpu().numpy()) == want["sha_neighbor_count"]
