@@ -147,6 +147,39 @@ int bg_frdc_from_host(int64_t node_rows, int64_t node_cols, const uint64_t* row_
 int bg_frdc_info_get(const bg_frdc* m, bg_frdc_info* info);
 /* Copy the three FRDC arrays to HOST buffers (row_ptr: tile_rows+1, others nnz). */
 int bg_frdc_download(const bg_frdc* m, uint64_t* row_ptr, uint32_t* col_ind, uint16_t* tiles);
+/* Tile sets: the gather unit of Algorithm 1 (ref: TileSet, bitsparse.hpp:62-71):
+ * ts = word_bits/4 consecutive tiles of a tile row, nibble row n of slot s at
+ * bits [word_bits-1-4s, word_bits-4-4s] of rows[n]; cols[s] = tile column,
+ * BG_TILESET_PAD_COL past the end of the row (and for slots >= ts). */
+#define BG_TILESET_PAD_COL 0xFFFFFFFFu
+typedef struct bg_tileset {
+  int32_t ts;
+  int32_t reserved;
+  uint64_t rows[4];
+  uint32_t cols[16];
+} bg_tileset;
+/* ref: tileset_count (bitsparse.cpp:129-134) */
+int bg_tileset_count(const bg_frdc* m, int64_t tile_row, int word_bits, int64_t* count);
+/* ref: gather_tileset (bitsparse.cpp:136-160), one set into a HOST struct;
+ * the reference's checks and messages (word_bits, tile_row, set_index). */
+int bg_gather_tileset(const bg_frdc* m, int64_t tile_row, int64_t set_index, int word_bits,
+                      bg_tileset* out);
+/* Every tile set of the matrix on the device (Algorithm 1 lines 1-5 for all
+ * tile rows at once).  set_ptr: DEVICE u64[tile_rows + 1], the exclusive scan
+ * of tileset_count (set_ptr[r] = first set of tile row r); *total = sets.
+ * sets: DEVICE bg_tileset[total], set set_ptr[r] + s = gather_tileset(m, r, s). */
+int bg_tileset_ptr(const bg_frdc* m, int word_bits, uint64_t* set_ptr, int64_t* total, bg_stream stream);
+int bg_gather_tilesets(const bg_frdc* m, int word_bits, const uint64_t* set_ptr, int64_t total,
+                       bg_tileset* sets, bg_stream stream);
+/* ref: frdc_to_dense (bitsparse.cpp:114-127): ZeroOne bits, DEVICE
+ * node_rows x bg_storage_words_per_row(node_cols, word_bits) u32. */
+int bg_frdc_to_dense(const bg_frdc* m, int word_bits, uint32_t* out, bg_stream stream);
+/* ref: FrdcStats / frdc_stats (bitsparse.hpp:83-90, bitsparse.cpp:162-169) */
+typedef struct bg_frdc_stats {
+  uint64_t nnz_tiles, nnz_bits, bytes;
+  double fill_ratio; /* nnz_bits / (16 nnz_tiles), 0 when empty */
+} bg_frdc_stats;
+int bg_frdc_stats_get(const bg_frdc* m, bg_frdc_stats* out);
 /* FRDC container (ref: write_frdc / read_frdc, bitsparse.cpp:171-222; layout
  * bitsparse.hpp:92-96): little-endian bytes identical to the reference writer.
  * Format and I/O faults are BG_RUNTIME_ERROR with the reference's messages
@@ -256,6 +289,24 @@ typedef struct bg_layer_desc {
 } bg_layer_desc;
 
 typedef struct bg_model bg_model;
+typedef struct bg_trace bg_trace; /* BIN-point trace, below */
+
+/* Single layers (ref: gcn_layer / sage_layer / graphconv_layer,
+ * graphops.hpp:94-105, graphops.cpp:270-335): x is a DEVICE operand, l the
+ * layer's plan and HOST weights (l->kind is ignored: the function names the
+ * kind), g the graph (A+I for gcn, loop-free A with mean / ones scales for
+ * sage / graph conv).  BIN points are appended to `trace` (may be NULL) with
+ * labels prefix + "mm.bin_in" ... as the reference's LayerHooks record them.
+ * out is caller-allocated per bg_layer_out_desc.  Synchronous.  Errors are the
+ * reference's (std::invalid_argument "gcn_conv: expected {mm, spmm} plan and
+ * weights", kernel contract messages), not wrapped in "layer i". */
+int bg_layer_out_desc(int kind, const bg_layer_desc* l, const bg_mat* x, int word_bits, bg_mat* out);
+int bg_gcn_layer(const bg_mat* x, const bg_layer_desc* l, const bg_graph* g, int strategy,
+                 bg_trace* trace, const char* prefix, int word_bits, bg_mat* out, bg_stream stream);
+int bg_sage_layer(const bg_mat* x, const bg_layer_desc* l, const bg_graph* g, int strategy,
+                  bg_trace* trace, const char* prefix, int word_bits, bg_mat* out, bg_stream stream);
+int bg_graphconv_layer(const bg_mat* x, const bg_layer_desc* l, const bg_graph* g, int strategy,
+                       bg_trace* trace, const char* prefix, int word_bits, bg_mat* out, bg_stream stream);
 
 /* ref: validate_model (graphops.cpp:245-268).  Returns the number of
  * problems; the messages, '\n'-separated and worded like the reference's,
@@ -284,7 +335,6 @@ int bg_model_forward_host(bg_model* m, const float* x_host, int64_t rows, int64_
                           float* out_host, float* logits_host, bg_stream stream);
 
 /* BIN-point trace (ref: RunTrace, graphops.hpp:114-122) */
-typedef struct bg_trace bg_trace;
 int bg_trace_create(bg_trace** out);
 void bg_trace_destroy(bg_trace* t);
 int bg_model_forward_traced(bg_model* m, const bg_mat* x0, float* out, float* logits,

@@ -15,8 +15,10 @@
 // captured forward on device pointers).
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -433,6 +435,57 @@ inline FrdcMatrix frdc_from_edges(const EdgeList& e, bool add_self_loops) {
   return detail::download(owned.get());
 }
 
+// ref: TileSet (bitsparse.hpp:62-71): the gather unit of Algorithm 1.
+struct TileSet {
+  static constexpr uint32_t kPadCol = BG_TILESET_PAD_COL;
+  int ts = 8;
+  std::array<uint64_t, 4> rows{};
+  std::array<uint32_t, 16> cols{};
+};
+
+// ref: tileset_count (bitsparse.cpp:129-134)
+inline int64_t tileset_count(const FrdcMatrix& m, int64_t tile_row, int word_bits = 32) {
+  auto h = detail::upload(m);
+  int64_t n = 0;
+  detail::check(bg_tileset_count(h.get(), tile_row, word_bits, &n));
+  return n;
+}
+
+// ref: gather_tileset (bitsparse.cpp:136-160); std::invalid_argument with the
+// reference's messages.
+inline TileSet gather_tileset(const FrdcMatrix& m, int64_t tile_row, int64_t set_index, int word_bits = 32) {
+  auto h = detail::upload(m);
+  bg_tileset t{};
+  detail::check(bg_gather_tileset(h.get(), tile_row, set_index, word_bits, &t));
+  TileSet out;
+  out.ts = t.ts;
+  for (int i = 0; i < 4; ++i) out.rows[static_cast<size_t>(i)] = t.rows[i];
+  for (int i = 0; i < 16; ++i) out.cols[static_cast<size_t>(i)] = t.cols[i];
+  return out;
+}
+
+// ref: frdc_to_dense (bitsparse.cpp:114-127)
+inline BitDenseMatrix frdc_to_dense(const FrdcMatrix& m, int word_bits = 32) {
+  BitDenseMatrix out(m.node_rows(), m.node_cols(), BitSemantics::ZeroOne, word_bits);
+  auto h = detail::upload(m);
+  detail::DeviceBuffer d(out.payload_bytes());
+  detail::check(bg_frdc_to_dense(h.get(), word_bits, d.as<uint32_t>(), nullptr));
+  d.download(out.data());
+  return out;
+}
+
+// ref: FrdcStats / frdc_stats (bitsparse.hpp:83-90)
+struct FrdcStats {
+  uint64_t nnz_tiles = 0, nnz_bits = 0, bytes = 0;
+  double fill_ratio = 0;
+};
+inline FrdcStats frdc_stats(const FrdcMatrix& m) {
+  auto h = detail::upload(m);
+  bg_frdc_stats s{};
+  detail::check(bg_frdc_stats_get(h.get(), &s));
+  return {s.nnz_tiles, s.nnz_bits, s.bytes, s.fill_ratio};
+}
+
 // ref: AdjacencyOperand (kernels.hpp:47-57): non-owning views.
 struct AdjacencyOperand {
   const FrdcMatrix* structure = nullptr;
@@ -743,6 +796,71 @@ inline ModelSpec rewrite_eliminate_scl(const ModelSpec& m) {
     out.layers.push_back(m.layers[i]);
   }
   return out;
+}
+
+// ---- single layers (ref: LayerHooks / gcn_layer / sage_layer / graphconv_layer,
+// graphops.hpp:88-105) ----------------------------------------------------------
+// record_bits sees every BIN point of the layer, in the reference's order and
+// with its labels (prefix + "mm.bin_in", ...); record_ns is not called (per-op
+// device times come from Model::run with timings).
+struct LayerHooks {
+  std::function<void(const std::string&, const BitDenseMatrix&)> record_bits;
+  std::function<void(const std::string&, int64_t)> record_ns;
+};
+
+namespace detail {
+inline MatOperand layer_call(int kind, const MatOperand& x, const LayerSpec& l, const GraphBundle& g,
+                             std::optional<TrinaryStrategy> strategy, const LayerHooks* hooks,
+                             const std::string& prefix, int word_bits) {
+  ModelSpec one;
+  one.layers.push_back(l);
+  auto descs = describe(one);
+  auto dx = upload(x);
+  bg_mat od{};
+  check(bg_layer_out_desc(kind, descs.data(), &dx.m, word_bits, &od));
+  auto out = allocate(od);
+  bg_trace* t = nullptr;
+  const bool want_bits = hooks && hooks->record_bits;
+  if (want_bits) check(bg_trace_create(&t));
+  std::unique_ptr<bg_trace, void (*)(bg_trace*)> owned(t, bg_trace_destroy);
+  auto fn = kind == BG_LAYER_GCN ? bg_gcn_layer : kind == BG_LAYER_SAGE ? bg_sage_layer : bg_graphconv_layer;
+  check(fn(&dx.m, descs.data(), g.handle(), strategy_code(strategy), t, prefix.c_str(), word_bits, &out.m,
+           nullptr));
+  if (want_bits) {
+    const int n = bg_trace_size(t);
+    for (int i = 0; i < n; ++i) {
+      const char* label = nullptr;
+      int64_t r = 0, c = 0;
+      int wb = 32;
+      const uint32_t* bits = nullptr;
+      check(bg_trace_point(t, i, &label, &r, &c, &wb, &bits));
+      BitDenseMatrix b(r, c, BitSemantics::PlusMinus, wb);
+      check(bg_memcpy(b.data(), bits, b.payload_bytes(), BG_COPY_D2H, nullptr));
+      hooks->record_bits(label, b);
+    }
+  }
+  return download(out);
+}
+}  // namespace detail
+
+// ref: gcn_layer (graphops.cpp:270-285)
+inline MatOperand gcn_layer(const MatOperand& x, const LayerSpec& l, const GraphBundle& g,
+                            std::optional<TrinaryStrategy> strategy = std::nullopt, const LayerHooks* hooks = nullptr,
+                            const std::string& prefix = "", int word_bits = 32) {
+  return detail::layer_call(BG_LAYER_GCN, x, l, g, strategy, hooks, prefix, word_bits);
+}
+// ref: sage_layer (graphops.cpp:325-329)
+inline MatOperand sage_layer(const MatOperand& x, const LayerSpec& l, const GraphBundle& g,
+                             std::optional<TrinaryStrategy> strategy = std::nullopt, const LayerHooks* hooks = nullptr,
+                             const std::string& prefix = "", int word_bits = 32) {
+  return detail::layer_call(BG_LAYER_SAGE, x, l, g, strategy, hooks, prefix, word_bits);
+}
+// ref: graphconv_layer (graphops.cpp:331-335)
+inline MatOperand graphconv_layer(const MatOperand& x, const LayerSpec& l, const GraphBundle& g,
+                                  std::optional<TrinaryStrategy> strategy = std::nullopt,
+                                  const LayerHooks* hooks = nullptr, const std::string& prefix = "",
+                                  int word_bits = 32) {
+  return detail::layer_call(BG_LAYER_GRAPHCONV, x, l, g, strategy, hooks, prefix, word_bits);
 }
 
 // ---- graph readers (ref: graphio.hpp:11-24) ----------------------------------

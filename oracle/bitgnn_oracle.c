@@ -254,6 +254,50 @@ void og_frdc_free(og_frdc* m) {
   memset(m, 0, sizeof *m);
 }
 
+/* ref: tileset_count, bitsparse.cpp:129-134 */
+int64_t og_tileset_count(const og_frdc* m, int64_t tile_row, int word_bits) {
+  const int64_t ts = word_bits / 4;
+  const int64_t nt = (int64_t)(m->row_ptr[tile_row + 1] - m->row_ptr[tile_row]);
+  return (nt + ts - 1) / ts;
+}
+
+/* ref: gather_tileset, bitsparse.cpp:136-160 (checks and messages in order) */
+int og_gather_tileset(const og_frdc* m, int64_t tile_row, int64_t set_index, int word_bits,
+                      og_tileset* out) {
+  if (word_bits != 32 && word_bits != 64) return fail("gather_tileset: word_bits must be 32 or 64");
+  if (tile_row < 0 || tile_row >= (m->rows + 3) / 4) return fail("gather_tileset: tile_row out of range");
+  memset(out, 0, sizeof *out);
+  out->ts = word_bits / 4;
+  if (set_index < 0 || set_index >= og_tileset_count(m, tile_row, word_bits))
+    return fail("gather_tileset: set_index out of range");
+  for (int s = 0; s < 16; ++s) out->cols[s] = 0xFFFFFFFFu;
+  const uint64_t begin = m->row_ptr[tile_row] + (uint64_t)set_index * (uint64_t)out->ts;
+  const uint64_t end = m->row_ptr[tile_row + 1];
+  for (int s = 0; s < out->ts; ++s) {
+    const uint64_t k = begin + (uint64_t)s;
+    if (k >= end) break;
+    out->cols[s] = m->col_ind[k];
+    const uint16_t t = m->tiles[k];
+    const int shift = word_bits - 4 - 4 * s;
+    for (int n = 0; n < 4; ++n) out->rows[n] |= (uint64_t)((t >> (12 - 4 * n)) & 0xF) << shift;
+  }
+  return 0;
+}
+
+/* ref: frdc_to_dense, bitsparse.cpp:114-127 (MSB-first bits, u32 storage) */
+void og_frdc_to_dense(const og_frdc* m, int word_bits, uint32_t* out) {
+  const int64_t w = og_spw(m->cols, word_bits), trows = (m->rows + 3) / 4;
+  memset(out, 0, (size_t)(m->rows * w) * 4);
+  for (int64_t r = 0; r < trows; ++r)
+    for (uint64_t k = m->row_ptr[r]; k < m->row_ptr[r + 1]; ++k)
+      for (int rl = 0; rl < 4; ++rl)
+        for (int cl = 0; cl < 4; ++cl)
+          if ((m->tiles[k] >> (15 - (4 * rl + cl))) & 1) {
+            const int64_t i = 4 * r + rl, j = 4 * (int64_t)m->col_ind[k] + cl;
+            out[i * w + j / 32] |= 1u << (31 - (j & 31));
+          }
+}
+
 /* ref: graphops.cpp:18-33 */
 void og_row_popcounts(const og_frdc* a, int64_t* deg) {
   const int64_t trows = (a->rows + 3) / 4;

@@ -67,6 +67,20 @@ void og_frdc_free(og_frdc* m);
 void og_row_popcounts(const og_frdc* m, int64_t* deg);
 int64_t og_frdc_nnz_bits(const og_frdc* m);
 
+/* Tile sets (ref: TileSet, bitsparse.hpp:62-71): same layout as bg_tileset. */
+typedef struct og_tileset {
+  int32_t ts, reserved;
+  uint64_t rows[4];
+  uint32_t cols[16];
+} og_tileset;
+/* ref: tileset_count (bitsparse.cpp:129-134) */
+int64_t og_tileset_count(const og_frdc* m, int64_t tile_row, int word_bits);
+/* ref: gather_tileset (bitsparse.cpp:136-160); 0, or nonzero with og_error() */
+int og_gather_tileset(const og_frdc* m, int64_t tile_row, int64_t set_index, int word_bits,
+                      og_tileset* out);
+/* ref: frdc_to_dense (bitsparse.cpp:114-127): ZeroOne rows x og_spw(cols) words */
+void og_frdc_to_dense(const og_frdc* m, int word_bits, uint32_t* out);
+
 /* ---- kernels.cpp -------------------------------------------------------- */
 typedef struct og_variant {
   int op, in1, in2, out;

@@ -127,6 +127,11 @@ def lib() -> C.CDLL:
                                    C.POINTER(C.POINTER(C.c_float)), C.POINTER(C.POINTER(C.c_float)),
                                    C.POINTER(C.c_int64), _TRACE_FN, C.c_void_p]
         L.og_free.argtypes = [C.c_void_p]
+        L.og_tileset_count.restype = C.c_int64
+        L.og_tileset_count.argtypes = [C.POINTER(_Frdc), C.c_int64, C.c_int]
+        L.og_gather_tileset.argtypes = [C.POINTER(_Frdc), C.c_int64, C.c_int64, C.c_int,
+                                        C.POINTER(TileSetC)]
+        L.og_frdc_to_dense.argtypes = [C.POINTER(_Frdc), C.c_int, C.c_void_p]
         _lib = L
     return _lib
 
@@ -227,6 +232,36 @@ class Frdc:
         s = self._c()
         lib().og_row_popcounts(C.byref(s), _ptr(deg))
         return deg
+
+
+class TileSetC(C.Structure):
+    """ref: TileSet (bitsparse.hpp:62-71); the layout of og_tileset / bg_tileset."""
+    _fields_ = [("ts", C.c_int32), ("reserved", C.c_int32), ("rows", C.c_uint64 * 4),
+                ("cols", C.c_uint32 * 16)]
+
+
+PAD_COL = 0xFFFFFFFF
+
+
+def tileset_count(m: Frdc, tile_row: int, word_bits: int = 32) -> int:
+    s = m._c()
+    return int(lib().og_tileset_count(C.byref(s), tile_row, word_bits))
+
+
+def gather_tileset(m: Frdc, tile_row: int, set_index: int, word_bits: int = 32):
+    """(ts, rows[4], cols[16]) of one tile set (bitsparse.cpp:136-160)."""
+    s, t = m._c(), TileSetC()
+    if lib().og_gather_tileset(C.byref(s), tile_row, set_index, word_bits, C.byref(t)):
+        raise ValueError(_err())
+    return t.ts, [int(v) for v in t.rows], [int(v) for v in t.cols]
+
+
+def frdc_to_dense(m: Frdc, word_bits: int = 32) -> np.ndarray:
+    """ZeroOne bits rows x spw(cols) (bitsparse.cpp:114-127)."""
+    out = np.zeros((m.rows, spw(m.cols, word_bits)), np.uint32)
+    s = m._c()
+    lib().og_frdc_to_dense(C.byref(s), word_bits, _ptr(out))
+    return out
 
 
 def _frdc_copy(s: _Frdc) -> Frdc:
@@ -622,6 +657,68 @@ def ref_spec_run(layers, graph: Optional["RefGraph"], x: np.ndarray, word_bits: 
     return out, lg, points
 
 
+def ref_layer_run(graph: "RefGraph", layer, x, word_bits: int = 32, prefix: str = "", x_word_bits: int = 32):
+    """One layer through the real reference's gcn_layer / sage_layer /
+    graphconv_layer (graphops.cpp:270-335) by layer.kind (0 / 1 / 2).  x: a
+    float32 matrix, or (bits u32 [rows, spw], rows, cols) for a binary input.
+    Returns (result, trace points): result is float32 rows x cols for an F
+    output, else (bits, rows, cols, word_bits)."""
+    arr = (_RefLayer * 1)()
+    d = arr[0]
+    keep = []
+    d.kind = int(layer.kind)
+    plan = "+".join(str(p) if isinstance(p, str) else p.name() for p in (layer.plan or []))
+    keep.append(plan.encode())
+    d.plan = keep[-1]
+    for name in ("w1", "w2"):
+        w = getattr(layer, name, None)
+        if w is not None:
+            w = np.ascontiguousarray(w, dtype=np.float32)
+            keep.append(w)
+            setattr(d, name, w.ctypes.data)
+            setattr(d, name + "_rows", w.shape[0])
+            setattr(d, name + "_cols", w.shape[1])
+    d.relu = int(bool(getattr(layer, "relu", False)))
+    if isinstance(x, tuple):
+        bits, rows, cols = x
+        xa, prec = np.ascontiguousarray(bits, dtype=np.uint32), 1
+    else:
+        xa, prec = np.ascontiguousarray(x, dtype=np.float32), 0
+        rows, cols = xa.shape
+    points: List[TracePoint] = []
+
+    def sink(_ctx, label, bits, r, c, wb):
+        n = r * spw(c, wb)
+        a = np.ctypeslib.as_array(bits, shape=(n,)).reshape(r, -1).copy() if n else \
+            np.zeros((r, spw(c, wb)), np.uint32)
+        points.append(TracePoint(label.decode(), a, r, c, wb))
+
+    cb = _TRACE_FN(sink)
+    L = ref()
+    L.ref_layer_run.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int64,
+                                C.c_int, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_void_p),
+                                C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int), _TRACE_FN,
+                                C.c_void_p]
+    L.ref_free.argtypes = [C.c_void_p]
+    op, outp, r, c, wb = C.c_int(), C.c_void_p(), C.c_int64(), C.c_int64(), C.c_int()
+    if L.ref_layer_run(graph.h, arr, word_bits, prec, _ptr(xa), rows, cols, x_word_bits, prefix.encode(),
+                       C.byref(op), C.byref(outp), C.byref(r), C.byref(c), C.byref(wb), cb, None):
+        raise ValueError(L.ref_error().decode())
+    try:
+        if op.value == 0:
+            n = r.value * c.value
+            res = np.ctypeslib.as_array(C.cast(outp, C.POINTER(C.c_float)), shape=(max(n, 1),))[:n] \
+                .reshape(r.value, c.value).copy()
+        else:
+            n = r.value * spw(c.value, wb.value)
+            bits = np.ctypeslib.as_array(C.cast(outp, C.POINTER(C.c_uint32)), shape=(max(n, 1),))[:n] \
+                .reshape(r.value, -1).copy()
+            res = (bits, r.value, c.value, wb.value)
+    finally:
+        L.ref_free(outp)
+    return res, points
+
+
 def ref_read_graph(kind: int, text, name: str = "<stream>", forced_nodes: int = -1, undirected: bool = False):
     """The reference's graphio readers (kind 0 read_edge_list, 1
     read_matrix_market, 2 load_graph(path=text)).  Returns (node_count, src,
@@ -780,6 +877,28 @@ def ref_bench_bspmm_bbb(nodes: int = 65536, density: float = 0.001, cols: int = 
             "engine_ms": em.value, "naive_csr_ms": bm.value, "values_match": bool(match.value),
             "gteps": edges.value / (em.value * 1e-3) / 1e9 if em.value > 0 else None,
             "threads": 1}
+
+
+def ref_gather_tileset(m: Frdc, tile_row: int, set_index: int, word_bits: int = 32):
+    """The real reference's gather_tileset (bitsparse.cpp:136-160)."""
+    L = ref()
+    ts = C.c_int32()
+    rows = (C.c_uint64 * 4)()
+    cols = (C.c_uint32 * 16)()
+    if L.ref_gather_tileset(C.c_int64(m.rows), C.c_int64(m.cols), _ptr(m.row_ptr), _ptr(m.col_ind),
+                            _ptr(m.tiles), C.c_int64(m.nnz), C.c_int64(tile_row), C.c_int64(set_index),
+                            C.c_int(word_bits), C.byref(ts), rows, cols):
+        raise ValueError(L.ref_error().decode())
+    return ts.value, [int(v) for v in rows], [int(v) for v in cols]
+
+
+def ref_frdc_to_dense(m: Frdc, word_bits: int = 32) -> np.ndarray:
+    L = ref()
+    out = np.zeros((m.rows, spw(m.cols, word_bits)), np.uint32)
+    if L.ref_frdc_to_dense(C.c_int64(m.rows), C.c_int64(m.cols), _ptr(m.row_ptr), _ptr(m.col_ind),
+                           _ptr(m.tiles), C.c_int64(m.nnz), C.c_int(word_bits), _ptr(out)):
+        raise ValueError(L.ref_error().decode())
+    return out
 
 
 def ref_enumerate_plans(model: str, layers: int):

@@ -314,6 +314,43 @@ int ref_bench_bspmm_bbb(int64_t nodes, double density, int64_t cols, uint64_t se
   }
 }
 
+// The reference's own tile-set gather and dense expansion over FRDC arrays
+// (bitsparse.cpp:114-160), through its validating FrdcMatrix constructor.
+namespace {
+FrdcMatrix frdc_of(int64_t rows, int64_t cols, const uint64_t* rp, const uint32_t* ci,
+                   const uint16_t* ti, int64_t nnz) {
+  const size_t tr = static_cast<size_t>((rows + 3) / 4) + 1;
+  return FrdcMatrix(rows, cols, std::vector<uint64_t>(rp, rp + tr), std::vector<uint32_t>(ci, ci + nnz),
+                    std::vector<uint16_t>(ti, ti + nnz));
+}
+}  // namespace
+
+int ref_gather_tileset(int64_t rows, int64_t cols, const uint64_t* rp, const uint32_t* ci,
+                       const uint16_t* ti, int64_t nnz, int64_t tile_row, int64_t set_index,
+                       int word_bits, int32_t* ts, uint64_t* out_rows, uint32_t* out_cols) {
+  try {
+    TileSet t = gather_tileset(frdc_of(rows, cols, rp, ci, ti, nnz), tile_row, set_index, word_bits);
+    *ts = t.ts;
+    for (int i = 0; i < 4; ++i) out_rows[i] = t.rows[static_cast<size_t>(i)];
+    for (int i = 0; i < 16; ++i) out_cols[i] = t.cols[static_cast<size_t>(i)];
+    return 0;
+  } catch (const std::exception& ex) {
+    return guard(ex);
+  }
+}
+
+int ref_frdc_to_dense(int64_t rows, int64_t cols, const uint64_t* rp, const uint32_t* ci,
+                      const uint16_t* ti, int64_t nnz, int word_bits, uint32_t* out) {
+  try {
+    BitDenseMatrix d = frdc_to_dense(frdc_of(rows, cols, rp, ci, ti, nnz), word_bits);
+    const int64_t w = d.storage_words_per_row();
+    for (int64_t i = 0; i < d.rows(); ++i) std::memcpy(out + i * w, d.row_span(i).data(), static_cast<size_t>(w) * 4);
+    return 0;
+  } catch (const std::exception& ex) {
+    return guard(ex);
+  }
+}
+
 // Kernel-level access for fixtures: binarize (bitdense.cpp:71-88).
 void ref_binarize(const float* x, int64_t rows, int64_t cols, int word_bits, uint32_t* out) {
   DenseMatrix m(rows, cols);
@@ -424,6 +461,78 @@ int ref_spec_run(void* graph, const ref_layer* layers, int n, int word_bits, con
     const bool has_logits = tr.logits.rows() * tr.logits.cols() == o.rows() * o.cols() && nb;
     if (has_logits) std::memcpy(*logits, tr.logits.row(0), nb);
     else if (nb) std::memcpy(*logits, o.row(0), nb);
+    return 0;
+  } catch (const std::exception& ex) {
+    return guard(ex);
+  }
+}
+
+// One layer through the reference's own gcn_layer / sage_layer /
+// graphconv_layer (graphops.cpp:270-335), with LayerHooks recording every BIN
+// point.  x: F (float rows x cols) or B (packed PlusMinus bits, x_wb).  The
+// result is malloc'd (free with ref_free): floats for F, packed words for B.
+int ref_layer_run(void* graph, const ref_layer* d, int word_bits, int x_prec, const void* x, int64_t rows,
+                  int64_t cols, int x_wb, const char* prefix, int* out_prec, void** out, int64_t* out_rows,
+                  int64_t* out_cols, int* out_wb, ref_trace_fn trace, void* ctx) {
+  try {
+    LayerSpec l;
+    l.kind = static_cast<LayerKind>(d->kind);
+    if (d->plan && *d->plan) l.plan = parse_plan_chain(d->plan);
+    auto dense = [](const float* p, int64_t r, int64_t c) {
+      auto m = std::make_shared<DenseMatrix>(r, c);
+      if (r * c) std::memcpy(m->row(0), p, static_cast<size_t>(r * c) * sizeof(float));
+      return m;
+    };
+    if (d->w1) l.w1 = dense(d->w1, d->w1_rows, d->w1_cols);
+    if (d->w2) l.w2 = dense(d->w2, d->w2_rows, d->w2_cols);
+    l.relu = d->relu != 0;
+    MatOperand xo;
+    if (x_prec == 0) {
+      DenseMatrix m(rows, cols);
+      if (rows * cols) std::memcpy(m.row(0), x, static_cast<size_t>(rows * cols) * sizeof(float));
+      xo = std::move(m);
+    } else {
+      BitDenseMatrix b(rows, cols, BitSemantics::PlusMinus, x_wb);
+      const int64_t w = b.storage_words_per_row();
+      for (int64_t r = 0; r < rows; ++r)
+        std::memcpy(b.row_span(r).data(), static_cast<const uint32_t*>(x) + r * w, static_cast<size_t>(w) * 4);
+      xo = BitOperand{std::move(b), std::nullopt};
+    }
+    LayerHooks hooks;
+    hooks.record_bits = [&](const std::string& label, const BitDenseMatrix& b) {
+      if (!trace) return;
+      const int64_t w = b.storage_words_per_row();
+      std::vector<uint32_t> words(static_cast<size_t>(b.rows() * w));
+      for (int64_t r = 0; r < b.rows(); ++r) std::memcpy(words.data() + r * w, b.row_span(r).data(), static_cast<size_t>(w) * 4);
+      trace(ctx, label.c_str(), words.data(), b.rows(), b.cols(), b.word_bits());
+    };
+    const GraphBundle& g = *static_cast<RefGraph*>(graph)->g;
+    const std::string pre = prefix ? prefix : "";
+    MatOperand r = d->kind == static_cast<int>(LayerKind::GcnConv)
+                       ? gcn_layer(xo, l, g, std::nullopt, &hooks, pre, word_bits)
+                   : d->kind == static_cast<int>(LayerKind::SageConv)
+                       ? sage_layer(xo, l, g, std::nullopt, &hooks, pre, word_bits)
+                       : graphconv_layer(xo, l, g, std::nullopt, &hooks, pre, word_bits);
+    if (std::holds_alternative<DenseMatrix>(r)) {
+      const DenseMatrix& o = std::get<DenseMatrix>(r);
+      *out_prec = 0;
+      *out_rows = o.rows();
+      *out_cols = o.cols();
+      *out_wb = 32;
+      const size_t nb = static_cast<size_t>(o.rows() * o.cols()) * 4;
+      *out = std::malloc(std::max<size_t>(nb, 4));
+      if (nb) std::memcpy(*out, o.row(0), nb);
+    } else {
+      const BitDenseMatrix& b = std::get<BitOperand>(r).bits;
+      const int64_t w = b.storage_words_per_row();
+      *out_prec = 1;
+      *out_rows = b.rows();
+      *out_cols = b.cols();
+      *out_wb = b.word_bits();
+      *out = std::malloc(std::max<size_t>(static_cast<size_t>(b.rows() * w) * 4, 4));
+      for (int64_t i = 0; i < b.rows(); ++i)
+        std::memcpy(static_cast<uint32_t*>(*out) + i * w, b.row_span(i).data(), static_cast<size_t>(w) * 4);
+    }
     return 0;
   } catch (const std::exception& ex) {
     return guard(ex);

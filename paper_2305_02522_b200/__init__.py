@@ -14,5 +14,7 @@ from .bitgnn import (AdjacencyOperand, BitDenseMatrix, BitOperand, FrdcMatrix,  
                      GraphBundle, KernelVariant, LayerSpec, Model, Rng, add, binarize,
                      binarize_with_scale, bmm, bspmm, build_model_spec, concat, EdgeList, frdc_from_edges,
                      load_graph, read_edge_list, read_matrix_market,
-                     prepare_graph, rewrite_eliminate_scl, run_model, transpose, unpack, validate_model)
+                     prepare_graph, rewrite_eliminate_scl, run_model, transpose, unpack, validate_model,
+                     TileSet, FrdcStats, gather_tileset, gather_tilesets, tileset_count, frdc_to_dense,
+                     frdc_stats, gcn_layer, sage_layer, graphconv_layer)
 from ._lib import (B, F, CudaError, InvalidArgument, LogicError, RuntimeFailure)  # noqa: E402,F401

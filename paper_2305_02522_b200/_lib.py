@@ -57,6 +57,16 @@ class LayerDesc(C.Structure):
                 ("scale_col", C.c_void_p), ("scale_col_len", C.c_int64)]
 
 
+class TileSetC(C.Structure):
+    _fields_ = [("ts", C.c_int32), ("reserved", C.c_int32), ("rows", C.c_uint64 * 4),
+                ("cols", C.c_uint32 * 16)]
+
+
+class FrdcStatsC(C.Structure):
+    _fields_ = [("nnz_tiles", C.c_uint64), ("nnz_bits", C.c_uint64), ("bytes", C.c_uint64),
+                ("fill_ratio", C.c_double)]
+
+
 class KernelTiming(C.Structure):
     _fields_ = [("label", C.c_char * 64), ("ms", C.c_double)]
 
@@ -93,6 +103,12 @@ PROTOTYPES = {
     "bg_frdc_info_get": (I32, [P, C.POINTER(FrdcInfo)]),
     "bg_frdc_download": (I32, [P, P, P, P]),
     "bg_frdc_corrupt_tile": (I32, [P, I64]),
+    "bg_tileset_count": (I32, [P, I64, I32, PI64]),
+    "bg_gather_tileset": (I32, [P, I64, I64, I32, C.POINTER(TileSetC)]),
+    "bg_tileset_ptr": (I32, [P, I32, P, PI64, P]),
+    "bg_gather_tilesets": (I32, [P, I32, P, I64, P, P]),
+    "bg_frdc_to_dense": (I32, [P, I32, P, P]),
+    "bg_frdc_stats_get": (I32, [P, C.POINTER(FrdcStatsC)]),
     "bg_frdc_serialized_size": (I32, [P, C.POINTER(C.c_size_t)]),
     "bg_frdc_serialize": (I32, [P, I32, P, C.c_size_t]),
     "bg_frdc_deserialize": (I32, [P, C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(C.c_int), P]),
@@ -122,6 +138,11 @@ PROTOTYPES = {
     "bg_batchnorm_infer": (I32, [P, I64, I64, P, P, P, P, P, P]),
     "bg_fused_mm_spmm": (I32, [Variant, Variant, C.POINTER(Mat), C.POINTER(Mat), P, P, P, I32,
                                C.POINTER(Mat), P]),
+    "bg_layer_out_desc": (I32, [I32, C.POINTER(LayerDesc), C.POINTER(Mat), I32, C.POINTER(Mat)]),
+    "bg_gcn_layer": (I32, [C.POINTER(Mat), C.POINTER(LayerDesc), P, I32, P, C.c_char_p, I32, C.POINTER(Mat), P]),
+    "bg_sage_layer": (I32, [C.POINTER(Mat), C.POINTER(LayerDesc), P, I32, P, C.c_char_p, I32, C.POINTER(Mat), P]),
+    "bg_graphconv_layer": (I32, [C.POINTER(Mat), C.POINTER(LayerDesc), P, I32, P, C.c_char_p, I32,
+                                 C.POINTER(Mat), P]),
     "bg_validate_model": (I32, [I32, I32, C.POINTER(LayerDesc), I32, C.c_char_p, C.c_size_t]),
     "bg_model_create": (I32, [P, I32, I32, I32, C.POINTER(LayerDesc), I32, C.POINTER(P), P]),
     "bg_model_destroy": (None, [P]),

@@ -410,6 +410,72 @@ def frdc_from_edges(node_count: int, src, dst, add_self_loops: bool) -> FrdcMatr
     return FrdcMatrix(h.value)
 
 
+# --------------------------------------------------------------------------- #
+# Tile sets, dense expansion, statistics (bitsparse.hpp:62-90)
+# --------------------------------------------------------------------------- #
+PAD_COL = 0xFFFFFFFF  # TileSet::kPadCol
+
+
+@dataclass
+class TileSet:
+    """bitsparse.hpp:66-71 -- ts tiles' nibble rows concatenated into 4 words."""
+    ts: int = 8
+    rows: Tuple[int, int, int, int] = (0, 0, 0, 0)
+    cols: Tuple[int, ...] = (PAD_COL,) * 16
+
+
+@dataclass
+class FrdcStats:
+    """bitsparse.hpp:83-88"""
+    nnz_tiles: int = 0
+    nnz_bits: int = 0
+    bytes: int = 0
+    fill_ratio: float = 0.0
+
+
+def tileset_count(m: FrdcMatrix, tile_row: int, word_bits: int = 32) -> int:
+    """bitsparse.cpp:129-134"""
+    n = C.c_int64()
+    check(lib().bg_tileset_count(m._h, tile_row, word_bits, C.byref(n)))
+    return n.value
+
+
+def gather_tileset(m: FrdcMatrix, tile_row: int, set_index: int, word_bits: int = 32) -> TileSet:
+    """bitsparse.cpp:136-160 (the reference's checks and messages)."""
+    t = L.TileSetC()
+    check(lib().bg_gather_tileset(m._h, tile_row, set_index, word_bits, C.byref(t)))
+    return TileSet(t.ts, tuple(int(v) for v in t.rows), tuple(int(v) for v in t.cols))
+
+
+def gather_tilesets(m: FrdcMatrix, word_bits: int = 32) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Every tile set of the matrix, assembled on the device (Algorithm 1
+    lines 1-5 for all tile rows): (set_ptr int64 [tile_rows+1] with set_ptr[r]
+    the first set of tile row r, sets uint8 [total, 96] of bg_tileset records:
+    ts i32, pad i32, rows u64[4], cols u32[16])."""
+    tr = m.tile_rows
+    set_ptr = torch.empty(tr + 1, dtype=torch.int64, device="cuda")
+    total = C.c_int64()
+    check(lib().bg_tileset_ptr(m._h, word_bits, set_ptr.data_ptr(), C.byref(total), _stream()))
+    sets = torch.empty((max(total.value, 0), C.sizeof(L.TileSetC)), dtype=torch.uint8, device="cuda")
+    check(lib().bg_gather_tilesets(m._h, word_bits, set_ptr.data_ptr(), total.value,
+                                   sets.data_ptr() if total.value else None, _stream()))
+    return set_ptr, sets
+
+
+def frdc_to_dense(m: FrdcMatrix, word_bits: int = 32) -> BitDenseMatrix:
+    """bitsparse.cpp:114-127 -- ZeroOne bits, node_rows x node_cols."""
+    out = BitDenseMatrix.empty(m.node_rows, m.node_cols, word_bits, ZERO_ONE)
+    check(lib().bg_frdc_to_dense(m._h, word_bits, out.words.data_ptr(), _stream()))
+    return out
+
+
+def frdc_stats(m: FrdcMatrix) -> FrdcStats:
+    """bitsparse.cpp:162-169"""
+    st = L.FrdcStatsC()
+    check(lib().bg_frdc_stats_get(m._h, C.byref(st)))
+    return FrdcStats(st.nnz_tiles, st.nnz_bits, st.bytes, st.fill_ratio)
+
+
 @dataclass
 class AdjacencyOperand:
     """kernels.hpp:52-57 -- raw structure, or diag(row)*A*diag(col) when factorized."""
@@ -704,12 +770,7 @@ class Model:
         check(lib().bg_trace_create(C.byref(t)))
         try:
             check(lib().bg_model_forward_traced(self._h, C.byref(cx), out.data_ptr(), logits.data_ptr(), t, _stream()))
-            pts = []
-            for i in range(lib().bg_trace_size(t)):
-                lab, r, c, wb, bits = C.c_char_p(), C.c_int64(), C.c_int64(), C.c_int(), C.c_void_p()
-                check(lib().bg_trace_point(t, i, C.byref(lab), C.byref(r), C.byref(c), C.byref(wb), C.byref(bits)))
-                view = device_view(bits.value, (r.value, storage_words_per_row(c.value, wb.value)), "<i4")
-                pts.append(TracePoint(lab.value.decode(), BitDenseMatrix(view.clone(), r.value, c.value, wb.value)))
+            pts = _trace_points(t)
         finally:
             lib().bg_trace_destroy(t)
         return out, logits, pts
@@ -753,6 +814,56 @@ class Model:
                 lib().bg_model_destroy(self._h)
         except Exception:
             pass
+
+
+def _trace_points(t) -> List["TracePoint"]:
+    pts = []
+    for i in range(lib().bg_trace_size(t)):
+        lab, r, c, wb, bits = C.c_char_p(), C.c_int64(), C.c_int64(), C.c_int(), C.c_void_p()
+        check(lib().bg_trace_point(t, i, C.byref(lab), C.byref(r), C.byref(c), C.byref(wb), C.byref(bits)))
+        view = device_view(bits.value, (r.value, storage_words_per_row(c.value, wb.value)), "<i4")
+        pts.append(TracePoint(lab.value.decode(), BitDenseMatrix(view.clone(), r.value, c.value, wb.value)))
+    return pts
+
+
+def _layer(kind: int, fn, x: MatOperand, l: LayerSpec, g: GraphBundle, strategy: Optional[int],
+           trace: Optional[list], prefix: str, word_bits: int) -> MatOperand:
+    arr, keep = _descs([l])
+    cx = _mat(x)
+    desc = L.Mat()
+    check(lib().bg_layer_out_desc(kind, arr, C.byref(cx), word_bits, C.byref(desc)))
+    out, desc = _alloc(desc)
+    t = C.c_void_p()
+    if trace is not None:
+        check(lib().bg_trace_create(C.byref(t)))
+    try:
+        check(fn(C.byref(cx), arr, g._h, -1 if strategy is None else int(strategy), t if trace is not None else None,
+                 prefix.encode(), word_bits, C.byref(desc), _stream()))
+        if trace is not None:
+            trace.extend(_trace_points(t))
+    finally:
+        if trace is not None:
+            lib().bg_trace_destroy(t)
+    return out
+
+
+def gcn_layer(x: MatOperand, l: LayerSpec, g: GraphBundle, strategy: Optional[int] = None,
+              trace: Optional[list] = None, prefix: str = "", word_bits: int = 32) -> MatOperand:
+    """graphops.cpp:270-285 -- {mm, spmm} over A+I (norm scales when in2 = F);
+    BIN points are appended to `trace` (a list of TracePoint) under `prefix`."""
+    return _layer(L.LAYER_GCN, lib().bg_gcn_layer, x, l, g, strategy, trace, prefix, word_bits)
+
+
+def sage_layer(x: MatOperand, l: LayerSpec, g: GraphBundle, strategy: Optional[int] = None,
+               trace: Optional[list] = None, prefix: str = "", word_bits: int = 32) -> MatOperand:
+    """graphops.cpp:325-329 -- neighborhood layer over loop-free A, mean aggregation."""
+    return _layer(L.LAYER_SAGE, lib().bg_sage_layer, x, l, g, strategy, trace, prefix, word_bits)
+
+
+def graphconv_layer(x: MatOperand, l: LayerSpec, g: GraphBundle, strategy: Optional[int] = None,
+                    trace: Optional[list] = None, prefix: str = "", word_bits: int = 32) -> MatOperand:
+    """graphops.cpp:331-335 -- neighborhood layer over loop-free A, sum aggregation."""
+    return _layer(L.LAYER_GRAPHCONV, lib().bg_graphconv_layer, x, l, g, strategy, trace, prefix, word_bits)
 
 
 def run_model(model: Model, x0: MatOperand, trace: bool = False):

@@ -395,6 +395,84 @@ int bg_fused_mm_spmm(bg_variant mm, bg_variant sp, const bg_mat* x, const bg_mat
   });
 }
 
+// ---- single layers (ref: gcn_layer / sage_layer / graphconv_layer) -----------
+namespace {
+
+// The reference's own slot checks (graphops.cpp:273, :292-294), then one layer
+// through the model executor on a throw-away one-layer model: weights
+// binarized with their column scales as run_mm_slot does per call
+// (graphops.cpp:47-77), BIN points appended to `trace` under `prefix`.
+void layer_call(int kind, const bg_mat* x, const bg_layer_desc* l, const bg_graph* g, int strategy,
+                bg_trace* trace, const char* prefix, int wb, bg_mat* out, bg_stream stream) {
+  need(x, "input operand");
+  need(l, "layer");
+  need(g, "graph");
+  check_wb(wb);
+  if (kind == BG_LAYER_GCN) {
+    if (l->n_plan != 2 || !l->w1) fail("gcn_conv: expected {mm, spmm} plan and weights");
+  } else if (l->n_plan != 4 || !l->w1 || !l->w2) {
+    fail("expected {mm_self, mm_neigh, spmm, add} plan and two weight matrices");
+  }
+  cudaStream_t s = S(stream);
+  const Op x0 = op_from_mat(x);
+  bg_model m;
+  m.graph = g;
+  m.input_prec = x0.prec;
+  m.strategy = strategy;
+  m.wb = wb;
+  m.capture = false;
+  LayerInfo info = layer_info(*l);
+  info.kind = kind;
+  m.infos.push_back(info);
+  m.layers.resize(1);
+  ModelLayer& ml = m.layers[0];
+  ml.info = info;
+  ml.relu = l->relu != 0;
+  ml.w1.upload(l->w1, l->w1_rows, l->w1_cols, wb, s);
+  if (kind != BG_LAYER_GCN) ml.w2.upload(l->w2, l->w2_rows, l->w2_cols, wb, s);
+  LayerCall call;
+  call.prefix = prefix ? prefix : "";
+  forward_impl(m, x0, nullptr, nullptr, trace, nullptr, s, nullptr, &call);
+  copy_out(call.result, out, s);
+  sync(s);
+}
+
+}  // namespace
+
+int bg_layer_out_desc(int kind, const bg_layer_desc* l, const bg_mat* x, int word_bits, bg_mat* out) {
+  return guard([&] {
+    need(l, "layer");
+    need(x, "input operand");
+    need(out, "output");
+    check_wb(word_bits);
+    const int slot = kind == BG_LAYER_GCN ? 1 : 3;
+    if (kind != BG_LAYER_GCN && kind != BG_LAYER_SAGE && kind != BG_LAYER_GRAPHCONV)
+      fail("layer_out_desc: kind must be gcn_conv, sage_conv or graph_conv");
+    if (l->n_plan <= slot || !l->w1) fail("layer_out_desc: plan or weights missing");
+    std::memset(out, 0, sizeof *out);
+    out->precision = l->plan[slot].out;
+    out->rows = x->rows;
+    out->cols = l->w1_cols;
+    out->word_bits = out->precision == BG_B ? word_bits : 32;
+    out->semantics = BG_PLUS_MINUS;
+  });
+}
+
+int bg_gcn_layer(const bg_mat* x, const bg_layer_desc* l, const bg_graph* g, int strategy, bg_trace* trace,
+                 const char* prefix, int word_bits, bg_mat* out, bg_stream s) {
+  return guard([&] { layer_call(BG_LAYER_GCN, x, l, g, strategy, trace, prefix, word_bits, out, s); });
+}
+
+int bg_sage_layer(const bg_mat* x, const bg_layer_desc* l, const bg_graph* g, int strategy, bg_trace* trace,
+                  const char* prefix, int word_bits, bg_mat* out, bg_stream s) {
+  return guard([&] { layer_call(BG_LAYER_SAGE, x, l, g, strategy, trace, prefix, word_bits, out, s); });
+}
+
+int bg_graphconv_layer(const bg_mat* x, const bg_layer_desc* l, const bg_graph* g, int strategy,
+                       bg_trace* trace, const char* prefix, int word_bits, bg_mat* out, bg_stream s) {
+  return guard([&] { layer_call(BG_LAYER_GRAPHCONV, x, l, g, strategy, trace, prefix, word_bits, out, s); });
+}
+
 // ---- models -----------------------------------------------------------------
 int bg_validate_model(int has_graph, int input_precision, const bg_layer_desc* layers, int n,
                       char* buf, size_t len) {

@@ -364,8 +364,8 @@ struct Exec {
 
 void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace* trace,
                   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>>* timing,
-                  cudaStream_t s, StreamChunks* chunks) {
-  {
+                  cudaStream_t s, StreamChunks* chunks, LayerCall* single) {
+  if (!single) {
     std::vector<std::string> errors = validate_model(m.graph != nullptr, m.input_prec, m.infos);
     if (!errors.empty()) {
       std::ostringstream os;
@@ -373,8 +373,8 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
       for (const auto& e : errors) os << "\n  " << e;
       fail(os.str());
     }
+    if (x0.prec != m.input_prec) fail("model input tag does not match the provided operand");
   }
-  if (x0.prec != m.input_prec) fail("model input tag does not match the provided operand");
   m.pool.reset();
   Hooks h;
   h.trace = trace;
@@ -400,7 +400,7 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
   const size_t nl = m.layers.size();
   for (size_t i = 0; i < nl; ++i) {
     ModelLayer& l = m.layers[i];
-    const std::string prefix = "layer" + std::to_string(i) + ".";
+    const std::string prefix = single ? single->prefix : "layer" + std::to_string(i) + ".";
     try {
       switch (l.info.kind) {
         case BG_LAYER_GCN: {  // ref: gcn_layer, graphops.cpp:270-285
@@ -560,9 +560,14 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
     } catch (const cuda_error&) {
       throw;
     } catch (const std::exception& e) {
+      if (single) throw;  // a layer function reports its own errors unwrapped
       throw std::runtime_error("layer " + std::to_string(i) + " (" + layer_kind_name(l.info.kind) +
                                "): " + e.what());
     }
+  }
+  if (single) {
+    single->result = cur;
+    return;
   }
   if (cur.prec != BG_F) fail("model output must be full precision");
   if (out && cur.f != out)

@@ -102,7 +102,14 @@ struct StreamChunks {
   RowChunks in, out;
   bool out_done = false;
 };
+// One layer called on its own (ref: gcn_layer / sage_layer / graphconv_layer,
+// graphops.cpp:270-335): labels start with `prefix`, the result may be
+// binary and is left in the model's pool.
+struct LayerCall {
+  std::string prefix;
+  Op result;
+};
 void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace* trace,
                   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>>* timing,
-                  cudaStream_t s, StreamChunks* chunks = nullptr);
+                  cudaStream_t s, StreamChunks* chunks = nullptr, LayerCall* single = nullptr);
 }

@@ -265,6 +265,41 @@ static void test_gpu() {
   b::DenseMatrix o1 = model.forward(X, &lg1), o2 = model.forward(X, &lg2);
   CHECK(o1 == out && o2 == out && lg1 == trace.logits && lg2 == lg1);
 
+  // single layers (ref: gcn_layer, graphops.cpp:270-285): the two layer calls
+  // compose to the model's logits; the hooks see the model's BIN points
+  {
+    std::vector<std::string> labels;
+    b::LayerHooks hooks;
+    hooks.record_bits = [&](const std::string& l, const b::BitDenseMatrix&) { labels.push_back(l); };
+    b::MatOperand h1 = b::gcn_layer(X, m.layers[0], *m.graph, std::nullopt, &hooks, "layer0.");
+    b::MatOperand h2 = b::gcn_layer(h1, m.layers[1], *m.graph, std::nullopt, &hooks, "layer1.");
+    CHECK(std::get<b::DenseMatrix>(h2) == trace.logits);
+    CHECK(labels.size() == trace.points.size());
+    for (size_t i = 0; i < labels.size() && i < trace.points.size(); ++i) CHECK(labels[i] == trace.points[i].label);
+    b::LayerSpec bad = m.layers[0];
+    bad.plan.pop_back();
+    CHECK(throws<std::invalid_argument>([&] { b::gcn_layer(X, bad, *m.graph); },
+                                        "gcn_conv: expected {mm, spmm} plan and weights"));
+  }
+
+  // tile sets (ref: test_bitsparse.cpp:131-161)
+  {
+    b::EdgeList row;
+    row.node_count = 40;
+    for (int c = 0; c < 10; ++c) row.edges.emplace_back(0, 4 * c);
+    b::FrdcMatrix T = b::frdc_from_edges(row, false);
+    CHECK(b::tileset_count(T, 0, 32) == 2 && b::tileset_count(T, 0, 64) == 1);
+    b::TileSet s0 = b::gather_tileset(T, 0, 0, 32), s1 = b::gather_tileset(T, 0, 1, 32);
+    CHECK(s0.ts == 8 && s0.rows[0] == 0x88888888u && s1.rows[0] == 0x88000000u && s1.cols[2] == b::TileSet::kPadCol);
+    CHECK(b::gather_tileset(T, 0, 0, 64).rows[0] == 0x8888888888000000ull);
+    CHECK(throws<std::invalid_argument>([&] { b::gather_tileset(T, 0, 2, 32); },
+                                        "gather_tileset: set_index out of range"));
+    b::BitDenseMatrix D = b::frdc_to_dense(T);
+    CHECK(D.bit(0, 0) && D.bit(0, 36) && !D.bit(0, 1) && !D.bit(1, 0));
+    b::FrdcStats st = b::frdc_stats(T);
+    CHECK(st.nnz_tiles == 10 && st.nnz_bits == 10 && st.fill_ratio == 10.0 / 160.0);
+  }
+
   // layer failures: std::runtime_error("layer i (kind): ...") (graphops.cpp:476-479)
   b::DenseMatrix Xbad = random_dense(&r, n, 69);
   CHECK(throws<std::runtime_error>([&] { b::run_model(m, Xbad); }, "layer 0 (gcn_conv): "));

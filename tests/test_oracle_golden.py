@@ -214,3 +214,88 @@ def test_oracle_matches_reference_random(model, seed):
     assert [a.label for a in p] == [b.label for b in rp]
     assert all(np.array_equal(a.bits, b.bits) for a, b in zip(p, rp))
     assert np.array_equal(l, rl) and np.array_equal(o, ro)
+
+
+# ------------------------------------------------------------- tile sets -----
+def _ten_tile_row():
+    # ref: test_bitsparse.cpp:131-135 -- node 0 -> nodes 0, 4, ..., 36
+    return po.frdc_from_edges(40, np.zeros(10, np.int64), 4 * np.arange(10, dtype=np.int64), False)
+
+
+def test_tileset_kat_ten_tiles():
+    # ref: test_bitsparse.cpp:131-161
+    m = _ten_tile_row()
+    assert m.nnz == 10
+    assert po.tileset_count(m, 0, 32) == 2 and po.tileset_count(m, 0, 64) == 1
+    assert po.tileset_count(m, 1, 32) == 0
+    ts0, r0, c0 = po.gather_tileset(m, 0, 0, 32)
+    ts1, r1, c1 = po.gather_tileset(m, 0, 1, 32)
+    assert ts0 == 8 and c0[:8] == list(range(8))
+    assert c1[0] == 8 and c1[1] == 9 and sum(c == po.PAD_COL for c in c1[2:8]) == 6
+    assert r0[0] == 0x88888888 and r1[0] == 0x88000000 and r1[1] == 0
+    tsw, rw, cw = po.gather_tileset(m, 0, 0, 64)
+    assert tsw == 16 and rw[0] == 0x8888888888000000 and cw[10] == po.PAD_COL
+
+
+@pytest.mark.parametrize("args,msg", [((0, 0, 16), "word_bits must be 32 or 64"),
+                                      ((10, 0, 32), "tile_row out of range"),
+                                      ((-1, 0, 32), "tile_row out of range"),
+                                      ((0, 2, 32), "set_index out of range"),
+                                      ((1, 0, 32), "set_index out of range")])
+def test_gather_tileset_rejects_like_the_reference(args, msg):
+    # ref: bitsparse.cpp:137-143
+    with pytest.raises(ValueError, match=msg):
+        po.gather_tileset(_ten_tile_row(), *args)
+
+
+@pytest.mark.parametrize("word_bits", [32, 64])
+def test_gather_reassembles_the_stored_tile_bits(word_bits):
+    # ref: test_bitsparse.cpp:163-197 -- every assembled bit against frdc_to_dense
+    rng = po.Rng(7)
+    for it in range(25):
+        n = 1 + rng.index(120)
+        m_edges = rng.index(6 * n + 1)
+        src, dst = rng.random_edges(n, m_edges, True)
+        m = po.frdc_from_edges(n, src, dst, False)
+        dense = po.frdc_to_dense(m)
+        ts = word_bits // 4
+        for tr in range((n + 3) // 4):
+            for s in range(po.tileset_count(m, tr, word_bits)):
+                g_ts, rows, cols = po.gather_tileset(m, tr, s, word_bits)
+                assert g_ts == ts
+                for slot in range(ts):
+                    tc = cols[slot]
+                    for r in range(4):
+                        for c in range(4):
+                            got = (rows[r] >> (word_bits - 1 - (4 * slot + c))) & 1
+                            gi, gj = 4 * tr + r, (-1 if tc == po.PAD_COL else 4 * tc + c)
+                            want = gj >= 0 and gi < n and gj < n and \
+                                (int(dense[gi, gj // 32]) >> (31 - gj % 32)) & 1
+                            assert got == int(bool(want))
+
+
+def test_frdc_to_dense_matches_edge_set():
+    rng = po.Rng(3)
+    n = 77
+    src, dst = rng.random_edges(n, 300, True)
+    m = po.frdc_from_edges(n, src, dst, True)
+    d = po.frdc_to_dense(m, 64)
+    assert d.shape == (n, po.spw(n, 64))
+    want = set(zip(src.tolist(), dst.tolist())) | {(i, i) for i in range(n)}
+    got = {(i, j) for i in range(n) for j in range(n) if (int(d[i, j // 32]) >> (31 - j % 32)) & 1}
+    assert got == want
+
+
+@pytest.mark.skipif(not po.ref_available(), reason="oracle/_ref not built")
+def test_tileset_oracle_matches_reference_library():
+    # the real reference's gather_tileset / frdc_to_dense through oracle/_ref
+    rng = po.Rng(11)
+    for it in range(6):
+        n = 5 + rng.index(200)
+        src, dst = rng.random_edges(n, rng.index(8 * n + 1), True)
+        m = po.frdc_from_edges(n, src, dst, False)
+        for wb in (32, 64):
+            assert np.array_equal(po.frdc_to_dense(m, wb), po.ref_frdc_to_dense(m, wb))
+            for tr in range((n + 3) // 4):
+                for s in range(po.tileset_count(m, tr, wb)):
+                    assert po.gather_tileset(m, tr, s, wb) == po.ref_gather_tileset(m, tr, s, wb)
