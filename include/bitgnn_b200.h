@@ -344,6 +344,42 @@ int bg_trace_size(const bg_trace* t);
 int bg_trace_point(const bg_trace* t, int i, const char** label, int64_t* rows, int64_t* cols,
                    int* word_bits, const uint32_t** bits);
 
+/* ---- verification (ref: verify_model / VerifyReport, runreport.hpp:13-31,
+ * runreport.cpp:51-135) -----------------------------------------------------
+ * The engine's BIN points and logits against a reference run supplied by the
+ * caller (the dense oracle, the reference engine, a recorded trace), compared
+ * on the device: bit mismatches over the valid columns with the first one
+ * (label, row, col) in trace order, max |e - o| / max(1, |o|), and argmax
+ * agreement with the reference's exact-tie rule; pass = no mismatch, full
+ * agreement, max_rel <= tolerance.  compare_bits = 0 is the reference's
+ * full-precision mode (no BIN points compared).  A trace of another length or
+ * a misaligned point is BG_LOGIC_ERROR with the reference's message. */
+typedef struct bg_verify_report {
+  double max_rel_logit_error;
+  int64_t bin_points, bin_values, bin_mismatches;
+  char first_mismatch_label[64];
+  int64_t first_mismatch_row, first_mismatch_col; /* -1 when no mismatch */
+  double argmax_agreement;
+  double tolerance;
+  int32_t pass;
+} bg_verify_report;
+typedef struct bg_ref_point { /* one reference BIN point, HOST packed bits */
+  const char* label;
+  int64_t rows, cols;
+  int32_t word_bits;
+  const uint32_t* bits; /* rows x bg_storage_words_per_row(cols, word_bits) */
+} bg_ref_point;
+/* A recorded engine trace + DEVICE logits (rows x cols) vs the reference
+ * (ref_logits: HOST double rows x cols). */
+int bg_verify_trace(const bg_trace* engine, const float* engine_logits, int64_t rows, int64_t cols,
+                    const bg_ref_point* ref, int n_ref, const double* ref_logits, int compare_bits,
+                    double tolerance, bg_verify_report* out, bg_stream stream);
+/* Traced forward of `m` on x0 (device), then bg_verify_trace against the
+ * reference (ref_logits HOST double ref_rows x ref_cols). */
+int bg_model_verify(bg_model* m, const bg_mat* x0, const bg_ref_point* ref, int n_ref, const double* ref_logits,
+                    int64_t ref_rows, int64_t ref_cols, int compare_bits, double tolerance,
+                    bg_verify_report* out, bg_stream stream);
+
 /* Per-kernel timing (ref: KernelTiming + record_ns hooks, graphops.cpp:53-84),
  * measured with CUDA events on `stream`. */
 typedef struct bg_kernel_timing {

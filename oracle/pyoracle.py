@@ -719,6 +719,51 @@ def ref_layer_run(graph: "RefGraph", layer, x, word_bits: int = 32, prefix: str 
     return res, points
 
 
+def ref_oracle_run(graph: "RefGraph", model: "RefModel", full_precision: bool = False, word_bits: int = 32):
+    """The reference's dense oracle::run_model (oracle.cpp:194-317): (trace
+    points as packed sign bits, logits float64).  O(N^2) memory: small graphs."""
+    L = ref()
+    L.ref_oracle_run.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _TRACE_FN, C.c_void_p,
+                                 C.POINTER(C.POINTER(C.c_double)), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    L.ref_free.argtypes = [C.c_void_p]
+    points: List[TracePoint] = []
+
+    def sink(_ctx, label, bits, r, c, wb):
+        n = r * spw(c, wb)
+        a = np.ctypeslib.as_array(bits, shape=(n,)).reshape(r, -1).copy() if n else \
+            np.zeros((r, spw(c, wb)), np.uint32)
+        points.append(TracePoint(label.decode(), a, r, c, wb))
+
+    cb = _TRACE_FN(sink)
+    lp, r, c = C.POINTER(C.c_double)(), C.c_int64(), C.c_int64()
+    if L.ref_oracle_run(graph.h, model.h, int(full_precision), word_bits, cb, None, C.byref(lp), C.byref(r),
+                        C.byref(c)):
+        raise ValueError(L.ref_error().decode())
+    n = r.value * c.value
+    lg = np.ctypeslib.as_array(lp, shape=(max(n, 1),))[:n].reshape(r.value, c.value).copy()
+    L.ref_free(C.cast(lp, C.c_void_p))
+    return points, lg
+
+
+def ref_verify_model(graph: "RefGraph", model: "RefModel", full_precision: bool = False,
+                     tolerance: float = 1e-6, corrupt_tile: int = -1) -> dict:
+    """The reference's own verify_model (runreport.cpp:51-135) report."""
+    L = ref()
+    L.ref_verify_model.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_int64,
+                                   C.POINTER(C.c_double), C.c_void_p, C.c_char_p, C.c_int,
+                                   C.POINTER(C.c_double), C.POINTER(C.c_int)]
+    mr, ag, ok = C.c_double(), C.c_double(), C.c_int()
+    counts = np.zeros(5, np.int64)
+    lab = C.create_string_buffer(128)
+    if L.ref_verify_model(graph.h, model.h, int(full_precision), tolerance, corrupt_tile, C.byref(mr),
+                          _ptr(counts), lab, 128, C.byref(ag), C.byref(ok)):
+        raise ValueError(L.ref_error().decode())
+    return {"max_rel_logit_error": mr.value, "bin_points": int(counts[0]), "bin_values": int(counts[1]),
+            "bin_mismatches": int(counts[2]), "first_mismatch_row": int(counts[3]),
+            "first_mismatch_col": int(counts[4]), "first_mismatch_label": lab.value.decode(),
+            "argmax_agreement": ag.value, "pass": bool(ok.value)}
+
+
 def ref_read_graph(kind: int, text, name: str = "<stream>", forced_nodes: int = -1, undirected: bool = False):
     """The reference's graphio readers (kind 0 read_edge_list, 1
     read_matrix_market, 2 load_graph(path=text)).  Returns (node_count, src,

@@ -26,6 +26,7 @@
 #include "bitgnn/kernelbench.hpp"
 #include "bitgnn/kernels.hpp"
 #include "bitgnn/modelconfig.hpp"
+#include "bitgnn/oracle.hpp"
 #include "bitgnn/rng.hpp"
 #include "bitgnn/runreport.hpp"
 #include "bitgnn/tune.hpp"
@@ -533,6 +534,67 @@ int ref_layer_run(void* graph, const ref_layer* d, int word_bits, int x_prec, co
       for (int64_t i = 0; i < b.rows(); ++i)
         std::memcpy(static_cast<uint32_t*>(*out) + i * w, b.row_span(i).data(), static_cast<size_t>(w) * 4);
     }
+    return 0;
+  } catch (const std::exception& ex) {
+    return guard(ex);
+  }
+}
+
+// The reference's dense oracle (oracle.cpp:194-317) on a built model and the
+// graph's edges: BIN points as packed bits (sign > 0 -> 1, the comparison of
+// runreport.cpp:92-93) through the trace callback, logits in double
+// (malloc'd, free with ref_free).  full_precision selects Mode::FullPrecision.
+int ref_oracle_run(void* graph, void* model, int full_precision, int word_bits, ref_trace_fn trace, void* ctx,
+                   double** logits, int64_t* rows, int64_t* cols) {
+  try {
+    auto* g = static_cast<RefGraph*>(graph);
+    auto* m = static_cast<RefModel*>(model);
+    oracle::Config cfg;
+    cfg.mode = full_precision ? oracle::Config::Mode::FullPrecision : oracle::Config::Mode::SimulatedBinarization;
+    oracle::GraphDense gd = oracle::graph_from_edges(g->edges);
+    oracle::Trace tr;
+    oracle::run_model(m->bm.spec, oracle::Mat::from(m->bm.features), gd, cfg, &tr);
+    if (trace)
+      for (const auto& p : tr.points) {
+        BitDenseMatrix b(p.signs.rows, p.signs.cols, BitSemantics::PlusMinus, word_bits);
+        for (int64_t i = 0; i < p.signs.rows; ++i)
+          for (int64_t j = 0; j < p.signs.cols; ++j) b.set_bit(i, j, p.signs.at(i, j) > 0);
+        const int64_t w = b.storage_words_per_row();
+        std::vector<uint32_t> words(static_cast<size_t>(b.rows() * w));
+        for (int64_t r = 0; r < b.rows(); ++r) std::memcpy(words.data() + r * w, b.row_span(r).data(), static_cast<size_t>(w) * 4);
+        trace(ctx, p.label.c_str(), words.data(), b.rows(), b.cols(), word_bits);
+      }
+    *rows = tr.logits.rows;
+    *cols = tr.logits.cols;
+    *logits = static_cast<double*>(std::malloc(std::max<size_t>(tr.logits.v.size() * 8, 8)));
+    if (!tr.logits.v.empty()) std::memcpy(*logits, tr.logits.v.data(), tr.logits.v.size() * 8);
+    return 0;
+  } catch (const std::exception& ex) {
+    return guard(ex);
+  }
+}
+
+// The reference's own verify_model (runreport.cpp:51-135), report fields out.
+int ref_verify_model(void* graph, void* model, int full_precision, double tolerance, int64_t corrupt_tile,
+                     double* max_rel, int64_t* counts /* points, values, mismatches, row, col */, char* label,
+                     int label_len, double* agreement, int* pass) {
+  try {
+    auto* g = static_cast<RefGraph*>(graph);
+    auto* m = static_cast<RefModel*>(model);
+    oracle::Config cfg;
+    cfg.mode = full_precision ? oracle::Config::Mode::FullPrecision : oracle::Config::Mode::SimulatedBinarization;
+    cfg.tolerance = tolerance;
+    VerifyReport r = verify_model(m->bm.spec, m->bm.features, g->edges, cfg, corrupt_tile);
+    *max_rel = r.max_rel_logit_error;
+    counts[0] = r.bin_points;
+    counts[1] = r.bin_values;
+    counts[2] = r.bin_mismatches;
+    counts[3] = r.first_mismatch_row;
+    counts[4] = r.first_mismatch_col;
+    std::strncpy(label, r.first_mismatch_label.c_str(), static_cast<size_t>(label_len - 1));
+    label[label_len - 1] = 0;
+    *agreement = r.argmax_agreement;
+    *pass = r.pass ? 1 : 0;
     return 0;
   } catch (const std::exception& ex) {
     return guard(ex);

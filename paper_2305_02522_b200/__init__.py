@@ -16,5 +16,6 @@ from .bitgnn import (AdjacencyOperand, BitDenseMatrix, BitOperand, FrdcMatrix,  
                      load_graph, read_edge_list, read_matrix_market,
                      prepare_graph, rewrite_eliminate_scl, run_model, transpose, unpack, validate_model,
                      TileSet, FrdcStats, gather_tileset, gather_tilesets, tileset_count, frdc_to_dense,
-                     frdc_stats, gcn_layer, sage_layer, graphconv_layer)
+                     frdc_stats, gcn_layer, sage_layer, graphconv_layer,
+                     VerifyReport, verify_model)
 from ._lib import (B, F, CudaError, InvalidArgument, LogicError, RuntimeFailure)  # noqa: E402,F401

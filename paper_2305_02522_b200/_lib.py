@@ -67,6 +67,18 @@ class FrdcStatsC(C.Structure):
                 ("fill_ratio", C.c_double)]
 
 
+class VerifyReportC(C.Structure):
+    _fields_ = [("max_rel_logit_error", C.c_double), ("bin_points", C.c_int64), ("bin_values", C.c_int64),
+                ("bin_mismatches", C.c_int64), ("first_mismatch_label", C.c_char * 64),
+                ("first_mismatch_row", C.c_int64), ("first_mismatch_col", C.c_int64),
+                ("argmax_agreement", C.c_double), ("tolerance", C.c_double), ("pass_", C.c_int32)]
+
+
+class RefPointC(C.Structure):
+    _fields_ = [("label", C.c_char_p), ("rows", C.c_int64), ("cols", C.c_int64), ("word_bits", C.c_int32),
+                ("bits", C.c_void_p)]
+
+
 class KernelTiming(C.Structure):
     _fields_ = [("label", C.c_char * 64), ("ms", C.c_double)]
 
@@ -156,6 +168,10 @@ PROTOTYPES = {
     "bg_trace_size": (I32, [P]),
     "bg_trace_point": (I32, [P, I32, C.POINTER(C.c_char_p), PI64, PI64, C.POINTER(C.c_int),
                              C.POINTER(P)]),
+    "bg_verify_trace": (I32, [P, P, I64, I64, C.POINTER(RefPointC), I32, P, I32, C.c_double,
+                              C.POINTER(VerifyReportC), P]),
+    "bg_model_verify": (I32, [P, C.POINTER(Mat), C.POINTER(RefPointC), I32, P, I64, I64, I32, C.c_double,
+                              C.POINTER(VerifyReportC), P]),
     "bg_model_forward_timed": (I32, [P, C.POINTER(Mat), P, P, C.POINTER(KernelTiming), I32,
                                      C.POINTER(C.c_int), P]),
     "bg_partition_rows": (I32, [P, I32, I32, PI64, PI64]),

@@ -866,6 +866,56 @@ def graphconv_layer(x: MatOperand, l: LayerSpec, g: GraphBundle, strategy: Optio
     return _layer(L.LAYER_GRAPHCONV, lib().bg_graphconv_layer, x, l, g, strategy, trace, prefix, word_bits)
 
 
+@dataclass
+class VerifyReport:
+    """runreport.hpp:13-25"""
+    max_rel_logit_error: float = 0.0
+    bin_points: int = 0
+    bin_values: int = 0
+    bin_mismatches: int = 0
+    first_mismatch_label: str = ""
+    first_mismatch_row: int = -1
+    first_mismatch_col: int = -1
+    argmax_agreement: float = 0.0
+    tolerance: float = 1e-6
+    passed: bool = False
+
+    def to_dict(self) -> dict:
+        """The fields of VerifyReport::to_json (runreport.cpp:137-152)."""
+        d = {"max_rel_logit_error": self.max_rel_logit_error, "tolerance": self.tolerance,
+             "bin_points": self.bin_points, "bin_values": self.bin_values,
+             "bin_mismatches": self.bin_mismatches}
+        if self.bin_mismatches > 0:
+            d["first_mismatch"] = {"label": self.first_mismatch_label, "row": self.first_mismatch_row,
+                                   "col": self.first_mismatch_col}
+        d.update(argmax_agreement=self.argmax_agreement, **{"pass": self.passed})
+        return d
+
+
+def verify_model(model: Model, x0: MatOperand, ref_points: Sequence, ref_logits: np.ndarray,
+                 tolerance: float = 1e-6, compare_bits: bool = True) -> VerifyReport:
+    """runreport.cpp:51-135 on the device: a traced forward of `model`
+    compared with a reference run -- ref_points (objects with label, bits
+    [rows, spw] u32, rows, cols, word_bits, in trace order) and ref_logits
+    (rows x cols, compared in double).  compare_bits=False is the
+    reference's full-precision mode.  Misaligned traces raise LogicError."""
+    cx = _mat(x0)
+    keep = []
+    arr = (L.RefPointC * max(len(ref_points), 1))()
+    for i, p in enumerate(ref_points):
+        b = np.ascontiguousarray(p.bits, dtype=np.uint32)
+        lab = p.label.encode()
+        keep += [b, lab]
+        arr[i] = L.RefPointC(lab, p.rows, p.cols, p.word_bits, b.ctypes.data)
+    lg = np.ascontiguousarray(ref_logits, dtype=np.float64)
+    r = L.VerifyReportC()
+    check(lib().bg_model_verify(model._h, C.byref(cx), arr, len(ref_points), lg.ctypes.data, lg.shape[0],
+                                lg.shape[1], int(compare_bits), tolerance, C.byref(r), _stream()))
+    return VerifyReport(r.max_rel_logit_error, r.bin_points, r.bin_values, r.bin_mismatches,
+                        r.first_mismatch_label.decode(), r.first_mismatch_row, r.first_mismatch_col,
+                        r.argmax_agreement, r.tolerance, bool(r.pass_))
+
+
 def run_model(model: Model, x0: MatOperand, trace: bool = False):
     """graphops.cpp:390-484 -- returns the final output (and the trace)."""
     if trace:

@@ -47,6 +47,13 @@ void copy_out(const Op& r, bg_mat* out, cudaStream_t s) {
 
 void sync(cudaStream_t s) { BG_CUDA(cudaStreamSynchronize(s)); }
 
+// Changes whenever either adjacency of the graph rebuilds a view (or is
+// corrupted by the fault hook): captured forwards are then re-recorded.
+uint64_t graph_generation(const bg_graph* g) {
+  if (!g) return 0;
+  return (g->structure ? g->structure->gen : 0) * 0x9E3779B97F4A7C15ull + (g->raw ? g->raw->gen : 0);
+}
+
 }  // namespace
 }  // namespace bg
 
@@ -590,6 +597,7 @@ int bg_model_forward(bg_model* m, const bg_mat* x0, float* out, float* logits, b
     // may have grown a slot since the capture: pool_gen then differs and the
     // graph, which holds the old pointers, is re-recorded.
     k.pool_gen = m->pool.gen;
+    k.graph_gen = graph_generation(m->graph);
     if (m->exec && k == m->key) {
       BG_CUDA(cudaGraphLaunch(m->exec, st));
       return;
@@ -603,6 +611,7 @@ int bg_model_forward(bg_model* m, const bg_mat* x0, float* out, float* logits, b
       forward_impl(*m, x, out, logits, nullptr, nullptr, st);
       m->key = k;
       m->key.pool_gen = m->pool.gen;
+      m->key.graph_gen = graph_generation(m->graph);
       return;
     }
     // Second run with the same binding: capture and replay from now on.

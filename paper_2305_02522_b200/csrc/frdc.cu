@@ -222,6 +222,7 @@ unsigned grid1(int64_t n, int bs = 256) { return static_cast<unsigned>(cdiv(n, b
 
 void frdc_finalize(bg_frdc& m, cudaStream_t s) {
   m.nslivers = -1;  // derived views are rebuilt on next use
+  ++m.gen;
   m.win.T = 0;
   m.nbits_view = -1;
   m.degree.alloc(static_cast<size_t>(std::max<int64_t>(m.rows, 1)) * 4);
@@ -286,6 +287,7 @@ void frdc_slivers(bg_frdc& m, cudaStream_t s) {
   BG_LAUNCH_CHECK();
   BG_CUDA(cudaStreamSynchronize(s));
   m.nslivers = static_cast<int64_t>(total);
+  ++m.gen;
   m.max_sl_row = hm[0];
   m.max_extra_bits = hm[1];
 }

@@ -75,10 +75,11 @@ struct bg_model {
     cudaStream_t s = nullptr;
     uint64_t agg_gen = 0;  // aggregation layout settings the graph was recorded with
     uint64_t pool_gen = 0;  // pool allocation state the graph's pointers come from
+    uint64_t graph_gen = 0;  // FRDC views the graph's pointers come from
     bool operator==(const Key& o) const {
       return x == o.x && rows == o.rows && cols == o.cols && prec == o.prec && wb == o.wb &&
              out == o.out && logits == o.logits && s == o.s && agg_gen == o.agg_gen &&
-             pool_gen == o.pool_gen;
+             pool_gen == o.pool_gen && graph_gen == o.graph_gen;
     }
   } key;
   int key_runs = 0;

@@ -18,6 +18,10 @@ struct bg_frdc {
   // (tile k of a tile row goes to lane k % 32) -- sizes the bit-sliced
   // counters of the aggregation kernels.  Index: 0 -> G=4, 1 -> G=8.
   int64_t max_slot[2] = {0, 0};
+  // Bumped whenever the arrays change (finalize) or a derived view below is
+  // (re)built: a CUDA graph captured over the views' pointers is valid only
+  // while gen is unchanged.
+  uint64_t gen = 0;
   bg::DevBuf row_ptr;  // u64[tile_rows + 1]
   bg::DevBuf col_ind;  // u32[nnz]
   bg::DevBuf tiles;    // u16[nnz]

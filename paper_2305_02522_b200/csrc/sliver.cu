@@ -638,6 +638,7 @@ void frdc_bitview(bg_frdc& m, cudaStream_t s) {
   BG_LAUNCH_CHECK();
   BG_CUDA(cudaStreamSynchronize(s));
   m.nbits_view = static_cast<int64_t>(total);
+  ++m.gen;
 }
 
 }  // namespace bg

@@ -675,6 +675,7 @@ void build_windows(bg_frdc& A, int RB, int RW, int Wh, cudaStream_t s) {
   BG_LAUNCH_CHECK();
   BG_CUDA(cudaStreamSynchronize(s));
   W.T = RB;
+  ++A.gen;
   W.rw = RW;
   W.Wn = Wh;
   W.nw = nh;

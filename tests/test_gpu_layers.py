@@ -27,7 +27,7 @@ CASES = [  # (kind, plan, input F?, hidden, relu)
     (GCN, ["MM.BBB", "BSpMM.BBF"], False, 33, True),
     (SAGE, ["MM.FBB", "MM.FBB", "BSpMM.BBB", "ADD.BBF"], True, 64, True),
     (SAGE, ["MM.FBF", "MM.FBF", "BSpMM.FFF", "ADD.FFF"], True, 16, True),
-    (SAGE, ["MM.FBB", "MM.FBB", "BSpMM.BBF", "ADD.FFF"], True, 20, False),
+    (SAGE, ["MM.FBF", "MM.FBB", "BSpMM.BBF", "ADD.FFF"], True, 20, False),
     (SAGE, ["MM.BBB", "MM.BBB", "BSpMM.BBB", "ADD.BBB"], False, 32, False),
     (GRAPHCONV, ["MM.FBB", "MM.FBB", "BSpMM.BFB", "ADD.BBF"], True, 48, True),
     (GRAPHCONV, ["MM.FBF", "MM.FBB", "BSpMM.BBF", "ADD.FFF"], True, 12, False),
