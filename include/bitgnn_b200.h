@@ -409,11 +409,30 @@ typedef struct bg_comm bg_comm; /* NCCL communicator, one rank per GPU */
 int bg_comm_unique_id(uint8_t* id, size_t id_len);
 int bg_comm_create(int world_size, int rank, const uint8_t* id, size_t id_len, bg_comm** out);
 void bg_comm_destroy(bg_comm* c);
+/* An exchange through the caller's transport instead of NCCL (tests, hosts
+ * without NVLink peers): before each neighbour aggregation the engine
+ * synchronizes `stream` and calls fn(ctx, buf, row_bytes, bounds, world, rank,
+ * stream) on the host.  buf is a DEVICE buffer of bounds[world] rows of
+ * row_bytes, rows [bounds[rank], bounds[rank+1]) produced by this rank; fn
+ * must fill every other rank's rows and return 0 (nonzero fails the forward
+ * with BG_RUNTIME_ERROR).  A forward using it is never graph-captured. */
+typedef int (*bg_allgather_fn)(void* ctx, void* buf, int64_t row_bytes, const int64_t* bounds, int world_size,
+                               int rank, bg_stream stream);
+int bg_comm_create_external(int world_size, int rank, bg_allgather_fn fn, void* ctx, bg_comm** out);
+
+/* A rank's share of a prepared graph: both adjacency structures cut to node
+ * rows [row_begin, row_end) (whole tile rows: multiples of 4, or the node
+ * count), the per-node scale vectors kept whole.  The source graph may be
+ * destroyed afterwards, so a rank holds FRDC/world of the adjacency.  A model
+ * on a shard runs bg_model_forward_sharded for that rank's range only. */
+int bg_graph_shard(const bg_graph* g, int64_t row_begin, int64_t row_end, bg_graph** out, bg_stream stream);
 
 /* Sharded ref: run_model.  With a communicator, x/out/logits hold this
  * rank's rows [bounds[rank], bounds[rank+1]) only.  With comm == NULL every
  * rank's range is computed in this process on this device ("virtual ranks",
- * x/out/logits full size) -- the same per-range kernels, no exchange. */
+ * x/out/logits full size) -- the same per-range kernels, no exchange.  With
+ * an NCCL communicator on a non-default stream the forward is captured as
+ * one CUDA graph from its second call with the same binding. */
 int bg_model_forward_sharded(bg_model* m, bg_comm* comm, const bg_mat* x, const int64_t* bounds,
                              int world_size, int rank, float* out, float* logits,
                              bg_stream stream);

@@ -179,6 +179,8 @@ PROTOTYPES = {
     "bg_comm_unique_id": (I32, [P, C.c_size_t]),
     "bg_comm_create": (I32, [I32, I32, P, C.c_size_t, C.POINTER(P)]),
     "bg_comm_destroy": (None, [P]),
+    "bg_comm_create_external": (I32, [I32, I32, P, P, C.POINTER(P)]),
+    "bg_graph_shard": (I32, [P, I64, I64, C.POINTER(P), P]),
     "bg_model_forward_sharded": (I32, [P, P, C.POINTER(Mat), P, I32, I32, P, P, P]),
     "bg_model_forward_sharded_timed": (I32, [P, P, C.POINTER(Mat), P, I32, I32, P, C.POINTER(KernelTiming), I32,
                                              C.POINTER(I32), P]),

@@ -508,6 +508,15 @@ class GraphBundle:
     def corrupt_tile(self, k: int) -> None:
         check(lib().bg_graph_corrupt_tile(self._h, k))
 
+    def shard(self, row_begin: int, row_end: int) -> "GraphBundle":
+        """This rank's share: both structures cut to node rows [row_begin,
+        row_end) (whole tile rows), the scale vectors whole (bg_graph_shard)."""
+        h = C.c_void_p()
+        check(lib().bg_graph_shard(self._h, row_begin, row_end, C.byref(h), _stream()))
+        g = GraphBundle(h.value)
+        g.row0 = row_begin
+        return g
+
     def partition_rows(self, world_size: int, rank: int) -> Tuple[int, int]:
         a, b = C.c_int64(), C.c_int64()
         check(lib().bg_partition_rows(self._h, world_size, rank, C.byref(a), C.byref(b)))

@@ -47,6 +47,13 @@ void copy_out(const Op& r, bg_mat* out, cudaStream_t s) {
 
 void sync(cudaStream_t s) { BG_CUDA(cudaStreamSynchronize(s)); }
 
+
+
+}  // namespace
+}  // namespace bg
+
+namespace bg {
+
 // Changes whenever either adjacency of the graph rebuilds a view (or is
 // corrupted by the fault hook): captured forwards are then re-recorded.
 uint64_t graph_generation(const bg_graph* g) {
@@ -54,7 +61,43 @@ uint64_t graph_generation(const bg_graph* g) {
   return (g->structure ? g->structure->gen : 0) * 0x9E3779B97F4A7C15ull + (g->raw ? g->raw->gen : 0);
 }
 
-}  // namespace
+void run_captured(bg_model& m, bg_model::CaptureSlot& slot, bg_model::Key k, cudaStream_t st,
+                  const std::function<void()>& run) {
+  k.agg_gen = aggregation_generation();
+  // Any other entry point sharing the pool (traced, timed, host, the other
+  // slot) may have grown a slot since the capture: pool_gen then differs and
+  // the graph, which holds the old pointers, is re-recorded.
+  k.pool_gen = m.pool.gen;
+  k.graph_gen = graph_generation(m.graph);
+  if (slot.exec && k == slot.key) {
+    BG_CUDA(cudaGraphLaunch(slot.exec, st));
+    return;
+  }
+  if (!(k == slot.key)) {
+    // First run with this binding: eager, which also sizes the pool.
+    slot.reset();
+    run();
+    slot.key = k;
+    slot.key.pool_gen = m.pool.gen;
+    slot.key.graph_gen = graph_generation(m.graph);
+    return;
+  }
+  // Second run with the same binding: capture and replay from now on.
+  cudaGraph_t graph = nullptr;
+  BG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  try {
+    run();
+  } catch (...) {
+    cudaStreamEndCapture(st, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  BG_CUDA(cudaStreamEndCapture(st, &graph));
+  BG_CUDA(cudaGraphInstantiate(&slot.exec, graph, 0));
+  cudaGraphDestroy(graph);
+  BG_CUDA(cudaGraphLaunch(slot.exec, st));
+}
+
 }  // namespace bg
 
 using namespace bg;
@@ -455,7 +498,10 @@ int bg_layer_out_desc(int kind, const bg_layer_desc* l, const bg_mat* x, int wor
     const int slot = kind == BG_LAYER_GCN ? 1 : 3;
     if (kind != BG_LAYER_GCN && kind != BG_LAYER_SAGE && kind != BG_LAYER_GRAPHCONV)
       fail("layer_out_desc: kind must be gcn_conv, sage_conv or graph_conv");
-    if (l->n_plan <= slot || !l->w1) fail("layer_out_desc: plan or weights missing");
+    // the layer functions' own slot checks (graphops.cpp:273, :292-294)
+    if (kind == BG_LAYER_GCN && (l->n_plan != 2 || !l->w1)) fail("gcn_conv: expected {mm, spmm} plan and weights");
+    if (kind != BG_LAYER_GCN && (l->n_plan != 4 || !l->w1 || !l->w2))
+      fail("expected {mm_self, mm_neigh, spmm, add} plan and two weight matrices");
     std::memset(out, 0, sizeof *out);
     out->precision = l->plan[slot].out;
     out->rows = x->rows;
@@ -566,11 +612,10 @@ int bg_model_set_graph_capture(bg_model* m, int enable) {
   return guard([&] {
     need(m, "model");
     m->capture = enable != 0;
-    if (!m->capture && m->exec) {
-      cudaGraphExecDestroy(m->exec);
-      m->exec = nullptr;
+    if (!m->capture) {
+      m->fwd.reset();
+      m->sharded.reset();
     }
-    m->key_runs = 0;
   });
 }
 
@@ -579,8 +624,9 @@ int bg_model_forward(bg_model* m, const bg_mat* x0, float* out, float* logits, b
     need(m, "model");
     const Op x = op_from_mat(x0);
     cudaStream_t st = S(s);
+    auto run = [&] { forward_impl(*m, x, out, logits, nullptr, nullptr, st); };
     if (!m->capture || st == nullptr) {
-      forward_impl(*m, x, out, logits, nullptr, nullptr, st);
+      run();
       return;
     }
     bg_model::Key k;
@@ -592,42 +638,7 @@ int bg_model_forward(bg_model* m, const bg_mat* x0, float* out, float* logits, b
     k.out = out;
     k.logits = logits;
     k.s = st;
-    k.agg_gen = aggregation_generation();
-    // Any other entry point sharing the pool (traced, timed, host, sharded)
-    // may have grown a slot since the capture: pool_gen then differs and the
-    // graph, which holds the old pointers, is re-recorded.
-    k.pool_gen = m->pool.gen;
-    k.graph_gen = graph_generation(m->graph);
-    if (m->exec && k == m->key) {
-      BG_CUDA(cudaGraphLaunch(m->exec, st));
-      return;
-    }
-    if (!(k == m->key)) {
-      // First run with this binding: eager, which also sizes the pool.
-      if (m->exec) {
-        cudaGraphExecDestroy(m->exec);
-        m->exec = nullptr;
-      }
-      forward_impl(*m, x, out, logits, nullptr, nullptr, st);
-      m->key = k;
-      m->key.pool_gen = m->pool.gen;
-      m->key.graph_gen = graph_generation(m->graph);
-      return;
-    }
-    // Second run with the same binding: capture and replay from now on.
-    cudaGraph_t graph = nullptr;
-    BG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    try {
-      forward_impl(*m, x, out, logits, nullptr, nullptr, st);
-    } catch (...) {
-      cudaStreamEndCapture(st, &graph);
-      if (graph) cudaGraphDestroy(graph);
-      throw;
-    }
-    BG_CUDA(cudaStreamEndCapture(st, &graph));
-    BG_CUDA(cudaGraphInstantiate(&m->exec, graph, 0));
-    cudaGraphDestroy(graph);
-    BG_CUDA(cudaGraphLaunch(m->exec, st));
+    run_captured(*m, m->fwd, k, st, run);
   });
 }
 

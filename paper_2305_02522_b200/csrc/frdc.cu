@@ -438,6 +438,69 @@ std::unique_ptr<bg_frdc> frdc_from_host(int64_t rows, int64_t cols, const uint64
   return m;
 }
 
+namespace {
+__global__ void k_rebase(const uint64_t* __restrict__ rp, int64_t n, uint64_t base, uint64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = rp[i] - base;
+}
+}  // namespace
+
+// Node rows [row0, row1) of A as a standalone FRDC (rows row1-row0, the same
+// columns): row0 is a multiple of 4, row1 too unless it is A.rows, so the
+// slice is whole tile rows -- row_ptr rebased, col_ind / tiles copied.
+std::unique_ptr<bg_frdc> frdc_slice(const bg_frdc& A, int64_t row0, int64_t row1, cudaStream_t s) {
+  if (row0 < 0 || row1 < row0 || row1 > A.rows || row0 % 4 || (row1 % 4 && row1 != A.rows))
+    fail("FRDC slice: rows must be whole tile rows inside the matrix");
+  const int64_t t0 = row0 / 4, t1 = cdiv(row1, 4);
+  uint64_t ends[2] = {0, 0};
+  BG_CUDA(cudaMemcpyAsync(&ends[0], A.rp() + t0, 8, cudaMemcpyDeviceToHost, s));
+  BG_CUDA(cudaMemcpyAsync(&ends[1], A.rp() + t1, 8, cudaMemcpyDeviceToHost, s));
+  BG_CUDA(cudaStreamSynchronize(s));
+  auto m = std::make_unique<bg_frdc>();
+  m->rows = row1 - row0;
+  m->cols = A.cols;
+  m->tile_rows = t1 - t0;
+  m->tile_cols = A.tile_cols;
+  m->nnz = static_cast<int64_t>(ends[1] - ends[0]);
+  m->row_ptr.alloc(static_cast<size_t>(m->tile_rows + 1) * 8);
+  m->col_ind.alloc(static_cast<size_t>(std::max<int64_t>(m->nnz, 1)) * 4);
+  m->tiles.alloc(static_cast<size_t>(std::max<int64_t>(m->nnz, 1)) * 2);
+  k_rebase<<<grid1(m->tile_rows + 1), 256, 0, s>>>(A.rp() + t0, m->tile_rows + 1, ends[0], m->row_ptr.as<uint64_t>());
+  BG_LAUNCH_CHECK();
+  if (m->nnz) {
+    BG_CUDA(cudaMemcpyAsync(m->col_ind.p, A.ci() + ends[0], static_cast<size_t>(m->nnz) * 4,
+                            cudaMemcpyDeviceToDevice, s));
+    BG_CUDA(cudaMemcpyAsync(m->tiles.p, A.ti() + ends[0], static_cast<size_t>(m->nnz) * 2,
+                            cudaMemcpyDeviceToDevice, s));
+  }
+  frdc_finalize(*m, s);
+  return m;
+}
+
+// A rank's share of a prepared graph (SURVEY §8e "each GPU holds its FRDC
+// slice"): both adjacency structures cut to node rows [row0, row1); the
+// per-node scale vectors stay whole (O(n): the column scales of an
+// aggregation index every node).
+std::unique_ptr<bg_graph> graph_shard(const bg_graph& g, int64_t row0, int64_t row1, cudaStream_t s) {
+  if (g.row0 != 0 || g.structure->rows != g.n) fail("graph shard: the source must be a whole graph");
+  auto o = std::make_unique<bg_graph>();
+  o->n = g.n;
+  o->row0 = row0;
+  o->structure = frdc_slice(*g.structure, row0, row1, s);
+  o->raw = frdc_slice(*g.raw, row0, row1, s);
+  auto copy = [&](DevBuf& d, const DevBuf& src) {
+    d.alloc(src.bytes);
+    if (src.bytes) BG_CUDA(cudaMemcpyAsync(d.p, src.p, src.bytes, cudaMemcpyDeviceToDevice, s));
+  };
+  copy(o->norm, g.norm);
+  copy(o->mean_row, g.mean_row);
+  copy(o->ones, g.ones);
+  copy(o->neighbor_count, g.neighbor_count);
+  BG_CUDA(cudaStreamSynchronize(s));
+  return o;
+}
+
 std::unique_ptr<bg_graph> prepare_graph(const int64_t* src, const int64_t* dst, int64_t e,
                                         int64_t n, cudaStream_t s) {
   auto g = std::make_unique<bg_graph>();

@@ -1,6 +1,7 @@
 // Model / trace objects behind the C ABI handles.
 #pragma once
 
+#include <functional>
 #include <string>
 #include <utility>
 #include <vector>
@@ -64,7 +65,8 @@ struct bg_model {
   std::vector<bg::ModelLayer> layers;
   bg::Pool pool;
   int64_t last_out_cols = -1;
-  // CUDA-graph replay of a forward bound to fixed buffers.
+  // CUDA-graph replay of a forward bound to fixed buffers (bg_model_forward,
+  // and the NCCL-sharded forward): one slot each.
   bool capture = true;
   struct Key {
     const void* x = nullptr;
@@ -73,23 +75,32 @@ struct bg_model {
     float* out = nullptr;
     float* logits = nullptr;
     cudaStream_t s = nullptr;
-    uint64_t agg_gen = 0;  // aggregation layout settings the graph was recorded with
-    uint64_t pool_gen = 0;  // pool allocation state the graph's pointers come from
+    uint64_t agg_gen = 0;    // aggregation layout settings the graph was recorded with
+    uint64_t pool_gen = 0;   // pool allocation state the graph's pointers come from
     uint64_t graph_gen = 0;  // FRDC views the graph's pointers come from
+    uint64_t extra = 0;      // sharded: communicator, rank and bounds
     bool operator==(const Key& o) const {
       return x == o.x && rows == o.rows && cols == o.cols && prec == o.prec && wb == o.wb &&
              out == o.out && logits == o.logits && s == o.s && agg_gen == o.agg_gen &&
-             pool_gen == o.pool_gen && graph_gen == o.graph_gen;
+             pool_gen == o.pool_gen && graph_gen == o.graph_gen && extra == o.extra;
     }
-  } key;
-  int key_runs = 0;
-  cudaGraphExec_t exec = nullptr;
+  };
+  struct CaptureSlot {
+    Key key;
+    cudaGraphExec_t exec = nullptr;
+    void reset() {
+      if (exec) cudaGraphExecDestroy(exec);
+      exec = nullptr;
+      key = Key{};
+    }
+    ~CaptureSlot() { reset(); }
+  };
+  CaptureSlot fwd, sharded;
   // Buffers of the host-pointer entry point.
   bg::DevBuf hx, hout, hlog;
   cudaStream_t copy_stream = nullptr;    // H2D / D2H of the host entry point
   std::vector<cudaEvent_t> chunk_events;  // 2 x chunks (input landed, output ready)
   ~bg_model() {
-    if (exec) cudaGraphExecDestroy(exec);
     for (cudaEvent_t e : chunk_events) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
   }
@@ -110,6 +121,13 @@ struct LayerCall {
   std::string prefix;
   Op result;
 };
+// Runs `run` on stream st through the slot's CUDA graph: the first call with
+// a binding runs eagerly (sizing the pool, building views), the second
+// captures, later ones replay -- re-recorded whenever the key (binding,
+// aggregation settings, pool or FRDC-view generation) changes.
+uint64_t graph_generation(const bg_graph* g);
+void run_captured(bg_model& m, bg_model::CaptureSlot& slot, bg_model::Key k, cudaStream_t st,
+                  const std::function<void()>& run);
 void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace* trace,
                   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>>* timing,
                   cudaStream_t s, StreamChunks* chunks = nullptr, LayerCall* single = nullptr);

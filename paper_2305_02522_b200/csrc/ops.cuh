@@ -64,7 +64,8 @@ struct bg_frdc {
 };
 
 struct bg_graph {
-  int64_t n = 0;
+  int64_t n = 0;     // node count of the whole graph
+  int64_t row0 = 0;  // a shard: the FRDC rows are node rows [row0, row0 + structure->rows)
   std::unique_ptr<bg_frdc> structure, raw;
   bg::DevBuf norm, mean_row, ones, neighbor_count;
 };
@@ -99,6 +100,8 @@ void frdc_slivers(bg_frdc& m, cudaStream_t s);   // build the node-major sliver 
 void frdc_bitview(bg_frdc& m, cudaStream_t s);   // build the bit-entry view once (from slivers)
 std::unique_ptr<bg_graph> prepare_graph(const int64_t* src, const int64_t* dst, int64_t e,
                                         int64_t n, cudaStream_t s);
+std::unique_ptr<bg_frdc> frdc_slice(const bg_frdc& A, int64_t row0, int64_t row1, cudaStream_t s);
+std::unique_ptr<bg_graph> graph_shard(const bg_graph& g, int64_t row0, int64_t row1, cudaStream_t s);
 
 // ---- bmm.cu --------------------------------------------------------------
 // Binary product against transposed weight bits wt (n x spw(k)).

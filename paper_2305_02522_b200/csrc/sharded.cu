@@ -67,8 +67,12 @@ const Nccl& nccl() {
 struct bg_comm {
   ncclComm_t comm = nullptr;
   int world = 1, rank = 0;
+  // External exchange (bg_comm_create_external): a host callback in place of
+  // NCCL, e.g. a host-staged all-gather over another transport.
+  bg_allgather_fn ext = nullptr;
+  void* ext_ctx = nullptr;
   ~bg_comm() {
-    if (comm) bg::nccl().comm_destroy(comm);
+    if (comm && !ext) bg::nccl().comm_destroy(comm);
   }
 };
 
@@ -106,6 +110,7 @@ struct Shard {
   bg_model& m;
   const std::vector<int64_t>& bounds;  // world + 1 node-row boundaries
   std::vector<std::pair<int64_t, int64_t>> ranges;  // ranges computed by this process
+  int64_t off;                         // node row of the model graph's first FRDC row (a shard's row0)
   bg_comm* comm;                       // null: virtual ranks in one process
   cudaStream_t s;
   Timer tm;
@@ -113,8 +118,15 @@ struct Shard {
 
   // Make rows [bounds[q], bounds[q+1]) of a full-size buffer valid on every rank.
   void allgather(void* buf, int64_t row_bytes) {
-    if (!comm || comm->world == 1) return;
+    if (!comm) return;
     tm.begin(prefix + "allgather");
+    if (comm->ext) {  // the callback runs on the host once this rank's rows are produced
+      BG_CUDA(cudaStreamSynchronize(s));
+      const int rc = comm->ext(comm->ext_ctx, buf, row_bytes, bounds.data(), comm->world, comm->rank, s);
+      if (rc) throw std::runtime_error("sharded forward: external all-gather failed (" + std::to_string(rc) + ")");
+      tm.end();
+      return;
+    }
     BG_NCCL(nccl().group_start());
     for (int q = 0; q < comm->world; ++q) {
       const int64_t r0 = bounds[q], r1 = bounds[q + 1];
@@ -247,10 +259,15 @@ struct Shard {
     }
     tm.begin(prefix + "spmm[" + variant_name(v) + "]");
     Op out = alloc_like(v.out, x.cols, v.in1 == BG_B ? x.wb : m.wb);
+    // FRDC rows are local (rows r - off of a shard); outputs and row scales
+    // are indexed by node row, so their bases move by off rows
+    const int64_t orow = out.prec == BG_F ? out.cols : spw(out.cols, out.wb);
+    uint32_t* obits = out.bits ? out.bits + off * orow : nullptr;
+    float* of = out.f ? out.f + off * orow : nullptr;
     for (auto [r0, r1] : ranges) {
       if (r1 <= r0) continue;
       if (v.in1 == BG_B && v.in2 == BG_B) {
-        bspmm_bb(*A, x.bits, x.cols, x.wb, out.bits, out.f, s, r0, r1);
+        bspmm_bb(*A, x.bits, x.cols, x.wb, obits, of, s, r0 - off, r1 - off);
       } else {
         SpmmFArgs a;
         a.f = x.cols;
@@ -260,12 +277,12 @@ struct Shard {
         } else {
           a.x_f = x.f;
         }
-        a.row_scale = v.in2 == BG_F ? rs : nullptr;
+        a.row_scale = v.in2 == BG_F && rs ? rs + off : nullptr;
         a.col_scale = v.in2 == BG_F ? cs : nullptr;
-        a.out_bits = out.bits;
+        a.out_bits = obits;
         a.owb = out.wb;
-        a.out_f = out.f;
-        bspmm_f(*A, a, s, r0, r1);
+        a.out_f = of;
+        bspmm_f(*A, a, s, r0 - off, r1 - off);
       }
     }
     tm.end();
@@ -317,10 +334,16 @@ void forward_sharded(bg_model& m, const Op& x0, const std::vector<int64_t>& boun
     if (!errors.empty()) fail("invalid model: " + errors.front());
   }
   m.pool.reset();
-  Shard sh{m, bounds, {}, comm, s, Timer{timing, s}, ""};
+  Shard sh{m, bounds, {}, m.graph->row0, comm, s, Timer{timing, s}, ""};
   if (comm) sh.ranges.push_back({bounds[rank], bounds[rank + 1]});
   else
     for (int q = 0; q < world; ++q) sh.ranges.push_back({bounds[q], bounds[q + 1]});
+  // the model's graph (whole, or this rank's shard) must hold every range
+  for (auto [r0, r1] : sh.ranges)
+    if (r1 > r0 && (r0 < m.graph->row0 || r1 > m.graph->row0 + m.graph->structure->rows ||
+                    r1 > m.graph->row0 + m.graph->raw->rows))
+      fail("sharded forward: the model's graph does not hold node rows [" + std::to_string(r0) + ", " +
+           std::to_string(r1) + ")");
 
   Op cur = x0;
   bool cur_full = comm == nullptr;  // virtual mode: every range is computed here
@@ -367,10 +390,11 @@ void forward_sharded(bg_model& m, const Op& x0, const std::vector<int64_t>& boun
             if (i + 1 < nl && m.layers[i + 1].info.kind == BG_LAYER_SOFTMAX)
               probs = (i + 2 == nl && out_base) ? out_base : static_cast<float*>(m.pool.get(o.bytes()));
             sh.tm.begin(sh.prefix + "spmm[" + variant_name(sp) + "]");
+            const int64_t C = l.w1.cols, off = sh.off;
             for (auto [r0, r1] : sh.ranges)
               if (r1 > r0)
-                gcn1_aggregate(A, recs, cur.cols, cur.wb, l.w1.wt.as<uint32_t>(), l.w1.scale.as<float>(),
-                               l.w1.cols, o.f, probs, s, r0, r1);
+                gcn1_aggregate(A, recs, cur.cols, cur.wb, l.w1.wt.as<uint32_t>(), l.w1.scale.as<float>(), C,
+                               o.f + off * C, probs ? probs + off * C : nullptr, s, r0 - off, r1 - off);
             sh.tm.end();
             probs_done = probs;
             cur = o;
@@ -546,9 +570,52 @@ int bg_comm_create(int world, int rank, const uint8_t* id, size_t len, bg_comm**
 
 void bg_comm_destroy(bg_comm* c) { delete c; }
 
+int bg_comm_create_external(int world, int rank, bg_allgather_fn fn, void* ctx, bg_comm** out) {
+  return guard([&] {
+    if (!out || !fn) fail("bad communicator arguments");
+    if (world < 1 || rank < 0 || rank >= world) fail("partition: bad rank/world size");
+    auto c = std::make_unique<bg_comm>();
+    c->world = world;
+    c->rank = rank;
+    c->ext = fn;
+    c->ext_ctx = ctx;
+    *out = c.release();
+  });
+}
+
+int bg_graph_shard(const bg_graph* g, int64_t row_begin, int64_t row_end, bg_graph** out, bg_stream stream) {
+  return guard([&] {
+    if (!g || !out) fail("graph shard: null argument");
+    *out = graph_shard(*g, row_begin, row_end, S(stream)).release();
+  });
+}
+
 int bg_model_forward_sharded(bg_model* m, bg_comm* comm, const bg_mat* x, const int64_t* bounds,
                              int world, int rank, float* out, float* logits, bg_stream stream) {
-  return guard([&] { sharded_entry(m, comm, x, bounds, world, rank, out, logits, stream, nullptr); });
+  return guard([&] {
+    auto run = [&] { sharded_entry(m, comm, x, bounds, world, rank, out, logits, stream, nullptr); };
+    cudaStream_t st = S(stream);
+    // An NCCL exchange is stream-ordered and capturable: the forward replays
+    // as one CUDA graph (kernels + broadcasts) like bg_model_forward.  The
+    // external exchange runs host code mid-forward and is never captured.
+    if (!m || !x || !bounds || !comm || comm->ext || !m->capture || st == nullptr) {
+      run();
+      return;
+    }
+    bg_model::Key k;
+    k.x = x->data;
+    k.rows = x->rows;
+    k.cols = x->cols;
+    k.prec = x->precision;
+    k.wb = x->word_bits;
+    k.out = out;
+    k.logits = logits;
+    k.s = st;
+    uint64_t h = reinterpret_cast<uintptr_t>(comm) * 0x9E3779B97F4A7C15ull ^ static_cast<uint64_t>(world * 131 + rank);
+    for (int q = 0; q <= world; ++q) h = h * 1000003ull ^ static_cast<uint64_t>(bounds[q]);
+    k.extra = h;
+    run_captured(*m, m->sharded, k, st, run);
+  });
 }
 
 int bg_model_forward_sharded_timed(bg_model* m, bg_comm* comm, const bg_mat* x, const int64_t* bounds,

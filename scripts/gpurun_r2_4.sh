@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests/test_gpu_layers.py tests/test_gpu_verify.py tests/test_cpp_shim.py -x -q > gpurun_out/r2_t4.log 2>&1
+echo "rc=$?" >> gpurun_out/r2_t4.log
+timeout 1500 python -m pytest tests/test_gpu_sharded_mp.py tests/test_gpu_sharded.py -x -q >> gpurun_out/r2_t4.log 2>&1
+echo "rc=$?" >> gpurun_out/r2_t4.log
+tail -5 gpurun_out/r2_t4.log
