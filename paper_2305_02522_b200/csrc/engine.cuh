@@ -23,9 +23,14 @@ struct Op {
   uint32_t* bits = nullptr;
   const float* scale = nullptr;
   int scale_axis = BG_AXIS_ROW;
+  // An F operand held as its bit pattern (packed.cu): value = bit ? pval : 0,
+  // bits in the packed layout at width wb.  Only the model executor makes
+  // and reads these; everything else sees materialized fp32.
+  float pval = 0.0f;
+  bool packed() const { return prec == BG_F && pval != 0.0f && bits && !f; }
   size_t bytes() const {
-    return prec == BG_F ? static_cast<size_t>(rows * cols) * 4
-                        : static_cast<size_t>(rows * spw(cols, wb)) * 4;
+    return prec == BG_F && !packed() ? static_cast<size_t>(rows * cols) * 4
+                                     : static_cast<size_t>(rows * spw(cols, wb)) * 4;
   }
 };
 
@@ -75,6 +80,10 @@ Op run_bspmm(bg_variant v, const bg_frdc* adj, const float* rs, const float* cs,
              int word_bits, Pool& pool, cudaStream_t s);
 // fuse_relu: apply the layer's ReLU inside the kernel when the result is F
 Op run_add(bg_variant v, const Op& a, const Op& b, Pool& pool, cudaStream_t s, bool fuse_relu = false);
+// ReLU(ADD.BBF(a, b)) = 2 (a AND b), returned packed (pval 2); the checks of run_add
+Op run_add_relu_packed(bg_variant v, const Op& a, const Op& b, Pool& pool, cudaStream_t s);
+// A packed F operand as fp32 (any other operand unchanged)
+Op materialize(const Op& x, Pool& pool, cudaStream_t s);
 Op run_concat(bg_variant v, const Op& a, const Op& b, Pool& pool, cudaStream_t s);
 
 // Output shapes (for caller allocation through the C ABI).

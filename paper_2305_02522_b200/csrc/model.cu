@@ -240,6 +240,12 @@ struct Exec {
 
   Op mm_slot(bg_variant mm, const Op& x, const WeightDev& w, const std::string& label) {
     if (mm.op != BG_BMM) fail(label + ": plan slot expects an MM variant");
+    if (x.packed()) {
+      if (is_dense_fff(mm) || (mm.out == BG_F && !packed_fbf_supported(w.cols)) || w.wb != m.wb ||
+          spw(w.cols, m.wb) > 64)
+        return mm_slot(mm, materialize(x, m.pool, s), w, label);
+      return mm_packed(mm, x, w, label, nullptr);
+    }
     if (in_chunks && x.f == x0f && (is_dense_fff(mm) || h.trace)) wait_all_in();
     if (is_dense_fff(mm)) {
       if (x.prec != BG_F) fail(label + ": MM.FFF expects a full-precision input");
@@ -271,6 +277,50 @@ struct Exec {
     return r;
   }
 
+  // An F-input product on a packed two-valued input (packed.cu): the
+  // binarized input is all ones, so B outputs are one constant row and
+  // MM.FBF needs one popcount per row; probs: the following softmax fused.
+  Op mm_packed(bg_variant mm, const Op& x, const WeightDev& w, const std::string& label, float* probs,
+               const RowChunks* out_chunks = nullptr) {
+    if (mm.in1 != BG_F) fail("bmm: in1 is tagged F but operand is binary");
+    if (!variant_valid(mm)) fail("bmm: " + variant_name(mm) + " is not a supported variant");
+    if (x.cols != w.rows) fail("bmm: inner dimensions disagree");
+    if (h.trace) {
+      const Op xf = materialize(x, m.pool, s);
+      auto* b = static_cast<uint32_t*>(m.pool.get(static_cast<size_t>(x.rows * spw(x.cols, m.wb)) * 4));
+      binarize(xf.f, x.rows, x.cols, m.wb, b, s);
+      h.bits(label + ".bin_in", b, x.rows, x.cols, m.wb);
+      h.bits(label + ".bin_w", w.bits.as<uint32_t>(), w.rows, w.cols, w.wb);
+    }
+    Op r;
+    r.rows = x.rows;
+    r.cols = w.cols;
+    r.wb = m.wb;
+    h.begin(label + "[" + variant_name(mm) + "]");
+    if (mm.out == BG_B) {
+      r.prec = BG_B;
+      r.bits = static_cast<uint32_t*>(m.pool.get(r.bytes()));
+      packed_const_rows(w.wt.as<uint32_t>(), w.rows, w.cols, m.wb, x.rows, r.bits, s);
+    } else {
+      r.prec = BG_F;
+      r.f = static_cast<float*>(m.pool.get(r.bytes()));
+      auto* tab = static_cast<float*>(m.pool.get(packed_fbf_table_bytes(x.cols, w.cols)));
+      if (out_chunks) {
+        for (int c = 0; c < out_chunks->n; ++c) {
+          packed_fbf(x.bits, out_chunks->bounds[c], out_chunks->bounds[c + 1], x.cols, x.wb, x.pval,
+                     w.wt.as<uint32_t>(), m.wb, w.scale.as<float>(), w.cols, r.f, probs, tab, s);
+          BG_CUDA(cudaEventRecord(out_chunks->ready[c], s));
+        }
+      } else {
+        packed_fbf(x.bits, 0, x.rows, x.cols, x.wb, x.pval, w.wt.as<uint32_t>(), m.wb, w.scale.as<float>(),
+                   w.cols, r.f, probs, tab, s);
+      }
+    }
+    h.end();
+    if (mm.out == BG_B) h.bits(label + ".out", r.bits, r.rows, r.cols, r.wb);
+    return r;
+  }
+
   // The two MMs of a SAGE / GraphConv layer when both are F -> B on the same
   // fp32 input (MM.FBB / MM.FFB): one paired product reads the input once
   // (bmm_pair).  Untraced forwards only (the traced one keeps the per-slot
@@ -278,7 +328,7 @@ struct Exec {
   bool mm_pair(ModelLayer& l, const Op& x, const std::string& prefix, Op& hs, Op& hn) {
     const bg_variant p0 = l.info.plan[0], p1 = l.info.plan[1];
     auto fb = [](bg_variant v) { return v.op == BG_BMM && v.in1 == BG_F && v.out == BG_B; };
-    if (h.trace || !fb(p0) || !fb(p1) || x.prec != BG_F || x.scale) return false;
+    if (h.trace || !fb(p0) || !fb(p1) || x.prec != BG_F || x.scale || x.packed()) return false;
     const WeightDev &w1 = l.w1, &w2 = l.w2;
     if (w1.rows != w2.rows || w1.cols != w2.cols || w1.wb != m.wb || w2.wb != m.wb || x.cols != w1.rows)
       return false;
@@ -354,7 +404,7 @@ struct Exec {
   }
 
   void relu_inplace(Op& x, const Op& x0) {
-    if (x.prec != BG_F) return;  // ref: graphops.cpp:89-97
+    if (x.prec != BG_F || x.packed()) return;  // ref: graphops.cpp:89-97; packed values are >= 0
     if (x.f == x0.f) x = own_f(x);
     relu(x.f, x.rows * x.cols, s);
   }
@@ -473,16 +523,39 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
             scale_rows_double(agg.f, agg.rows, agg.cols, m.graph->neighbor_count.as<int64_t>(), s);
           // the layer's ReLU rides in the ADD kernel when the sum is F (on a B
           // sum it is a no-op, graphops.cpp:89-97)
-          cur = run_add(l.info.plan[3], hs, agg, m.pool, s, l.relu && l.info.plan[3].out == BG_F);
+          const bg_variant av = l.info.plan[3];
+          if (av.op == BG_ADD && av.in1 == BG_B && av.out == BG_F && l.relu && hs.prec == BG_B && agg.prec == BG_B) {
+            // ReLU(ADD.BBF) = 2 (a AND b): kept packed (packed.cu), 1/32 of the fp32 bytes
+            cur = run_add_relu_packed(av, hs, agg, m.pool, s);
+            break;
+          }
+          cur = run_add(av, hs, agg, m.pool, s, l.relu && av.out == BG_F);
           if (l.info.plan[3].out == BG_B) h.bits(prefix + "add.out", cur.bits, cur.rows, cur.cols, cur.wb);
           break;
         }
         case BG_LAYER_FC: {
+          const bg_variant mm = l.info.plan[0];
+          if (cur.packed() && mm.op == BG_BMM && mm.in1 == BG_F && mm.in2 == BG_B && mm.out == BG_F && !l.relu &&
+              i + 1 < nl && m.layers[i + 1].info.kind == BG_LAYER_SOFTMAX && packed_fbf_supported(l.w1.cols) &&
+              cur.cols == l.w1.rows && l.w1.wb == m.wb) {
+            // MM.FBF on the packed input with the following softmax in the
+            // same pass: logits and probabilities from one popcount per row
+            float* probs = (i + 2 == nl && out) ? out : static_cast<float*>(m.pool.get(
+                static_cast<size_t>(cur.rows * l.w1.cols) * 4));
+            const bool chunked = probs == out && out && chunked_out(i + 2);
+            Op o = ex.mm_packed(mm, cur, l.w1, prefix + "mm", probs, chunked ? &chunks->out : nullptr);
+            if (chunked) chunks->out_done = true;
+            fused_probs = probs;
+            fused_logits = o.f;
+            cur = o;
+            break;
+          }
           cur = ex.mm_slot(l.info.plan[0], cur, l.w1, prefix + "mm");
           if (l.relu) ex.relu_inplace(cur, x0);
           break;
         }
         case BG_LAYER_AGGREGATE: {
+          cur = materialize(cur, m.pool, s);
           const bg_variant sp = l.info.plan[0];
           const bool fac = sp.in2 == BG_F;
           cur = ex.spmm_slot(sp, m.graph->structure.get(), fac ? m.graph->norm.as<float>() : nullptr,
@@ -494,6 +567,7 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
           break;
         case BG_LAYER_BATCHNORM: {
           if (cur.prec != BG_F) fail("bad variant access");
+          cur = materialize(cur, m.pool, s);
           if (l.bn_len != cur.cols)
             fail("batchnorm: parameter lengths do not match " + std::to_string(cur.cols) + " columns");
           Op o = cur;
@@ -505,6 +579,7 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
         }
         case BG_LAYER_SOFTMAX: {
           if (cur.prec != BG_F) fail("bad variant access");
+          cur = materialize(cur, m.pool, s);
           if (logits) {
             BG_CUDA(cudaMemcpyAsync(logits, cur.f, cur.bytes(), cudaMemcpyDeviceToDevice, s));
             logits_set = true;
@@ -534,6 +609,7 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
         }
         case BG_LAYER_BINARIZE: {
           if (cur.prec != BG_F) fail("bad variant access");
+          cur = materialize(cur, m.pool, s);
           Op o;
           o.prec = BG_B;
           o.rows = cur.rows;
@@ -547,6 +623,7 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
         }
         case BG_LAYER_SCALE: {
           if (cur.prec != BG_F) fail("bad variant access");
+          cur = materialize(cur, m.pool, s);
           if (l.sr_len != cur.rows || l.sc_len != cur.cols) fail("scl: scale length mismatch");
           Op o = cur;
           o.f = static_cast<float*>(m.pool.get(cur.bytes()));
@@ -565,6 +642,7 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
                                "): " + e.what());
     }
   }
+  cur = materialize(cur, m.pool, s);  // a packed two-valued result leaves as fp32
   if (single) {
     single->result = cur;
     return;

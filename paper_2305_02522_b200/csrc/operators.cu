@@ -344,6 +344,34 @@ Op run_add(bg_variant v, const Op& a, const Op& b, Pool& pool, cudaStream_t s, b
   return out;
 }
 
+Op run_add_relu_packed(bg_variant v, const Op& a, const Op& b, Pool& pool, cudaStream_t s) {
+  if (v.op != BG_ADD) fail("add: variant " + variant_name(v) + " is not an ADD variant");
+  if (!variant_valid(v)) fail("add: " + variant_name(v) + " is not a supported variant");
+  if (a.rows != b.rows || a.cols != b.cols) fail("add: operand shapes disagree");
+  if (v.in1 != BG_B || v.out != BG_F) fail("add: packed ReLU sum needs ADD.BBF");
+  binary_pair(v, a, b, "add");
+  Op out;
+  out.prec = BG_F;
+  out.rows = a.rows;
+  out.cols = a.cols;
+  out.wb = a.wb;
+  out.pval = 2.0f;  // ReLU(2 (a + b) - 2) = 2 (a AND b)  (kernels.cpp:619-624)
+  out.bits = static_cast<uint32_t*>(pool.get(out.bytes()));
+  and_words(a.bits, b.bits, a.rows * spw(a.cols, a.wb), out.bits, s);
+  return out;
+}
+
+Op materialize(const Op& x, Pool& pool, cudaStream_t s) {
+  if (!x.packed()) return x;
+  Op o;
+  o.prec = BG_F;
+  o.rows = x.rows;
+  o.cols = x.cols;
+  o.f = static_cast<float*>(pool.get(static_cast<size_t>(x.rows * x.cols) * 4));
+  expand_packed(x.bits, x.rows, x.cols, x.wb, x.pval, o.f, s);
+  return o;
+}
+
 Op run_concat(bg_variant v, const Op& a, const Op& b, Pool& pool, cudaStream_t s) {
   if (v.op != BG_CONCAT) fail("concat: variant " + variant_name(v) + " is not a CONCAT variant");
   if (!variant_valid(v)) fail("concat: " + variant_name(v) + " is not a supported variant");

@@ -190,6 +190,19 @@ bool window_bb(bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* out_b
 bool rowgroup_bb(bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uint32_t* out_bits, float* out_f,
                  cudaStream_t s, int64_t r0, int64_t r1);
 
+// ---- packed.cu: two-valued F activations kept as bits ----------------------
+void and_words(const uint32_t* a, const uint32_t* b, int64_t n, uint32_t* out, cudaStream_t s);
+void expand_packed(const uint32_t* bits, int64_t rows, int64_t cols, int wb, float pval, float* out, cudaStream_t s);
+// every row of an F->B product on an all-ones input (the binarized packed tensor)
+void packed_const_rows(const uint32_t* wt, int64_t k, int64_t n, int wb, int64_t rows, uint32_t* out,
+                       cudaStream_t s);
+bool packed_fbf_supported(int64_t n);
+// MM.FBF on rows [r0, r1) of a packed input (+ the row softmax into probs)
+// (table: packed_fbf_table_bytes of workspace)
+size_t packed_fbf_table_bytes(int64_t k, int64_t n);
+void packed_fbf(const uint32_t* bits, int64_t r0, int64_t r1, int64_t k, int xwb, float pval, const uint32_t* wt,
+                int wb, const float* beta, int64_t n, float* logits, float* probs, float* table, cudaStream_t s);
+
 // ---- elementwise.cu ------------------------------------------------------
 void add_bbb(const uint32_t* a, const uint32_t* b, int64_t words, uint32_t* out, cudaStream_t s);
 void add_bbf(const uint32_t* a, const uint32_t* b, int64_t rows, int64_t cols, int wb, float* out,

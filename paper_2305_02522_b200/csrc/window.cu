@@ -469,12 +469,14 @@ __global__ void __launch_bounds__(TPR == 1 ? (NP <= 10 ? kWinMaxThreads : 480) :
     uint32_t v[8][W];
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
-      const uint32_t off = (m & 1) ? (pk[m >> 1] >> 12) & 0xFFFF0u : (pk[m >> 1] << 4) & 0xFFFF0u;
+      // entry -> byte address: extract + one shift-add (LOP3/SHF + LEA)
+      const uint32_t ent = (m & 1) ? (pk[m >> 1] >> 16) : (pk[m >> 1] & 0xFFFFu);
+      const uint32_t addr = sbw + (ent << 4);
       if (W == 4) {
-        const uint4 t = lds128(sbw + off);
+        const uint4 t = lds128(addr);
         v[m][0] = t.x, v[m][1] = t.y, v[m][W > 2 ? 2 : 0] = t.z, v[m][W > 3 ? 3 : 0] = t.w;
       } else {
-        const uint2 t = lds64(sbw + off);
+        const uint2 t = lds64(addr);
         v[m][0] = t.x, v[m][1] = t.y;
       }
     }
@@ -506,7 +508,7 @@ __global__ void __launch_bounds__(TPR == 1 ? (NP <= 10 ? kWinMaxThreads : 480) :
   auto wait_next = [&]() {
     if (S + 1 < nsteps) {
       const int s1 = slot == kSlots - 1 ? 0 : slot + 1;
-      mbar_wait(&full[s1], (use + (slot == kSlots - 1)) & 1u);
+      mbar_wait_sleep(&full[s1], (use + (slot == kSlots - 1)) & 1u);
     }
   };
   if (nsteps > 0) mbar_wait(&full[0], 0u);
@@ -748,7 +750,9 @@ bool launch_win_np(bg_frdc& A, const uint32_t* x, int64_t f, uint32_t* ob, float
 
 bool window_bb(bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* out_bits, float* out_f,
                cudaStream_t s, int64_t r0, int64_t r1) {
-  if (spw(f, wb) != 4 || A.rows != A.cols || A.rows == 0 || r1 <= r0) return false;
+  // A may be a rank's row slice (rows < cols): blocks index its rows, the
+  // streamed operand has A.cols rows
+  if (spw(f, wb) != 4 || A.rows == 0 || A.cols == 0 || r1 <= r0) return false;
   if (reinterpret_cast<uintptr_t>(x) % 16 != 0) return false;
   const int mode = aggregation_mode();
   if (mode == BG_AGG_SLIVERS || mode == BG_AGG_TILES) return false;

@@ -42,6 +42,27 @@ __global__ void k_ldg(const uint4* __restrict__ rec, const uint32_t* __restrict_
   if (acc == 0x12345678u) out[0] = acc;
 }
 
+// records of RB bytes (16/32/64), RB/16 lanes per record
+template <int RB>
+__global__ void k_ldg_sz(const uint4* __restrict__ rec, const uint32_t* __restrict__ idx, int64_t e,
+                         uint32_t* __restrict__ out) {
+  constexpr int LPR = RB / 16, RPI = 32 / LPR;  // lanes per record, records per instruction
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  uint32_t acc = 0;
+  for (int64_t b = warp * 32; b < e; b += warps * 32) {
+    const uint32_t my = b + lane < e ? __ldg(idx + b + lane) : 0;
+#pragma unroll
+    for (int k = 0; k < 32 / RPI; ++k) {
+      const uint32_t j = __shfl_sync(0xFFFFFFFFu, my, RPI * k + lane / LPR);
+      const uint4 v = __ldg(rec + static_cast<int64_t>(j) * LPR + (lane % LPR));
+      acc ^= v.x + v.y + v.z + v.w;
+    }
+  }
+  if (acc == 0x12345678u) out[0] = acc;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -60,11 +81,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
 }
 
 constexpr int kStages = 4;
-constexpr int kWarps = 8;
+constexpr int kWarps = 4;
 
 // One warp per stream of edges, a ring of kStages x 32 records per warp.
 template <int MODE>  // 0: one bulk copy per record, 1: gather4
-__global__ void __launch_bounds__(kWarps * 32) k_tma(const uint4* __restrict__ rec, const CUtensorMap* __restrict__ tm,
+__global__ void __launch_bounds__(kWarps * 32) k_tma(const uint4* __restrict__ rec, const __grid_constant__ CUtensorMap tm,
                                                      const uint32_t* __restrict__ idx, int64_t e,
                                                      uint32_t* __restrict__ out) {
   __shared__ __align__(128) uint4 ring[kWarps][kStages][32 * 4];
@@ -98,7 +119,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_tma(const uint4* __restrict__ r
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
             " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(&ring[w][s][lane * 16])),
-            "l"(tm), "r"(0), "r"(j0), "r"(j1), "r"(j2), "r"(j3), "r"(smem_u32(&bar[w][s]))
+            "l"(&tm), "r"(0), "r"(j0), "r"(j1), "r"(j2), "r"(j3), "r"(smem_u32(&bar[w][s]))
             : "memory");
     }
   };
@@ -171,12 +192,16 @@ int main() {
   for (int occ : {4, 8, 16})
     time(occ == 4 ? "ldg x4" : occ == 8 ? "ldg x8" : "ldg x16",
          [&] { k_ldg<<<sms * occ, 256>>>(rec, idx, e, out); });
-  for (int occ : {2, 4, 8}) {
-    time(occ == 2 ? "bulk x2" : occ == 4 ? "bulk x4" : "bulk x8",
-         [&] { k_tma<0><<<sms * occ, kWarps * 32>>>(rec, tm, idx, e, out); });
+  time("ldg16 x8", [&] { k_ldg_sz<16><<<sms * 8, 256>>>(rec, idx, e, out); });
+  time("ldg32 x8", [&] { k_ldg_sz<32><<<sms * 8, 256>>>(rec, idx, e, out); });
+  time("ldg64 x8", [&] { k_ldg_sz<64><<<sms * 8, 256>>>(rec, idx, e, out); });
+  time("ldg32 x16", [&] { k_ldg_sz<32><<<sms * 16, 256>>>(rec, idx, e, out); });
+  for (int occ : {4, 8, 16}) {
+    time(occ == 4 ? "bulk x4" : occ == 8 ? "bulk x8" : "bulk x16",
+         [&] { k_tma<0><<<sms * occ, kWarps * 32>>>(rec, tmh, idx, e, out); });
     if (r == CUDA_SUCCESS)
-      time(occ == 2 ? "gath4 x2" : occ == 4 ? "gath4 x4" : "gath4 x8",
-           [&] { k_tma<1><<<sms * occ, kWarps * 32>>>(rec, tm, idx, e, out); });
+      time(occ == 4 ? "gath4 x4" : occ == 8 ? "gath4 x8" : "gath4 x16",
+           [&] { k_tma<1><<<sms * occ, kWarps * 32>>>(rec, tmh, idx, e, out); });
   }
   CK(cudaGetLastError());
   return 0;
