@@ -52,6 +52,12 @@ int bg_version(void);
 enum { BG_AGG_AUTO = 0, BG_AGG_SLIVERS = 1, BG_AGG_TILES = 2, BG_AGG_WINDOW = 3 };
 int bg_set_aggregation(int mode, int window_nodes);
 int bg_get_aggregation(int* mode, int* window_nodes);
+/* Whole-forward persistent kernel for small graphs (one cooperative launch
+ * for a binary GCN chain, results identical to the layer-by-layer forward).
+ * Off by default (measured slower on B200 than the captured layer-by-layer
+ * forward); enable = 1 turns it on process-wide (as does env
+ * BG_PERSISTENT=1).  Traced and timed forwards always run layer by layer. */
+int bg_set_persistent(int enable);
 
 /* ---- device memory (so C/C++ hosts need no CUDA headers) ---------------- */
 enum { BG_COPY_H2D = 0, BG_COPY_D2H = 1, BG_COPY_D2D = 2 };

@@ -96,6 +96,7 @@ PROTOTYPES = {
     "bg_version": (I32, []),
     "bg_set_aggregation": (I32, [I32, I32]),
     "bg_get_aggregation": (I32, [C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "bg_set_persistent": (I32, [I32]),
     "bg_device_count": (I32, [C.POINTER(C.c_int)]),
     "bg_device_alloc": (I32, [C.c_size_t, C.POINTER(C.c_void_p)]),
     "bg_device_free": (I32, [P]),

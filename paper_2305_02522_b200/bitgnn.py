@@ -42,6 +42,12 @@ def set_aggregation(mode: int, window_nodes: int = 0) -> None:
     L.check(L.lib().bg_set_aggregation(int(mode), int(window_nodes)))
 
 
+def set_persistent(enable: bool) -> None:
+    """Whole-forward persistent kernel for small binary GCN chains (opt-in;
+    identical results, see bg_set_persistent)."""
+    L.check(L.lib().bg_set_persistent(int(enable)))
+
+
 def get_aggregation() -> Tuple[int, int]:
     m, w = C.c_int(), C.c_int()
     L.check(L.lib().bg_get_aggregation(C.byref(m), C.byref(w)))

@@ -63,7 +63,7 @@ uint64_t graph_generation(const bg_graph* g) {
 
 void run_captured(bg_model& m, bg_model::CaptureSlot& slot, bg_model::Key k, cudaStream_t st,
                   const std::function<void()>& run) {
-  k.agg_gen = aggregation_generation();
+  k.agg_gen = aggregation_generation() * 2 + (persistent_forced() ? 1 : 0);  // settings the graph was recorded with
   // Any other entry point sharing the pool (traced, timed, host, the other
   // slot) may have grown a slot since the capture: pool_gen then differs and
   // the graph, which holds the old pointers, is re-recorded.
@@ -109,6 +109,10 @@ int bg_version(void) { return 100; }
 
 int bg_set_aggregation(int mode, int window_nodes) {
   return guard([&] { set_aggregation(mode, window_nodes); });
+}
+
+int bg_set_persistent(int enable) {
+  return guard([&] { set_persistent_forced(enable != 0); });
 }
 
 int bg_get_aggregation(int* mode, int* window_nodes) {

@@ -426,6 +426,10 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
     if (x0.prec != m.input_prec) fail("model input tag does not match the provided operand");
   }
   m.pool.reset();
+  if (!trace && !timing && !chunks && !single && persistent_forward(m, x0, out, logits, s)) {
+    m.last_out_cols = m.layers[m.layers.size() - 2].w1.cols;
+    return;
+  }
   Hooks h;
   h.trace = trace;
   h.timing = timing;

@@ -128,6 +128,11 @@ struct LayerCall {
 uint64_t graph_generation(const bg_graph* g);
 void run_captured(bg_model& m, bg_model::CaptureSlot& slot, bg_model::Key k, cudaStream_t st,
                   const std::function<void()>& run);
+// persistent.cu: the whole forward as one cooperative kernel for small
+// graphs and binary GCN chains; false when not eligible (nothing launched).
+bool persistent_forward(bg_model& m, const Op& x0, float* out, float* logits, cudaStream_t s);
+bool persistent_forced();             // bg_set_persistent(1)
+void set_persistent_forced(bool on);
 void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace* trace,
                   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>>* timing,
                   cudaStream_t s, StreamChunks* chunks = nullptr, LayerCall* single = nullptr);
