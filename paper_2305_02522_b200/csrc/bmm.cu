@@ -22,6 +22,7 @@ namespace {
 
 constexpr int kWarps = 8;
 constexpr int kMaxOutPerLane = 8;  // output columns per lane per pass (256 per pass)
+constexpr int kRowBatch = 16;      // fp32 row words loaded per round (k_bmm)
 
 template <bool AF, bool OUTB, int M>
 __global__ void __launch_bounds__(kWarps * 32)
@@ -36,41 +37,44 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // fp32 input: the first batch of this warp's first row goes out before the
   // weight staging, so the two latencies overlap (few-row shapes such as
-  // Cora run one row per warp: staging and loads were the whole kernel)
-  float pre[8];
+  // Cora run one row per warp: staging and loads were the whole kernel).
+  // Batches of kRowBatch words (16 x 32 floats in flight per lane): a
+  // 1,433-feature row is 3 dependent load rounds instead of 6.
+  constexpr int B = kRowBatch;
+  float pre[B];
   const int64_t row_first = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
   if (AF && row_first < rows) {
 #pragma unroll
-    for (int m = 0; m < 8; ++m) {
+    for (int m = 0; m < B; ++m) {
       const int64_t j = 32 * m + lane;
       pre[m] = j < k ? __ldg(a_f + row_first * k + j) : -1.0f;
     }
   }
-  for (int64_t t = threadIdx.x; t < nc * kspw; t += blockDim.x) {
-    const int64_t j = t / kspw, w = t % kspw;
-    sw[j * ld + w] = __ldg(wt + (c0 + j) * kspw + w);
-  }
+  // warp per weight row, lanes along its words (no 64-bit division: the
+  // staging loop was half of Cora's FBB instructions)
+  for (int j = warp; j < nc; j += kWarps)
+    for (int w = lane; w < kspw; w += 32) sw[j * ld + w] = __ldg(wt + (c0 + j) * kspw + w);
   __syncthreads();
   uint32_t* arow = srow + warp * kspw;
   for (int64_t row = row_first; row < rows; row += static_cast<int64_t>(gridDim.x) * kWarps) {
     if (AF) {
       const float* xr = a_f + row * k;
-      for (int64_t w0 = 0; w0 < kspw; w0 += 8) {
-        float v[8];
+      for (int64_t w0 = 0; w0 < kspw; w0 += B) {
+        float v[B];
         if (w0 == 0 && row == row_first) {
 #pragma unroll
-          for (int m = 0; m < 8; ++m) v[m] = pre[m];
+          for (int m = 0; m < B; ++m) v[m] = pre[m];
         } else {
 #pragma unroll
-          for (int m = 0; m < 8; ++m) {
+          for (int m = 0; m < B; ++m) {
             const int64_t j = 32 * (w0 + m) + lane;
             v[m] = j < k ? __ldg(xr + j) : -1.0f;
           }
         }
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
+        for (int m = 0; m < B; ++m) {
           const uint32_t word = __brev(__ballot_sync(0xFFFFFFFFu, v[m] >= 0.0f));
-          if (lane == m && w0 + m < kspw) arow[w0 + m] = word;
+          if (lane == (m & 31) && w0 + m < kspw) arow[w0 + m] = word;
         }
       }
     } else {
