@@ -542,14 +542,18 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
       bulk_g2s(ring + static_cast<size_t>(slot) * (tile_bytes / 4), a_f + nt * TR * static_cast<int64_t>(k),
                tile_bytes, &full[slot]);
     }
-    for (int hm = 0; hm < halves * mb; ++hm) {
-    const int mblk = hm % mb, half = hm / mb;
-    uint32_t* const ob = half ? out_bits2 : out_bits;
-    int acc[4][4];
+    for (int mblk = 0; mblk < mb; ++mblk) {
+    // both halves of a paired product share each A fragment load and run as
+    // independent accumulator chains (twice the MMA ILP per k step)
+    int acc[2][4][4];
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) acc[jj][0] = acc[jj][1] = acc[jj][2] = acc[jj][3] = 0;
+    for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) acc[hf][jj][0] = acc[hf][jj][1] = acc[hf][jj][2] = acc[hf][jj][3] = 0;
     const uint8_t* ab = mine + (16 * mblk + g) * lda + 4 * t4;
-    const uint8_t* bb = w8 + (32 * (wq + NW * half) + g) * lda + 4 * t4;
+    const uint8_t* bb0 = w8 + (32 * wq + g) * lda + 4 * t4;
+    const uint8_t* bb1 = w8 + (32 * (wq + NW) + g) * lda + 4 * t4;
+#pragma unroll 4
     for (int ks = 0; ks < ksteps; ++ks) {
       uint32_t a[4];
       a[0] = *reinterpret_cast<const uint32_t*>(ab + 32 * ks);
@@ -558,19 +562,29 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
       a[3] = *reinterpret_cast<const uint32_t*>(ab + 8 * lda + 32 * ks + 16);
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
-        const uint8_t* bp = bb + 8 * jj * lda + 32 * ks;
-        mma_s8(acc[jj], a, *reinterpret_cast<const uint32_t*>(bp), *reinterpret_cast<const uint32_t*>(bp + 16));
+        const uint8_t* bp = bb0 + 8 * jj * lda + 32 * ks;
+        mma_s8(acc[0][jj], a, *reinterpret_cast<const uint32_t*>(bp), *reinterpret_cast<const uint32_t*>(bp + 16));
+      }
+      if (halves == 2) {
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const uint8_t* bp = bb1 + 8 * jj * lda + 32 * ks;
+          mma_s8(acc[1][jj], a, *reinterpret_cast<const uint32_t*>(bp), *reinterpret_cast<const uint32_t*>(bp + 16));
+        }
       }
     }
+    for (int half = 0; half < halves; ++half) {
+    uint32_t* const ob = half ? out_bits2 : out_bits;
     // c0,c1: row g, columns 8jj+2t4, +1; c2,c3: row g+8; bit 31-c of word wq
     uint32_t m0 = 0, m1 = 0;
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj) {
       const int c = 8 * jj + 2 * t4;
-      if (acc[jj][0] >= 0) m0 |= 0x80000000u >> c;
-      if (acc[jj][1] >= 0) m0 |= 0x40000000u >> c;
-      if (acc[jj][2] >= 0) m1 |= 0x80000000u >> c;
-      if (acc[jj][3] >= 0) m1 |= 0x40000000u >> c;
+      const int* ac = acc[half][jj];
+      if (ac[0] >= 0) m0 |= 0x80000000u >> c;
+      if (ac[1] >= 0) m0 |= 0x40000000u >> c;
+      if (ac[2] >= 0) m1 |= 0x80000000u >> c;
+      if (ac[3] >= 0) m1 |= 0x40000000u >> c;
     }
     m0 |= __shfl_xor_sync(0xFFFFFFFFu, m0, 1);
     m0 |= __shfl_xor_sync(0xFFFFFFFFu, m0, 2);
@@ -591,6 +605,7 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
         if (r0 < rows) ob[r0 * ospw + w] = 0u;
         if (r0 + 8 < rows) ob[(r0 + 8) * ospw + w] = 0u;
       }
+    }  // half
     }  // m16 block
     asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(nthr) : "memory");  // int8 tile reusable
   }
@@ -1157,7 +1172,7 @@ int fbb_force() {
   const char* e = std::getenv("BG_FBB");
   if (!e) return 0;
   const std::string v(e);
-  return v == "scalar" ? 1 : v == "imma" ? 2 : v == "tma" ? 3 : 0;
+  return v == "scalar" ? 1 : v == "imma" ? 2 : v == "tma" ? 3 : v == "tc" ? 5 : 0;
 }
 
 bool bmm_pair(const BmmArgs& a, cudaStream_t s) {
@@ -1173,6 +1188,7 @@ bool bmm_pair(const BmmArgs& a, cudaStream_t s) {
     launch<true, true>(a, s);
     return true;
   }
+  if ((force == 0 || force == 5) && fbb_tc(a, s)) return true;
   if (force == 0 || force == 3) return imma_ok(a) && fbb_tma(a, s) == a.rows;
   return false;  // other forced kernels take the products one at a time
 }
@@ -1197,7 +1213,9 @@ void bmm(const BmmArgs& a, cudaStream_t s) {
   }
   if (imma_ok(a)) {
     if (ob) {
-      // whole 16-row tiles on the TMA-fed kernel, the rest on the direct one
+      // the warp-specialized tcgen05 kernel (fbb_tc.cu); else whole 16-row
+      // tiles on the TMA-fed mma.sync kernel, the rest on the direct one
+      if ((force == 0 || force == 5) && fbb_tc(a, s)) return;
       if (fbb_umma(a, s)) return;
       if (fbb_umma2(a, s)) return;
       const int64_t done = force == 2 ? 0 : fbb_tma(a, s);

@@ -128,6 +128,8 @@ void bmm(const BmmArgs& a, cudaStream_t s);
 // Both products of a paired BmmArgs; false (nothing launched) when no kernel
 // takes the pair, so the caller runs the two products separately.
 bool bmm_pair(const BmmArgs& a, cudaStream_t s);
+// fbb_tc.cu: F->B products (and pairs) on tcgen05.mma.kind::i8; false when not eligible
+bool fbb_tc(const BmmArgs& a, cudaStream_t s);
 
 // ---- bspmm.cu ------------------------------------------------------------
 // Integer path (BBB / BBF): out(i,k) = 2*#{j in N(i): x_jk = 1} - deg_i.
