@@ -33,8 +33,8 @@ namespace bg {
 namespace {
 
 constexpr int kTcM = 128;
-constexpr int kTcConv = 8;                       // converter warps
-constexpr int kTcThreads = (6 + kTcConv) * 32;   // 14 warps
+constexpr int kTcConv = 12;                      // converter warps
+constexpr int kTcThreads = (6 + kTcConv) * 32;   // 18 warps
 // warp roles: 0 producer, 1 MMA, 2..3 converters, 4..7 epilogue (warp % 4 =
 // its TMEM lane quarter), 8..13 converters
 __device__ __forceinline__ bool tc_is_conv(int w) { return w == 2 || w == 3 || w >= 8; }
@@ -75,7 +75,7 @@ struct TcArgs {
   const float* x;
   const uint32_t* wt;  // ncols x kspw transposed weight bits (pair: W1 | pad | W2)
   int64_t rows;
-  int k, kspw, kpad, n, ncols, ospw, pr, slots, abufs;
+  int k, kspw, kpad, n, ncols, ospw, pr, prlog, slots, abufs;
   uint32_t pmagic;     // t / gp by magic multiply (item -> row group)
   uint32_t* out;
   uint32_t* out2;      // pair: columns [ncols/2, ncols) of the accumulator
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_fbb_tc(const TcArgs a) {
       uint8_t* At = A + static_cast<size_t>(ab) * kpad * kTcM;
       const int rbase = a.pr * static_cast<int>(u % ppt);
       for (int t = ct; t < items; t += kTcConv * 32) {
-        const int r = t % a.pr, g = t / a.pr;
+        const int r = t & (a.pr - 1), g = t >> a.prlog;  // pr is a power of two
         const int c0 = 16 * g;
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
         if (r < nr) {
@@ -350,6 +350,8 @@ bool fbb_tc(const BmmArgs& a, cudaStream_t s) {
   // mma.sync kernel, which therefore keeps that shape.
   const char* force = std::getenv("BG_FBB");
   if (!force && (t.abufs < 2 || t.pr < 32)) return false;
+  t.prlog = 0;
+  while ((1 << t.prlog) < t.pr) ++t.prlog;
   const size_t smem = wbytes + t.abufs * abytes + static_cast<size_t>(t.slots) * (static_cast<size_t>(t.pr) * a.k + 16) * 4;
   static int attr_done = 0;
   if (!attr_done) {
