@@ -81,3 +81,16 @@ def test_reference_arm_never_maps_the_product_library():
     assert cb["host_cpu"]["logical_cpus"] >= 1
     kb = cb["kernelbench_bspmm_bbb_1thread"]
     assert kb["values_match"] and kb["edges"] > 0 and kb["gteps"] > 0
+
+
+def test_packed_layers_count_bits_and_fused_softmax():
+    # products-shape SAINT: layer 1's MMs and the FC read the packed two-valued
+    # activation; the FC writes logits and probabilities
+    n = 2_449_029
+    sh = {"nodes": n, "features": 100, "hidden": 128, "classes": 47, "model": "saint", "last_conv": 2,
+          "loops_tile_rows": (n + 3) // 4, "loops_nnz_tiles": 0, "raw_tile_rows": (n + 3) // 4,
+          "raw_nnz_tiles": 61_854_024, "packed_layers": [1, 2], "fused_softmax_layer": 2}
+    w = 4 * 128 * 4 + 4 * 128
+    assert bench.kernel_bytes("layer1.mm_self[BMM.FBB]", sh) == 16 * n + w + 16 * n
+    assert bench.kernel_bytes("layer2.mm[BMM.FBF]", sh) == 16 * n + 4 * 47 * 4 + 4 * 47 + 2 * 4 * n * 47
+    assert bench.kernel_bytes("layer0.mm_pair[BMM.FBB]", sh) == 400 * n + 2 * (4 * 128 * 4 + 4 * 128 + 16 * n)
