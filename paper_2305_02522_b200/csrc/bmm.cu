@@ -459,7 +459,7 @@ __device__ __forceinline__ void fbb_convert4(const float* __restrict__ src, int 
   }
 }
 
-template <int NW>  // output words per row (N <= 32*NW); one warp per word
+template <int NW, int HALVES>  // output words per row (N <= 32*NW); one warp per word; 2: paired product
 __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
     k_fbb_tma(const float* __restrict__ a_f, const uint32_t* __restrict__ wt, int64_t rows, int k,
               int kspw, int n, int ksteps, int ospw, uint32_t qmagic, uint32_t kmagic, int mb,
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
   // out_bits2: paired product -- weight columns [32*NW, 64*NW) of wt are a
   // second matrix (same n) whose result goes there; each warp then runs its
   // MMAs twice on the same converted tile
-  const int halves = out_bits2 ? 2 : 1;
+  constexpr int halves = HALVES;
   extern __shared__ __align__(16) uint8_t fbb_smem[];
   __shared__ __align__(8) uint64_t full[kFbbStages];
   const int kpad = 32 * ksteps;
@@ -545,9 +545,9 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
     for (int mblk = 0; mblk < mb; ++mblk) {
     // both halves of a paired product share each A fragment load and run as
     // independent accumulator chains (twice the MMA ILP per k step)
-    int acc[2][4][4];
+    int acc[HALVES][4][4];
 #pragma unroll
-    for (int hf = 0; hf < 2; ++hf)
+    for (int hf = 0; hf < HALVES; ++hf)
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) acc[hf][jj][0] = acc[hf][jj][1] = acc[hf][jj][2] = acc[hf][jj][3] = 0;
     const uint8_t* ab = mine + (16 * mblk + g) * lda + 4 * t4;
@@ -565,15 +565,17 @@ __global__ void __launch_bounds__(kFbbTeams * NW * 32, 1)
         const uint8_t* bp = bb0 + 8 * jj * lda + 32 * ks;
         mma_s8(acc[0][jj], a, *reinterpret_cast<const uint32_t*>(bp), *reinterpret_cast<const uint32_t*>(bp + 16));
       }
-      if (halves == 2) {
+      if constexpr (HALVES == 2) {
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
           const uint8_t* bp = bb1 + 8 * jj * lda + 32 * ks;
-          mma_s8(acc[1][jj], a, *reinterpret_cast<const uint32_t*>(bp), *reinterpret_cast<const uint32_t*>(bp + 16));
+          mma_s8(acc[HALVES - 1][jj], a, *reinterpret_cast<const uint32_t*>(bp),
+                 *reinterpret_cast<const uint32_t*>(bp + 16));
         }
       }
     }
-    for (int half = 0; half < halves; ++half) {
+#pragma unroll
+    for (int half = 0; half < HALVES; ++half) {
     uint32_t* const ob = half ? out_bits2 : out_bits;
     // c0,c1: row g, columns 8jj+2t4, +1; c2,c3: row g+8; bit 31-c of word wq
     uint32_t m0 = 0, m1 = 0;
@@ -1065,9 +1067,15 @@ int64_t fbb_tma(const BmmArgs& a, cudaStream_t s) {
         a.a_f, a.wt, a.rows, static_cast<int>(a.k), kspw, static_cast<int>(a.n), ksteps, ospw, qmagic, kmagic, mb,
         a.out_bits, a.out_bits2);
   };
-  if (NW == 1) go(k_fbb_tma<1>);
-  else if (NW == 2) go(k_fbb_tma<2>);
-  else go(k_fbb_tma<4>);
+  if (halves == 2) {
+    if (NW == 1) go(k_fbb_tma<1, 2>);
+    else if (NW == 2) go(k_fbb_tma<2, 2>);
+    else go(k_fbb_tma<4, 2>);
+  } else {
+    if (NW == 1) go(k_fbb_tma<1, 1>);
+    else if (NW == 2) go(k_fbb_tma<2, 1>);
+    else go(k_fbb_tma<4, 1>);
+  }
   BG_LAUNCH_CHECK();
   return a.rows;
 }
