@@ -131,6 +131,8 @@ void launch_bb_np(const bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, 
   if (per_lane < (1 << 10)) return launch_bb<G, 10, OUTB>(A, x, f, xspw, ob, of, t0, t1, s);
   if (per_lane < (1 << 13)) return launch_bb<G, 13, OUTB>(A, x, f, xspw, ob, of, t0, t1, s);
   if (per_lane < (1 << 16)) return launch_bb<G, 16, OUTB>(A, x, f, xspw, ob, of, t0, t1, s);
+  if (per_lane < (1 << 20)) return launch_bb<G, 20, OUTB>(A, x, f, xspw, ob, of, t0, t1, s);
+  if (per_lane < (1 << 26)) return launch_bb<G, 26, OUTB>(A, x, f, xspw, ob, of, t0, t1, s);
   fail("bspmm: node degree " + std::to_string(A.max_deg) + " exceeds the counter range");
 }
 

@@ -479,6 +479,8 @@ void launch_sl_bb(const bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, 
   else if (per_lane < (1 << 10)) go(k_sl_bb<G, 10, OUTB>);
   else if (per_lane < (1 << 13)) go(k_sl_bb<G, 13, OUTB>);
   else if (per_lane < (1 << 16)) go(k_sl_bb<G, 16, OUTB>);
+  else if (per_lane < (1 << 20)) go(k_sl_bb<G, 20, OUTB>);  // hub rows (power-law graphs)
+  else if (per_lane < (1 << 26)) go(k_sl_bb<G, 26, OUTB>);
   else fail("bspmm: node degree " + std::to_string(A.max_deg) + " exceeds the counter range");
   BG_LAUNCH_CHECK();
 }

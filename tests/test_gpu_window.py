@@ -194,3 +194,65 @@ def test_window_threads_per_row_variants(window_mode, monkeypatch, tpr, v):
         assert bits_equal(got.bits.numpy(), want.bits)
     else:
         assert np.array_equal(got.cpu().numpy(), want.f)
+
+
+def _power_law_edges(n, e, seed, a=1.4):
+    """Directed edges with Zipf-distributed endpoints (heavy-tailed degrees:
+    a few rows of thousands of neighbours next to rows of one or two)."""
+    g = np.random.default_rng(seed)
+    perm = g.permutation(n)
+    s = perm[np.minimum(g.zipf(a, e), n) - 1]
+    d = perm[np.minimum(g.zipf(a, e), n) - 1]
+    mix = g.random(e) < 0.5  # half the draws uniform, so most rows are non-empty
+    s = np.where(mix, g.integers(0, n, e), s)
+    return s.astype(np.int64), d.astype(np.int64)
+
+
+@pytest.mark.parametrize("mode", [L.AGG_AUTO, L.AGG_WINDOW, L.AGG_SLIVERS])
+@pytest.mark.parametrize("v", ["BSpMM.BBB", "BSpMM.BBF"])
+def test_skewed_degree_graph_every_layout(mode, v):
+    # the windowed kernel gives a warp's 32 rows one loop count per step: on a
+    # heavy-tailed degree profile (max degree in the thousands) the rows of a
+    # warp are far apart -- results must stay exact
+    n, e = 20000, 1_500_000
+    s, d = _power_law_edges(n, e, 17)
+    A = po.frdc_from_edges(n, s, d, True)
+    dA = bg.frdc_from_edges(n, s, d, True)
+    assert dA.info().max_row_degree > 2000
+    X = po.Rng(17).random_dense(n, 128)
+    dx, ox = _bits_operand(X, 32)
+    bg.set_aggregation(mode, 0)
+    try:
+        got = bg.bspmm(v, bg.AdjacencyOperand(dA), dx, None, 32)
+    finally:
+        bg.set_aggregation(L.AGG_AUTO, 0)
+    want = po.bspmm(v, A, ox, None, None, 32)
+    if want.prec == po.B:
+        assert bits_equal(got.bits.numpy(), want.bits)
+    else:
+        assert np.array_equal(got.cpu().numpy(), want.f)
+
+
+@pytest.mark.parametrize("mode", [L.AGG_AUTO, L.AGG_SLIVERS, L.AGG_TILES])
+def test_hub_row_beyond_16_bit_counters(mode):
+    # a hub row with ~150 K neighbours (multi-bit nibbles throughout): every
+    # layout must count past 2^16 per lane, as the reference does at any degree
+    n = 160_000
+    hub = np.zeros(150_000, np.int64)
+    s = np.concatenate([hub, np.arange(n, dtype=np.int64)])
+    d = np.concatenate([np.arange(150_000, dtype=np.int64), (np.arange(n, dtype=np.int64) * 7) % n])
+    A = po.frdc_from_edges(n, s, d, True)
+    dA = bg.frdc_from_edges(n, s, d, True)
+    X = po.Rng(31).random_dense(n, 128)
+    dx, ox = _bits_operand(X, 32)
+    bg.set_aggregation(mode, 0)
+    try:
+        for v in ("BSpMM.BBB", "BSpMM.BBF"):
+            got = bg.bspmm(v, bg.AdjacencyOperand(dA), dx, None, 32)
+            want = po.bspmm(v, A, ox, None, None, 32)
+            if want.prec == po.B:
+                assert bits_equal(got.bits.numpy(), want.bits)
+            else:
+                assert np.array_equal(got.cpu().numpy(), want.f)
+    finally:
+        bg.set_aggregation(L.AGG_AUTO, 0)
