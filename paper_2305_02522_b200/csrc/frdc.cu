@@ -149,8 +149,10 @@ __global__ void k_sliver_count(const uint64_t* __restrict__ rp, const uint16_t* 
     if (lane == 0 && 4 * tr + r < rows) {
       const int padded = (c[r] + kSliverPad - 1) / kSliverPad * kSliverPad;
       cnt[4 * tr + r] = static_cast<unsigned long long>(padded);
-      atomicMax(maxima, padded);
-      atomicMax(maxima + 1, deg[4 * tr + r] - c[r]);
+      if (deg[4 * tr + r] < kHubDeg) {  // hub rows: hubs.cu
+        atomicMax(maxima, padded);
+        atomicMax(maxima + 1, deg[4 * tr + r] - c[r]);
+      }
     }
   }
 }
@@ -223,6 +225,8 @@ unsigned grid1(int64_t n, int bs = 256) { return static_cast<unsigned>(cdiv(n, b
 void frdc_finalize(bg_frdc& m, cudaStream_t s) {
   m.nslivers = -1;  // derived views are rebuilt on next use
   ++m.gen;
+  m.hub.n = -1;
+  m.hub.cnt_words = 0;
   m.win.T = 0;
   m.nbits_view = -1;
   m.degree.alloc(static_cast<size_t>(std::max<int64_t>(m.rows, 1)) * 4);

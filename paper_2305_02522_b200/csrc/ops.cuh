@@ -11,6 +11,9 @@ constexpr int kSliverPad = 8;
 constexpr uint32_t kSliverSentinel = 0xFFFFFFF8u;  // node column 2^29-1, no extra bits
 constexpr int kBitPad = 64;
 
+// Node rows at least this long are hub rows of the BB aggregations (hubs.cu).
+constexpr int kHubDeg = 2048;
+
 struct bg_frdc {
   int64_t rows = 0, cols = 0, tile_rows = 0, tile_cols = 0, nnz = 0, nnz_bits = 0;
   int64_t max_deg = 0;
@@ -35,8 +38,10 @@ struct bg_frdc {
   bg::DevBuf sliver_ptr;  // u64[rows + 1]
   bg::DevBuf slivers;     // u32[nslivers]
   int64_t nslivers = -1;  // -1: not built
-  int64_t max_sl_row = 0;      // most entries (padded) in one node row
-  int64_t max_extra_bits = 0;  // most (bits - slivers) in one node row
+  // most entries (padded) / most (bits - slivers) in one node row of degree
+  // < kHubDeg (the hub rows are counted by hub_bb)
+  int64_t max_sl_row = 0;
+  int64_t max_extra_bits = 0;
   // Bit-entry view (frdc_bitview), built once on first use: for node row i,
   // the node column of every adjacency bit in ascending order (the
   // reference's walk order), padded to a multiple of kBitPad entries with the
@@ -55,6 +60,18 @@ struct bg_frdc {
     bg::DevBuf steplen;  // u16[nb*(T/32)*nw] groups per step
     bg::DevBuf ell;      // u16 entries (ring record index)
   } win;
+  // Hub rows (hubs.cu), found once on first use: node rows of degree >=
+  // kHubDeg.  The BB aggregation kernels see them as empty rows and hub_bb
+  // counts them split over the SMs.
+  struct Hubs {
+    int64_t n = -1;  // -1: not built
+    int64_t nchunks = 0;
+    int64_t max_light_deg = 0;  // largest degree of the other rows
+    bg::DevBuf rows;            // i32[n]
+    bg::DevBuf chunks;          // uint4[nchunks]: first tile, tiles, hub << 2 | row in tile row
+    bg::DevBuf cnt;             // i32[n * cnt_words * 32], zero between calls
+    int64_t cnt_words = 0;
+  } hub;
   const uint64_t* srp() const { return sliver_ptr.as<uint64_t>(); }
   const uint32_t* sl() const { return slivers.as<uint32_t>(); }
   const uint64_t* rp() const { return row_ptr.as<uint64_t>(); }
@@ -189,6 +206,11 @@ bool window_bb(bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* out_b
                float* out_f, cudaStream_t s, int64_t r0, int64_t r1);
 // sliver.cu: BBB/BBF for short rows (lane group per row over the bit-entry
 // view); false when not eligible (mode != AUTO, > 8 words, average degree >= 64).
+// hubs.cu: the hub rows of [r0, r1) (BSpMM.BBB / BBF), after the main kernel
+void frdc_hubs(bg_frdc& m, cudaStream_t s);
+int64_t light_max_deg(bg_frdc& m, cudaStream_t s);  // largest degree below kHubDeg
+void hub_bb(bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uint32_t* out_bits, float* out_f,
+            cudaStream_t s, int64_t r0, int64_t r1);
 bool rowgroup_bb(bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uint32_t* out_bits, float* out_f,
                  cudaStream_t s, int64_t r0, int64_t r1);
 

@@ -56,7 +56,9 @@ __global__ void __launch_bounds__(kSlWarps * 32)
 #pragma unroll
     for (int q = 0; q < NP; ++q) P[q] = 0;
     const uint64_t e0 = srp[i];
-    const uint32_t len = static_cast<uint32_t>(srp[i + 1] - e0);  // multiple of kSliverPad
+    const uint32_t deg = static_cast<uint32_t>(__ldg(degree + i));
+    // multiple of kSliverPad; hub rows are counted by hub_bb (hubs.cu)
+    const uint32_t len = deg < kHubDeg ? static_cast<uint32_t>(srp[i + 1] - e0) : 0u;
     const uint32_t* rowp = sl + e0 + slot;
     for (uint32_t off = 0; off < len; off += B) {
       const uint32_t mcount = min(8u, (len - off) / S);  // warp-uniform (len % 8 == 0, S | 8)
@@ -92,7 +94,6 @@ __global__ void __launch_bounds__(kSlWarps * 32)
     __syncwarp();
     uint32_t Q[NQ];
     slot_reduce<G, NP, NQ>(P, Q);
-    const uint32_t deg = static_cast<uint32_t>(__ldg(degree + i));
     if (!word_ok) {
     } else if (OUTB) {
       // cnt >= ceil(deg/2)  <=>  2*cnt - deg >= 0   (kernels.cpp:440-454)
@@ -132,14 +133,15 @@ __global__ void __launch_bounds__(256)
     const int64_t i = i0 + r;
     const bool ok = i < row1;
     const uint32_t deg = ok ? static_cast<uint32_t>(__ldg(degree + i)) : 0u;
-    uint32_t mx = deg;
+    const uint32_t walk = deg < kHubDeg ? deg : 0u;  // hub rows: hub_bb (hubs.cu)
+    uint32_t mx = walk;
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
     const uint32_t* cols = bc + (ok ? bp[i] : 0);
     uint32_t P[NP];
 #pragma unroll
     for (int q = 0; q < NP; ++q) P[q] = 0u;
-    const uint32_t padded = (deg + kBitPad - 1) / kBitPad * kBitPad;  // this row's view length
+    const uint32_t padded = (walk + kBitPad - 1) / kBitPad * kBitPad;  // this row's view length
     for (uint32_t j = 0; j < mx; j += 8) {
       // the row's next 8 column indices as two 16-byte loads (the 4 lanes of
       // a row read the same address: one request), not 8 scalar loads per
@@ -154,7 +156,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int m = 0; m < 8; ++m) {
         v[m] = 0u;
-        if (j + m < deg && word_ok) v[m] = __ldg(xg + static_cast<int64_t>(cc[m]) * xspw);
+        if (j + m < walk && word_ok) v[m] = __ldg(xg + static_cast<int64_t>(cc[m]) * xspw);
       }
       hs_add8<NP>(P, v);
     }
@@ -516,7 +518,7 @@ bool launch_bv_bb(bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uint32
     kern<<<blocks, 256, 0, s>>>(A.bit_ptr.as<uint64_t>(), A.bit_cols.as<uint32_t>(), r0, r1, A.deg(), x, xspw,
                                 f, ob, of);
   };
-  const int64_t d = A.max_deg;
+  const int64_t d = light_max_deg(A, s);
   if (d < (1 << 6)) go(k_bv_bb<G, 6, OUTB>);
   else if (d < (1 << 9)) go(k_bv_bb<G, 9, OUTB>);
   else if (d < (1 << 12)) go(k_bv_bb<G, 12, OUTB>);
@@ -531,7 +533,7 @@ bool rowgroup_bb(bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uint32_
                  cudaStream_t s, int64_t r0, int64_t r1) {
   // AUTO only: the SLIVERS / TILES / WINDOW modes keep their kernels (coverage)
   if (aggregation_mode() != BG_AGG_AUTO) return false;
-  if (xspw > 8 || A.rows == 0 || A.max_deg >= (int64_t{1} << 16)) return false;
+  if (xspw > 8 || A.rows == 0) return false;
   if (A.nnz_bits >= 64 * A.rows) return false;  // long rows: the 8-slot sliver split balances better
   const bool ob = out_bits != nullptr;
   auto run = [&](auto gtag) {
@@ -550,8 +552,8 @@ void sliver_bb(bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* out_b
   if (r1 < 0) r1 = A.rows;
   const int64_t xspw = spw(f, wb);
   if (r1 <= r0 || xspw == 0) return;
-  if (window_bb(A, x, f, wb, out_bits, out_f, s, r0, r1)) return;
-  if (rowgroup_bb(A, x, f, xspw, out_bits, out_f, s, r0, r1)) return;
+  if (window_bb(A, x, f, wb, out_bits, out_f, s, r0, r1) || rowgroup_bb(A, x, f, xspw, out_bits, out_f, s, r0, r1))
+    return hub_bb(A, x, f, xspw, out_bits, out_f, s, r0, r1);
   frdc_slivers(A, s);
   const bool ob = out_bits != nullptr;
   if (xspw <= 4) {
@@ -567,6 +569,7 @@ void sliver_bb(bg_frdc& A, const uint32_t* x, int64_t f, int wb, uint32_t* out_b
     if (ob) launch_sl_bb<32, true>(A, x, f, xspw, out_bits, out_f, r0, r1, s);
     else launch_sl_bb<32, false>(A, x, f, xspw, out_bits, out_f, r0, r1, s);
   }
+  hub_bb(A, x, f, xspw, out_bits, out_f, s, r0, r1);
 }
 
 void sliver_f(bg_frdc& A, const SpmmFArgs& a, cudaStream_t s, int64_t r0, int64_t r1) {

@@ -67,9 +67,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 // Thread per node row: entries per half-window (u16, row-major rows x nh).
 __global__ void k_win_count(const uint64_t* __restrict__ srp, const uint32_t* __restrict__ sl,
-                            int64_t rows, int Wh, int nh, uint16_t* __restrict__ cnt) {
+                            int64_t rows, int Wh, int nh, const int32_t* __restrict__ deg,
+                            uint16_t* __restrict__ cnt) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= rows) return;
+  if (i >= rows || deg[i] >= kHubDeg) return;  // hub rows: no entries (hubs.cu)
   uint16_t* c = cnt + i * nh;
   int cur = -1;
   uint32_t run = 0;
@@ -131,9 +132,9 @@ __global__ void k_fill_u16(uint16_t* __restrict__ p, int64_t n, uint16_t v) {
 __global__ void k_win_fill(const uint64_t* __restrict__ srp, const uint32_t* __restrict__ sl,
                            int64_t rows, int RW, int Wh, int nh, const uint16_t* __restrict__ nk,
                            const uint32_t* __restrict__ sbase, const uint16_t* __restrict__ steplen,
-                           uint16_t* __restrict__ ell) {
+                           const int32_t* __restrict__ deg, uint16_t* __restrict__ ell) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= rows) return;
+  if (i >= rows || deg[i] >= kHubDeg) return;
   const int64_t wv = i / RW;  // = b * (RB/RW) + v (RB is a multiple of RW)
   const int lane = static_cast<int>(i % RW);
   const uint16_t* n = nk + i * nh;
@@ -644,7 +645,7 @@ void build_windows(bg_frdc& A, int RB, int RW, int Wh, cudaStream_t s) {
   BG_CUDA(cudaMemsetAsync(total.p, 0, total.bytes, s));
   if (rows > 0)
     k_win_count<<<static_cast<unsigned>(cdiv(rows, 256)), 256, 0, s>>>(A.srp(), A.sl(), rows, Wh, nh,
-                                                                       cnt.as<uint16_t>());
+                                                                       A.deg(), cnt.as<uint16_t>());
   BG_LAUNCH_CHECK();
   if (nbv > 0)
     k_win_sched<<<static_cast<unsigned>(cdiv(nbv * 32, 256)), 256, 0, s>>>(
@@ -669,7 +670,7 @@ void build_windows(bg_frdc& A, int RB, int RW, int Wh, cudaStream_t s) {
   if (rows > 0)
     k_win_fill<<<static_cast<unsigned>(cdiv(rows, 256)), 256, 0, s>>>(
         A.srp(), A.sl(), rows, RW, Wh, nh, nk.as<uint16_t>(), W.seg.as<uint32_t>(), W.steplen.as<uint16_t>(),
-        W.ell.as<uint16_t>());
+        A.deg(), W.ell.as<uint16_t>());
   BG_LAUNCH_CHECK();
   if (nbv > 0)
     k_win_bankorder<<<static_cast<unsigned>(cdiv(nbv * (RW / 8), 128)), 128, 0, s>>>(
@@ -734,7 +735,7 @@ bool launch_win(bg_frdc& A, const uint32_t* x, int64_t f, uint32_t* ob, float* o
 template <bool OUTB>
 bool launch_win_np(bg_frdc& A, const uint32_t* x, int64_t f, uint32_t* ob, float* of, int64_t r0,
                    int64_t r1, cudaStream_t s) {
-  const int64_t d = A.max_deg;
+  const int64_t d = light_max_deg(A, s);  // hub rows: hubs.cu
   auto go = [&](auto tpr) {
     constexpr int TPR = decltype(tpr)::value;
     if (d < (1 << 6)) return launch_win<6, OUTB, TPR>(A, x, f, ob, of, r0, r1, s);

@@ -18,7 +18,7 @@ from test_gpu_window import _power_law_edges  # noqa: E402
 
 n, e = 232_965, 114_615_892
 out = {}
-for name in ("uniform", "zipf1.4"):
+for name in (sys.argv[1:] or ("uniform", "zipf1.4")):
     if name == "uniform":
         s, d = bg.Rng(100).random_edges(n, e, False)
     else:

@@ -256,3 +256,61 @@ def test_hub_row_beyond_16_bit_counters(mode):
                 assert np.array_equal(got.cpu().numpy(), want.f)
     finally:
         bg.set_aggregation(L.AGG_AUTO, 0)
+
+
+def _hub_graph(n, e, seed, a=1.3):
+    s, d = _power_law_edges(n, e, seed, a)
+    dA = bg.frdc_from_edges(n, s, d, True)
+    deg = np.bincount(s[s != d], minlength=n) + 1  # + self loop (upper bound: duplicates merge)
+    return s, d, dA, int((deg >= 2048).sum())
+
+
+@pytest.mark.parametrize("mode", [L.AGG_AUTO, L.AGG_WINDOW, L.AGG_SLIVERS])
+@pytest.mark.parametrize("f,wb", [(128, 32), (40, 32), (300, 32), (128, 64)])
+def test_hub_rows_split_over_the_gpu(mode, f, wb):
+    # rows of degree >= 2048 leave the per-row kernels and are counted by
+    # the split hub kernel (hubs.cu): many hubs, every feature width, both
+    # outputs -- bit-identical to the reference's per-row walk
+    n, e = 60000, 4_000_000
+    s, d, dA, hubs = _hub_graph(n, e, 23)
+    assert hubs >= 20 and dA.info().max_row_degree > 15000
+    A = po.frdc_from_edges(n, s, d, True)
+    X = po.Rng(23).random_dense(n, f)
+    dx, ox = _bits_operand(X, wb)
+    bg.set_aggregation(mode, 0)
+    try:
+        for v in ("BSpMM.BBB", "BSpMM.BBF"):
+            got = bg.bspmm(v, bg.AdjacencyOperand(dA), dx, None, wb)
+            want = po.bspmm(v, A, ox, None, None, wb)
+            if want.prec == po.B:
+                assert bits_equal(got.bits.numpy(), want.bits)
+            else:
+                assert np.array_equal(got.cpu().numpy(), want.f)
+    finally:
+        bg.set_aggregation(L.AGG_AUTO, 0)
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_hub_graph_model_forward_sharded_and_captured(world):
+    # a 3-layer binary GCN on the power-law graph: hub rows in every rank's
+    # row range, the forward captured and replayed; equal to the
+    # layer-by-layer forward and to the oracle
+    from paper_2305_02522_b200.sharded import forward_virtual_ranks, partition_bounds
+    n, e, f, h, c = 60000, 4_000_000, 100, 128, 9
+    s, d = _power_law_edges(n, e, 29, 1.3)
+    plan = ["MM.FBB+BSpMM.BBB", "MM.BBB+BSpMM.BBB", "MM.BBF+BSpMM.FBF"]
+    layers, X = po.build_model("gcn", f, h, c, 99, n, plan)
+    g = bg.prepare_graph(n, s, d)
+    m = bg.Model(to_layer_specs(bg, layers), g)
+    x = torch.from_numpy(X).cuda()
+    ref_out, ref_log, _ = m.forward_traced(x)
+    for _ in range(3):  # eager, captured, replayed
+        out = m.forward(x)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref_out)
+    rp, _, _ = g.structure.download()
+    out, lg = forward_virtual_ranks(m, x, partition_bounds(rp, n, world), logits=True)
+    torch.cuda.synchronize()
+    assert torch.equal(lg, ref_log) and torch.equal(out, ref_out)
+    o_out, o_log, _ = po.run_model(layers, po.Graph(n, s, d), X)
+    assert np.array_equal(lg.cpu().numpy(), o_log)
