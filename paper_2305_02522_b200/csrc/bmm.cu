@@ -22,7 +22,7 @@ namespace {
 
 constexpr int kWarps = 8;
 constexpr int kMaxOutPerLane = 8;  // output columns per lane per pass (256 per pass)
-constexpr int kRowBatch = 16;      // fp32 row words loaded per round (k_bmm)
+constexpr int kF4 = 4;             // float4 chunks per lane in flight (k_bmm fp32 rows: 512 floats per warp round)
 
 template <bool AF, bool OUTB, int M>
 __global__ void __launch_bounds__(kWarps * 32)
@@ -35,48 +35,88 @@ __global__ void __launch_bounds__(kWarps * 32)
   uint32_t* sw = smem;                       // nc x ld transposed weight words
   uint32_t* srow = smem + 32 * M * ld;       // kWarps x kspw packed activation rows (after all 32*M weight rows the lanes read)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // fp32 input: the first batch of this warp's first row goes out before the
-  // weight staging, so the two latencies overlap (few-row shapes such as
-  // Cora run one row per warp: staging and loads were the whole kernel).
-  // Batches of kRowBatch words (16 x 32 floats in flight per lane): a
-  // 1,433-feature row is 3 dependent load rounds instead of 6.
-  constexpr int B = kRowBatch;
-  float pre[B];
+  // fp32 input: 16-byte loads from the row's 16-byte-aligned frame (t = the
+  // float's index from the aligned address below the row start, s = the row
+  // start's offset in it), lane per float4 chunk: a nibble of signs per
+  // chunk, 8 lanes' nibbles OR-shuffled into one aligned word A_v (floats t
+  // in [32v, 32v+32)), then each packed row word is the funnel shift
+  // (A_w, A_w+1) << s.  kF4 chunks per lane are in flight at once (1,536
+  // floats per warp: a Cora row is one DRAM round trip).  The first batch of
+  // this warp's first row goes out before the weight staging, so the two
+  // latencies overlap.
+  constexpr int B4 = kF4;
+  // 32-bit index math below (row offsets stay 64-bit): k < 2^28 floats
+  const int kk = static_cast<int>(k), kw = static_cast<int>(kspw);
+  const int nwa = kw + 1;  // aligned words A_0 .. A_kspw
+  const int nch = 8 * nwa; // chunks covering them
+  uint32_t* araw = srow + kWarps * kw + warp * (kw + 2);
+  auto frame = [&](int64_t row, int& sh) {
+    const uintptr_t p = reinterpret_cast<uintptr_t>(a_f + row * k);
+    sh = static_cast<int>((p >> 2) & 3);
+    return reinterpret_cast<const float4*>(p - 4 * static_cast<uintptr_t>(sh));
+  };
+  auto load = [&](const float4* xa, int sh, int c0, float4 (&v)[B4]) {
+    const int lim = (sh + kk + 3) >> 2;  // chunks holding row floats
+#pragma unroll
+    for (int m = 0; m < B4; ++m) {
+      const int c = c0 + 32 * m + lane;
+      v[m] = c < lim ? __ldg(xa + c) : make_float4(-1.0f, -1.0f, -1.0f, -1.0f);
+    }
+  };
+  float4 pre[B4];
   const int64_t row_first = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
   if (AF && row_first < rows) {
-#pragma unroll
-    for (int m = 0; m < B; ++m) {
-      const int64_t j = 32 * m + lane;
-      pre[m] = j < k ? __ldg(a_f + row_first * k + j) : -1.0f;
+    int sh;
+    const float4* xa = frame(row_first, sh);
+    load(xa, sh, 0, pre);
+  }
+  // warp per weight row, lanes along its words; asynchronous copies, so
+  // every word is in flight at once instead of one L2 round trip per row
+  {
+    // the pass's nc x kspw weight words are contiguous: a flat copy, word t
+    // of weight row j = t / kspw landing at t + j * (ld - kspw)
+    const uint32_t* wsrc = wt + c0 * kspw;
+    const uint32_t total = static_cast<uint32_t>(nc * kspw), pad = static_cast<uint32_t>(ld - kspw);
+    if (pad == 0 && (total & 3u) == 0 && (reinterpret_cast<uintptr_t>(wsrc) & 15) == 0) {
+      for (uint32_t t = 4 * threadIdx.x; t < total; t += 4 * blockDim.x) cp_async16(sw + t, wsrc + t);
+    } else {
+      const uint32_t magic = 0xFFFFFFFFu / static_cast<uint32_t>(kw) + 1u;  // t / kspw = umulhi(t, magic) (t * kspw < 2^31)
+      for (uint32_t t = threadIdx.x; t < total; t += blockDim.x)
+        cp_async4(sw + t + __umulhi(t, magic) * pad, wsrc + t);
     }
   }
-  // warp per weight row, lanes along its words (no 64-bit division: the
-  // staging loop was half of Cora's FBB instructions)
-  for (int j = warp; j < nc; j += kWarps)
-    for (int w = lane; w < kspw; w += 32) sw[j * ld + w] = __ldg(wt + (c0 + j) * kspw + w);
+  cp_async_wait_all();
   __syncthreads();
   uint32_t* arow = srow + warp * kspw;
   for (int64_t row = row_first; row < rows; row += static_cast<int64_t>(gridDim.x) * kWarps) {
     if (AF) {
-      const float* xr = a_f + row * k;
-      for (int64_t w0 = 0; w0 < kspw; w0 += B) {
-        float v[B];
-        if (w0 == 0 && row == row_first) {
+      int sh;
+      const float4* xa = frame(row, sh);
+      const int lo = sh, hi = sh + kk;  // row floats: t in [lo, hi)
+      for (int c0 = 0; c0 < nch; c0 += 32 * B4) {
+        float4 (&v)[B4] = pre;  // the first batch of the first row is already in flight
+        if (c0 != 0 || row != row_first) load(xa, sh, c0, v);
 #pragma unroll
-          for (int m = 0; m < B; ++m) v[m] = pre[m];
-        } else {
+        for (int m = 0; m < B4; ++m) {
+          if (c0 + 32 * m >= nch) break;  // warp-uniform
+          const int c = c0 + 32 * m + lane, t0 = 4 * c;
+          uint32_t nib = (v[m].x >= 0.0f ? 8u : 0u) | (v[m].y >= 0.0f ? 4u : 0u) | (v[m].z >= 0.0f ? 2u : 0u) |
+                         (v[m].w >= 0.0f ? 1u : 0u);
+          if (t0 < lo || t0 + 4 > hi) {  // chunk straddles the row's ends
+            uint32_t msk = 0;
 #pragma unroll
-          for (int m = 0; m < B; ++m) {
-            const int64_t j = 32 * (w0 + m) + lane;
-            v[m] = j < k ? __ldg(xr + j) : -1.0f;
+            for (int q = 0; q < 4; ++q) msk |= (t0 + q >= lo && t0 + q < hi) ? (8u >> q) : 0u;
+            nib &= msk;
           }
-        }
-#pragma unroll
-        for (int m = 0; m < B; ++m) {
-          const uint32_t word = __brev(__ballot_sync(0xFFFFFFFFu, v[m] >= 0.0f));
-          if (lane == (m & 31) && w0 + m < kspw) arow[w0 + m] = word;
+          uint32_t w = nib << (28 - 4 * (lane & 7));
+          w |= __shfl_xor_sync(0xFFFFFFFFu, w, 1);
+          w |= __shfl_xor_sync(0xFFFFFFFFu, w, 2);
+          w |= __shfl_xor_sync(0xFFFFFFFFu, w, 4);
+          if ((lane & 7) == 0 && (c >> 3) < nwa) araw[c >> 3] = w;
         }
       }
+      __syncwarp();
+      for (int w = lane; w < kw; w += 32) arow[w] = __funnelshift_l(araw[w + 1], araw[w], sh);
     } else {
       for (int64_t w = lane; w < kspw; w += 32) arow[w] = __ldg(a_bits + row * kspw + w);
     }
@@ -85,10 +125,12 @@ __global__ void __launch_bounds__(kWarps * 32)
 #pragma unroll
     for (int m = 0; m < M; ++m) diff[m] = 0;
     const uint32_t* swl = sw + lane * ld;
-    for (int64_t w = 0; w < kspw; ++w) {
+    const int kw2 = static_cast<int>(kspw), ld2 = static_cast<int>(ld);
+#pragma unroll 4
+    for (int w = 0; w < kw2; ++w) {
       const uint32_t aw = arow[w];
 #pragma unroll
-      for (int m = 0; m < M; ++m) diff[m] += __popc(aw ^ swl[32 * m * ld + w]);
+      for (int m = 0; m < M; ++m) diff[m] += __popc(aw ^ swl[32 * m * ld2 + w]);
     }
     __syncwarp();
     if (OUTB) {
@@ -150,8 +192,10 @@ __global__ void __launch_bounds__(kLrWarps * 32)
   uint32_t* stage = sw + kspw * npad + (threadIdx.x >> 5) * 32 * ld;
   for (int t = threadIdx.x; t < kspw * npad; t += blockDim.x) {
     const int w = t / npad, o = t % npad;
-    sw[t] = o < n ? __ldg(wt + static_cast<int64_t>(o) * kspw + w) : 0u;
+    if (o < n) cp_async4(sw + t, wt + static_cast<int64_t>(o) * kspw + w);  // all in flight at once
+    else sw[t] = 0u;
   }
+  cp_async_wait_all();
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = static_cast<int64_t>(blockIdx.x) * kLrWarps + (threadIdx.x >> 5);
@@ -1160,7 +1204,7 @@ void launch(const BmmArgs& a, cudaStream_t s) {
   for (int64_t c0 = 0; c0 < ntot; c0 += pass) {
     const int64_t nc = std::min(pass, ntot - c0);
     const int64_t mcols = nc <= 32 ? 32 : nc <= 64 ? 64 : nc <= 128 ? 128 : nc <= 256 ? 256 : 512;  // 32*M of pick(nc)
-    const size_t smem = static_cast<size_t>(mcols * ld + kWarps * kspw) * 4;
+    const size_t smem = static_cast<size_t>(mcols * ld + kWarps * kspw + (AF ? kWarps * (kspw + 2) : 0)) * 4;
     auto kern = pick(nc);
     if (smem > 48 * 1024) BG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                       static_cast<int>(smem)));

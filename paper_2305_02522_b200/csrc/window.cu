@@ -44,6 +44,13 @@ constexpr int kWinRec = 16;             // bytes per packed node row (4 u32 word
 #define BG_WIN_SLOTS 3
 #endif
 constexpr int kSlots = BG_WIN_SLOTS;    // ring slots; half h lives in slot h % kSlots
+#ifndef BG_WIN_CHOICES
+#define BG_WIN_CHOICES (BG_WIN_SLOTS >= 4 ? 3 : 2)
+#endif
+// halves a step may count: step k finishes half k and tops its lanes up with
+// the first edges of halves k+1 .. k+kChoices-1 (in column order)
+constexpr int kChoices = BG_WIN_CHOICES;
+static_assert(kSlots > kChoices && kChoices >= 2, "the ring holds the step's halves plus one refill");
 // records per ring slot: 4 x 56 KB (or 3 x 64 KB) of shared memory
 constexpr int kSlotRec = kSlots == 4 ? 3584 : 4096;  // 64 KB slots by default
 constexpr int kWinHalf = kSlotRec - 1;  // node rows per half-window (the last record stays zero)
@@ -104,16 +111,27 @@ __global__ void k_win_sched(const uint16_t* __restrict__ cnt, int64_t rows, int 
   const int v = static_cast<int>(wv % streams);
   const int64_t i = b * RB + v * RW + lane;
   const bool ok = lane < RW && i < rows;
-  uint32_t q0 = ok ? cnt[i * nh] : 0u, sum = 0;
+  uint32_t left[kChoices];  // entries of halves k .. k+kChoices-1 not yet scheduled
+#pragma unroll
+  for (int c = 0; c < kChoices; ++c) left[c] = (ok && c < kChoices - 1 && c < nh) ? cnt[i * nh + c] : 0u;
+  uint32_t sum = 0;
   for (int k = 0; k < nh; ++k) {
-    uint32_t m = q0;
+    uint32_t m = left[0];
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
     const uint32_t K = (m + 7) & ~7u;
-    const uint32_t c1 = (ok && k + 1 < nh) ? cnt[i * nh + k + 1] : 0u;
-    const uint32_t take1 = min(K - q0, c1);
-    if (ok) nk[i * nh + k] = static_cast<uint16_t>(q0 + take1);
-    q0 = c1 - take1;
+    left[kChoices - 1] = (ok && k + kChoices - 1 < nh) ? cnt[i * nh + k + kChoices - 1] : 0u;
+    uint32_t room = K - left[0], n = left[0];
+#pragma unroll
+    for (int c = 1; c < kChoices; ++c) {  // in column order: half k+1 before k+2
+      const uint32_t t = min(room, left[c]);
+      left[c] -= t;
+      room -= t;
+      n += t;
+    }
+    if (ok) nk[i * nh + k] = static_cast<uint16_t>(n);
+#pragma unroll
+    for (int c = 0; c + 1 < kChoices; ++c) left[c] = left[c + 1];
     if (lane == 0) steplen[wv * nh + k] = static_cast<uint16_t>(K / 4);
     sum += K / 4;
   }
@@ -444,8 +462,8 @@ __global__ void __launch_bounds__(TPR == 1 ? (NP <= 10 ? kWinMaxThreads : 480) :
   __syncthreads();
   const int mine = b1 - b0 - static_cast<int>(blockIdx.x);
   const int nblk = mine > 0 ? (mine + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x) : 0;
-  const int nsteps = nblk * nh;  // one half-window per step; nh % 3 == 0
-  auto issue = [&](int H) {      // half H of this CTA's sequence into slot H % 3
+  const int nsteps = nblk * nh;  // one half-window per step; nh % kSlots == 0
+  auto issue = [&](int H) {      // half H of this CTA's sequence into slot H % kSlots
     const int64_t n0 = static_cast<int64_t>(H % nh) * Wh;
     const int64_t nodes = min(static_cast<int64_t>(Wh), xrows - n0);
     uint64_t* bar = &full[H % kSlots];
@@ -504,15 +522,14 @@ __global__ void __launch_bounds__(TPR == 1 ? (NP <= 10 ? kWinMaxThreads : 480) :
     ++S;
     if (++slot == kSlots) slot = 0, ++use;
   };
-  // step S may count entries of halves S and S+1: S was waited for at step
-  // S-1 (its slot cannot be refilled before every warp has finished step S)
-  auto wait_next = [&]() {
-    if (S + 1 < nsteps) {
-      const int s1 = slot == kSlots - 1 ? 0 : slot + 1;
-      mbar_wait_sleep(&full[s1], (use + (slot == kSlots - 1)) & 1u);
-    }
+  // step S may count entries of halves S .. S+kChoices-1: all but the last
+  // were waited for at earlier steps (a slot cannot be refilled before every
+  // warp has finished the step of its half)
+  auto wait_half = [&](int H) {
+    if (H < nsteps) mbar_wait_sleep(&full[H % kSlots], static_cast<uint32_t>(H / kSlots) & 1u);
   };
-  if (nsteps > 0) mbar_wait(&full[0], 0u);
+  auto wait_next = [&]() { wait_half(S + kChoices - 1); };
+  for (int H = 0; H + 1 < kChoices; ++H) wait_half(H);
   for (int bi = 0; bi < nblk; ++bi) {
 #pragma unroll
     for (int q = 0; q < W; ++q)
