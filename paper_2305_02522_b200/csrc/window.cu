@@ -467,7 +467,11 @@ __global__ void __launch_bounds__(TPR == 1 ? (NP <= 10 ? kWinMaxThreads : 480) :
     const int64_t n0 = static_cast<int64_t>(H % nh) * Wh;
     const int64_t nodes = min(static_cast<int64_t>(Wh), xrows - n0);
     uint64_t* bar = &full[H % kSlots];
+#if defined(BG_WIN_PROBE) && BG_WIN_PROBE >= 2
+    if (false) {  // timing probe: no refills, results are wrong
+#else
     if (nodes > 0) {
+#endif
       const uint32_t bytes = static_cast<uint32_t>(nodes) * kWinRec;
       mbar_expect_tx(bar, bytes);
       bulk_g2s(sbuf + (H % kSlots) * kSlotRec, x + n0, bytes, bar);
@@ -526,6 +530,9 @@ __global__ void __launch_bounds__(TPR == 1 ? (NP <= 10 ? kWinMaxThreads : 480) :
   // were waited for at earlier steps (a slot cannot be refilled before every
   // warp has finished the step of its half)
   auto wait_half = [&](int H) {
+#if defined(BG_WIN_PROBE) && BG_WIN_PROBE == 3
+    return;  // timing probe: no ring waits, results are wrong
+#endif
     if (H < nsteps) mbar_wait_sleep(&full[H % kSlots], static_cast<uint32_t>(H / kSlots) & 1u);
   };
   auto wait_next = [&]() { wait_half(S + kChoices - 1); };
@@ -581,7 +588,12 @@ __global__ void __launch_bounds__(TPR == 1 ? (NP <= 10 ? kWinMaxThreads : 480) :
         fq[(2 * u) % kWinQ] = ld_nc_v2(es + static_cast<size_t>(g + 2 * u + kWinQ) * RW);
         fq[(2 * u + 1) % kWinQ] = ld_nc_v2(es + static_cast<size_t>(g + 2 * u + kWinQ + 1) * RW);
         uint32_t e[W];
+#if defined(BG_WIN_PROBE) && BG_WIN_PROBE == 1
+#pragma unroll
+        for (int q = 0; q < W; ++q) e[q] = a.x ^ c.y ^ q;  // timing probe: no counting, results are wrong
+#else
         batch8(a, c, e);
+#endif
 #pragma unroll
         for (int q = 0; q < W; ++q) {
           if (u == 0 || u == 2) {
