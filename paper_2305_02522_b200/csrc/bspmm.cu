@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(kBBWarps * 32)
     k_bspmm_bb(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ ci,
                const uint16_t* __restrict__ ti, int64_t tr0, int64_t trows, int64_t rows,
                const int32_t* __restrict__ degree, const uint32_t* __restrict__ x, int64_t xspw,
-               int64_t f, uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
+               int64_t f, uint32_t* __restrict__ out_bits, float* __restrict__ out_f, const FEpi ep) {
   constexpr int S = 32 / G;
   constexpr int B = 8 * S;  // edges per drained batch
   constexpr int LOGS = S == 1 ? 0 : S == 2 ? 1 : S == 4 ? 2 : S == 8 ? 3 : S == 16 ? 4 : 5;
@@ -96,12 +96,17 @@ __global__ void __launch_bounds__(kBBWarps * 32)
         uint32_t ge = planes_ge<NQ>(Q, (deg + 1) >> 1);
         if (32 * (word + 1) > f) ge &= (32 * word >= f) ? 0u : tail_mask32(f);
         if (slot == 0) out_bits[row * xspw + word] = ge;
+      } else if (ep.bits) {  // every slot lane holds the totals: one packs the word
+        if (slot == 0)
+          fepi_store_word(ep, out_f, row, f, word, [&](int b) {
+            return static_cast<float>(2 * static_cast<int64_t>(plane_count<NQ>(Q, b)) - static_cast<int64_t>(deg));
+          });
       } else {
         for (int b = slot; b < 32; b += S) {
           const int64_t k = 32 * word + b;
           if (k >= f) break;
-          out_f[row * f + k] = static_cast<float>(2 * static_cast<int64_t>(plane_count<NQ>(Q, b)) -
-                                                  static_cast<int64_t>(deg));
+          out_f[row * f + k] = fepi_apply(
+              ep, static_cast<float>(2 * static_cast<int64_t>(plane_count<NQ>(Q, b)) - static_cast<int64_t>(deg)), k);
         }
       }
     }
@@ -116,7 +121,7 @@ void launch_bb(const bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uin
       1, std::min<int64_t>(cdiv(t1 - t0, kBBWarps), static_cast<int64_t>(sm_count()) * 64));
   dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(groups));
   k_bspmm_bb<G, NP, OUTB><<<grid, kBBWarps * 32, 0, s>>>(A.rp(), A.ci(), A.ti(), t0, t1,
-                                                         A.rows, A.deg(), x, xspw, f, ob, of);
+                                                         A.rows, A.deg(), x, xspw, f, ob, of, current_fepi());
   BG_LAUNCH_CHECK();
 }
 
@@ -143,7 +148,7 @@ __global__ void __launch_bounds__(256)
               const uint16_t* __restrict__ ti, int64_t rows, const float* __restrict__ xf,
               const uint32_t* __restrict__ xb, int64_t xspw, const float* __restrict__ rs,
               const float* __restrict__ cs, int64_t f, int64_t ospw,
-              uint32_t* __restrict__ out_bits, float* __restrict__ out_f, int64_t row0) {
+              uint32_t* __restrict__ out_bits, float* __restrict__ out_f, int64_t row0, const FEpi ep) {
   const int64_t i = row0 + ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
   if (i >= rows) return;
   const int lane = threadIdx.x & 31;
@@ -196,8 +201,8 @@ __global__ void __launch_bounds__(256)
       const uint32_t word = __brev(__ballot_sync(0xFFFFFFFFu, k < f && v >= 0.0));
       const int64_t w = (fbase >> 5) + m;
       if (lane == 0 && w < ospw) out_bits[i * ospw + w] = word;
-    } else if (k < f) {
-      out_f[i * f + k] = __double2float_rn(v);
+    } else {
+      fepi_store_lane(ep, out_f, i, f, k, __double2float_rn(v));
     }
   }
   if (OUTB && lane == 0 && blockIdx.y == gridDim.y - 1)
@@ -212,7 +217,7 @@ void launch_f(const bg_frdc& A, const SpmmFArgs& a, int64_t row0, int64_t row1, 
   const int64_t ospw = OUTB ? spw(a.f, a.owb) : 0;
   k_bspmm_f<M, XBITS, OUTB><<<grid, 256, 0, s>>>(A.rp(), A.ci(), A.ti(), row1, a.x_f, a.x_bits,
                                                  xspw, a.row_scale, a.col_scale, a.f, ospw,
-                                                 a.out_bits, a.out_f, row0);
+                                                 a.out_bits, a.out_f, row0, current_fepi());
   BG_LAUNCH_CHECK();
 }
 

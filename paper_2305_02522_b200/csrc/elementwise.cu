@@ -194,6 +194,25 @@ __global__ void k_bn(const float* __restrict__ x, int64_t rows, int64_t cols,
   o[t] = __double2float_rn(__dadd_rn(__ddiv_rn(num, sigma), static_cast<double>(b[j])));
 }
 
+// BatchNorm [ReLU] [binarize] fused: floats out, or warp per (row, word)
+// with lanes over columns and one ballot per packed word.
+__global__ void k_bn_act_f(const float* __restrict__ x, int64_t n, int64_t cols, const FEpi e, float* __restrict__ o) {
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    o[t] = fepi_apply(e, x[t], t % cols);
+}
+__global__ void k_bn_act_b(const float* __restrict__ x, int64_t rows, int64_t cols, const FEpi e) {
+  const int64_t words = (cols + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < rows * words;
+       w += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t i = w / words, k = 32 * (w % words) + lane;
+    fepi_store_lane(e, nullptr, i, cols, k, k < cols ? x[i * cols + k] : 0.0f);
+    if (lane == 0 && w % words == words - 1)
+      for (int64_t p = words; p < e.bspw; ++p) e.bits[i * e.bspw + p] = 0u;  // 64-bit word padding
+  }
+}
+
 // x * row[i] * col[j] in double, left to right (kernels.cpp:560-571).
 __global__ void k_scl(const float* __restrict__ x, int64_t rows, int64_t cols,
                       const float* __restrict__ r, const float* __restrict__ c,
@@ -310,6 +329,13 @@ void batchnorm(const float* x, int64_t rows, int64_t cols, const float* g, const
                const float* m, const float* sg, float* out, cudaStream_t s) {
   if (rows * cols == 0) return;
   k_bn<<<grid1(rows * cols), 256, 0, s>>>(x, rows, cols, g, b, m, sg, out);
+  BG_LAUNCH_CHECK();
+}
+
+void bn_act(const float* x, int64_t rows, int64_t cols, const FEpi& e, float* out_f, cudaStream_t s) {
+  if (rows * cols == 0) return;
+  if (e.bits) k_bn_act_b<<<grid1(rows * ((cols + 31) / 32) * 32), 256, 0, s>>>(x, rows, cols, e);
+  else k_bn_act_f<<<grid1(rows * cols), 256, 0, s>>>(x, rows * cols, cols, e, out_f);
   BG_LAUNCH_CHECK();
 }
 

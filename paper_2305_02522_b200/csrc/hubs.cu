@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256)
 // Block per hub, thread per (word, bit).
 __global__ void k_hub_final(const int32_t* __restrict__ hub_rows, int64_t nhubs, int64_t r0, int64_t r1,
                             const int32_t* __restrict__ degree, int64_t xspw, int64_t f, int32_t* __restrict__ cnt,
-                            uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
+                            uint32_t* __restrict__ out_bits, float* __restrict__ out_f, const FEpi ep) {
   const int64_t h = blockIdx.x;
   if (h >= nhubs) return;
   const int64_t i = hub_rows[h];
@@ -104,8 +104,8 @@ __global__ void k_hub_final(const int32_t* __restrict__ hub_rows, int64_t nhubs,
     if (out_bits) {
       const uint32_t word = __brev(__ballot_sync(0xFFFFFFFFu, k < f && 2 * c - deg >= 0));
       if (lane == 0) out_bits[i * xspw + w] = word;
-    } else if (k < f) {
-      out_f[i * f + k] = static_cast<float>(2 * c - deg);
+    } else {
+      fepi_store_lane(ep, out_f, i, f, k, static_cast<float>(2 * c - deg));
     }
   }
 }
@@ -184,7 +184,7 @@ void hub_bb(bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uint32_t* ou
                                                                                      A.ci(), A.ti(), x, xspw, cnt);
   }
   BG_LAUNCH_CHECK();
-  k_hub_final<<<static_cast<unsigned>(H.n), 128, 0, s>>>(hr, H.n, r0, r1, A.deg(), xspw, f, cnt, out_bits, out_f);
+  k_hub_final<<<static_cast<unsigned>(H.n), 128, 0, s>>>(hr, H.n, r0, r1, A.deg(), xspw, f, cnt, out_bits, out_f, current_fepi());
   BG_LAUNCH_CHECK();
 }
 

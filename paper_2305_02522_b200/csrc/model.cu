@@ -403,6 +403,73 @@ struct Exec {
     return o;
   }
 
+  // Fused epilogue (ops.cuh FEpi): layers bn, bn+1, .. that are BatchNorm
+  // [ReLU] [Binarize] fold into the stores of the F result before them.
+  // Returns how many layers it covers (0: none).
+  size_t plan_epi(size_t bn, int64_t cols, FEpi& e, size_t& bin_layer) {
+    static const bool on = [] {
+      const char* v = std::getenv("BG_FUSE_EPI");
+      return !(v && std::atoi(v) == 0);
+    }();
+    const size_t nl = m.layers.size();
+    if (!on || bn >= nl || m.layers[bn].info.kind != BG_LAYER_BATCHNORM) return 0;
+    const size_t i = bn - 1;  // the producer's layer (wraps for bn == 0; only i + k is used)
+    const ModelLayer& bnl = m.layers[bn];
+    if (bnl.bn_len != cols) return 0;  // the unfused path reports the mismatch
+    e = FEpi{};
+    e.g = bnl.bn_g.as<float>();
+    e.b = bnl.bn_b.as<float>();
+    e.m = bnl.bn_m.as<float>();
+    e.s = bnl.bn_s.as<float>();
+    size_t n = 1;
+    if (i + n + 1 < nl && m.layers[i + n + 1].info.kind == BG_LAYER_RELU) {
+      e.relu = 1;
+      ++n;
+    }
+    if (i + n + 1 < nl && m.layers[i + n + 1].info.kind == BG_LAYER_BINARIZE) {
+      bin_layer = i + n + 1;
+      ++n;
+    }
+    return n;
+  }
+
+  // The packed output of a fused binarize (zeroed when 64-bit words pad a column).
+  Op bits_out(int64_t rows, int64_t cols, FEpi& e) {
+    Op o;
+    o.prec = BG_B;
+    o.rows = rows;
+    o.cols = cols;
+    o.wb = m.wb;
+    o.bits = static_cast<uint32_t*>(m.pool.get(o.bytes()));
+    e.bits = o.bits;
+    e.bspw = spw(cols, m.wb);
+    if (e.bspw * 32 - cols >= 32) BG_CUDA(cudaMemsetAsync(o.bits, 0, o.bytes(), s));
+    return o;
+  }
+
+  // An F aggregation with its BatchNorm [ReLU] [Binarize] epilogue; advances i
+  // past the fused layers.
+  bool spmm_epi(size_t& i, bg_variant sp, const bg_frdc* adj, const float* rs, const float* cs, const Op& x,
+                const std::string& label, Op& cur) {
+    if (sp.out != BG_F) return false;
+    FEpi e;
+    size_t bin_layer = 0;
+    const size_t n = plan_epi(i + 1, x.cols, e, bin_layer);
+    if (n == 0) return false;
+    Op bits;
+    if (bin_layer) bits = bits_out(adj->rows, x.cols, e);
+    {
+      FEpiScope scope(e);
+      cur = spmm_slot(sp, adj, rs, cs, x, label);
+    }
+    if (bin_layer) {
+      cur = bits;
+      h.bits("layer" + std::to_string(bin_layer) + ".bin.out", cur.bits, cur.rows, cur.cols, cur.wb);
+    }
+    i += n;
+    return true;
+  }
+
   void relu_inplace(Op& x, const Op& x0) {
     if (x.prec != BG_F || x.packed()) return;  // ref: graphops.cpp:89-97; packed values are >= 0
     if (x.f == x0.f) x = own_f(x);
@@ -505,8 +572,10 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
           }
           Op hh = ex.mm_slot(l.info.plan[0], cur, l.w1, prefix + "mm");
           const bool fac = sp.in2 == BG_F;
-          cur = ex.spmm_slot(sp, m.graph->structure.get(), fac ? m.graph->norm.as<float>() : nullptr,
-                             fac ? m.graph->norm.as<float>() : nullptr, hh, prefix + "spmm");
+          const float* sc = fac ? m.graph->norm.as<float>() : nullptr;
+          if (!single && !l.relu && ex.spmm_epi(i, sp, m.graph->structure.get(), sc, sc, hh, prefix + "spmm", cur))
+            break;
+          cur = ex.spmm_slot(sp, m.graph->structure.get(), sc, sc, hh, prefix + "spmm");
           if (l.relu) ex.relu_inplace(cur, x0);
           break;
         }
@@ -562,8 +631,9 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
           cur = materialize(cur, m.pool, s);
           const bg_variant sp = l.info.plan[0];
           const bool fac = sp.in2 == BG_F;
-          cur = ex.spmm_slot(sp, m.graph->structure.get(), fac ? m.graph->norm.as<float>() : nullptr,
-                             fac ? m.graph->norm.as<float>() : nullptr, cur, prefix + "spmm");
+          const float* sc = fac ? m.graph->norm.as<float>() : nullptr;
+          if (!single && ex.spmm_epi(i, sp, m.graph->structure.get(), sc, sc, cur, prefix + "spmm", cur)) break;
+          cur = ex.spmm_slot(sp, m.graph->structure.get(), sc, sc, cur, prefix + "spmm");
           break;
         }
         case BG_LAYER_RELU:
@@ -574,6 +644,24 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
           cur = materialize(cur, m.pool, s);
           if (l.bn_len != cur.cols)
             fail("batchnorm: parameter lengths do not match " + std::to_string(cur.cols) + " columns");
+          FEpi e;
+          size_t bin_layer = 0;
+          // BatchNorm [ReLU] [Binarize] of an F producer without its own
+          // epilogue: one pass (plan_epi looks from the layer before)
+          const size_t n = single ? 0 : ex.plan_epi(i, cur.cols, e, bin_layer);
+          if (n > 0) {
+            Op o = cur;
+            if (bin_layer) {
+              o = ex.bits_out(cur.rows, cur.cols, e);
+            } else {
+              o.f = static_cast<float*>(m.pool.get(cur.bytes()));
+            }
+            bn_act(cur.f, cur.rows, cur.cols, e, o.f, s);
+            if (bin_layer) h.bits("layer" + std::to_string(bin_layer) + ".bin.out", o.bits, o.rows, o.cols, o.wb);
+            cur = o;
+            i += n - 1;
+            break;
+          }
           Op o = cur;
           o.f = static_cast<float*>(m.pool.get(cur.bytes()));
           batchnorm(cur.f, cur.rows, cur.cols, l.bn_g.as<float>(), l.bn_b.as<float>(),

@@ -405,4 +405,13 @@ Op run_concat(bg_variant v, const Op& a, const Op& b, Pool& pool, cudaStream_t s
   return out;
 }
 
+// The active fused epilogue (ops.cuh FEpi): per host thread, scoped by the
+// executor around one aggregation.
+namespace {
+thread_local FEpi g_fepi;
+}  // namespace
+const FEpi& current_fepi() { return g_fepi; }
+FEpiScope::FEpiScope(const FEpi& e) { g_fepi = e; }
+FEpiScope::~FEpiScope() { g_fepi = FEpi{}; }
+
 }  // namespace bg

@@ -14,6 +14,77 @@ constexpr int kBitPad = 64;
 // Node rows at least this long are hub rows of the BB aggregations (hubs.cu).
 constexpr int kHubDeg = 2048;
 
+namespace bg {
+// Fused epilogue of an F-output aggregation (north-star item 4): when the
+// aggregation's F result feeds BatchNorm [ReLU] [Binarize] (graphops.cpp:
+// 337-355, :89-97; binarize bitdense.cpp:83), the kernels apply BatchNorm
+// (and ReLU) to each value as they produce it and either store the floats or
+// -- with a following Binarize -- the packed sign bits only, so the
+// activation never round-trips through HBM unpacked.  Set by the executor
+// around the call (FEpiScope); zero = plain store.
+struct FEpi {
+  const float* g = nullptr;  // BatchNorm gamma, beta, mean, sigma (g null: none)
+  const float* b = nullptr;
+  const float* m = nullptr;
+  const float* s = nullptr;
+  int relu = 0;
+  uint32_t* bits = nullptr;  // binarize-pack output: MSB-first u32 words, bspw per row
+  int64_t bspw = 0;
+};
+const FEpi& current_fepi();
+struct FEpiScope {
+  explicit FEpiScope(const FEpi& e);
+  ~FEpiScope();
+  FEpiScope(const FEpiScope&) = delete;
+  FEpiScope& operator=(const FEpiScope&) = delete;
+};
+
+// BatchNorm in double with the reference's operation order, then ReLU.
+__device__ __forceinline__ float fepi_apply(const FEpi& e, float v, int64_t k) {
+  if (e.g) {
+    const double sigma = fmax(static_cast<double>(e.s[k]), 1e-12);
+    const double num = __dmul_rn(static_cast<double>(e.g[k]), __dsub_rn(static_cast<double>(v), static_cast<double>(e.m[k])));
+    v = __double2float_rn(__dadd_rn(__ddiv_rn(num, sigma), static_cast<double>(e.b[k])));
+  }
+  if (e.relu) v = v > 0.0f ? v : 0.0f;
+  return v;
+}
+
+// One thread owns output word wd (columns 32*wd .. 32*wd+31) of row i:
+// val(bb) is the plain value of column 32*wd+bb.  Stores the epilogue's
+// floats or, with e.bits, the packed word (columns >= f stay zero).
+template <class V>
+__device__ __forceinline__ void fepi_store_word(const FEpi& e, float* out_f, int64_t i, int64_t f, int64_t wd, V&& val) {
+  if (e.bits) {
+    uint32_t w = 0;
+    for (int bb = 0; bb < 32; ++bb) {
+      const int64_t k = 32 * wd + bb;
+      if (k >= f) break;
+      if (fepi_apply(e, val(bb), k) >= 0.0f) w |= 0x80000000u >> bb;
+    }
+    e.bits[i * e.bspw + wd] = w;
+  } else {
+    for (int bb = 0; bb < 32; ++bb) {
+      const int64_t k = 32 * wd + bb;
+      if (k >= f) break;
+      out_f[i * f + k] = fepi_apply(e, val(bb), k);
+    }
+  }
+}
+
+// Lanes of a warp own columns fbase+lane (fbase a multiple of 32, the call
+// warp-uniform): store value v of column k through the epilogue.
+__device__ __forceinline__ void fepi_store_lane(const FEpi& e, float* out_f, int64_t i, int64_t f, int64_t k, float v) {
+  const float y = k < f ? fepi_apply(e, v, k) : 0.0f;
+  if (e.bits) {
+    const uint32_t word = __brev(__ballot_sync(0xFFFFFFFFu, k < f && y >= 0.0f));
+    if ((threadIdx.x & 31) == 0) e.bits[i * e.bspw + (k >> 5)] = word;
+  } else if (k < f) {
+    out_f[i * f + k] = y;
+  }
+}
+}  // namespace bg
+
 struct bg_frdc {
   int64_t rows = 0, cols = 0, tile_rows = 0, tile_cols = 0, nnz = 0, nnz_bits = 0;
   int64_t max_deg = 0;
@@ -235,6 +306,10 @@ void add_fff(const float* a, const float* b, int64_t n, float* out, cudaStream_t
 void relu(float* x, int64_t n, cudaStream_t s);
 void softmax_rows(const float* x, int64_t rows, int64_t cols, float* out, cudaStream_t s);
 void scale_rows_double(float* x, int64_t rows, int64_t cols, const int64_t* cnt, cudaStream_t s);
+// BatchNorm [+ ReLU] [+ binarize-pack] in one pass over x (the epilogue of
+// an F producer that does not take FEpi itself): out_bits (bspw words per
+// row) instead of out_f when non-null.
+void bn_act(const float* x, int64_t rows, int64_t cols, const FEpi& e, float* out_f, cudaStream_t s);
 void batchnorm(const float* x, int64_t rows, int64_t cols, const float* g, const float* b,
                const float* m, const float* sg, float* out, cudaStream_t s);
 void scl(const float* x, int64_t rows, int64_t cols, const float* r, const float* c, float* out,

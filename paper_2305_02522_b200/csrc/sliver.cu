@@ -39,7 +39,7 @@ template <int G, int NP, bool OUTB>
 __global__ void __launch_bounds__(kSlWarps * 32)
     k_sl_bb(const uint64_t* __restrict__ srp, const uint32_t* __restrict__ sl, int64_t row0,
             int64_t row1, const int32_t* __restrict__ degree, const uint32_t* __restrict__ x,
-            int64_t xspw, int64_t f, uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
+            int64_t xspw, int64_t f, uint32_t* __restrict__ out_bits, float* __restrict__ out_f, const FEpi ep) {
   constexpr int S = 32 / G, B = 8 * S;
   constexpr int LOGS = S == 1 ? 0 : S == 2 ? 1 : S == 4 ? 2 : S == 8 ? 3 : S == 16 ? 4 : 5;
   constexpr int NQ = NP + LOGS;
@@ -100,12 +100,17 @@ __global__ void __launch_bounds__(kSlWarps * 32)
       uint32_t ge = planes_ge<NQ>(Q, (deg + 1) >> 1);
       if (32 * (word + 1) > f) ge &= (32 * word >= f) ? 0u : tail_mask32(f);
       if (slot == 0) out_bits[i * xspw + word] = ge;
+    } else if (ep.bits) {  // every slot lane holds the totals: one packs the word
+      if (slot == 0)
+        fepi_store_word(ep, out_f, i, f, word, [&](int b) {
+          return static_cast<float>(2 * static_cast<int64_t>(plane_count<NQ>(Q, b)) - static_cast<int64_t>(deg));
+        });
     } else {
       for (int b = slot; b < 32; b += S) {
         const int64_t k = 32 * word + b;
         if (k >= f) break;
-        out_f[i * f + k] = static_cast<float>(2 * static_cast<int64_t>(plane_count<NQ>(Q, b)) -
-                                              static_cast<int64_t>(deg));
+        out_f[i * f + k] = fepi_apply(
+            ep, static_cast<float>(2 * static_cast<int64_t>(plane_count<NQ>(Q, b)) - static_cast<int64_t>(deg)), k);
       }
     }
   }
@@ -122,7 +127,7 @@ template <int G, int NP, bool OUTB>
 __global__ void __launch_bounds__(256)
     k_bv_bb(const uint64_t* __restrict__ bp, const uint32_t* __restrict__ bc, int64_t row0, int64_t row1,
             const int32_t* __restrict__ degree, const uint32_t* __restrict__ x, int64_t xspw, int64_t f,
-            uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
+            uint32_t* __restrict__ out_bits, float* __restrict__ out_f, const FEpi ep) {
   constexpr int R = 32 / G;
   const int lane = threadIdx.x & 31, r = lane / G, g = lane % G;
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -167,12 +172,9 @@ __global__ void __launch_bounds__(256)
       if (32 * (g + 1) > f) ge &= (32 * g >= f) ? 0u : tail_mask32(f);
       out_bits[i * xspw + g] = ge;
     } else {
-      for (int b = 0; b < 32; ++b) {
-        const int64_t k = 32 * static_cast<int64_t>(g) + b;
-        if (k >= f) break;
-        out_f[i * f + k] = static_cast<float>(2 * static_cast<int64_t>(plane_count<NP>(P, b)) -
-                                              static_cast<int64_t>(deg));
-      }
+      fepi_store_word(ep, out_f, i, f, g, [&](int b) {
+        return static_cast<float>(2 * static_cast<int64_t>(plane_count<NP>(P, b)) - static_cast<int64_t>(deg));
+      });
     }
   }
 }
@@ -403,7 +405,7 @@ __global__ void __launch_bounds__(256)
     k_sl_f(const uint64_t* __restrict__ srp, const uint32_t* __restrict__ sl, int64_t row0,
            int64_t row1, const float* __restrict__ xf, const uint32_t* __restrict__ xb,
            int64_t xspw, const float* __restrict__ rs, const float* __restrict__ cs, int64_t f,
-           int64_t ospw, uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
+           int64_t ospw, uint32_t* __restrict__ out_bits, float* __restrict__ out_f, const FEpi ep) {
   const int64_t i = row0 + ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
   if (i >= row1) return;
   const int lane = threadIdx.x & 31;
@@ -451,8 +453,8 @@ __global__ void __launch_bounds__(256)
       const uint32_t word = __brev(__ballot_sync(0xFFFFFFFFu, k < f && v >= 0.0));
       const int64_t w = (fbase >> 5) + m;
       if (lane == 0 && w < ospw) out_bits[i * ospw + w] = word;
-    } else if (k < f) {
-      out_f[i * f + k] = __double2float_rn(v);
+    } else {
+      fepi_store_lane(ep, out_f, i, f, k, __double2float_rn(v));
     }
   }
   if (OUTB && lane == 0 && blockIdx.y == gridDim.y - 1)
@@ -475,7 +477,7 @@ void launch_sl_bb(const bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, 
   const int64_t per_lane = lane_bound(A, 32 / G);
   dim3 grid(static_cast<unsigned>(grid_warps(r1 - r0)), static_cast<unsigned>(cdiv(xspw, G)));
   auto go = [&](auto kern) {
-    kern<<<grid, kSlWarps * 32, 0, s>>>(A.srp(), A.sl(), r0, r1, A.deg(), x, xspw, f, ob, of);
+    kern<<<grid, kSlWarps * 32, 0, s>>>(A.srp(), A.sl(), r0, r1, A.deg(), x, xspw, f, ob, of, current_fepi());
   };
   if (per_lane < (1 << 7)) go(k_sl_bb<G, 7, OUTB>);
   else if (per_lane < (1 << 10)) go(k_sl_bb<G, 10, OUTB>);
@@ -494,7 +496,7 @@ void launch_sl_f(const bg_frdc& A, const SpmmFArgs& a, int64_t r0, int64_t r1, c
   const int64_t ospw = OUTB ? spw(a.f, a.owb) : 0;
   k_sl_f<M, XBITS, OUTB><<<grid, 256, 0, s>>>(A.srp(), A.sl(), r0, r1, a.x_f, a.x_bits, xspw,
                                               a.row_scale, a.col_scale, a.f, ospw, a.out_bits,
-                                              a.out_f);
+                                              a.out_f, current_fepi());
   BG_LAUNCH_CHECK();
 }
 
@@ -516,7 +518,7 @@ bool launch_bv_bb(bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, uint32
   const unsigned blocks = static_cast<unsigned>(cdiv(warps * 32, 256));
   auto go = [&](auto kern) {
     kern<<<blocks, 256, 0, s>>>(A.bit_ptr.as<uint64_t>(), A.bit_cols.as<uint32_t>(), r0, r1, A.deg(), x, xspw,
-                                f, ob, of);
+                                f, ob, of, current_fepi());
   };
   const int64_t d = light_max_deg(A, s);
   if (d < (1 << 6)) go(k_bv_bb<G, 6, OUTB>);

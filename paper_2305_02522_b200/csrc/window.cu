@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(TPR == 1 ? (NP <= 10 ? kWinMaxThreads : 480) :
              const uint16_t* __restrict__ ell, int nh, int Wh,
              int64_t xrows, int64_t row0, int64_t row1, int b0, int b1,
              const int32_t* __restrict__ degree, const uint4* __restrict__ x, int64_t f,
-             uint32_t* __restrict__ out_bits, float* __restrict__ out_f) {
+             uint32_t* __restrict__ out_bits, float* __restrict__ out_f, const FEpi ep) {
   static_assert(NP >= 6, "three-level Harley-Seal needs planes 0..5");
   constexpr int W = 4 / TPR, RW = 32 / TPR;  // words per thread, rows per warp stream
   extern __shared__ __align__(16) uint4 sbuf[];  // kSlots x kSlotRec records
@@ -628,12 +628,9 @@ __global__ void __launch_bounds__(TPR == 1 ? (NP <= 10 ? kWinMaxThreads : 480) :
       } else {
 #pragma unroll
         for (int q = 0; q < W; ++q)
-          for (int bb = 0; bb < 32; ++bb) {
-            const int64_t kk2 = 32 * (part * W + q) + bb;
-            if (kk2 >= f) break;
-            out_f[i * f + kk2] = static_cast<float>(2 * static_cast<int64_t>(plane_count<NP>(P[q], bb)) -
-                                                    static_cast<int64_t>(deg));
-          }
+          fepi_store_word(ep, out_f, i, f, part * W + q, [&](int bb) {
+            return static_cast<float>(2 * static_cast<int64_t>(plane_count<NP>(P[q], bb)) - static_cast<int64_t>(deg));
+          });
       }
     }
   }
@@ -756,7 +753,7 @@ bool launch_win(bg_frdc& A, const uint32_t* x, int64_t f, uint32_t* ob, float* o
   const int grid = std::min(sms, b1 - b0);
   kern<<<grid, RB * TPR, kWinSmem, s>>>(W.seg.as<uint32_t>(), W.steplen.as<uint16_t>(), W.ell.as<uint16_t>(), W.nw,
                                         W.Wn, A.cols, r0, r1, b0, b1, A.deg(), reinterpret_cast<const uint4*>(x), f,
-                                        ob, of);
+                                        ob, of, current_fepi());
   BG_LAUNCH_CHECK();
   return true;
 }
