@@ -1,7 +1,7 @@
 # per-kernel durations (ncu launch list) of one small-workload bench run: WL=cora|pubmed|...
 cd $GRAFT_REPO_ROOT
 for w in ${WLS:-cora pubmed}; do
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launch_$w.csv python bench.py --workload $w --steps 2 --warmup 3 --no-cpu-baseline --no-clocks > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control ${NCU_CACHE:-all} --csv --log-file gpurun_out/launch_$w.csv python bench.py --workload $w --steps 2 --warmup 3 --no-cpu-baseline --no-clocks > /dev/null 2>&1
 python - $w <<'P'
 import csv,sys,collections
 w=sys.argv[1]
