@@ -1224,7 +1224,7 @@ int fbb_force() {
   const char* e = std::getenv("BG_FBB");
   if (!e) return 0;
   const std::string v(e);
-  return v == "scalar" ? 1 : v == "imma" ? 2 : v == "tma" ? 3 : v == "tc" ? 5 : 0;
+  return v == "scalar" ? 1 : v == "imma" ? 2 : v == "tma" ? 3 : v == "tc" ? 5 : v == "bulk" ? 6 : 0;
 }
 
 bool bmm_pair(const BmmArgs& a, cudaStream_t s) {
@@ -1232,6 +1232,7 @@ bool bmm_pair(const BmmArgs& a, cudaStream_t s) {
   if (a.rows == 0) return true;
   const int force = fbb_force();
   const bool few_rows = a.rows < 24576 && std::getenv("BG_FBB") == nullptr;  // as bmm()
+  if (force == 6 && fbb_bulk(a, s)) return true;
   if (force == 1 || few_rows) {
     // warp per row: pairs up to 256 combined columns (8 per lane); wider
     // pairs measured slower than two products (Flickr, 2 x 256 columns:
@@ -1258,6 +1259,10 @@ void bmm(const BmmArgs& a, cudaStream_t s) {
   // row kernel) stays on the warp-per-row kernel at any row count.
   // F output keeps the tensor-core kernel (Flickr FBF 63 vs 83 us).
   const bool few_rows = af && ob && (a.rows < 24576 || a.n > 128) && std::getenv("BG_FBB") == nullptr;
+  // opt-in (BG_FBB=bulk): every row requested at once by bulk copies
+  // (fbb_bulk.cu); measured slower than the warp-per-row kernel on Cora and
+  // PubMed (DESIGN 4.3)
+  if (force == 6 && fbb_bulk(a, s)) return;
   if (force == 1 || few_rows) {
     if (ob) launch<true, true>(a, s);
     else launch<true, false>(a, s);

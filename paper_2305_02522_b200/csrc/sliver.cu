@@ -20,6 +20,7 @@
 
 #include <cub/cub.cuh>
 
+#include "async.cuh"
 #include "ops.cuh"
 #include "tilewalk.cuh"
 
@@ -29,6 +30,13 @@ namespace {
 constexpr int kSlWarps = 8;
 
 // base + a * b with one IMAD.WIDE.U32 (gather address of node a, row stride b bytes).
+__device__ __forceinline__ uint4 ld_nc_v4(const uint4* p) {
+  uint4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(p));
+  return v;
+}
 __device__ __forceinline__ uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t base) {
   uint64_t r;
   asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(base));
@@ -204,7 +212,7 @@ __device__ __forceinline__ float logit_of(float beta, int64_t sdot, int qsum) {
 constexpr int kRec = 16;
 
 template <int NP>
-__global__ void __launch_bounds__(kSlWarps * 32)
+__global__ void __launch_bounds__(kSlWarps * 32, 5)
     k_bv_gcn1(const uint64_t* __restrict__ bp, const uint32_t* __restrict__ bc, int64_t row0,
               int64_t row1, const int32_t* __restrict__ degree, const uint32_t* __restrict__ rec,
               const uint32_t* __restrict__ wt, int hspw, int K, const float* __restrict__ beta,
@@ -234,14 +242,16 @@ __global__ void __launch_bounds__(kSlWarps * 32)
     uint32_t lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     const uint64_t e0 = bp[i];
     const uint32_t len = static_cast<uint32_t>(bp[i + 1] - e0);  // multiple of kBitPad
-    const uint32_t* rowp = bc + e0 + slot;
+    // slot s takes entries 8s .. 8s+7 of each 64-entry block: two 16-byte
+    // loads per lane (a warp instruction covers one 128-byte line) instead
+    // of eight 4-byte ones (eight lines); the sums are order-free integers
+    const uint4* rowp = reinterpret_cast<const uint4*>(bc + e0) + 2 * slot;
     for (uint32_t off = 0; off < len; off += B) {
+      const uint4 ca = ld_nc_v4(rowp + off / 4), cb = ld_nc_v4(rowp + off / 4 + 1);
+      const uint32_t cols[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
       uint4 v[8];
 #pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        const uint32_t col = ld_nc_u32(rowp + off + S * m);
-        v[m] = __ldg(reinterpret_cast<const uint4*>(mad_wide(col, kRec * 4, rbase)));
-      }
+      for (int m = 0; m < 8; ++m) v[m] = __ldg(reinterpret_cast<const uint4*>(mad_wide(cols[m], kRec * 4, rbase)));
       uint32_t h[8];
 #pragma unroll
       for (int m = 0; m < 8; ++m) h[m] = v[m].x;

@@ -16,7 +16,7 @@ import paper_2305_02522_b200 as bg
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["default", "scalar", "tma", "tc"])
+@pytest.fixture(params=["default", "scalar", "tma", "tc", "bulk"])
 def fbb_kernel(monkeypatch, request):
     if request.param != "default":
         monkeypatch.setenv("BG_FBB", request.param)
