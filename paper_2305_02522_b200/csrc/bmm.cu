@@ -1224,7 +1224,7 @@ int fbb_force() {
   const char* e = std::getenv("BG_FBB");
   if (!e) return 0;
   const std::string v(e);
-  return v == "scalar" ? 1 : v == "imma" ? 2 : v == "tma" ? 3 : v == "tc" ? 5 : v == "bulk" ? 6 : 0;
+  return v == "scalar" ? 1 : v == "imma" ? 2 : v == "tma" ? 3 : v == "tc" ? 5 : v == "bulk" ? 6 : v == "tmem" ? 7 : 0;
 }
 
 bool bmm_pair(const BmmArgs& a, cudaStream_t s) {
@@ -1273,6 +1273,7 @@ void bmm(const BmmArgs& a, cudaStream_t s) {
       // the warp-specialized tcgen05 kernel (fbb_tc.cu); else whole 16-row
       // tiles on the TMA-fed mma.sync kernel, the rest on the direct one
       if ((force == 0 || force == 5) && fbb_tc(a, s)) return;
+      if (force == 7 && fbb_tmem(a, s)) return;
       if (fbb_umma(a, s)) return;
       if (fbb_umma2(a, s)) return;
       const int64_t done = force == 2 ? 0 : fbb_tma(a, s);

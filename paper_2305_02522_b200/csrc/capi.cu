@@ -1,6 +1,7 @@
 // extern "C" entry points (include/bitgnn_b200.h).  Every function converts
 // exceptions into status codes; the message stays in bg_last_error().
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <random>
 #include <sstream>
@@ -678,15 +679,23 @@ int bg_model_forward_host(bg_model* m, const float* xh, int64_t rows, int64_t co
     std::vector<int64_t> bounds(nc + 1);
     for (int c = 0; c <= nc; ++c) bounds[c] = rows * c / nc / 16 * 16;
     bounds[nc] = rows;
+    // BG_HOST_TRACE=1: print the timeline of this call (stderr) -- last input
+    // byte landed, forward done, last output byte back -- for the e2e analysis
+    static const bool trace_tl = std::getenv("BG_HOST_TRACE") != nullptr;
+    cudaEvent_t tl[4] = {};
+    if (trace_tl)
+      for (auto& e : tl) BG_CUDA(cudaEventCreate(&e));
     // the copy stream starts after everything already queued on the caller's stream
     BG_CUDA(cudaEventRecord(done_ev, st));
     BG_CUDA(cudaStreamWaitEvent(cs, done_ev, 0));
+    if (trace_tl) BG_CUDA(cudaEventRecord(tl[0], cs));
     auto* hx = m->hx.as<float>();
     for (int c = 0; c < nc; ++c) {
       const size_t off = static_cast<size_t>(bounds[c] * cols), n = static_cast<size_t>((bounds[c + 1] - bounds[c]) * cols);
       if (n) BG_CUDA(cudaMemcpyAsync(hx + off, xh + off, n * 4, cudaMemcpyHostToDevice, cs));
       BG_CUDA(cudaEventRecord(in_ev[c], cs));
     }
+    if (trace_tl) BG_CUDA(cudaEventRecord(tl[1], cs));
     StreamChunks sc;
     sc.in = RowChunks{nc, bounds.data(), in_ev};
     sc.out = RowChunks{nc, bounds.data(), out_ev};
@@ -700,6 +709,7 @@ int bg_model_forward_host(bg_model* m, const float* xh, int64_t rows, int64_t co
     }();
     if (x0.prec != m->input_prec) fail("model input tag does not match the provided operand");
     forward_impl(*m, x0, m->hout.as<float>(), logh ? m->hlog.as<float>() : nullptr, nullptr, nullptr, st, &sc);
+    if (trace_tl) BG_CUDA(cudaEventRecord(tl[2], st));
     auto* ho = m->hout.as<float>();
     if (sc.out_done) {
       for (int c = 0; c < nc; ++c) {
@@ -712,8 +722,18 @@ int bg_model_forward_host(bg_model* m, const float* xh, int64_t rows, int64_t co
     BG_CUDA(cudaStreamWaitEvent(cs, done_ev, 0));
     if (!sc.out_done) BG_CUDA(cudaMemcpyAsync(outh, ho, ob, cudaMemcpyDeviceToHost, cs));
     if (logh) BG_CUDA(cudaMemcpyAsync(logh, m->hlog.p, ob, cudaMemcpyDeviceToHost, cs));
+    if (trace_tl) BG_CUDA(cudaEventRecord(tl[3], cs));
     BG_CUDA(cudaStreamSynchronize(cs));
     BG_CUDA(cudaStreamSynchronize(st));
+    if (trace_tl) {
+      float a = 0, b = 0, c = 0;
+      BG_CUDA(cudaEventElapsedTime(&a, tl[0], tl[1]));
+      BG_CUDA(cudaEventElapsedTime(&b, tl[0], tl[2]));
+      BG_CUDA(cudaEventElapsedTime(&c, tl[0], tl[3]));
+      std::fprintf(stderr, "host_tl: inputs landed %.3f ms, forward done %.3f ms, outputs back %.3f ms (%d chunks)\n",
+                   a, b, c, nc);
+      for (auto& e : tl) cudaEventDestroy(e);
+    }
   });
 }
 

@@ -1,0 +1,345 @@
+// MM.FBB / FFB for a wide fp32 input (Reddit: K = 602) on the 5th-generation
+// tensor cores with the A operand in TENSOR MEMORY (ref: bmm B-output path,
+// kernels.cpp:140-176; binarize x >= 0, bitdense.cpp:83).
+//
+// fbb_tc.cu keeps A (the +-1 bytes of a 128-row tile) in shared memory next
+// to the weights; at K = 602 the two take 156 KB and leave room for only
+// ~58 KB of fp32 row pieces in flight, which is below the per-SM
+// bandwidth-latency product of HBM (~44 KB/us x ~2 us), so that kernel runs
+// at 0.26-0.29 ms where the stream needs 86 us.  Here A never touches shared
+// memory: converter threads own one row each (thread t of a warp = TMEM lane
+// 32*(warp%4) + t) and write the row's +-1 bytes straight into TMEM with
+// tcgen05.st, four K values per 32-bit column, and tcgen05.mma reads A from
+// TMEM.  Shared memory then holds the weights (78 KB) and a 115 KB ring of
+// fp32 row pieces.
+//
+// One CTA per SM walks 128-row tiles.  Roles:
+//   * producer (warp 0, one lane): pieces of PR = 16 consecutive rows
+//     (contiguous in HBM) into a ring of 3 slots by cp.async.bulk (full /
+//     empty mbarrier per slot);
+//   * MMA issuer (warp 1, one lane): ceil(K/32) tcgen05.mma.kind::i8 per tile
+//     (M = 128, N = the product's columns rounded to 32, A from TMEM buffer
+//     tile % 2, B = the weights in shared memory) into the TMEM accumulator,
+//     then tcgen05.commit to the accumulator-full and A-empty barriers;
+//   * epilogue (warps 4..7, TMEM lane quarter warp % 4): tcgen05.ld of the
+//     accumulator, dot >= 0 -> bit, MSB-first words, one row per thread;
+//   * converters (warps 8..23): warp (quarter q, part j) converts K steps
+//     [j*S/4, (j+1)*S/4) of the 32 rows of quarter q: per 32 floats, 16 LDS.64
+//     of its row in the slot, sign bytes (x >= 0 -> +1, else -1; K past the
+//     row meets zero weights), one tcgen05.st.32x32b.x8.
+// Integer dots are exact: the bits equal the reference's for any order.
+#include <cstdlib>
+#include <string>
+
+#include "async.cuh"
+#include "ops.cuh"
+
+namespace bg {
+namespace {
+
+constexpr int kTmM = 128;
+constexpr int kTmPR = 16;                              // rows per fp32 piece
+constexpr int kTmSlots = 3;
+constexpr int kTmParts = 4;                            // converter warps per TMEM lane quarter
+constexpr int kTmConv = 4 * kTmParts;                  // 16 converter warps
+constexpr int kTmThreads = (8 + kTmConv) * 32;         // 24 warps
+constexpr int kTmPieces = kTmM / kTmPR;                // pieces per tile
+
+__device__ __forceinline__ uint32_t tm_sign4(float x0, float x1, float x2, float x3) {
+  const uint32_t m = static_cast<uint32_t>(x0 >= 0.0f) | (static_cast<uint32_t>(x1 >= 0.0f) << 1) |
+                     (static_cast<uint32_t>(x2 >= 0.0f) << 2) | (static_cast<uint32_t>(x3 >= 0.0f) << 3);
+  return 0xFFFFFFFFu - 0xFEu * ((m * 0x00204081u) & 0x01010101u);  // 1 -> 0x01, 0 -> 0xFF per byte
+}
+
+__device__ __forceinline__ void tm_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+// a wait that traps instead of hanging if a phase never completes
+__device__ __forceinline__ void tm_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  for (uint32_t it = 0; it < (1u << 26) && !ok; ++it)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  if (!ok) __trap();
+}
+
+__device__ __forceinline__ uint64_t tm_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // sm_100 descriptor version; no swizzle, base offset 0
+  return d;
+}
+
+struct TmArgs {
+  const float* x;
+  const uint32_t* wt;  // n x kspw transposed weight bits
+  int64_t rows;
+  int k, kspw, kpad, n, N, ospw;
+  uint32_t a_cols;     // TMEM columns per A buffer (multiple of 32)
+  uint32_t* out;
+};
+
+__global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ __align__(8) uint64_t full[kTmSlots], empty[kTmSlots], a_full[2], a_empty[2], acc_full, acc_empty;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int kpad = a.kpad, N = a.N;
+  const uint32_t bchunk = static_cast<uint32_t>(N) * 16u;
+  uint8_t* B = sm;  // kpad/16 chunks x N rows x 16 B (canonical K-major, no swizzle)
+  const uint32_t slot_floats = static_cast<uint32_t>(kTmPR * a.k) + 32;  // + pad: the last row's last step reads past
+  float* ring = reinterpret_cast<float*>(B + static_cast<size_t>(kpad) * N);
+  // weights as +-1 bytes (0 past K and for columns >= n)
+  for (int t = tid; t < N * (kpad / 4); t += blockDim.x) {
+    const int o = t / (kpad / 4), p4 = (t % (kpad / 4)) * 4;
+    uint32_t v = 0;
+    if (o < a.n && p4 < a.k) {
+      const uint32_t word = __ldg(a.wt + static_cast<int64_t>(o) * a.kspw + (p4 >> 5));
+      const uint32_t nib = (word >> (28 - (p4 & 31))) & 0xFu;
+      const uint32_t spread = ((nib >> 3) & 1u) | (((nib >> 2) & 1u) << 8) | (((nib >> 1) & 1u) << 16) | ((nib & 1u) << 24);
+      v = 0xFFFFFFFFu - 0xFEu * spread;
+      if (p4 + 4 > a.k) v &= 0xFFFFFFFFu >> (8 * (p4 + 4 - a.k));
+    }
+    *reinterpret_cast<uint32_t*>(B + (p4 >> 4) * bchunk + o * 16 + (p4 & 15)) = v;
+  }
+  const int64_t tiles = (a.rows + kTmM - 1) / kTmM;
+  const int64_t my = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t npieces = my * kTmPieces;
+  if (warp == 1) {  // TMEM: two A buffers + one accumulator
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_base)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kTmSlots; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTmConv);  // every converter warp releases every piece
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&a_full[b], kTmConv);
+      mbar_init(&a_empty[b], 1);
+    }
+    mbar_init(&acc_full, 1);
+    mbar_init(&acc_empty, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // weights -> tensor core
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base;
+  const uint32_t acc_col = 0, a_col0 = 128;  // accumulator at column 0, A buffers after it
+  auto tile_row0 = [&](int64_t j) { return (blockIdx.x + j * gridDim.x) * kTmM; };
+
+  if (warp == 0) {
+    // ---------------- producer ----------------
+    if (lane == 0)
+      for (int64_t u = 0; u < npieces; ++u) {
+        const int s = static_cast<int>(u % kTmSlots);
+        if (u >= kTmSlots) tm_wait(&empty[s], static_cast<uint32_t>((u / kTmSlots - 1) & 1));
+        const int64_t r0 = tile_row0(u / kTmPieces) + kTmPR * (u % kTmPieces);
+        const int64_t left = a.rows - r0;
+        const int nr = static_cast<int>(left <= 0 ? 0 : left < kTmPR ? left : kTmPR);
+        const uint32_t bytes = static_cast<uint32_t>(nr) * static_cast<uint32_t>(a.k) * 4u;
+        if (nr == kTmPR && bytes % 16 == 0) {
+          mbar_expect_tx(&full[s], bytes);
+          bulk_g2s(ring + s * slot_floats, a.x + r0 * a.k, bytes, &full[s]);
+        } else {
+          tm_arrive(&full[s]);  // partial piece: the converters read it from global memory
+        }
+      }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+                           (static_cast<uint32_t>(kTmM >> 4) << 24);  // kind::i8, s32 += s8 x s8, K-major
+    for (int64_t j = 0; j < my; ++j) {
+      const int b = static_cast<int>(j & 1);
+      tm_wait(&a_full[b], static_cast<uint32_t>((j >> 1) & 1));
+      if (j >= 1) tm_wait(&acc_empty, static_cast<uint32_t>((j - 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (lane == 0) {
+        const uint32_t bbase = smem_addr(B);
+        const uint32_t acol = tmem + a_col0 + static_cast<uint32_t>(b) * a.a_cols, dcol = tmem + acc_col;
+        for (int ks = 0; ks < kpad / 32; ++ks) {
+          const uint64_t bd = tm_desc(bbase + 2 * ks * bchunk, bchunk, 128);
+          const uint32_t accum = ks > 0 ? 1u : 0u;
+          asm volatile(
+              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+              " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dcol),
+              "r"(acol + 8u * ks), "l"(bd), "r"(idesc), "r"(accum)
+              : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_addr(&acc_full))
+                     : "memory");
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_addr(&a_empty[b]))
+                     : "memory");
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------- epilogue: TMEM lanes 32*(warp-4) .. +31 ----------------
+    const int q = warp - 4;
+    for (int64_t j = 0; j < my; ++j) {
+      tm_wait(&acc_full, static_cast<uint32_t>(j & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t row = tile_row0(j) + 32 * q + lane;
+      uint32_t words[4] = {0u, 0u, 0u, 0u};
+      for (int cw = 0; cw < N / 32; ++cw) {
+        uint32_t d[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
+              "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]),
+              "=r"(d[15]), "=r"(d[16]), "=r"(d[17]), "=r"(d[18]), "=r"(d[19]), "=r"(d[20]), "=r"(d[21]),
+              "=r"(d[22]), "=r"(d[23]), "=r"(d[24]), "=r"(d[25]), "=r"(d[26]), "=r"(d[27]), "=r"(d[28]),
+              "=r"(d[29]), "=r"(d[30]), "=r"(d[31])
+            : "r"(tmem + (static_cast<uint32_t>(32 * q) << 16) + acc_col + static_cast<uint32_t>(32 * cw)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        uint32_t m = 0;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) m |= (static_cast<int32_t>(d[t]) >= 0 ? 1u : 0u) << (31 - t);
+        if (32 * cw + 32 > a.n) m &= 32 * cw >= a.n ? 0u : tail_mask32(a.n);  // columns >= n stay 0
+        words[cw] = m;
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) tm_arrive(&acc_empty);
+      if (row < a.rows) {
+        uint32_t* o = a.out + row * a.ospw;
+        if (a.ospw == 4) {
+          *reinterpret_cast<uint4*>(o) = make_uint4(words[0], words[1], words[2], words[3]);
+        } else {
+          for (int w = 0; w < a.ospw; ++w) o[w] = w < 4 ? words[w] : 0u;
+        }
+      }
+    }
+  } else if (warp >= 8) {
+    // ---------------- converters ----------------
+    const int q = warp & 3, part = (warp - 8) >> 2;  // TMEM lane quarter, K part
+    const int steps = kpad / 32;
+    const int s0 = steps * part / kTmParts, s1 = steps * (part + 1) / kTmParts;
+    const int pq = 32 / kTmPR;  // pieces per lane quarter
+    for (int64_t j = 0; j < my; ++j) {
+      const int b = static_cast<int>(j & 1);
+      if (j >= 2) tm_wait(&a_empty[b], static_cast<uint32_t>(((j >> 1) - 1) & 1));
+      // Every converter warp waits for EVERY piece of the tile in order and
+      // releases the ones it does not read at once: a warp that skipped a
+      // slot's earlier phases could take that phase's parity for the one it
+      // wants (an mbarrier parity wait only tells the current phase from the
+      // previous one), and the producer refills a slot only when all 16
+      // warps have released it.
+      const int64_t u0 = j * kTmPieces + pq * q;  // this quarter's pieces u0 .. u0+pq-1
+      for (int p = 0; p < pq * q; ++p) {
+        const int64_t v = j * kTmPieces + p;
+        tm_wait(&full[v % kTmSlots], static_cast<uint32_t>((v / kTmSlots) & 1));
+        if (lane == 0) tm_arrive(&empty[v % kTmSlots]);
+      }
+      for (int p = 0; p < pq; ++p)
+        tm_wait(&full[(u0 + p) % kTmSlots], static_cast<uint32_t>(((u0 + p) / kTmSlots) & 1));
+      // this lane's row: piece u0 + lane / PR, row lane % PR in it
+      const int64_t u = u0 + lane / kTmPR;
+      const int64_t r = tile_row0(j) + 32 * q + lane;
+      const int64_t pr0 = tile_row0(j) + kTmPR * (u % kTmPieces);
+      const bool staged = a.rows - pr0 >= kTmPR && (static_cast<uint32_t>(kTmPR) * a.k * 4u) % 16 == 0;
+      const float* src = staged ? ring + (u % kTmSlots) * slot_floats + static_cast<int64_t>(lane % kTmPR) * a.k
+                                : a.x + r * a.k;
+      const bool live = r < a.rows;
+      const uint32_t tcol = tmem + (static_cast<uint32_t>(32 * q) << 16) + a_col0 + static_cast<uint32_t>(b) * a.a_cols;
+      for (int ks = s0; ks < s1; ++ks) {
+        uint32_t c[8];
+        const int k0 = 32 * ks;
+        if (staged && (a.k & 1) == 0) {
+          // the row is 8-byte aligned in the slot; floats past K (the last
+          // step) read the next row or the slot pad and meet zero weights
+          const float2* p2 = reinterpret_cast<const float2*>(src + k0);
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            const float2 v0 = p2[2 * h], v1 = p2[2 * h + 1];
+            c[h] = tm_sign4(v0.x, v0.y, v1.x, v1.y);
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            float e[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int kk = k0 + 4 * h + t;
+              e[t] = live && kk < a.k ? (staged ? src[kk] : __ldg(src + kk)) : 0.0f;  // slot or HBM
+            }
+            c[h] = tm_sign4(e[0], e[1], e[2], e[3]);
+          }
+        }
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                         tcol + 8u * static_cast<uint32_t>(ks)),
+                     "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(c[5]), "r"(c[6]), "r"(c[7])
+                     : "memory");
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        for (int p = 0; p < pq; ++p) tm_arrive(&empty[(u0 + p) % kTmSlots]);
+        tm_arrive(&a_full[b]);
+      }
+      for (int p = pq * (q + 1); p < kTmPieces; ++p) {  // the later quarters' pieces
+        const int64_t v = j * kTmPieces + p;
+        tm_wait(&full[v % kTmSlots], static_cast<uint32_t>((v / kTmSlots) & 1));
+        if (lane == 0) tm_arrive(&empty[v % kTmSlots]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+}
+
+}  // namespace
+
+// FBB on k_fbb_tmem: false (nothing launched) when not eligible.  Single
+// products with <= 128 output columns whose A tile fits two TMEM buffers next
+// to the accumulator (K <= 768).
+bool fbb_tmem(const BmmArgs& a, cudaStream_t s) {
+  if (!a.a_f || !a.out_bits || a.out_bits2 || a.n == 0 || a.n > 128 || a.k <= 0 || a.rows == 0) return false;
+  if (reinterpret_cast<uintptr_t>(a.a_f) % 16 != 0) return false;
+  TmArgs t{};
+  t.x = a.a_f;
+  t.wt = a.wt;
+  t.rows = a.rows;
+  t.k = static_cast<int>(a.k);
+  t.kspw = static_cast<int>(spw(a.k, a.wb));
+  t.kpad = static_cast<int>(32 * cdiv(a.k, 32));
+  t.n = static_cast<int>(a.n);
+  t.N = static_cast<int>(32 * cdiv(a.n, 32));
+  t.ospw = static_cast<int>(spw(a.n, a.wb));
+  t.out = a.out_bits;
+  t.a_cols = static_cast<uint32_t>(32 * cdiv(t.kpad / 4, 32));
+  if (128 + 2 * t.a_cols > 512) return false;
+  const size_t smem = static_cast<size_t>(t.kpad) * t.N +
+                      static_cast<size_t>(kTmSlots) * (static_cast<size_t>(kTmPR) * a.k + 32) * 4;
+  const size_t cap = 227 * 1024 - 1024;  // static shared memory (barriers, TMEM base) counts too
+  if (smem > cap) return false;
+  static int attr_done = 0;
+  if (!attr_done) {
+    BG_CUDA(cudaFuncSetAttribute(k_fbb_tmem, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap)));
+    attr_done = 1;
+  }
+  const int64_t tiles = cdiv(a.rows, kTmM);
+  const int64_t blocks = std::min<int64_t>(tiles, sm_count());
+  k_fbb_tmem<<<static_cast<unsigned>(blocks), kTmThreads, smem, s>>>(t);
+  BG_LAUNCH_CHECK();
+  return true;
+}
+
+}  // namespace bg
