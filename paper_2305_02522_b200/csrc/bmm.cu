@@ -1259,6 +1259,11 @@ void bmm(const BmmArgs& a, cudaStream_t s) {
   // row kernel) stays on the warp-per-row kernel at any row count.
   // F output keeps the tensor-core kernel (Flickr FBF 63 vs 83 us).
   const bool few_rows = af && ob && (a.rows < 24576 || a.n > 128) && std::getenv("BG_FBB") == nullptr;
+  // Wide products (N > 128, Flickr's 256 columns) from ~16K rows: the
+  // tcgen05 kernel with A in tensor memory (fbb_tmem.cu), Flickr 0.139 ->
+  // 0.065 ms per product; at N <= 128 (Reddit) the TMA-fed mma.sync kernel
+  // below measured 3 % faster and stays (scripts/fbb_rows_probe.py)
+  if (((force == 0 && af && a.n > 128 && a.rows >= 16384) || force == 7) && ob && fbb_tmem(a, s)) return;
   // opt-in (BG_FBB=bulk): every row requested at once by bulk copies
   // (fbb_bulk.cu); measured slower than the warp-per-row kernel on Cora and
   // PubMed (DESIGN 4.3)
@@ -1273,7 +1278,6 @@ void bmm(const BmmArgs& a, cudaStream_t s) {
       // the warp-specialized tcgen05 kernel (fbb_tc.cu); else whole 16-row
       // tiles on the TMA-fed mma.sync kernel, the rest on the direct one
       if ((force == 0 || force == 5) && fbb_tc(a, s)) return;
-      if (force == 7 && fbb_tmem(a, s)) return;
       if (fbb_umma(a, s)) return;
       if (fbb_umma2(a, s)) return;
       const int64_t done = force == 2 ? 0 : fbb_tma(a, s);

@@ -38,6 +38,7 @@
 // no room for more slots.  (A lane quarter waiting only for its own pieces
 // raced: an mbarrier parity wait cannot tell a slot's phase u from u - 2, so
 // every converter warp now waits for -- and releases -- every piece.)
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 
@@ -92,6 +93,7 @@ struct TmArgs {
   int64_t rows;
   int k, kspw, kpad, n, N, ospw;
   uint32_t a_cols;     // TMEM columns per A buffer (multiple of 32)
+  uint32_t a_col0;     // first A buffer's column (after the N accumulator columns)
   uint32_t* out;
 };
 
@@ -105,12 +107,20 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
   uint8_t* B = sm;  // kpad/16 chunks x N rows x 16 B (canonical K-major, no swizzle)
   const uint32_t slot_floats = static_cast<uint32_t>(kTmPR * a.k) + 32;  // + pad: the last row's last step reads past
   float* ring = reinterpret_cast<float*>(B + static_cast<size_t>(kpad) * N);
-  // weights as +-1 bytes (0 past K and for columns >= n)
+  // weights as +-1 bytes (0 past K and for columns >= n): the packed words
+  // are staged in the (still idle) ring by asynchronous copies first, so the
+  // expansion below does not wait one L2 round trip per iteration
+  {
+    uint32_t* wst = reinterpret_cast<uint32_t*>(ring);
+    for (int t = tid; t < a.n * a.kspw; t += blockDim.x) cp_async4(wst + t, a.wt + t);
+    cp_async_wait_all();
+    __syncthreads();
+  }
   for (int t = tid; t < N * (kpad / 4); t += blockDim.x) {
     const int o = t / (kpad / 4), p4 = (t % (kpad / 4)) * 4;
     uint32_t v = 0;
     if (o < a.n && p4 < a.k) {
-      const uint32_t word = __ldg(a.wt + static_cast<int64_t>(o) * a.kspw + (p4 >> 5));
+      const uint32_t word = reinterpret_cast<const uint32_t*>(ring)[o * a.kspw + (p4 >> 5)];
       const uint32_t nib = (word >> (28 - (p4 & 31))) & 0xFu;
       const uint32_t spread = ((nib >> 3) & 1u) | (((nib >> 2) & 1u) << 8) | (((nib >> 1) & 1u) << 16) | ((nib & 1u) << 24);
       v = 0xFFFFFFFFu - 0xFEu * spread;
@@ -145,7 +155,7 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
-  const uint32_t acc_col = 0, a_col0 = 128;  // accumulator at column 0, A buffers after it
+  const uint32_t acc_col = 0, a_col0 = a.a_col0;  // accumulator at column 0, A buffers after it
   auto tile_row0 = [&](int64_t j) { return (blockIdx.x + j * gridDim.x) * kTmM; };
 
   if (warp == 0) {
@@ -202,7 +212,7 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
       tm_wait(&acc_full, static_cast<uint32_t>(j & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t row = tile_row0(j) + 32 * q + lane;
-      uint32_t words[4] = {0u, 0u, 0u, 0u};
+      uint32_t words[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
       for (int cw = 0; cw < N / 32; ++cw) {
         uint32_t d[32];
         asm volatile(
@@ -228,84 +238,85 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
         uint32_t* o = a.out + row * a.ospw;
         if (a.ospw == 4) {
           *reinterpret_cast<uint4*>(o) = make_uint4(words[0], words[1], words[2], words[3]);
+        } else if (a.ospw == 8) {
+          reinterpret_cast<uint4*>(o)[0] = make_uint4(words[0], words[1], words[2], words[3]);
+          reinterpret_cast<uint4*>(o)[1] = make_uint4(words[4], words[5], words[6], words[7]);
         } else {
-          for (int w = 0; w < a.ospw; ++w) o[w] = w < 4 ? words[w] : 0u;
+          for (int w = 0; w < a.ospw; ++w) o[w] = w < 8 ? words[w] : 0u;
         }
       }
     }
   } else if (warp >= 8) {
     // ---------------- converters ----------------
+    // Warp (quarter q, part j) converts K steps [j*S/4, (j+1)*S/4) of the two
+    // 16-row pieces of lane quarter q (TMEM lanes 32q .. 32q+15 and +16 ..
+    // +31) with 16-lane stores (tcgen05.st.16x256b: thread t holds lanes t/4
+    // and t/4 + 8, columns 2(t%4) and 2(t%4)+1 of an 8-column K step, i.e.
+    // floats 8(t%4) .. 8(t%4)+7 of two rows), so each piece is released as
+    // soon as it is converted.  Every converter warp waits for EVERY piece of
+    // the tile in order and releases the ones it does not read at once: a
+    // warp that skipped a slot's earlier phases could take that phase's
+    // parity for the one it wants (an mbarrier parity wait only tells the
+    // current phase from the previous one), and the producer refills a slot
+    // only when all 16 warps have released it.
     const int q = warp & 3, part = (warp - 8) >> 2;  // TMEM lane quarter, K part
     const int steps = kpad / 32;
     const int s0 = steps * part / kTmParts, s1 = steps * (part + 1) / kTmParts;
     const int pq = 32 / kTmPR;  // pieces per lane quarter
+    const int tr = lane >> 2, tc = lane & 3;  // rows tr and tr+8 of a piece, floats 8tc .. 8tc+7 of a step
     for (int64_t j = 0; j < my; ++j) {
       const int b = static_cast<int>(j & 1);
       if (j >= 2) tm_wait(&a_empty[b], static_cast<uint32_t>(((j >> 1) - 1) & 1));
-      // Every converter warp waits for EVERY piece of the tile in order and
-      // releases the ones it does not read at once: a warp that skipped a
-      // slot's earlier phases could take that phase's parity for the one it
-      // wants (an mbarrier parity wait only tells the current phase from the
-      // previous one), and the producer refills a slot only when all 16
-      // warps have released it.
-      const int64_t u0 = j * kTmPieces + pq * q;  // this quarter's pieces u0 .. u0+pq-1
-      for (int p = 0; p < pq * q; ++p) {
+      for (int p = 0; p < kTmPieces; ++p) {
         const int64_t v = j * kTmPieces + p;
-        tm_wait(&full[v % kTmSlots], static_cast<uint32_t>((v / kTmSlots) & 1));
-        if (lane == 0) tm_arrive(&empty[v % kTmSlots]);
-      }
-      for (int p = 0; p < pq; ++p)
-        tm_wait(&full[(u0 + p) % kTmSlots], static_cast<uint32_t>(((u0 + p) / kTmSlots) & 1));
-      // this lane's row: piece u0 + lane / PR, row lane % PR in it
-      const int64_t u = u0 + lane / kTmPR;
-      const int64_t r = tile_row0(j) + 32 * q + lane;
-      const int64_t pr0 = tile_row0(j) + kTmPR * (u % kTmPieces);
-      const bool staged = a.rows - pr0 >= kTmPR && (static_cast<uint32_t>(kTmPR) * a.k * 4u) % 16 == 0;
-      const float* src = staged ? ring + (u % kTmSlots) * slot_floats + static_cast<int64_t>(lane % kTmPR) * a.k
-                                : a.x + r * a.k;
-      const bool live = r < a.rows;
-      const uint32_t tcol = tmem + (static_cast<uint32_t>(32 * q) << 16) + a_col0 + static_cast<uint32_t>(b) * a.a_cols;
-      for (int ks = s0; ks < s1; ++ks) {
-        uint32_t c[8];
-        const int k0 = 32 * ks;
-        if (staged && (a.k & 1) == 0) {
-          // the row is 8-byte aligned in the slot; floats past K (the last
-          // step) read the next row or the slot pad and meet zero weights
-          const float2* p2 = reinterpret_cast<const float2*>(src + k0);
+        const int s = static_cast<int>(v % kTmSlots);
+        tm_wait(&full[s], static_cast<uint32_t>((v / kTmSlots) & 1));
+        if (p / pq == q) {
+          const int h = p % pq;  // which 16 lanes of the quarter
+          const int64_t pr0 = tile_row0(j) + kTmPR * p;
+          const bool staged = a.rows - pr0 >= kTmPR && (static_cast<uint32_t>(kTmPR) * a.k * 4u) % 16 == 0;
+          const float* slot = ring + s * slot_floats;
+          const uint32_t tcol = tmem + (static_cast<uint32_t>(32 * q + 16 * h) << 16) + a_col0 +
+                                static_cast<uint32_t>(b) * a.a_cols;
+          for (int ks = s0; ks < s1; ++ks) {
+            const int k0 = 32 * ks + 8 * tc;
+            uint32_t c[4];
 #pragma unroll
-          for (int h = 0; h < 8; ++h) {
-            const float2 v0 = p2[2 * h], v1 = p2[2 * h + 1];
-            c[h] = tm_sign4(v0.x, v0.y, v1.x, v1.y);
-          }
-        } else {
+            for (int rr = 0; rr < 2; ++rr) {
+              const int ri = tr + 8 * rr;  // row in the piece
+              if (staged && (a.k & 1) == 0) {
+                // rows are 8-byte aligned in the slot; floats past K (the last
+                // step) read the next row or the slot pad and meet zero weights
+                const float2* p2 = reinterpret_cast<const float2*>(slot + static_cast<int64_t>(ri) * a.k + k0);
+                const float2 x0 = p2[0], x1 = p2[1], x2 = p2[2], x3 = p2[3];
+                c[2 * rr] = tm_sign4(x0.x, x0.y, x1.x, x1.y);
+                c[2 * rr + 1] = tm_sign4(x2.x, x2.y, x3.x, x3.y);
+              } else {
+                const int64_t r = pr0 + ri;
+                const float* src = staged ? slot + static_cast<int64_t>(ri) * a.k : a.x + r * a.k;
+                float e[8];
 #pragma unroll
-          for (int h = 0; h < 8; ++h) {
-            float e[4];
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              const int kk = k0 + 4 * h + t;
-              e[t] = live && kk < a.k ? (staged ? src[kk] : __ldg(src + kk)) : 0.0f;  // slot or HBM
+                for (int t = 0; t < 8; ++t) {
+                  const int kk = k0 + t;
+                  e[t] = r < a.rows && kk < a.k ? (staged ? src[kk] : __ldg(src + kk)) : 0.0f;  // slot or HBM
+                }
+                c[2 * rr] = tm_sign4(e[0], e[1], e[2], e[3]);
+                c[2 * rr + 1] = tm_sign4(e[4], e[5], e[6], e[7]);
+              }
             }
-            c[h] = tm_sign4(e[0], e[1], e[2], e[3]);
+            asm volatile("tcgen05.st.sync.aligned.16x256b.x1.b32 [%0], {%1,%2,%3,%4};" ::"r"(
+                             tcol + 8u * static_cast<uint32_t>(ks)),
+                         "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3])
+                         : "memory");
           }
         }
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
-                         tcol + 8u * static_cast<uint32_t>(ks)),
-                     "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(c[5]), "r"(c[6]), "r"(c[7])
-                     : "memory");
+        __syncwarp();
+        if (lane == 0) tm_arrive(&empty[s]);  // the slot's floats are in registers / TMEM now
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) {
-        for (int p = 0; p < pq; ++p) tm_arrive(&empty[(u0 + p) % kTmSlots]);
-        tm_arrive(&a_full[b]);
-      }
-      for (int p = pq * (q + 1); p < kTmPieces; ++p) {  // the later quarters' pieces
-        const int64_t v = j * kTmPieces + p;
-        tm_wait(&full[v % kTmSlots], static_cast<uint32_t>((v / kTmSlots) & 1));
-        if (lane == 0) tm_arrive(&empty[v % kTmSlots]);
-      }
+      if (lane == 0) tm_arrive(&a_full[b]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -318,10 +329,11 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
 }  // namespace
 
 // FBB on k_fbb_tmem: false (nothing launched) when not eligible.  Single
-// products with <= 128 output columns whose A tile fits two TMEM buffers next
-// to the accumulator (K <= 768).
+// products with <= 256 output columns whose A tile fits two TMEM buffers next
+// to the accumulator (N <= 128: K <= 768; N = 256: K <= 512) and whose
+// weights and ring fit in shared memory.
 bool fbb_tmem(const BmmArgs& a, cudaStream_t s) {
-  if (!a.a_f || !a.out_bits || a.out_bits2 || a.n == 0 || a.n > 128 || a.k <= 0 || a.rows == 0) return false;
+  if (!a.a_f || !a.out_bits || a.out_bits2 || a.n == 0 || a.n > 256 || a.k <= 0 || a.rows == 0) return false;
   if (reinterpret_cast<uintptr_t>(a.a_f) % 16 != 0) return false;
   TmArgs t{};
   t.x = a.a_f;
@@ -335,7 +347,8 @@ bool fbb_tmem(const BmmArgs& a, cudaStream_t s) {
   t.ospw = static_cast<int>(spw(a.n, a.wb));
   t.out = a.out_bits;
   t.a_cols = static_cast<uint32_t>(32 * cdiv(t.kpad / 4, 32));
-  if (128 + 2 * t.a_cols > 512) return false;
+  t.a_col0 = static_cast<uint32_t>(std::max(128, t.N));
+  if (t.a_col0 + 2 * t.a_cols > 512) return false;
   const size_t smem = static_cast<size_t>(t.kpad) * t.N +
                       static_cast<size_t>(kTmSlots) * (static_cast<size_t>(kTmPR) * a.k + 32) * 4;
   const size_t cap = 227 * 1024 - 1024;  // static shared memory (barriers, TMEM base) counts too
