@@ -4,14 +4,13 @@
 //
 // fbb_tc.cu keeps A (the +-1 bytes of a 128-row tile) in shared memory next
 // to the weights; at K = 602 the two take 156 KB and leave room for only
-// ~58 KB of fp32 row pieces in flight, which is below the per-SM
-// bandwidth-latency product of HBM (~44 KB/us x ~2 us), so that kernel runs
-// at 0.26-0.29 ms where the stream needs 86 us.  Here A never touches shared
-// memory: converter threads own one row each (thread t of a warp = TMEM lane
-// 32*(warp%4) + t) and write the row's +-1 bytes straight into TMEM with
-// tcgen05.st, four K values per 32-bit column, and tcgen05.mma reads A from
-// TMEM.  Shared memory then holds the weights (78 KB) and a 115 KB ring of
-// fp32 row pieces.
+// ~58 KB of fp32 row pieces in flight, below the per-SM bandwidth-latency
+// product of HBM (~44 KB/us x ~2 us), so that kernel runs at 0.26-0.29 ms
+// where the stream needs 86 us.  Here A never touches shared memory: the
+// converters write each row's +-1 bytes straight into TMEM with tcgen05.st
+// (four K values per 32-bit column; TMEM lane = row of the tile) and
+// tcgen05.mma reads A from TMEM.  Shared memory holds the weights (Reddit 78
+// KB, Flickr's 256 columns 128 KB) and a ring of fp32 row pieces.
 //
 // One CTA per SM walks 128-row tiles.  Roles:
 //   * producer (warp 0, one lane): pieces of PR = 16 consecutive rows
@@ -24,20 +23,18 @@
 //   * epilogue (warps 4..7, TMEM lane quarter warp % 4): tcgen05.ld of the
 //     accumulator, dot >= 0 -> bit, MSB-first words, one row per thread;
 //   * converters (warps 8..23): warp (quarter q, part j) converts K steps
-//     [j*S/4, (j+1)*S/4) of the 32 rows of quarter q: per 32 floats, 16 LDS.64
-//     of its row in the slot, sign bytes (x >= 0 -> +1, else -1; K past the
-//     row meets zero weights), one tcgen05.st.32x32b.x8.
+//     [j*S/4, (j+1)*S/4) of the two pieces of lane quarter q with 16-lane
+//     stores (tcgen05.st.16x256b), so a piece is released as soon as it is
+//     converted -- a 32-lane store would hold a piece until its sibling
+//     landed too (measured: one piece in flight, 0.213 ms on Reddit).
 // Integer dots are exact: the bits equal the reference's for any order.
 //
-// Opt-in (BG_FBB=tmem).  Measured on Reddit (ncu, 1 B200): 0.213-0.225 ms
-// against 0.136 ms for the TMA-fed mma.sync kernel (bmm.cu k_fbb_tma), with
-// 2.5 TB/s of DRAM reads and warps waiting on the ring 80 % of the time.  A
-// 32x32b TMEM store covers a whole lane quarter (32 rows), i.e. two 16-row
-// pieces, so a slot is held until its sibling piece has landed too and only
-// about one piece (38.5 KB) is in flight per SM; the 78 KB of weights leave
-// no room for more slots.  (A lane quarter waiting only for its own pieces
-// raced: an mbarrier parity wait cannot tell a slot's phase u from u - 2, so
-// every converter warp now waits for -- and releases -- every piece.)
+// Measured (1 B200, in-graph CUDA events): Flickr's 256-column products
+// 0.139 -> 0.065 ms each (the default for N > 128 from 16 K rows); Reddit
+// (N = 128) 0.136 ms, level with the TMA-fed mma.sync kernel (bmm.cu
+// k_fbb_tma, 3 % ahead in scripts/fbb_rows_probe.py), which stays the
+// default there: the 78 KB of weights leave room for three 38.5 KB slots,
+// about two pieces in flight per SM (4.1 TB/s).
 #include <algorithm>
 #include <cstdlib>
 #include <string>
