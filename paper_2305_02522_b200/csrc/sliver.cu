@@ -499,6 +499,65 @@ void launch_sl_bb(const bg_frdc& A, const uint32_t* x, int64_t f, int64_t xspw, 
   BG_LAUNCH_CHECK();
 }
 
+// Narrow F outputs (f <= 16: Flickr's 7 classes): G = 8 or 16 lanes per row,
+// 32/G rows per warp, so the lanes that a warp per row would leave idle past
+// column f walk other rows.  Each lane group walks its row's slivers in the
+// same ascending order with the same double accumulation (bit-identical to
+// k_sl_f); the entry loop runs to the longest row of the warp, shorter rows
+// idle through the rest.
+template <int G, bool XBITS>
+__global__ void __launch_bounds__(256)
+    k_sl_f_sub(const uint64_t* __restrict__ srp, const uint32_t* __restrict__ sl, int64_t row0,
+               int64_t row1, const float* __restrict__ xf, const uint32_t* __restrict__ xb,
+               int64_t xspw, const float* __restrict__ rs, const float* __restrict__ cs, int64_t f,
+               float* __restrict__ out_f, const FEpi ep) {
+  const int lane = threadIdx.x & 31, grp = lane / G, t = lane % G;
+  const int64_t i = row0 + ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * (32 / G) + grp;
+  if (row0 + ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * (32 / G) >= row1) return;
+  const bool live = i < row1;
+  double d = 0.0;
+  const uint64_t e0 = live ? srp[i] : 0;
+  const uint32_t len = live ? static_cast<uint32_t>(srp[i + 1] - e0) : 0u;
+  uint32_t lmax = len;  // the warp's longest row
+#pragma unroll
+  for (int o = G; o < 32; o <<= 1) lmax = max(lmax, __shfl_xor_sync(0xFFFFFFFFu, lmax, o));
+  for (uint32_t base = 0; base < lmax; base += G) {
+    const uint32_t mine = base + t < len ? ld_nc_u32(sl + e0 + base + t) : kSliverSentinel;
+    const int cnt = static_cast<int>(min(static_cast<uint32_t>(G), lmax - base));
+    for (int L = 0; L < cnt; ++L) {  // slivers in order, then columns in order
+      const uint32_t ent = __shfl_sync(0xFFFFFFFFu, mine, L, G);
+      if (ent == kSliverSentinel) continue;  // row padding or past this row's end (group-uniform)
+      const uint32_t first = ent >> 3;
+      uint32_t more = ent & 7u, col = first;
+      for (;;) {
+        const int64_t j = col;
+        const double w = cs ? static_cast<double>(__ldg(cs + j)) : 1.0;
+        if (t < f) {
+          if (XBITS) {
+            const uint32_t bit = (__ldg(xb + j * xspw) >> (31 - t)) & 1u;
+            d = __dadd_rn(d, bit ? w : -w);
+          } else {
+            d = __dadd_rn(d, __dmul_rn(w, static_cast<double>(__ldg(xf + j * f + t))));
+          }
+        }
+        if (!more) break;
+        col = first + __ffs(more);
+        more &= more - 1;
+      }
+    }
+  }
+  const double si = rs && live ? static_cast<double>(rs[i]) : 1.0;
+  const float v = __double2float_rn(__dmul_rn(si, d));
+  const float y = live && t < f ? fepi_apply(ep, v, t) : 0.0f;
+  if (ep.bits) {  // fused Binarize: the group's sign bits, MSB-first
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, live && t < f && y >= 0.0f);
+    const uint32_t mine = (bal >> (grp * G)) & ((1u << G) - 1u);
+    if (live && t == 0) ep.bits[i * ep.bspw] = __brev(mine);
+  } else if (live && t < f) {
+    out_f[i * f + t] = y;
+  }
+}
+
 template <int M, bool XBITS, bool OUTB>
 void launch_sl_f(const bg_frdc& A, const SpmmFArgs& a, int64_t r0, int64_t r1, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>(cdiv((r1 - r0) * 32, 256)), static_cast<unsigned>(cdiv(a.f, 32 * M)));
@@ -512,6 +571,19 @@ void launch_sl_f(const bg_frdc& A, const SpmmFArgs& a, int64_t r0, int64_t r1, c
 
 template <bool XBITS, bool OUTB>
 void launch_sl_f_m(const bg_frdc& A, const SpmmFArgs& a, int64_t r0, int64_t r1, cudaStream_t s) {
+  if (!OUTB && a.f <= 16 && std::getenv("BG_SLF_WARP") == nullptr) {
+    // narrow rows: G lanes per row (k_sl_f_sub)
+    auto go = [&](auto kern, int G) {
+      const int64_t warps = cdiv(r1 - r0, 32 / G);
+      kern<<<static_cast<unsigned>(cdiv(warps * 32, 256)), 256, 0, s>>>(
+          A.srp(), A.sl(), r0, r1, a.x_f, a.x_bits, XBITS ? spw(a.f, a.xwb) : 0, a.row_scale, a.col_scale, a.f,
+          a.out_f, current_fepi());
+      BG_LAUNCH_CHECK();
+    };
+    if (a.f <= 8) go(k_sl_f_sub<8, XBITS>, 8);
+    else go(k_sl_f_sub<16, XBITS>, 16);
+    return;
+  }
   if (a.f <= 32) launch_sl_f<1, XBITS, OUTB>(A, a, r0, r1, s);
   else if (a.f <= 64) launch_sl_f<2, XBITS, OUTB>(A, a, r0, r1, s);
   else launch_sl_f<4, XBITS, OUTB>(A, a, r0, r1, s);
