@@ -91,6 +91,7 @@ struct TmArgs {
   int k, kspw, kpad, n, N, ospw;
   uint32_t a_cols;     // TMEM columns per A buffer (multiple of 32)
   uint32_t a_col0;     // first A buffer's column (after the N accumulator columns)
+  int64_t span;        // rows per CTA (multiple of 16): CTA b owns [b*span, min(rows, (b+1)*span))
   uint32_t* out;
 };
 
@@ -104,36 +105,32 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
   uint8_t* B = sm;  // kpad/16 chunks x N rows x 16 B (canonical K-major, no swizzle)
   const uint32_t slot_floats = static_cast<uint32_t>(kTmPR * a.k) + 32;  // + pad: the last row's last step reads past
   float* ring = reinterpret_cast<float*>(B + static_cast<size_t>(kpad) * N);
-  // weights as +-1 bytes (0 past K and for columns >= n): the packed words
-  // are staged in the (still idle) ring by asynchronous copies first, so the
-  // expansion below does not wait one L2 round trip per iteration
-  {
-    uint32_t* wst = reinterpret_cast<uint32_t*>(ring);
-    for (int t = tid; t < a.n * a.kspw; t += blockDim.x) cp_async4(wst + t, a.wt + t);
-    cp_async_wait_all();
-    __syncthreads();
-  }
-  for (int t = tid; t < N * (kpad / 4); t += blockDim.x) {
-    const int o = t / (kpad / 4), p4 = (t % (kpad / 4)) * 4;
-    uint32_t v = 0;
-    if (o < a.n && p4 < a.k) {
-      const uint32_t word = reinterpret_cast<const uint32_t*>(ring)[o * a.kspw + (p4 >> 5)];
-      const uint32_t nib = (word >> (28 - (p4 & 31))) & 0xFu;
-      const uint32_t spread = ((nib >> 3) & 1u) | (((nib >> 2) & 1u) << 8) | (((nib >> 1) & 1u) << 16) | ((nib & 1u) << 24);
-      v = 0xFFFFFFFFu - 0xFEu * spread;
-      if (p4 + 4 > a.k) v &= 0xFFFFFFFFu >> (8 * (p4 + 4 - a.k));
-    }
-    *reinterpret_cast<uint32_t*>(B + (p4 >> 4) * bchunk + o * 16 + (p4 & 15)) = v;
-  }
-  const int64_t tiles = (a.rows + kTmM - 1) / kTmM;
-  const int64_t my = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // this CTA's rows: one contiguous, 16-aligned range (all CTAs finish
+  // together; the last tile of a range is partial)
+  const int64_t rb0 = static_cast<int64_t>(blockIdx.x) * a.span, rb1 = std::min(a.rows, rb0 + a.span);
+  const int64_t my = rb1 > rb0 ? (rb1 - rb0 + kTmM - 1) / kTmM : 0;
   const int64_t npieces = my * kTmPieces;
-  if (warp == 1) {  // TMEM: two A buffers + one accumulator
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_base)),
-                 "r"(512)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
+  auto tile_row0 = [&](int64_t j) { return rb0 + j * kTmM; };
+  // piece u of this CTA: rows [r0, r0 + nr); bulk-copied when its byte
+  // count is a multiple of 16 (every full piece), else read from HBM
+  auto piece = [&](int64_t u, int64_t* r0) {
+    *r0 = tile_row0(u / kTmPieces) + kTmPR * (u % kTmPieces);
+    const int64_t left = rb1 - *r0;
+    return static_cast<int>(left <= 0 ? 0 : left < kTmPR ? left : kTmPR);
+  };
+  auto staged_piece = [&](int nr) { return nr > 0 && (static_cast<uint32_t>(nr) * a.k * 4u) % 16 == 0; };
+  auto issue = [&](int64_t u) {
+    const int s = static_cast<int>(u % kTmSlots);
+    int64_t r0;
+    const int nr = piece(u, &r0);
+    if (staged_piece(nr)) {
+      const uint32_t bytes = static_cast<uint32_t>(nr) * static_cast<uint32_t>(a.k) * 4u;
+      mbar_expect_tx(&full[s], bytes);
+      bulk_g2s(ring + s * slot_floats, a.x + r0 * a.k, bytes, &full[s]);
+    } else {
+      tm_arrive(&full[s]);  // empty or unaligned piece: the converters read HBM
+    }
+  };
   if (tid == 0) {
     for (int s = 0; s < kTmSlots; ++s) {
       mbar_init(&full[s], 1);
@@ -146,31 +143,50 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
     mbar_init(&acc_full, 1);
     mbar_init(&acc_empty, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the first two pieces go out before the weights are set up
+    for (int64_t u = 0; u < std::min<int64_t>(kTmSlots - 1, npieces); ++u) issue(u);
   }
+  // weights as +-1 bytes (0 past K and for columns >= n): the packed words
+  // are staged in the last (still idle) ring slot by asynchronous copies
+  // first, so the expansion below does not wait one L2 round trip per
+  // iteration
+  const uint32_t* wst = reinterpret_cast<const uint32_t*>(ring + (kTmSlots - 1) * slot_floats);
+  for (int t = tid; t < a.n * a.kspw; t += blockDim.x) cp_async4(const_cast<uint32_t*>(wst) + t, a.wt + t);
+  cp_async_wait_all();
+  __syncthreads();
+  for (int t = tid; t < N * (kpad / 4); t += blockDim.x) {
+    const int o = t / (kpad / 4), p4 = (t % (kpad / 4)) * 4;
+    uint32_t v = 0;
+    if (o < a.n && p4 < a.k) {
+      const uint32_t word = wst[o * a.kspw + (p4 >> 5)];
+      const uint32_t nib = (word >> (28 - (p4 & 31))) & 0xFu;
+      const uint32_t spread = ((nib >> 3) & 1u) | (((nib >> 2) & 1u) << 8) | (((nib >> 1) & 1u) << 16) | ((nib & 1u) << 24);
+      v = 0xFFFFFFFFu - 0xFEu * spread;
+      if (p4 + 4 > a.k) v &= 0xFFFFFFFFu >> (8 * (p4 + 4 - a.k));
+    }
+    *reinterpret_cast<uint32_t*>(B + (p4 >> 4) * bchunk + o * 16 + (p4 & 15)) = v;
+  }
+  if (warp == 1) {  // TMEM: two A buffers + one accumulator
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_base)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // weights -> tensor core
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
   const uint32_t acc_col = 0, a_col0 = a.a_col0;  // accumulator at column 0, A buffers after it
-  auto tile_row0 = [&](int64_t j) { return (blockIdx.x + j * gridDim.x) * kTmM; };
 
   if (warp == 0) {
     // ---------------- producer ----------------
     if (lane == 0)
-      for (int64_t u = 0; u < npieces; ++u) {
+      for (int64_t u = kTmSlots - 1; u < npieces; ++u) {  // pieces 0, 1 went out in the prologue
         const int s = static_cast<int>(u % kTmSlots);
         if (u >= kTmSlots) tm_wait(&empty[s], static_cast<uint32_t>((u / kTmSlots - 1) & 1));
-        const int64_t r0 = tile_row0(u / kTmPieces) + kTmPR * (u % kTmPieces);
-        const int64_t left = a.rows - r0;
-        const int nr = static_cast<int>(left <= 0 ? 0 : left < kTmPR ? left : kTmPR);
-        const uint32_t bytes = static_cast<uint32_t>(nr) * static_cast<uint32_t>(a.k) * 4u;
-        if (nr == kTmPR && bytes % 16 == 0) {
-          mbar_expect_tx(&full[s], bytes);
-          bulk_g2s(ring + s * slot_floats, a.x + r0 * a.k, bytes, &full[s]);
-        } else {
-          tm_arrive(&full[s]);  // partial piece: the converters read it from global memory
-        }
+        issue(u);
       }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
@@ -231,7 +247,7 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) tm_arrive(&acc_empty);
-      if (row < a.rows) {
+      if (row < rb1) {
         uint32_t* o = a.out + row * a.ospw;
         if (a.ospw == 4) {
           *reinterpret_cast<uint4*>(o) = make_uint4(words[0], words[1], words[2], words[3]);
@@ -270,8 +286,8 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
         tm_wait(&full[s], static_cast<uint32_t>((v / kTmSlots) & 1));
         if (p / pq == q) {
           const int h = p % pq;  // which 16 lanes of the quarter
-          const int64_t pr0 = tile_row0(j) + kTmPR * p;
-          const bool staged = a.rows - pr0 >= kTmPR && (static_cast<uint32_t>(kTmPR) * a.k * 4u) % 16 == 0;
+          int64_t pr0;
+          const bool staged = staged_piece(piece(v, &pr0));  // rows past the range read stale floats: never stored
           const float* slot = ring + s * slot_floats;
           const uint32_t tcol = tmem + (static_cast<uint32_t>(32 * q + 16 * h) << 16) + a_col0 +
                                 static_cast<uint32_t>(b) * a.a_cols;
@@ -295,7 +311,7 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
 #pragma unroll
                 for (int t = 0; t < 8; ++t) {
                   const int kk = k0 + t;
-                  e[t] = r < a.rows && kk < a.k ? (staged ? src[kk] : __ldg(src + kk)) : 0.0f;  // slot or HBM
+                  e[t] = r < rb1 && kk < a.k ? (staged ? src[kk] : __ldg(src + kk)) : 0.0f;  // slot or HBM
                 }
                 c[2 * rr] = tm_sign4(e[0], e[1], e[2], e[3]);
                 c[2 * rr + 1] = tm_sign4(e[4], e[5], e[6], e[7]);
@@ -355,8 +371,9 @@ bool fbb_tmem(const BmmArgs& a, cudaStream_t s) {
     BG_CUDA(cudaFuncSetAttribute(k_fbb_tmem, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap)));
     attr_done = 1;
   }
-  const int64_t tiles = cdiv(a.rows, kTmM);
-  const int64_t blocks = std::min<int64_t>(tiles, sm_count());
+  // one contiguous 16-aligned row range per CTA, as even as 16 rows allow
+  t.span = 16 * cdiv(cdiv(a.rows, sm_count()), 16);
+  const int64_t blocks = cdiv(a.rows, t.span);
   k_fbb_tmem<<<static_cast<unsigned>(blocks), kTmThreads, smem, s>>>(t);
   BG_LAUNCH_CHECK();
   return true;
