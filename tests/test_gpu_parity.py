@@ -178,7 +178,9 @@ BSPMM_VARIANTS = [f"BSpMM.{a}{b}{c}" for a in "FB" for b in "FB" for c in "FB"]
 @pytest.mark.parametrize("v", BSPMM_VARIANTS)
 @pytest.mark.parametrize("nef", [(5, 9, 3), (37, 150, 31), (64, 400, 33), (200, 4000, 40), (17, 40, 1),
                                  (300, 30000, 128), (150, 3000, 70), (90, 800, 520), (120, 2500, 300),
-                                 (64, 900, 250), (200, 1500, 1000)])
+                                 (64, 900, 250), (200, 1500, 1000),
+                                 # narrow F rows (sliver.cu k_sl_f_sub: 8 / 16 lanes per row)
+                                 (400, 5000, 7), (600, 9000, 16), (500, 6000, 9), (1000, 20000, 2)])
 def test_bspmm_every_variant(v, wb, nef):
     n, e, f = nef
     rng = po.Rng(2000 + n + e + f)
@@ -372,3 +374,25 @@ def test_streamed_host_forward_matches_device_forward(model, plan):
         assert torch.equal(lg, dev_log.cpu())
     host2 = m.forward_host(X)  # pageable input
     assert torch.equal(host2, dev)
+
+
+@pytest.mark.parametrize("v", ["BSpMM.FFF", "BSpMM.FBF", "BSpMM.BFF"])
+@pytest.mark.parametrize("f", [1, 5, 7, 8, 9, 13, 16])
+def test_narrow_rows_equal_warp_per_row(monkeypatch, v, f):
+    # k_sl_f_sub (8 or 16 lanes per row) against k_sl_f (a warp per row,
+    # BG_SLF_WARP=1): the same ascending double sums, so bit-identical
+    n, e = 3000, 40000
+    rng = po.Rng(7000 + f)
+    s, d = rng.random_edges(n, e, False)
+    dA = bg.frdc_from_edges(n, s, d, False)
+    srow = (0.1 + np.array([rng.uniform() for _ in range(n)])).astype(np.float32)
+    scol = (0.1 + np.array([rng.uniform() for _ in range(n)])).astype(np.float32)
+    X = rng.random_dense(n, f)
+    tv = po.parse_variant(v)
+    dx, _ = _operand(tv[1], X, 32)
+    fac = tv[2] == po.F
+    adj = bg.AdjacencyOperand(dA, cuda(srow[None])[0] if fac else None, cuda(scol[None])[0] if fac else None)
+    sub = bg.bspmm(v, adj, dx, None, 32).cpu()
+    monkeypatch.setenv("BG_SLF_WARP", "1")
+    warp = bg.bspmm(v, adj, dx, None, 32).cpu()
+    assert torch.equal(sub, warp)
