@@ -365,48 +365,56 @@ __global__ void __launch_bounds__(256)
                       const uint32_t* __restrict__ wt, const float* __restrict__ beta, int C,
                       uint32_t* __restrict__ rec, bool h_v4) {
   __shared__ uint4 wt_s[48];
-  __shared__ float beta_s[48];
+  __shared__ float beta_s[48], inv2u_s[48];
   for (int t = threadIdx.x; t < 48 * 4; t += blockDim.x) {
     const int k = t >> 2, w = t & 3;
     reinterpret_cast<uint32_t*>(wt_s)[t] = (k < C && w < hspw) ? wt[k * hspw + w] : 0u;
   }
-  for (int k = threadIdx.x; k < 48; k += blockDim.x) beta_s[k] = k < C ? beta[k] : 1.0f;
+  for (int k = threadIdx.x; k < 48; k += blockDim.x) {
+    const float bk = k < C ? beta[k] : 1.0f;
+    beta_s[k] = bk;
+    const int ex = ((__float_as_int(bk) >> 23) & 0xFF) - 127;
+    inv2u_s[k] = __int_as_float((127 + 22 - ex) << 23);  // 1 / (2u): u = the ulp unit of beta
+  }
   __syncthreads();
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= (rows + 1) * 4) return;
   uint4* rec4 = reinterpret_cast<uint4*>(rec);
-  if (t >= rows * 4) {
-    rec4[t] = make_uint4(0u, 0u, 0u, 0u);
-    return;
-  }
-  const int64_t j = t >> 2;
-  const int g = static_cast<int>(t & 3);
-  uint32_t hw[4] = {0, 0, 0, 0};
-  if (h_v4) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(h) + j);
-    hw[0] = v.x, hw[1] = v.y, hw[2] = v.z, hw[3] = v.w;
-  } else {
-    for (int q = 0; q < hspw; ++q) hw[q] = __ldg(h + j * hspw + q);
-  }
-  uint32_t out[3] = {0u, 0u, 0u};
-#pragma unroll
-  for (int p = 0; p < 3; ++p)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int k = 12 * g + 4 * p + b;
-      if (k >= C) continue;
-      const uint4 wk = wt_s[k];
-      const int diff = __popc(hw[0] ^ wk.x) + __popc(hw[1] ^ wk.y) + __popc(hw[2] ^ wk.z) + __popc(hw[3] ^ wk.w);
-      const float fd = static_cast<float>(K - 2 * diff);  // exact
-      const float bk = beta_s[k];
-      const float x = __fmul_rn(fd, bk);
-      const float e = __fmaf_rn(fd, bk, -x);  // exact rounding error of the product
-      const int ex = ((__float_as_int(bk) >> 23) & 0xFF) - 127;
-      const float inv2u = __int_as_float((127 + 22 - ex) << 23);
-      const int q = __float2int_rn(e * inv2u);  // in [-32, 32]
-      out[p] |= static_cast<uint32_t>(q + 32) << (8 * b);
+  // grid-stride over (node, word group) items: each block stages the weights once
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < (rows + 1) * 4;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (t >= rows * 4) {
+      rec4[t] = make_uint4(0u, 0u, 0u, 0u);
+      continue;
     }
-  rec4[t] = make_uint4(hw[g], out[0], out[1], out[2]);
+    const int64_t j = t >> 2;
+    const int g = static_cast<int>(t & 3);
+    uint32_t hw[4] = {0, 0, 0, 0};
+    if (h_v4) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(h) + j);
+      hw[0] = v.x, hw[1] = v.y, hw[2] = v.z, hw[3] = v.w;
+    } else {
+      for (int q = 0; q < hspw; ++q) hw[q] = __ldg(h + j * hspw + q);
+    }
+    uint32_t out[3] = {0u, 0u, 0u};
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int k = 12 * g + 4 * p + b;
+        if (k >= C) continue;
+        const uint4 wk = wt_s[k];
+        const int diff = __popc(hw[0] ^ wk.x) + __popc(hw[1] ^ wk.y) + __popc(hw[2] ^ wk.z) + __popc(hw[3] ^ wk.w);
+        // int <-> float through the 2^23 magic instead of I2F / F2I (those
+        // share the quarter-rate pipe with the 164 POPCs of a node)
+        const float fd = __int_as_float(0x4B000000 + K - 2 * diff + 0x400000) - 12582912.0f;  // exact (|dot| <= 2^21)
+        const float bk = beta_s[k];
+        const float x = __fmul_rn(fd, bk);
+        const float e = __fmaf_rn(fd, bk, -x);  // exact rounding error of the product
+        // q = e / (2u), an integer in [-32, 32]: exact in fp32, rounded by the magic add
+        const int q = __float_as_int(__fmaf_rn(e, inv2u_s[k], 12582912.0f)) - 0x4B400000;
+        out[p] |= static_cast<uint32_t>(q + 32) << (8 * b);
+      }
+    rec4[t] = make_uint4(hw[g], out[0], out[1], out[2]);
+  }
 }
 
 // ---- real-valued walk in ascending column order ------------------------------
@@ -671,7 +679,7 @@ void sliver_gcn1_records(const uint32_t* h, int64_t n, int64_t K, int wb, const 
                          const float* beta, int64_t C, uint32_t* rec, cudaStream_t s) {
   const int hspw = static_cast<int>(spw(K, wb));
   const bool v4 = hspw == 4 && reinterpret_cast<uintptr_t>(h) % 16 == 0;
-  k_sl_gcn1_records<<<static_cast<unsigned>(cdiv((n + 1) * 4, 256)), 256, 0, s>>>(
+  k_sl_gcn1_records<<<static_cast<unsigned>(std::min<int64_t>(cdiv((n + 1) * 4, 256), sm_count() * 8)), 256, 0, s>>>(
       h, n, hspw, static_cast<int>(K), wt, beta, static_cast<int>(C), rec, v4);
   BG_LAUNCH_CHECK();
 }
