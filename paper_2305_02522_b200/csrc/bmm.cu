@@ -1224,7 +1224,7 @@ int fbb_force() {
   const char* e = std::getenv("BG_FBB");
   if (!e) return 0;
   const std::string v(e);
-  return v == "scalar" ? 1 : v == "imma" ? 2 : v == "tma" ? 3 : v == "tc" ? 5 : v == "bulk" ? 6 : v == "tmem" ? 7 : 0;
+  return v == "scalar" ? 1 : v == "imma" ? 2 : v == "tma" ? 3 : v == "tc" ? 5 : v == "bulk" ? 6 : v == "tmem" ? 7 : v == "tmem2" ? 8 : 0;
 }
 
 bool bmm_pair(const BmmArgs& a, cudaStream_t s) {
@@ -1233,6 +1233,8 @@ bool bmm_pair(const BmmArgs& a, cudaStream_t s) {
   const int force = fbb_force();
   const bool few_rows = a.rows < 24576 && std::getenv("BG_FBB") == nullptr;  // as bmm()
   if (force == 6 && fbb_bulk(a, s)) return true;
+  if (force == 7 && fbb_tmem(a, s)) return true;
+  if (force == 8 && fbb_tmem(a, s, true)) return true;
   if (force == 1 || few_rows) {
     // warp per row: pairs up to 256 combined columns (8 per lane); wider
     // pairs measured slower than two products (Flickr, 2 x 256 columns:
@@ -1259,11 +1261,14 @@ void bmm(const BmmArgs& a, cudaStream_t s) {
   // row kernel) stays on the warp-per-row kernel at any row count.
   // F output keeps the tensor-core kernel (Flickr FBF 63 vs 83 us).
   const bool few_rows = af && ob && (a.rows < 24576 || a.n > 128) && std::getenv("BG_FBB") == nullptr;
-  // Wide products (N > 128, Flickr's 256 columns) from ~16K rows: the
-  // tcgen05 kernel with A in tensor memory (fbb_tmem.cu), Flickr 0.139 ->
-  // 0.065 ms per product; at N <= 128 (Reddit) the TMA-fed mma.sync kernel
-  // below measured 3 % faster and stays (scripts/fbb_rows_probe.py)
+  // The tcgen05 kernel with A in tensor memory (fbb_tmem.cu), as 2-CTA
+  // clusters (cta_group::2: each CTA holds half the weights, four ring
+  // slots): Flickr's 256-column products 0.139 -> 0.055 ms, Reddit 0.136 ->
+  // 0.12 ms; below ~100K rows at N <= 128 the TMA-fed mma.sync kernel is as
+  // fast or faster (scripts/fbb_rows_probe.py) and keeps those shapes
+  if (force == 0 && af && ob && a.n >= 64 && a.rows >= (a.n > 128 ? 8192 : 98304) && fbb_tmem(a, s, true)) return;
   if (((force == 0 && af && a.n > 128 && a.rows >= 16384) || force == 7) && ob && fbb_tmem(a, s)) return;
+  if (force == 8 && ob && fbb_tmem(a, s, true)) return;
   // opt-in (BG_FBB=bulk): every row requested at once by bulk copies
   // (fbb_bulk.cu); measured slower than the warp-per-row kernel on Cora and
   // PubMed (DESIGN 4.3)

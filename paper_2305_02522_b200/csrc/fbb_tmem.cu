@@ -47,11 +47,11 @@ namespace {
 
 constexpr int kTmM = 128;
 constexpr int kTmPR = 16;                              // rows per fp32 piece
-constexpr int kTmSlots = 3;
 constexpr int kTmParts = 4;                            // converter warps per TMEM lane quarter
 constexpr int kTmConv = 4 * kTmParts;                  // 16 converter warps
 constexpr int kTmThreads = (8 + kTmConv) * 32;         // 24 warps
 constexpr int kTmPieces = kTmM / kTmPR;                // pieces per tile
+constexpr int kTmMaxSlots = 16;
 
 __device__ __forceinline__ uint32_t tm_sign4(float x0, float x1, float x2, float x3) {
   const uint32_t m = static_cast<uint32_t>(x0 >= 0.0f) | (static_cast<uint32_t>(x1 >= 0.0f) << 1) |
@@ -75,6 +75,36 @@ __device__ __forceinline__ void tm_wait(uint64_t* bar, uint32_t parity) {
   if (!ok) __trap();
 }
 
+// the same wait with cluster-scope acquire (barriers the peer CTA arrives on)
+__device__ __forceinline__ void tm_wait_cl(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  for (uint32_t it = 0; it < (1u << 26) && !ok; ++it)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  if (!ok) __trap();
+}
+
+// arrive on the barrier at the same shared-memory offset in CTA `cta` of the cluster
+__device__ __forceinline__ void tm_arrive_cta(uint64_t* bar, uint32_t cta) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ uint64_t tm_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
@@ -92,25 +122,41 @@ struct TmArgs {
   uint32_t a_cols;     // TMEM columns per A buffer (multiple of 32)
   uint32_t a_col0;     // first A buffer's column (after the N accumulator columns)
   int64_t span;        // rows per CTA (multiple of 16): CTA b owns [b*span, min(rows, (b+1)*span))
+  int slots;           // fp32 ring slots (<= kTmMaxSlots)
+  int wcols;           // rows of wt (a pair: W1 | zero pad | W2)
+  int half;            // a pair: the second product's first column (0: single product)
+  uint32_t* out2;      // a pair: the second product's bits
   uint32_t* out;
 };
 
+// PAIR: a 2-CTA cluster runs tcgen05.mma.cta_group::2 (M = 256, one 128-row
+// tile per CTA): each CTA holds half of the weight columns, so the freed 39 KB
+// (Reddit) buy a fourth ring slot; the leader CTA issues the MMAs, the peer's
+// converters and epilogue warps arrive on the leader's barriers remotely, and
+// the leader's commits are multicast to both CTAs.
+template <bool PAIR>
 __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
+  const int kTmSlots = a.slots;
+  constexpr int kTile = PAIR ? 2 * kTmM : kTmM;  // rows per (pair) tile
   extern __shared__ __align__(1024) uint8_t sm[];
-  __shared__ __align__(8) uint64_t full[kTmSlots], empty[kTmSlots], a_full[2], a_empty[2], acc_full, acc_empty;
+  __shared__ __align__(8) uint64_t full[kTmMaxSlots], empty[kTmMaxSlots], a_full[2], a_empty[2], acc_full, acc_empty;
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int kpad = a.kpad, N = a.N;
-  const uint32_t bchunk = static_cast<uint32_t>(N) * 16u;
-  uint8_t* B = sm;  // kpad/16 chunks x N rows x 16 B (canonical K-major, no swizzle)
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const bool leader = rank == 0;
+  const int kpad = a.kpad, N = a.N, NB = PAIR ? a.N / 2 : a.N;  // NB: weight columns held here
+  const uint32_t bchunk = static_cast<uint32_t>(NB) * 16u;
+  uint8_t* B = sm;  // kpad/16 chunks x NB rows x 16 B (canonical K-major, no swizzle)
   const uint32_t slot_floats = static_cast<uint32_t>(kTmPR * a.k) + 32;  // + pad: the last row's last step reads past
-  float* ring = reinterpret_cast<float*>(B + static_cast<size_t>(kpad) * N);
-  // this CTA's rows: one contiguous, 16-aligned range (all CTAs finish
-  // together; the last tile of a range is partial)
-  const int64_t rb0 = static_cast<int64_t>(blockIdx.x) * a.span, rb1 = std::min(a.rows, rb0 + a.span);
-  const int64_t my = rb1 > rb0 ? (rb1 - rb0 + kTmM - 1) / kTmM : 0;
+  float* ring = reinterpret_cast<float*>(B + static_cast<size_t>(kpad) * NB);
+  // this CTA's rows: one contiguous, 16-aligned range per CTA (per pair: the
+  // pair's tiles of 256 rows, the leader taking the first 128 of each); all
+  // ranges finish together, the last tile of a range is partial
+  const int64_t unit = PAIR ? blockIdx.x >> 1 : blockIdx.x;
+  const int64_t rb0 = unit * a.span, rb1 = std::min(a.rows, rb0 + a.span);
+  const int64_t my = rb1 > rb0 ? (rb1 - rb0 + kTile - 1) / kTile : 0;
   const int64_t npieces = my * kTmPieces;
-  auto tile_row0 = [&](int64_t j) { return rb0 + j * kTmM; };
+  auto tile_row0 = [&](int64_t j) { return rb0 + j * kTile + static_cast<int64_t>(kTmM) * rank; };
   // piece u of this CTA: rows [r0, r0 + nr); bulk-copied when its byte
   // count is a multiple of 16 (every full piece), else read from HBM
   auto piece = [&](int64_t u, int64_t* r0) {
@@ -119,8 +165,7 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
     return static_cast<int>(left <= 0 ? 0 : left < kTmPR ? left : kTmPR);
   };
   auto staged_piece = [&](int nr) { return nr > 0 && (static_cast<uint32_t>(nr) * a.k * 4u) % 16 == 0; };
-  auto issue = [&](int64_t u) {
-    const int s = static_cast<int>(u % kTmSlots);
+  auto issue = [&](int64_t u, int s) {  // piece u into slot s (= u % slots)
     int64_t r0;
     const int nr = piece(u, &r0);
     if (staged_piece(nr)) {
@@ -137,28 +182,30 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
       mbar_init(&empty[s], kTmConv);  // every converter warp releases every piece
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&a_full[b], kTmConv);
+      mbar_init(&a_full[b], PAIR ? 2 * kTmConv : kTmConv);  // (leader) both CTAs' converters
       mbar_init(&a_empty[b], 1);
     }
     mbar_init(&acc_full, 1);
-    mbar_init(&acc_empty, 4);
+    mbar_init(&acc_empty, PAIR ? 8 : 4);  // (leader) both CTAs' epilogue warps
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // the first two pieces go out before the weights are set up
-    for (int64_t u = 0; u < std::min<int64_t>(kTmSlots - 1, npieces); ++u) issue(u);
+    for (int64_t u = 0; u < std::min<int64_t>(kTmSlots - 1, npieces); ++u) issue(u, static_cast<int>(u));
   }
   // weights as +-1 bytes (0 past K and for columns >= n): the packed words
   // are staged in the last (still idle) ring slot by asynchronous copies
   // first, so the expansion below does not wait one L2 round trip per
   // iteration
   const uint32_t* wst = reinterpret_cast<const uint32_t*>(ring + (kTmSlots - 1) * slot_floats);
-  for (int t = tid; t < a.n * a.kspw; t += blockDim.x) cp_async4(const_cast<uint32_t*>(wst) + t, a.wt + t);
+  for (int t = tid; t < a.wcols * a.kspw; t += blockDim.x) cp_async4(const_cast<uint32_t*>(wst) + t, a.wt + t);
   cp_async_wait_all();
   __syncthreads();
-  for (int t = tid; t < N * (kpad / 4); t += blockDim.x) {
+  for (int t = tid; t < NB * (kpad / 4); t += blockDim.x) {
     const int o = t / (kpad / 4), p4 = (t % (kpad / 4)) * 4;
+    const int oc = o + static_cast<int>(rank) * NB;  // the weight column
     uint32_t v = 0;
-    if (o < a.n && p4 < a.k) {
-      const uint32_t word = wst[o * a.kspw + (p4 >> 5)];
+    const bool col_ok = a.half ? (oc < a.half ? oc < a.n : oc - a.half < a.n) : oc < a.n;
+    if (col_ok && p4 < a.k) {
+      const uint32_t word = wst[oc * a.kspw + (p4 >> 5)];
       const uint32_t nib = (word >> (28 - (p4 & 31))) & 0xFu;
       const uint32_t spread = ((nib >> 3) & 1u) | (((nib >> 2) & 1u) << 8) | (((nib >> 1) & 1u) << 16) | ((nib & 1u) << 24);
       v = 0xFFFFFFFFu - 0xFEu * spread;
@@ -167,35 +214,47 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
     *reinterpret_cast<uint32_t*>(B + (p4 >> 4) * bchunk + o * 16 + (p4 & 15)) = v;
   }
   if (warp == 1) {  // TMEM: two A buffers + one accumulator
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_base)),
-                 "r"(512)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_base)),
+                   "r"(512)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_base)),
+                   "r"(512)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
 
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // weights -> tensor core
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (PAIR) cluster_sync_all();  // the peer's weights, barriers and TMEM are ready
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
   const uint32_t acc_col = 0, a_col0 = a.a_col0;  // accumulator at column 0, A buffers after it
 
   if (warp == 0) {
     // ---------------- producer ----------------
-    if (lane == 0)
-      for (int64_t u = kTmSlots - 1; u < npieces; ++u) {  // pieces 0, 1 went out in the prologue
-        const int s = static_cast<int>(u % kTmSlots);
-        if (u >= kTmSlots) tm_wait(&empty[s], static_cast<uint32_t>((u / kTmSlots - 1) & 1));
-        issue(u);
+    if (lane == 0) {
+      // slot s and use count k of piece u (u = k * slots + s) kept incrementally
+      int s = kTmSlots - 1;
+      uint32_t k = 0;
+      for (int64_t u = kTmSlots - 1; u < npieces; ++u) {  // the first slots - 1 pieces went out in the prologue
+        if (k > 0) tm_wait(&empty[s], (k - 1) & 1u);
+        issue(u, s);
+        if (++s == kTmSlots) s = 0, ++k;
       }
-  } else if (warp == 1) {
+    }
+  } else if (warp == 1 && leader) {
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
-                           (static_cast<uint32_t>(kTmM >> 4) << 24);  // kind::i8, s32 += s8 x s8, K-major
+                           (static_cast<uint32_t>(kTile >> 4) << 24);  // kind::i8, s32 += s8 x s8, K-major
     for (int64_t j = 0; j < my; ++j) {
       const int b = static_cast<int>(j & 1);
-      tm_wait(&a_full[b], static_cast<uint32_t>((j >> 1) & 1));
-      if (j >= 1) tm_wait(&acc_empty, static_cast<uint32_t>((j - 1) & 1));
+      tm_wait_cl(&a_full[b], static_cast<uint32_t>((j >> 1) & 1));
+      if (j >= 1) tm_wait_cl(&acc_empty, static_cast<uint32_t>((j - 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (lane == 0) {
         const uint32_t bbase = smem_addr(B);
@@ -203,18 +262,38 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
         for (int ks = 0; ks < kpad / 32; ++ks) {
           const uint64_t bd = tm_desc(bbase + 2 * ks * bchunk, bchunk, 128);
           const uint32_t accum = ks > 0 ? 1u : 0u;
-          asm volatile(
-              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-              " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dcol),
-              "r"(acol + 8u * ks), "l"(bd), "r"(idesc), "r"(accum)
-              : "memory");
+          if (PAIR)
+            asm volatile(
+                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                " tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dcol),
+                "r"(acol + 8u * ks), "l"(bd), "r"(idesc), "r"(accum)
+                : "memory");
+          else
+            asm volatile(
+                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dcol),
+                "r"(acol + 8u * ks), "l"(bd), "r"(idesc), "r"(accum)
+                : "memory");
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         smem_addr(&acc_full))
-                     : "memory");
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         smem_addr(&a_empty[b]))
-                     : "memory");
+        if (PAIR) {  // both CTAs' barriers
+          asm volatile(
+              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                  smem_addr(&acc_full)),
+              "h"(static_cast<uint16_t>(3))
+              : "memory");
+          asm volatile(
+              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                  smem_addr(&a_empty[b])),
+              "h"(static_cast<uint16_t>(3))
+              : "memory");
+        } else {
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_addr(&acc_full))
+                       : "memory");
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_addr(&a_empty[b]))
+                       : "memory");
+        }
       }
       __syncwarp();
     }
@@ -241,15 +320,26 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
         uint32_t m = 0;
 #pragma unroll
         for (int t = 0; t < 32; ++t) m |= (static_cast<int32_t>(d[t]) >= 0 ? 1u : 0u) << (31 - t);
-        if (32 * cw + 32 > a.n) m &= 32 * cw >= a.n ? 0u : tail_mask32(a.n);  // columns >= n stay 0
+        const int c0 = a.half && 32 * cw >= a.half ? 32 * cw - a.half : 32 * cw;  // column in its product
+        if (c0 + 32 > a.n) m &= c0 >= a.n ? 0u : tail_mask32(a.n);  // columns >= n stay 0
         words[cw] = m;
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) tm_arrive(&acc_empty);
+      if (lane == 0) {
+        if (PAIR) tm_arrive_cta(&acc_empty, 0);  // the leader's
+        else tm_arrive(&acc_empty);
+      }
       if (row < rb1) {
         uint32_t* o = a.out + row * a.ospw;
-        if (a.ospw == 4) {
+        if (a.half) {  // a pair: words of the first product, then of the second
+          const int hw = a.half / 32;
+          uint32_t* o2 = a.out2 + row * a.ospw;
+          for (int w = 0; w < a.ospw; ++w) {
+            o[w] = w < hw ? words[w] : 0u;
+            o2[w] = w < hw && hw + w < 8 ? words[hw + w] : 0u;
+          }
+        } else if (a.ospw == 4) {
           *reinterpret_cast<uint4*>(o) = make_uint4(words[0], words[1], words[2], words[3]);
         } else if (a.ospw == 8) {
           reinterpret_cast<uint4*>(o)[0] = make_uint4(words[0], words[1], words[2], words[3]);
@@ -277,13 +367,16 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
     const int s0 = steps * part / kTmParts, s1 = steps * (part + 1) / kTmParts;
     const int pq = 32 / kTmPR;  // pieces per lane quarter
     const int tr = lane >> 2, tc = lane & 3;  // rows tr and tr+8 of a piece, floats 8tc .. 8tc+7 of a step
+    int cs = 0;        // slot of the next piece (pieces are consumed in order)
+    uint32_t ck = 0;   // its use count
     for (int64_t j = 0; j < my; ++j) {
       const int b = static_cast<int>(j & 1);
       if (j >= 2) tm_wait(&a_empty[b], static_cast<uint32_t>(((j >> 1) - 1) & 1));
       for (int p = 0; p < kTmPieces; ++p) {
         const int64_t v = j * kTmPieces + p;
-        const int s = static_cast<int>(v % kTmSlots);
-        tm_wait(&full[s], static_cast<uint32_t>((v / kTmSlots) & 1));
+        const int s = cs;
+        tm_wait(&full[s], ck & 1u);
+        if (++cs == kTmSlots) cs = 0, ++ck;
         if (p / pq == q) {
           const int h = p % pq;  // which 16 lanes of the quarter
           int64_t pr0;
@@ -329,14 +422,22 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) tm_arrive(&a_full[b]);
+      if (lane == 0) {
+        if (PAIR) tm_arrive_cta(&a_full[b], 0);  // the leader's
+        else tm_arrive(&a_full[b]);
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (PAIR) cluster_sync_all();  // the leader's MMAs have read this CTA's TMEM for the last time
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+  if (warp == 1) {
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+  }
 }
 
 }  // namespace
@@ -344,9 +445,12 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
 // FBB on k_fbb_tmem: false (nothing launched) when not eligible.  Single
 // products with <= 256 output columns whose A tile fits two TMEM buffers next
 // to the accumulator (N <= 128: K <= 768; N = 256: K <= 512) and whose
-// weights and ring fit in shared memory.
-bool fbb_tmem(const BmmArgs& a, cudaStream_t s) {
-  if (!a.a_f || !a.out_bits || a.out_bits2 || a.n == 0 || a.n > 256 || a.k <= 0 || a.rows == 0) return false;
+// weights and ring fit in shared memory.  pair: the 2-CTA cta_group::2 form
+// (N >= 64).
+bool fbb_tmem(const BmmArgs& a, cudaStream_t s, bool pair) {
+  if (!a.a_f || !a.out_bits || a.n == 0 || a.n > 256 || a.k <= 0 || a.rows == 0) return false;
+  const bool paired = a.out_bits2 != nullptr;
+  if (paired && (a.n2 != a.n || 2 * 32 * cdiv(a.n, 32) > 256)) return false;
   if (reinterpret_cast<uintptr_t>(a.a_f) % 16 != 0) return false;
   TmArgs t{};
   t.x = a.a_f;
@@ -356,25 +460,61 @@ bool fbb_tmem(const BmmArgs& a, cudaStream_t s) {
   t.kspw = static_cast<int>(spw(a.k, a.wb));
   t.kpad = static_cast<int>(32 * cdiv(a.k, 32));
   t.n = static_cast<int>(a.n);
-  t.N = static_cast<int>(32 * cdiv(a.n, 32));
+  t.half = paired ? static_cast<int>(32 * cdiv(a.n, 32)) : 0;
+  t.N = paired ? 2 * t.half : static_cast<int>(32 * cdiv(a.n, 32));
+  t.wcols = paired ? t.half + t.n : t.n;
   t.ospw = static_cast<int>(spw(a.n, a.wb));
   t.out = a.out_bits;
+  t.out2 = a.out_bits2;
   t.a_cols = static_cast<uint32_t>(32 * cdiv(t.kpad / 4, 32));
   t.a_col0 = static_cast<uint32_t>(std::max(128, t.N));
   if (t.a_col0 + 2 * t.a_cols > 512) return false;
-  const size_t smem = static_cast<size_t>(t.kpad) * t.N +
-                      static_cast<size_t>(kTmSlots) * (static_cast<size_t>(kTmPR) * a.k + 32) * 4;
+  if (pair && t.N < 64) return false;
+  // as many 16-row fp32 slots as the shared memory left by the weights
+  // holds, at least three and at most four (Reddit: 3, or 4 as a pair;
+  // Flickr as a pair: 4 slots 94.6 us, 5 slots 98.5 us; BG_TMEM_SLOTS caps
+  // lower)
+  const int nb = pair ? t.N / 2 : t.N;
   const size_t cap = 227 * 1024 - 1024;  // static shared memory (barriers, TMEM base) counts too
-  if (smem > cap) return false;
-  static int attr_done = 0;
-  if (!attr_done) {
-    BG_CUDA(cudaFuncSetAttribute(k_fbb_tmem, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap)));
-    attr_done = 1;
+  const size_t wbytes = static_cast<size_t>(t.kpad) * nb, sbytes = (static_cast<size_t>(kTmPR) * a.k + 32) * 4;
+  if (wbytes + 3 * sbytes > cap) return false;
+  t.slots = static_cast<int>(std::min<size_t>(4, (cap - wbytes) / sbytes));
+  if (const char* e = std::getenv("BG_TMEM_SLOTS")) t.slots = std::max(3, std::min(t.slots, std::atoi(e)));
+  // the packed weights are staged in the last slot before the ring starts
+  if (static_cast<size_t>(t.wcols) * t.kspw * 4 > sbytes) return false;
+  const size_t smem = wbytes + static_cast<size_t>(t.slots) * sbytes;
+  static int attr_done[2] = {0, 0};
+  auto kern = pair ? k_fbb_tmem<true> : k_fbb_tmem<false>;
+  if (!attr_done[pair]) {
+    BG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap)));
+    attr_done[pair] = 1;
   }
-  // one contiguous 16-aligned row range per CTA, as even as 16 rows allow
-  t.span = 16 * cdiv(cdiv(a.rows, sm_count()), 16);
-  const int64_t blocks = cdiv(a.rows, t.span);
-  k_fbb_tmem<<<static_cast<unsigned>(blocks), kTmThreads, smem, s>>>(t);
+  if (!pair) {
+    // one contiguous 16-aligned row range per CTA, as even as 16 rows allow
+    t.span = 16 * cdiv(cdiv(a.rows, sm_count()), 16);
+    const int64_t blocks = cdiv(a.rows, t.span);
+    kern<<<static_cast<unsigned>(blocks), kTmThreads, smem, s>>>(t);
+  } else {
+    // one contiguous range of 256-row tiles per CTA pair (2-CTA clusters);
+    // 32-row ranges that use every pair of the chip but end in a partial
+    // tile measured 4 % slower (Reddit 162 vs 156 us, Flickr 97 vs 93 us)
+    const int64_t pairs = std::max<int64_t>(1, std::min<int64_t>(sm_count() / 2, cdiv(a.rows, 256)));
+    t.span = 256 * cdiv(cdiv(a.rows, pairs), 256);
+    const int64_t used = cdiv(a.rows, t.span);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * used));
+    cfg.blockDim = dim3(kTmThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    BG_CUDA(cudaLaunchKernelEx(&cfg, kern, t));
+  }
   BG_LAUNCH_CHECK();
   return true;
 }

@@ -222,7 +222,7 @@ bool fbb_tc(const BmmArgs& a, cudaStream_t s);
 // every row requested at kernel start by bulk copies; false when not eligible
 bool fbb_bulk(const BmmArgs& a, cudaStream_t s);
 // fbb_tmem.cu: F->B products with the A operand in tensor memory (wide K)
-bool fbb_tmem(const BmmArgs& a, cudaStream_t s);
+bool fbb_tmem(const BmmArgs& a, cudaStream_t s, bool pair = false);
 
 // ---- bspmm.cu ------------------------------------------------------------
 // Integer path (BBB / BBF): out(i,k) = 2*#{j in N(i): x_jk = 1} - deg_i.

@@ -16,7 +16,7 @@ import paper_2305_02522_b200 as bg
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["tc", "umma", "umma2", "tma", "imma", "scalar", "bulk", "tmem"])
+@pytest.fixture(params=["tc", "umma", "umma2", "tma", "imma", "scalar", "bulk", "tmem", "tmem2"])
 def umma(monkeypatch, request):
     # umma: LDG-fed conversion; umma2: bulk-copied fp32 sub-tiles (TMA ring);
     # and the non-tcgen05 paths the default dispatch picks by shape: the
