@@ -471,14 +471,15 @@ bool fbb_tmem(const BmmArgs& a, cudaStream_t s, bool pair) {
   if (t.a_col0 + 2 * t.a_cols > 512) return false;
   if (pair && t.N < 64) return false;
   // as many 16-row fp32 slots as the shared memory left by the weights
-  // holds, at least three and at most four (Reddit: 3, or 4 as a pair;
-  // Flickr as a pair: 4 slots 94.6 us, 5 slots 98.5 us; BG_TMEM_SLOTS caps
-  // lower)
+  // holds, at least three, about 140 KB of them at most (Reddit: 3, or 4 as
+  // a pair; Flickr as a pair: 4 slots of 32 KB 94.6 us, 5 slots 98.5 us;
+  // BG_TMEM_SLOTS caps lower)
   const int nb = pair ? t.N / 2 : t.N;
   const size_t cap = 227 * 1024 - 1024;  // static shared memory (barriers, TMEM base) counts too
   const size_t wbytes = static_cast<size_t>(t.kpad) * nb, sbytes = (static_cast<size_t>(kTmPR) * a.k + 32) * 4;
   if (wbytes + 3 * sbytes > cap) return false;
-  t.slots = static_cast<int>(std::min<size_t>(4, (cap - wbytes) / sbytes));
+  t.slots = static_cast<int>(std::min<size_t>({kTmMaxSlots, (cap - wbytes) / sbytes,
+                                                std::max<size_t>(3, (140 * 1024) / sbytes)}));
   if (const char* e = std::getenv("BG_TMEM_SLOTS")) t.slots = std::max(3, std::min(t.slots, std::atoi(e)));
   // the packed weights are staged in the last slot before the ring starts
   if (static_cast<size_t>(t.wcols) * t.kspw * 4 > sbytes) return false;
