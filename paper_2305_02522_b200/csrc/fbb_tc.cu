@@ -212,9 +212,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_fbb_tc(const TcArgs a) {
                 "=r"(d[29]), "=r"(d[30]), "=r"(d[31])
               : "r"(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(b * N + h * half_cols + 32 * cw)));
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          // the sign bits shift in one funnel shift each (MSB-first); bit = dot >= 0
           uint32_t m = 0;
 #pragma unroll
-          for (int t = 0; t < 32; ++t) m |= (static_cast<int32_t>(d[t]) >= 0 ? 1u : 0u) << (31 - t);
+          for (int t = 0; t < 32; ++t) m = __funnelshift_l(d[t], m, 1);
+          m = ~m;
           if (32 * cw + 32 > a.n) m &= 32 * cw >= a.n ? 0u : tail_mask32(a.n);  // columns >= n stay 0
           words[cw] = m;
         }

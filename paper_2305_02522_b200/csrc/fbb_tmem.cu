@@ -317,9 +317,11 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
               "=r"(d[29]), "=r"(d[30]), "=r"(d[31])
             : "r"(tmem + (static_cast<uint32_t>(32 * q) << 16) + acc_col + static_cast<uint32_t>(32 * cw)));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        // the sign bits shift in one funnel shift each (MSB-first); bit = dot >= 0
         uint32_t m = 0;
 #pragma unroll
-        for (int t = 0; t < 32; ++t) m |= (static_cast<int32_t>(d[t]) >= 0 ? 1u : 0u) << (31 - t);
+        for (int t = 0; t < 32; ++t) m = __funnelshift_l(d[t], m, 1);
+        m = ~m;
         const int c0 = a.half && 32 * cw >= a.half ? 32 * cw - a.half : 32 * cw;  // column in its product
         if (c0 + 32 > a.n) m &= c0 >= a.n ? 0u : tail_mask32(a.n);  // columns >= n stay 0
         words[cw] = m;
