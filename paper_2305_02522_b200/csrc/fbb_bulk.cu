@@ -153,7 +153,10 @@ __global__ void __launch_bounds__(kBkWarps * 32, 1) k_fbb_bulk(const BulkArgs a)
       for (int m = 0; m < M; ++m) diff[m] += __popc(aw ^ swl[32 * m * a.ld + w]);
     }
     __syncwarp();
-    if (lane == 0 && t + a.d < nrows) issue(t + a.d);  // every lane has read slot s
+    if (lane == 0 && t + a.d < nrows) {  // every lane has read slot s
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async-proxy refill
+      issue(t + a.d);
+    }
     if (++s == a.d) s = 0, phase ^= 1u;
     if (OUTB) {
       uint32_t mine = 0;

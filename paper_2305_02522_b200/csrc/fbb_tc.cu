@@ -146,7 +146,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_fbb_tc(const TcArgs a) {
     if (lane == 0)
       for (int64_t u = 0; u < npieces; ++u) {
         const int s = static_cast<int>(u % a.slots);
-        if (u >= a.slots) tc_wait(&empty[s], static_cast<uint32_t>((u / a.slots - 1) & 1));
+        if (u >= a.slots) {
+          tc_wait(&empty[s], static_cast<uint32_t>((u / a.slots - 1) & 1));
+          // the converters' generic reads of the slot before the bulk copy's async-proxy writes
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
         int64_t r0;
         const int nr = piece_rows(u, &r0);
         const uint32_t bytes = static_cast<uint32_t>(nr) * static_cast<uint32_t>(a.k) * 4u;

@@ -243,6 +243,9 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
       uint32_t k = 0;
       for (int64_t u = kTmSlots - 1; u < npieces; ++u) {  // the first slots - 1 pieces went out in the prologue
         if (k > 0) tm_wait(&empty[s], (k - 1) & 1u);
+        // the generic reads of the slot (converters; for the last slot's first
+        // piece, the weight expansion) before the bulk copy's async-proxy writes
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue(u, s);
         if (++s == kTmSlots) s = 0, ++k;
       }
@@ -473,15 +476,14 @@ bool fbb_tmem(const BmmArgs& a, cudaStream_t s, bool pair) {
   if (t.a_col0 + 2 * t.a_cols > 512) return false;
   if (pair && t.N < 64) return false;
   // as many 16-row fp32 slots as the shared memory left by the weights
-  // holds, at least three, about 140 KB of them at most (Reddit: 3, or 4 as
-  // a pair; Flickr as a pair: 4 slots of 32 KB 94.6 us, 5 slots 98.5 us;
+  // holds, at least three and at most four (Reddit: 3, or 4 as a pair;
+  // Flickr as a pair: 4 slots of 32 KB 94.6 us, 5 slots 98.5 us;
   // BG_TMEM_SLOTS caps lower)
   const int nb = pair ? t.N / 2 : t.N;
   const size_t cap = 227 * 1024 - 1024;  // static shared memory (barriers, TMEM base) counts too
   const size_t wbytes = static_cast<size_t>(t.kpad) * nb, sbytes = (static_cast<size_t>(kTmPR) * a.k + 32) * 4;
   if (wbytes + 3 * sbytes > cap) return false;
-  t.slots = static_cast<int>(std::min<size_t>({kTmMaxSlots, (cap - wbytes) / sbytes,
-                                                std::max<size_t>(3, (140 * 1024) / sbytes)}));
+  t.slots = static_cast<int>(std::min<size_t>(4, (cap - wbytes) / sbytes));
   if (const char* e = std::getenv("BG_TMEM_SLOTS")) t.slots = std::max(3, std::min(t.slots, std::atoi(e)));
   // the packed weights are staged in the last slot before the ring starts
   if (static_cast<size_t>(t.wcols) * t.kspw * 4 > sbytes) return false;
