@@ -141,7 +141,10 @@ __global__ void __launch_bounds__(256)
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   const bool word_ok = g < xspw;
-  const uint32_t* xg = x + (word_ok ? g : 0);
+  // gather address = base + col * row stride: one IMAD.WIDE.U32 per load (a
+  // 64-bit col * xspw product costs several IMADs)
+  const uint64_t xbase = reinterpret_cast<uint64_t>(x + (word_ok ? g : 0));
+  const uint32_t xsb = static_cast<uint32_t>(xspw) * 4u;
   for (int64_t i0 = row0 + wid * R; i0 < row1; i0 += nw * R) {
     const int64_t i = i0 + r;
     const bool ok = i < row1;
@@ -169,7 +172,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int m = 0; m < 8; ++m) {
         v[m] = 0u;
-        if (j + m < walk && word_ok) v[m] = __ldg(xg + static_cast<int64_t>(cc[m]) * xspw);
+        if (j + m < walk && word_ok) v[m] = __ldg(reinterpret_cast<const uint32_t*>(mad_wide(cc[m], xsb, xbase)));
       }
       hs_add8<NP>(P, v);
     }
