@@ -434,6 +434,9 @@ __global__ void __launch_bounds__(256)
   double d[M];
 #pragma unroll
   for (int m = 0; m < M; ++m) d[m] = 0.0;
+  // operand row address = base + col * row bytes by one IMAD.WIDE.U32
+  const uint32_t xrs = XBITS ? static_cast<uint32_t>(xspw) * 4u : static_cast<uint32_t>(f) * 4u;
+  const uint64_t xrow0 = XBITS ? reinterpret_cast<uint64_t>(xb) : reinterpret_cast<uint64_t>(xf);
   const uint64_t e0 = srp[i];
   const uint32_t len = static_cast<uint32_t>(srp[i + 1] - e0);
   for (uint32_t base = 0; base < len; base += 32) {
@@ -452,10 +455,12 @@ __global__ void __launch_bounds__(256)
           const int64_t k = fbase + 32 * m + lane;
           if (k < f) {
             if (XBITS) {
-              const uint32_t bit = (__ldg(xb + j * xspw + (k >> 5)) >> (31 - (k & 31))) & 1u;
+              const uint32_t* xr = reinterpret_cast<const uint32_t*>(mad_wide(col, xrs, xrow0));
+              const uint32_t bit = (__ldg(xr + (k >> 5)) >> (31 - (k & 31))) & 1u;
               d[m] = __dadd_rn(d[m], bit ? w : -w);
             } else {
-              d[m] = __dadd_rn(d[m], __dmul_rn(w, static_cast<double>(__ldg(xf + j * f + k))));
+              const float* xr = reinterpret_cast<const float*>(mad_wide(col, xrs, xrow0));
+              d[m] = __dadd_rn(d[m], __dmul_rn(w, static_cast<double>(__ldg(xr + k))));
             }
           }
         }
@@ -527,6 +532,9 @@ __global__ void __launch_bounds__(256)
   if (row0 + ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * (32 / G) >= row1) return;
   const bool live = i < row1;
   double d = 0.0;
+  // operand row address = base + col * row bytes by one IMAD.WIDE.U32
+  const uint32_t xrs = XBITS ? static_cast<uint32_t>(xspw) * 4u : static_cast<uint32_t>(f) * 4u;
+  const uint64_t xrow0 = XBITS ? reinterpret_cast<uint64_t>(xb) : reinterpret_cast<uint64_t>(xf);
   const uint64_t e0 = live ? srp[i] : 0;
   const uint32_t len = live ? static_cast<uint32_t>(srp[i + 1] - e0) : 0u;
   uint32_t lmax = len;  // the warp's longest row
@@ -545,10 +553,10 @@ __global__ void __launch_bounds__(256)
         const double w = cs ? static_cast<double>(__ldg(cs + j)) : 1.0;
         if (t < f) {
           if (XBITS) {
-            const uint32_t bit = (__ldg(xb + j * xspw) >> (31 - t)) & 1u;
+            const uint32_t bit = (__ldg(reinterpret_cast<const uint32_t*>(mad_wide(col, xrs, xrow0))) >> (31 - t)) & 1u;
             d = __dadd_rn(d, bit ? w : -w);
           } else {
-            d = __dadd_rn(d, __dmul_rn(w, static_cast<double>(__ldg(xf + j * f + t))));
+            d = __dadd_rn(d, __dmul_rn(w, static_cast<double>(__ldg(reinterpret_cast<const float*>(mad_wide(col, xrs, xrow0)) + t))));
           }
         }
         if (!more) break;
