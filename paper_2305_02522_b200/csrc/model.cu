@@ -281,7 +281,7 @@ struct Exec {
   // binarized input is all ones, so B outputs are one constant row and
   // MM.FBF needs one popcount per row; probs: the following softmax fused.
   Op mm_packed(bg_variant mm, const Op& x, const WeightDev& w, const std::string& label, float* probs,
-               const RowChunks* out_chunks = nullptr) {
+               const RowChunks* out_chunks = nullptr, bool keep_logits = true) {
     if (mm.in1 != BG_F) fail("bmm: in1 is tagged F but operand is binary");
     if (!variant_valid(mm)) fail("bmm: " + variant_name(mm) + " is not a supported variant");
     if (x.cols != w.rows) fail("bmm: inner dimensions disagree");
@@ -308,12 +308,12 @@ struct Exec {
       if (out_chunks) {
         for (int c = 0; c < out_chunks->n; ++c) {
           packed_fbf(x.bits, out_chunks->bounds[c], out_chunks->bounds[c + 1], x.cols, x.wb, x.pval,
-                     w.wt.as<uint32_t>(), m.wb, w.scale.as<float>(), w.cols, r.f, probs, tab, s);
+                     w.wt.as<uint32_t>(), m.wb, w.scale.as<float>(), w.cols, keep_logits ? r.f : nullptr, probs, tab, s);
           BG_CUDA(cudaEventRecord(out_chunks->ready[c], s));
         }
       } else {
         packed_fbf(x.bits, 0, x.rows, x.cols, x.wb, x.pval, w.wt.as<uint32_t>(), m.wb, w.scale.as<float>(),
-                   w.cols, r.f, probs, tab, s);
+                   w.cols, keep_logits ? r.f : nullptr, probs, tab, s);
       }
     }
     h.end();
@@ -552,19 +552,22 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
               fused_probs = probs;
               fused_logits = o.f;
             }
+            // the logits are only written when something reads them (a fused
+            // softmax that is the model's output, no caller logits, no trace)
+            const bool keep_lg = !probs || logits || h.trace || h.timing || single || i + 2 != nl;
             h.begin(prefix + "spmm[" + variant_name(sp) + "]");
             if (probs == out && out && chunked_out(i + 2)) {
               for (int c = 0; c < chunks->out.n; ++c) {
                 const int64_t r0 = chunks->out.bounds[c], r1 = chunks->out.bounds[c + 1];
                 if (r1 > r0)
                   gcn1_aggregate(A, recs, cur.cols, cur.wb, l.w1.wt.as<uint32_t>(), l.w1.scale.as<float>(),
-                                 l.w1.cols, o.f, probs, s, r0, r1);
+                                 l.w1.cols, keep_lg ? o.f : nullptr, probs, s, r0, r1);
                 BG_CUDA(cudaEventRecord(chunks->out.ready[c], s));
               }
               chunks->out_done = true;
             } else {
               gcn1_aggregate(A, recs, cur.cols, cur.wb, l.w1.wt.as<uint32_t>(), l.w1.scale.as<float>(),
-                             l.w1.cols, o.f, probs, s);
+                             l.w1.cols, keep_lg ? o.f : nullptr, probs, s);
             }
             h.end();
             cur = o;
@@ -616,7 +619,9 @@ void forward_impl(bg_model& m, const Op& x0, float* out, float* logits, bg_trace
             float* probs = (i + 2 == nl && out) ? out : static_cast<float*>(m.pool.get(
                 static_cast<size_t>(cur.rows * l.w1.cols) * 4));
             const bool chunked = probs == out && out && chunked_out(i + 2);
-            Op o = ex.mm_packed(mm, cur, l.w1, prefix + "mm", probs, chunked ? &chunks->out : nullptr);
+            // the logits are only written when something reads them
+            const bool keep = logits || h.trace || h.timing || single || i + 2 != nl;
+            Op o = ex.mm_packed(mm, cur, l.w1, prefix + "mm", probs, chunked ? &chunks->out : nullptr, keep);
             if (chunked) chunks->out_done = true;
             fused_probs = probs;
             fused_logits = o.f;

@@ -123,7 +123,8 @@ __global__ void k_fbf_table(int64_t k, double pval, const uint32_t* __restrict__
 // the table rows they pick (coalesced stores, 32-bit index arithmetic).
 constexpr int kLookRows = 256;
 __global__ void __launch_bounds__(256) k_fbf_lookup(const uint32_t* __restrict__ bits, int64_t r0, int64_t r1,
-                                                    int xspw, int n, const float* __restrict__ tab_logits,
+                                                    int xspw, int n, uint32_t nmagic,
+                                                    const float* __restrict__ tab_logits,
                                                     const float* __restrict__ tab_probs, float* __restrict__ logits,
                                                     float* __restrict__ probs) {
   __shared__ int cnt[kLookRows];
@@ -138,13 +139,13 @@ __global__ void __launch_bounds__(256) k_fbf_lookup(const uint32_t* __restrict__
       cnt[threadIdx.x] = c;
     }
     __syncthreads();
-    float* ol = logits + b0 * n;
+    float* ol = logits ? logits + b0 * n : nullptr;  // null: the logits are not wanted
     float* op = probs ? probs + b0 * n : nullptr;
     const int total = nr * n;
     for (int e = threadIdx.x; e < total; e += blockDim.x) {
-      const int r = e / n, j = e - r * n;
+      const int r = static_cast<int>(__umulhi(static_cast<uint32_t>(e), nmagic)), j = e - r * n;  // e / n
       const int src = cnt[r] * n + j;
-      ol[e] = __ldg(tab_logits + src);
+      if (ol) ol[e] = __ldg(tab_logits + src);
       if (op) op[e] = __ldg(tab_probs + src);
     }
   }
@@ -192,8 +193,10 @@ void packed_fbf(const uint32_t* bits, int64_t r0, int64_t r1, int64_t k, int xwb
                                                                    beta, n, probs ? 1 : 0, tl, tp);
   BG_LAUNCH_CHECK();
   const int64_t blocks = std::min<int64_t>(cdiv(r1 - r0, kLookRows), 16LL * sm_count());
+  // e / n == umulhi(e, ceil(2^32 / n)) for e < kLookRows * n (e * n < 2^32)
+  const uint32_t nmagic = static_cast<uint32_t>(((uint64_t{1} << 32) + n - 1) / n);
   k_fbf_lookup<<<static_cast<unsigned>(blocks), 256, 0, s>>>(bits, r0, r1, static_cast<int>(spw(k, xwb)),
-                                                             static_cast<int>(n), tl, tp, logits, probs);
+                                                             static_cast<int>(n), nmagic, tl, tp, logits, probs);
   BG_LAUNCH_CHECK();
 }
 
