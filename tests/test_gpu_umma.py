@@ -66,3 +66,21 @@ def test_fbf_matches_oracle(umma, wb, mkn):
     got = bg.bmm("BMM.FBF", torch.from_numpy(A).cuda(), dw, wb)
     want = po.bmm("BMM.FBF", po.Mat.dense(A), ow, wb)
     assert np.array_equal(got.cpu().numpy(), want.f)
+
+
+@pytest.mark.parametrize("mkn", [(120000, 602, 128), (20000, 500, 256), (100003, 301, 96)])
+def test_default_fbb_at_dispatch_sizes(mkn):
+    # the default dispatch at the sizes where the 2-CTA tcgen05 kernel
+    # (fbb_tmem.cu, cta_group::2) takes over: Reddit-like rows, Flickr-like
+    # 256 columns, a ragged shape -- against the oracle
+    m, k, n = mkn
+    rng = po.Rng(777 + m + k + n)
+    A, W = rng.random_dense(m, k), rng.random_dense(k, n)
+    A.flat[::13] = 0.0
+    A.flat[5::17] = -0.0
+    wbits = po.binarize(W, 32)
+    dw = bg.BitOperand(bg.BitDenseMatrix.from_numpy(wbits, k, n, 32))
+    ow = po.Mat.binary(wbits, k, n, 32)
+    got = bg.bmm("BMM.FBB", torch.from_numpy(A).cuda(), dw, 32)
+    want = po.bmm("BMM.FBB", po.Mat.dense(A), ow, 32)
+    assert bits_equal(got.bits.numpy(), want.bits)
