@@ -1235,6 +1235,11 @@ bool bmm_pair(const BmmArgs& a, cudaStream_t s) {
   if (force == 6 && fbb_bulk(a, s)) return true;
   if (force == 7 && fbb_tmem(a, s)) return true;
   if (force == 8 && fbb_tmem(a, s, true)) return true;
+  // a wide-K pair (Flickr's SAGE layer: K = 500, 2 x 256 columns) as two MMA
+  // rounds per tile of the 2-CTA tcgen05 kernel: the input is read once
+  if (force == 0 && a.k >= 256 && a.rows >= 8192 && a.n >= 64 && !std::getenv("BG_TMEM_NOPAIR") &&
+      fbb_tmem(a, s, true))
+    return true;
   if (force == 1 || few_rows) {
     // warp per row: pairs up to 256 combined columns (8 per lane); wider
     // pairs measured slower than two products (Flickr, 2 x 256 columns:

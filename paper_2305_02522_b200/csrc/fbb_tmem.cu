@@ -123,8 +123,10 @@ struct TmArgs {
   uint32_t a_col0;     // first A buffer's column (after the N accumulator columns)
   int64_t span;        // rows per CTA (multiple of 16): CTA b owns [b*span, min(rows, (b+1)*span))
   int slots;           // fp32 ring slots (<= kTmMaxSlots)
+  int stage_slots;     // trailing slots that hold the packed weights until they are expanded
   int wcols;           // rows of wt (a pair: W1 | zero pad | W2)
-  int half;            // a pair: the second product's first column (0: single product)
+  int half;            // a pair: the second product's first weight row (0: single product)
+  int rounds;          // MMA rounds per tile: 1, or 2 for a pair (W1 then W2 into the same accumulator)
   uint32_t* out2;      // a pair: the second product's bits
   uint32_t* out;
 };
@@ -144,11 +146,11 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = PAIR ? cluster_rank() : 0u;
   const bool leader = rank == 0;
-  const int kpad = a.kpad, N = a.N, NB = PAIR ? a.N / 2 : a.N;  // NB: weight columns held here
+  const int kpad = a.kpad, N = a.N, NB = PAIR ? a.N / 2 : a.N;  // N per MMA round; NB: columns held here per round
   const uint32_t bchunk = static_cast<uint32_t>(NB) * 16u;
   uint8_t* B = sm;  // kpad/16 chunks x NB rows x 16 B (canonical K-major, no swizzle)
   const uint32_t slot_floats = static_cast<uint32_t>(kTmPR * a.k) + 32;  // + pad: the last row's last step reads past
-  float* ring = reinterpret_cast<float*>(B + static_cast<size_t>(kpad) * NB);
+  float* ring = reinterpret_cast<float*>(B + static_cast<size_t>(a.rounds) * kpad * NB);
   // this CTA's rows: one contiguous, 16-aligned range per CTA (per pair: the
   // pair's tiles of 256 rows, the leader taking the first 128 of each); all
   // ranges finish together, the last tile of a range is partial
@@ -189,29 +191,30 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
     mbar_init(&acc_empty, PAIR ? 8 : 4);  // (leader) both CTAs' epilogue warps
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // the first two pieces go out before the weights are set up
-    for (int64_t u = 0; u < std::min<int64_t>(kTmSlots - 1, npieces); ++u) issue(u, static_cast<int>(u));
+    for (int64_t u = 0; u < std::min<int64_t>(kTmSlots - a.stage_slots, npieces); ++u) issue(u, static_cast<int>(u));
   }
   // weights as +-1 bytes (0 past K and for columns >= n): the packed words
   // are staged in the last (still idle) ring slot by asynchronous copies
   // first, so the expansion below does not wait one L2 round trip per
   // iteration
-  const uint32_t* wst = reinterpret_cast<const uint32_t*>(ring + (kTmSlots - 1) * slot_floats);
+  const uint32_t* wst = reinterpret_cast<const uint32_t*>(ring + (kTmSlots - a.stage_slots) * slot_floats);
   for (int t = tid; t < a.wcols * a.kspw; t += blockDim.x) cp_async4(const_cast<uint32_t*>(wst) + t, a.wt + t);
   cp_async_wait_all();
   __syncthreads();
-  for (int t = tid; t < NB * (kpad / 4); t += blockDim.x) {
-    const int o = t / (kpad / 4), p4 = (t % (kpad / 4)) * 4;
-    const int oc = o + static_cast<int>(rank) * NB;  // the weight column
+  for (int t = tid; t < a.rounds * NB * (kpad / 4); t += blockDim.x) {
+    const int ro = t / (NB * (kpad / 4)), tr = t - ro * NB * (kpad / 4);  // round, item in it
+    const int o = tr / (kpad / 4), p4 = (tr % (kpad / 4)) * 4;
+    const int pc = o + static_cast<int>(rank) * NB;  // the column in its product
+    const int oc = ro ? a.half + pc : pc;           // the weight row (a pair: W1 | pad | W2)
     uint32_t v = 0;
-    const bool col_ok = a.half ? (oc < a.half ? oc < a.n : oc - a.half < a.n) : oc < a.n;
-    if (col_ok && p4 < a.k) {
+    if (pc < a.n && p4 < a.k) {
       const uint32_t word = wst[oc * a.kspw + (p4 >> 5)];
       const uint32_t nib = (word >> (28 - (p4 & 31))) & 0xFu;
       const uint32_t spread = ((nib >> 3) & 1u) | (((nib >> 2) & 1u) << 8) | (((nib >> 1) & 1u) << 16) | ((nib & 1u) << 24);
       v = 0xFFFFFFFFu - 0xFEu * spread;
       if (p4 + 4 > a.k) v &= 0xFFFFFFFFu >> (8 * (p4 + 4 - a.k));
     }
-    *reinterpret_cast<uint32_t*>(B + (p4 >> 4) * bchunk + o * 16 + (p4 & 15)) = v;
+    *reinterpret_cast<uint32_t*>(B + static_cast<size_t>(ro) * kpad * NB + (p4 >> 4) * bchunk + o * 16 + (p4 & 15)) = v;
   }
   if (warp == 1) {  // TMEM: two A buffers + one accumulator
     if (PAIR) {
@@ -239,9 +242,9 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
     // ---------------- producer ----------------
     if (lane == 0) {
       // slot s and use count k of piece u (u = k * slots + s) kept incrementally
-      int s = kTmSlots - 1;
+      int s = kTmSlots - a.stage_slots;
       uint32_t k = 0;
-      for (int64_t u = kTmSlots - 1; u < npieces; ++u) {  // the first slots - 1 pieces went out in the prologue
+      for (int64_t u = s; u < npieces; ++u) {  // the first slots - stage_slots pieces went out in the prologue
         if (k > 0) tm_wait(&empty[s], (k - 1) & 1u);
         // the generic reads of the slot (converters; for the last slot's first
         // piece, the weight expansion) before the bulk copy's async-proxy writes
@@ -257,57 +260,66 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
     for (int64_t j = 0; j < my; ++j) {
       const int b = static_cast<int>(j & 1);
       tm_wait_cl(&a_full[b], static_cast<uint32_t>((j >> 1) & 1));
-      if (j >= 1) tm_wait_cl(&acc_empty, static_cast<uint32_t>((j - 1) & 1));
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (lane == 0) {
-        const uint32_t bbase = smem_addr(B);
-        const uint32_t acol = tmem + a_col0 + static_cast<uint32_t>(b) * a.a_cols, dcol = tmem + acc_col;
-        for (int ks = 0; ks < kpad / 32; ++ks) {
-          const uint64_t bd = tm_desc(bbase + 2 * ks * bchunk, bchunk, 128);
-          const uint32_t accum = ks > 0 ? 1u : 0u;
-          if (PAIR)
+      for (int ro = 0; ro < a.rounds; ++ro) {
+        const int64_t R = j * a.rounds + ro;  // accumulator use
+        if (R >= 1) tm_wait_cl(&acc_empty, static_cast<uint32_t>((R - 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          const uint32_t bbase = smem_addr(B) + static_cast<uint32_t>(ro * kpad * NB);
+          const uint32_t acol = tmem + a_col0 + static_cast<uint32_t>(b) * a.a_cols, dcol = tmem + acc_col;
+          for (int ks = 0; ks < kpad / 32; ++ks) {
+            const uint64_t bd = tm_desc(bbase + 2 * ks * bchunk, bchunk, 128);
+            const uint32_t accum = ks > 0 ? 1u : 0u;
+            if (PAIR)
+              asm volatile(
+                  "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                  " tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dcol),
+                  "r"(acol + 8u * ks), "l"(bd), "r"(idesc), "r"(accum)
+                  : "memory");
+            else
+              asm volatile(
+                  "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                  " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dcol),
+                  "r"(acol + 8u * ks), "l"(bd), "r"(idesc), "r"(accum)
+                  : "memory");
+          }
+          const bool last = ro + 1 == a.rounds;
+          if (PAIR) {  // both CTAs' barriers
             asm volatile(
-                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                " tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dcol),
-                "r"(acol + 8u * ks), "l"(bd), "r"(idesc), "r"(accum)
+                "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                    smem_addr(&acc_full)),
+                "h"(static_cast<uint16_t>(3))
                 : "memory");
-          else
-            asm volatile(
-                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dcol),
-                "r"(acol + 8u * ks), "l"(bd), "r"(idesc), "r"(accum)
-                : "memory");
+            if (last)
+              asm volatile(
+                  "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                      smem_addr(&a_empty[b])),
+                  "h"(static_cast<uint16_t>(3))
+                  : "memory");
+          } else {
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_addr(&acc_full))
+                         : "memory");
+            if (last)
+              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                               smem_addr(&a_empty[b]))
+                           : "memory");
+          }
         }
-        if (PAIR) {  // both CTAs' barriers
-          asm volatile(
-              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                  smem_addr(&acc_full)),
-              "h"(static_cast<uint16_t>(3))
-              : "memory");
-          asm volatile(
-              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                  smem_addr(&a_empty[b])),
-              "h"(static_cast<uint16_t>(3))
-              : "memory");
-        } else {
-          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                           smem_addr(&acc_full))
-                       : "memory");
-          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                           smem_addr(&a_empty[b]))
-                       : "memory");
-        }
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else if (warp >= 4 && warp < 8) {
     // ---------------- epilogue: TMEM lanes 32*(warp-4) .. +31 ----------------
     const int q = warp - 4;
     for (int64_t j = 0; j < my; ++j) {
-      tm_wait(&acc_full, static_cast<uint32_t>(j & 1));
+     for (int ro = 0; ro < a.rounds; ++ro) {  // round ro's product: out, or the pair's out2
+      const int64_t R = j * a.rounds + ro;
+      tm_wait(&acc_full, static_cast<uint32_t>(R & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t row = tile_row0(j) + 32 * q + lane;
-      uint32_t words[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+      uint32_t* o = (ro ? a.out2 : a.out) + row * a.ospw;
+      const bool live = row < rb1;
       for (int cw = 0; cw < N / 32; ++cw) {
         uint32_t d[32];
         asm volatile(
@@ -325,9 +337,8 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
 #pragma unroll
         for (int t = 0; t < 32; ++t) m = __funnelshift_l(d[t], m, 1);
         m = ~m;
-        const int c0 = a.half && 32 * cw >= a.half ? 32 * cw - a.half : 32 * cw;  // column in its product
-        if (c0 + 32 > a.n) m &= c0 >= a.n ? 0u : tail_mask32(a.n);  // columns >= n stay 0
-        words[cw] = m;
+        if (32 * cw + 32 > a.n) m &= 32 * cw >= a.n ? 0u : tail_mask32(a.n);  // columns >= n stay 0
+        if (live && cw < a.ospw) o[cw] = m;
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -335,24 +346,9 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
         if (PAIR) tm_arrive_cta(&acc_empty, 0);  // the leader's
         else tm_arrive(&acc_empty);
       }
-      if (row < rb1) {
-        uint32_t* o = a.out + row * a.ospw;
-        if (a.half) {  // a pair: words of the first product, then of the second
-          const int hw = a.half / 32;
-          uint32_t* o2 = a.out2 + row * a.ospw;
-          for (int w = 0; w < a.ospw; ++w) {
-            o[w] = w < hw ? words[w] : 0u;
-            o2[w] = w < hw && hw + w < 8 ? words[hw + w] : 0u;
-          }
-        } else if (a.ospw == 4) {
-          *reinterpret_cast<uint4*>(o) = make_uint4(words[0], words[1], words[2], words[3]);
-        } else if (a.ospw == 8) {
-          reinterpret_cast<uint4*>(o)[0] = make_uint4(words[0], words[1], words[2], words[3]);
-          reinterpret_cast<uint4*>(o)[1] = make_uint4(words[4], words[5], words[6], words[7]);
-        } else {
-          for (int w = 0; w < a.ospw; ++w) o[w] = w < 8 ? words[w] : 0u;
-        }
-      }
+      if (live)
+        for (int w = N / 32; w < a.ospw; ++w) o[w] = 0u;  // 64-bit word padding
+     }
     }
   } else if (warp >= 8) {
     // ---------------- converters ----------------
@@ -455,7 +451,7 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
 bool fbb_tmem(const BmmArgs& a, cudaStream_t s, bool pair) {
   if (!a.a_f || !a.out_bits || a.n == 0 || a.n > 256 || a.k <= 0 || a.rows == 0) return false;
   const bool paired = a.out_bits2 != nullptr;
-  if (paired && (a.n2 != a.n || 2 * 32 * cdiv(a.n, 32) > 256)) return false;
+  if (paired && a.n2 != a.n) return false;
   if (reinterpret_cast<uintptr_t>(a.a_f) % 16 != 0) return false;
   TmArgs t{};
   t.x = a.a_f;
@@ -465,8 +461,10 @@ bool fbb_tmem(const BmmArgs& a, cudaStream_t s, bool pair) {
   t.kspw = static_cast<int>(spw(a.k, a.wb));
   t.kpad = static_cast<int>(32 * cdiv(a.k, 32));
   t.n = static_cast<int>(a.n);
+  // a pair runs two MMA rounds per tile (W1, then W2) into one accumulator
   t.half = paired ? static_cast<int>(32 * cdiv(a.n, 32)) : 0;
-  t.N = paired ? 2 * t.half : static_cast<int>(32 * cdiv(a.n, 32));
+  t.rounds = paired ? 2 : 1;
+  t.N = static_cast<int>(32 * cdiv(a.n, 32));
   t.wcols = paired ? t.half + t.n : t.n;
   t.ospw = static_cast<int>(spw(a.n, a.wb));
   t.out = a.out_bits;
@@ -481,12 +479,13 @@ bool fbb_tmem(const BmmArgs& a, cudaStream_t s, bool pair) {
   // BG_TMEM_SLOTS caps lower)
   const int nb = pair ? t.N / 2 : t.N;
   const size_t cap = 227 * 1024 - 1024;  // static shared memory (barriers, TMEM base) counts too
-  const size_t wbytes = static_cast<size_t>(t.kpad) * nb, sbytes = (static_cast<size_t>(kTmPR) * a.k + 32) * 4;
+  const size_t wbytes = static_cast<size_t>(t.rounds) * t.kpad * nb, sbytes = (static_cast<size_t>(kTmPR) * a.k + 32) * 4;
   if (wbytes + 3 * sbytes > cap) return false;
   t.slots = static_cast<int>(std::min<size_t>(4, (cap - wbytes) / sbytes));
   if (const char* e = std::getenv("BG_TMEM_SLOTS")) t.slots = std::max(3, std::min(t.slots, std::atoi(e)));
-  // the packed weights are staged in the last slot before the ring starts
-  if (static_cast<size_t>(t.wcols) * t.kspw * 4 > sbytes) return false;
+  // the packed weights are staged in the last slot(s) before the ring starts
+  t.stage_slots = static_cast<int>(cdiv(static_cast<int64_t>(t.wcols) * t.kspw * 4, static_cast<int64_t>(sbytes)));
+  if (t.stage_slots >= t.slots) return false;
   const size_t smem = wbytes + static_cast<size_t>(t.slots) * sbytes;
   static int attr_done[2] = {0, 0};
   auto kern = pair ? k_fbb_tmem<true> : k_fbb_tmem<false>;
