@@ -29,12 +29,13 @@
 //     landed too (measured: one piece in flight, 0.213 ms on Reddit).
 // Integer dots are exact: the bits equal the reference's for any order.
 //
-// Measured (1 B200, in-graph CUDA events): Flickr's 256-column products
-// 0.139 -> 0.065 ms each (the default for N > 128 from 16 K rows); Reddit
-// (N = 128) 0.136 ms, level with the TMA-fed mma.sync kernel (bmm.cu
-// k_fbb_tma, 3 % ahead in scripts/fbb_rows_probe.py), which stays the
-// default there: the 78 KB of weights leave room for three 38.5 KB slots,
-// about two pieces in flight per SM (4.1 TB/s).
+// The default form is the 2-CTA one (PAIR below: tcgen05.mma.cta_group::2,
+// each CTA holding half of the weight columns, four ring slots); a paired
+// product (a SAGE / GraphConv layer's W1 and W2 on one input) runs two MMA
+// rounds per tile into the same accumulator, the input read once.
+// Measured (1 B200, in-graph CUDA events): Reddit 0.136 (mma.sync) -> 0.122
+// ms (ncu 0.115 ms, 4.9 TB/s); Flickr's 256-column pair 2 x 0.139 (warp per
+// row) -> one pass, forward 0.526 -> 0.142 ms over the round.
 #include <algorithm>
 #include <cstdlib>
 #include <string>
@@ -51,7 +52,7 @@ constexpr int kTmParts = 4;                            // converter warps per TM
 constexpr int kTmConv = 4 * kTmParts;                  // 16 converter warps
 constexpr int kTmThreads = (8 + kTmConv) * 32;         // 24 warps
 constexpr int kTmPieces = kTmM / kTmPR;                // pieces per tile
-constexpr int kTmMaxSlots = 16;
+constexpr int kTmMaxSlots = 4;
 
 __device__ __forceinline__ uint32_t tm_sign4(float x0, float x1, float x2, float x3) {
   const uint32_t m = static_cast<uint32_t>(x0 >= 0.0f) | (static_cast<uint32_t>(x1 >= 0.0f) << 1) |
@@ -443,11 +444,11 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
 
 }  // namespace
 
-// FBB on k_fbb_tmem: false (nothing launched) when not eligible.  Single
-// products with <= 256 output columns whose A tile fits two TMEM buffers next
-// to the accumulator (N <= 128: K <= 768; N = 256: K <= 512) and whose
-// weights and ring fit in shared memory.  pair: the 2-CTA cta_group::2 form
-// (N >= 64).
+// FBB on k_fbb_tmem: false (nothing launched) when not eligible.  Products
+// (or pairs, BmmArgs::out_bits2) with <= 256 output columns each whose A tile
+// fits two TMEM buffers next to the accumulator (N <= 128: K <= 768; N = 256:
+// K <= 512) and whose weights and ring fit in shared memory.  pair: the 2-CTA
+// cta_group::2 form (N >= 64).
 bool fbb_tmem(const BmmArgs& a, cudaStream_t s, bool pair) {
   if (!a.a_f || !a.out_bits || a.n == 0 || a.n > 256 || a.k <= 0 || a.rows == 0) return false;
   const bool paired = a.out_bits2 != nullptr;
