@@ -38,6 +38,39 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
       "r"(parity), "r"(1000000u)
       : "memory");
 }
+// Four fp32 values -> four +-1 bytes for a kind::i8 operand (x >= 0 -> 0x01,
+// else 0xFF; -0.0 -> 0x01, NaN -> 0xFF, the oracle's comparison): one
+// FSET.BF per value (1.0f / 0.0f: byte 2 is 0x80 / 0x00), byte 2 of each
+// gathered sign-replicated (PRMT selector nibble 8 + 2, 8 + 6) into a 0xFF /
+// 0x00 mask per byte by three byte permutes, then ~(mask & 0xFE) -- 8
+// instructions per 4 values (a compare-and-select build takes 13).
+__device__ __forceinline__ uint32_t ge0_bf(float x) {
+  float m;
+  asm("set.ge.f32.f32 %0, %1, 0f00000000;" : "=f"(m) : "f"(x));
+  return __float_as_uint(m);
+}
+__device__ __forceinline__ uint32_t prmt_sx(uint32_t a, uint32_t b) {  // bytes: sx(a.b2), sx(b.b2), 0, 0
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, 0x00EA;" : "=r"(r) : "r"(a), "r"(b));  // __byte_perm drops the nibbles' sign bit
+  return r;
+}
+__device__ __forceinline__ uint32_t pm1_bytes4(float x0, float x1, float x2, float x3) {
+  const uint32_t lo = prmt_sx(ge0_bf(x0), ge0_bf(x1)), hi = prmt_sx(ge0_bf(x2), ge0_bf(x3));
+  return ~(__byte_perm(lo, hi, 0x5410u) & 0xFEFEFEFEu);
+}
+// 8-byte shared-memory load by shared-window address
+__device__ __forceinline__ float2 lds_f2(uint32_t saddr) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(saddr));
+  return v;
+}
+// 16-byte shared-memory load by shared-window address
+__device__ __forceinline__ float4 lds_f4(uint32_t saddr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(saddr));
+  return v;
+}
+
 // global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

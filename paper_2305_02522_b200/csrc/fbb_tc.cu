@@ -41,25 +41,39 @@ __device__ __forceinline__ bool tc_is_conv(int w) { return w == 2 || w == 3 || w
 __device__ __forceinline__ int tc_conv_index(int w) { return w < 4 ? w - 2 : w - 6; }
 
 __device__ __forceinline__ uint32_t sign4(float x0, float x1, float x2, float x3) {
-  const uint32_t m = static_cast<uint32_t>(x0 >= 0.0f) | (static_cast<uint32_t>(x1 >= 0.0f) << 1) |
-                     (static_cast<uint32_t>(x2 >= 0.0f) << 2) | (static_cast<uint32_t>(x3 >= 0.0f) << 3);
-  return 0xFFFFFFFFu - 0xFEu * ((m * 0x00204081u) & 0x01010101u);  // 1 -> 0x01, 0 -> 0xFF per byte
+  return pm1_bytes4(x0, x1, x2, x3);
 }
 
 __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
-// a wait that traps instead of hanging if a phase never completes
-__device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t ok = 0;
-  for (uint32_t it = 0; it < (1u << 26) && !ok; ++it)
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(smem_addr(bar)), "r"(parity)
-        : "memory");
-  if (!ok) __trap();
+// A wait that traps instead of hanging if a phase never completes (2 s of
+// global time).  Each try suspends the thread until the phase completes or
+// `hint` ns pass, so a warp parked behind the pipeline does not spin through
+// issue slots the converters and the epilogue need (hint 0: the hardware's
+// own short limit).
+__device__ __forceinline__ uint32_t tc_try(uint64_t* bar, uint32_t parity, uint32_t hint) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity), "r"(hint)
+      : "memory");
+  return ok;
+}
+__device__ __forceinline__ uint64_t tc_now() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __noinline__ void tc_wait_slow(uint64_t* bar, uint32_t parity, uint32_t hint) {
+  const uint64_t t0 = tc_now();
+  while (!tc_try(bar, parity, hint))
+    if (tc_now() - t0 > 2000000000ull) __trap();
+}
+__device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity, uint32_t hint) {
+  if (!tc_try(bar, parity, hint)) tc_wait_slow(bar, parity, hint);
 }
 
 __device__ __forceinline__ uint64_t tc_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -76,6 +90,7 @@ struct TcArgs {
   const uint32_t* wt;  // ncols x kspw transposed weight bits (pair: W1 | pad | W2)
   int64_t rows;
   int k, kspw, kpad, n, ncols, ospw, pr, prlog, slots, abufs;
+  uint32_t hint;       // try_wait suspend hint, ns
   uint32_t pmagic;     // t / gp by magic multiply (item -> row group)
   uint32_t* out;
   uint32_t* out2;      // pair: columns [ncols/2, ncols) of the accumulator
@@ -134,25 +149,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_fbb_tc(const TcArgs a) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
-  // piece u of this CTA: tile blockIdx.x + (u / ppt) * grid, rows + pr * (u % ppt)
-  auto piece_rows = [&](int64_t u, int64_t* r0) {
-    *r0 = (blockIdx.x + (u / ppt) * gridDim.x) * kTcM + static_cast<int64_t>(a.pr) * (u % ppt);
-    const int64_t left = a.rows - *r0;
+  // Piece u of this CTA is piece p = u % ppt of tile j = u / ppt (rows
+  // tile0 + pr * p, tile0 = (blockIdx.x + j * grid) * 128) and uses ring slot
+  // u % slots and A buffer j % abufs; every role walks these with counters
+  // (no 64-bit divisions per piece).
+  const int64_t tstep = static_cast<int64_t>(gridDim.x) * kTcM;
+  auto piece_len = [&](int64_t r0) {
+    const int64_t left = a.rows - r0;
     return static_cast<int>(left <= 0 ? 0 : left < a.pr ? left : a.pr);
   };
 
   if (warp == 0) {
     // ---------------- producer ----------------
-    if (lane == 0)
+    if (lane == 0) {
+      int s = 0, p = 0;
+      uint32_t ph = 0;  // (u / slots) & 1
+      int64_t tile0 = static_cast<int64_t>(blockIdx.x) * kTcM;
       for (int64_t u = 0; u < npieces; ++u) {
-        const int s = static_cast<int>(u % a.slots);
         if (u >= a.slots) {
-          tc_wait(&empty[s], static_cast<uint32_t>((u / a.slots - 1) & 1));
+          tc_wait(&empty[s], ph ^ 1u, a.hint);
           // the converters' generic reads of the slot before the bulk copy's async-proxy writes
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
-        int64_t r0;
-        const int nr = piece_rows(u, &r0);
+        const int64_t r0 = tile0 + static_cast<int64_t>(a.pr) * p;
+        const int nr = piece_len(r0);
         const uint32_t bytes = static_cast<uint32_t>(nr) * static_cast<uint32_t>(a.k) * 4u;
         if (nr == a.pr && bytes % 16 == 0) {
           mbar_expect_tx(&full[s], bytes);
@@ -160,15 +180,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_fbb_tc(const TcArgs a) {
         } else {
           mbar_arrive1(&full[s]);  // partial piece: the converters read it from global memory
         }
+        if (++s == a.slots) s = 0, ph ^= 1u;
+        if (++p == ppt) p = 0, tile0 += tstep;
       }
+    }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
                            (static_cast<uint32_t>(kTcM >> 4) << 24);  // kind::i8, s32 += s8 x s8, K-major
+    int ab = 0;
+    uint32_t aph = 0;  // (j / abufs) & 1
     for (int64_t j = 0; j < my; ++j) {
-      const int b = static_cast<int>(j & 1), ab = static_cast<int>(j % a.abufs);
-      tc_wait(&a_full[ab], static_cast<uint32_t>((j / a.abufs) & 1));
-      if (j >= 2) tc_wait(&acc_empty[b], static_cast<uint32_t>((j / 2 - 1) & 1));
+      const int b = static_cast<int>(j & 1);
+      tc_wait(&a_full[ab], aph, a.hint);
+      if (j >= 2) tc_wait(&acc_empty[b], static_cast<uint32_t>(((j >> 1) - 1) & 1), a.hint);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (lane == 0) {
         const uint32_t abase = smem_addr(A + static_cast<size_t>(ab) * kpad * kTcM), bbase = smem_addr(B);
@@ -191,13 +216,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_fbb_tc(const TcArgs a) {
                      : "memory");
       }
       __syncwarp();
+      if (++ab == a.abufs) ab = 0, aph ^= 1u;
     }
   } else if (warp >= 4 && warp < 8) {
     // ---------------- epilogue: TMEM lanes 32*(warp-4) .. +31 ----------------
     const int q = warp - 4;
     for (int64_t j = 0; j < my; ++j) {
       const int b = static_cast<int>(j & 1);
-      tc_wait(&acc_full[b], static_cast<uint32_t>((j / 2) & 1));
+      tc_wait(&acc_full[b], static_cast<uint32_t>((j >> 1) & 1), a.hint);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t row = (blockIdx.x + j * gridDim.x) * kTcM + 32 * q + lane;
       for (int h = 0; h < (a.out2 ? 2 : 1); ++h) {
@@ -242,18 +268,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_fbb_tc(const TcArgs a) {
     const int cw = tc_conv_index(warp), ct = cw * 32 + lane;
     const int gp = (a.k + 15) / 16;                // 16-column groups per row
     const int items = a.pr * gp;                   // (row, group) per piece; item t -> row t % pr, group t / pr
+    int s = 0, p = 0, ab = 0;
+    uint32_t ph = 0, aph = 0;  // (u / slots) & 1, (j / abufs) & 1
+    int64_t j = 0, tile0 = static_cast<int64_t>(blockIdx.x) * kTcM;
     for (int64_t u = 0; u < npieces; ++u) {
-      const int s = static_cast<int>(u % a.slots);
-      const int64_t j = u / ppt;
-      const int ab = static_cast<int>(j % a.abufs);
-      if (u % ppt == 0 && j >= a.abufs) tc_wait(&a_empty[ab], static_cast<uint32_t>((j / a.abufs - 1) & 1));
-      tc_wait(&full[s], static_cast<uint32_t>((u / a.slots) & 1));
-      int64_t r0;
-      const int nr = piece_rows(u, &r0);
+      if (p == 0 && j >= a.abufs) tc_wait(&a_empty[ab], aph ^ 1u, a.hint);
+      tc_wait(&full[s], ph, a.hint);
+      const int64_t r0 = tile0 + static_cast<int64_t>(a.pr) * p;
+      const int nr = piece_len(r0);
       const bool staged = nr == a.pr && (static_cast<uint32_t>(nr) * a.k * 4u) % 16 == 0;
       const float* src = staged ? ring + s * slot_floats : a.x + r0 * a.k;
       uint8_t* At = A + static_cast<size_t>(ab) * kpad * kTcM;
-      const int rbase = a.pr * static_cast<int>(u % ppt);
+      const int rbase = a.pr * p;
       for (int t = ct; t < items; t += kTcConv * 32) {
         const int r = t & (a.pr - 1), g = t >> a.prlog;  // pr is a power of two
         const int c0 = 16 * g;
@@ -265,7 +291,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_fbb_tc(const TcArgs a) {
             if ((a.k & 3) == 0) {
 #pragma unroll
               for (int h = 0; h < 4; ++h) {
-                const float4 f = reinterpret_cast<const float4*>(xr)[h];
+                const float4 f = lds_f4(smem_addr(xr) + 16u * h);
                 e[4 * h] = f.x, e[4 * h + 1] = f.y, e[4 * h + 2] = f.z, e[4 * h + 3] = f.w;
               }
             } else if ((a.k & 1) == 0) {
@@ -291,7 +317,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_fbb_tc(const TcArgs a) {
       __syncwarp();
       if (lane == 0) {
         mbar_arrive1(&empty[s]);
-        if (u % ppt == ppt - 1) mbar_arrive1(&a_full[ab]);
+        if (p == ppt - 1) mbar_arrive1(&a_full[ab]);
+      }
+      if (++s == a.slots) s = 0, ph ^= 1u;
+      if (++p == ppt) {
+        p = 0, ++j, tile0 += tstep;
+        if (++ab == a.abufs) ab = 0, aph ^= 1u;
       }
     }
   }
@@ -331,6 +362,8 @@ bool fbb_tc(const BmmArgs& a, cudaStream_t s) {
   t.ospw = static_cast<int>(spw(a.n, a.wb));
   t.out = a.out_bits;
   t.out2 = a.out_bits2;
+  t.hint = 0;
+  if (const char* e = std::getenv("BG_TC_HINT")) t.hint = static_cast<uint32_t>(std::atoi(e));
   // shared memory: weights + A buffers + the fp32 ring; the largest pieces
   // (rows) and then two A buffers if they fit
   const size_t wbytes = static_cast<size_t>(t.kpad) * N, abytes = static_cast<size_t>(t.kpad) * kTcM;

@@ -55,9 +55,7 @@ constexpr int kTmPieces = kTmM / kTmPR;                // pieces per tile
 constexpr int kTmMaxSlots = 4;
 
 __device__ __forceinline__ uint32_t tm_sign4(float x0, float x1, float x2, float x3) {
-  const uint32_t m = static_cast<uint32_t>(x0 >= 0.0f) | (static_cast<uint32_t>(x1 >= 0.0f) << 1) |
-                     (static_cast<uint32_t>(x2 >= 0.0f) << 2) | (static_cast<uint32_t>(x3 >= 0.0f) << 3);
-  return 0xFFFFFFFFu - 0xFEu * ((m * 0x00204081u) & 0x01010101u);  // 1 -> 0x01, 0 -> 0xFF per byte
+  return pm1_bytes4(x0, x1, x2, x3);
 }
 
 __device__ __forceinline__ void tm_arrive(uint64_t* bar) {
@@ -395,8 +393,8 @@ __global__ void __launch_bounds__(kTmThreads, 1) k_fbb_tmem(const TmArgs a) {
               if (staged && (a.k & 1) == 0) {
                 // rows are 8-byte aligned in the slot; floats past K (the last
                 // step) read the next row or the slot pad and meet zero weights
-                const float2* p2 = reinterpret_cast<const float2*>(slot + static_cast<int64_t>(ri) * a.k + k0);
-                const float2 x0 = p2[0], x1 = p2[1], x2 = p2[2], x3 = p2[3];
+                const uint32_t p2 = smem_addr(slot) + 4u * static_cast<uint32_t>(ri * a.k + k0);
+                const float2 x0 = lds_f2(p2), x1 = lds_f2(p2 + 8), x2 = lds_f2(p2 + 16), x3 = lds_f2(p2 + 24);
                 c[2 * rr] = tm_sign4(x0.x, x0.y, x1.x, x1.y);
                 c[2 * rr + 1] = tm_sign4(x2.x, x2.y, x3.x, x3.y);
               } else {

@@ -15,6 +15,8 @@
 // float((alpha_i dot_k) beta_k) (kernels.cpp:179-190) from one popcount per
 // row, optionally with the following row softmax (graphops.cpp:372-386) in
 // the same pass.  Any other consumer materializes the fp32 tensor first.
+#include <cstdlib>
+
 #include "ops.cuh"
 
 namespace bg {
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(256) k_fbf_lookup(const uint32_t* __restrict__
                                                     int xspw, int n, uint32_t nmagic,
                                                     const float* __restrict__ tab_logits,
                                                     const float* __restrict__ tab_probs, float* __restrict__ logits,
-                                                    float* __restrict__ probs) {
+                                                    float* __restrict__ probs, int vec4) {
   __shared__ int cnt[kLookRows];
   for (int64_t b0 = r0 + static_cast<int64_t>(blockIdx.x) * kLookRows; b0 < r1;
        b0 += static_cast<int64_t>(gridDim.x) * kLookRows) {
@@ -142,6 +144,22 @@ __global__ void __launch_bounds__(256) k_fbf_lookup(const uint32_t* __restrict__
     float* ol = logits ? logits + b0 * n : nullptr;  // null: the logits are not wanted
     float* op = probs ? probs + b0 * n : nullptr;
     const int total = nr * n;
+    if (vec4) {  // four consecutive elements per thread, one 16-byte store per output
+      for (int e = 4 * static_cast<int>(threadIdx.x); e < total; e += 4 * static_cast<int>(blockDim.x)) {
+        int r = static_cast<int>(__umulhi(static_cast<uint32_t>(e), nmagic)), j = e - r * n;
+        float vl[4], vp[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int src = cnt[r] * n + j;
+          if (ol) vl[i] = __ldg(tab_logits + src);
+          if (op) vp[i] = __ldg(tab_probs + src);
+          if (++j == n) j = 0, ++r;
+        }
+        if (ol) __stcs(reinterpret_cast<float4*>(ol + e), make_float4(vl[0], vl[1], vl[2], vl[3]));
+        if (op) __stcs(reinterpret_cast<float4*>(op + e), make_float4(vp[0], vp[1], vp[2], vp[3]));
+      }
+      continue;
+    }
     for (int e = threadIdx.x; e < total; e += blockDim.x) {
       const int r = static_cast<int>(__umulhi(static_cast<uint32_t>(e), nmagic)), j = e - r * n;  // e / n
       const int src = cnt[r] * n + j;
@@ -195,8 +213,14 @@ void packed_fbf(const uint32_t* bits, int64_t r0, int64_t r1, int64_t k, int xwb
   const int64_t blocks = std::min<int64_t>(cdiv(r1 - r0, kLookRows), 16LL * sm_count());
   // e / n == umulhi(e, ceil(2^32 / n)) for e < kLookRows * n (e * n < 2^32)
   const uint32_t nmagic = static_cast<uint32_t>(((uint64_t{1} << 32) + n - 1) / n);
+  // 16-byte stores when every block's span starts 16-byte aligned (kLookRows * n
+  // floats per full block; the last block's tail is a multiple of 4 too)
+  auto al16 = [](const float* p) { return p == nullptr || reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+  const bool v4 = !std::getenv("BG_LOOKUP_SCALAR") && (r1 - r0) * n % 4 == 0 && al16(logits ? logits + r0 * n : nullptr) &&
+                  al16(probs ? probs + r0 * n : nullptr);
   k_fbf_lookup<<<static_cast<unsigned>(blocks), 256, 0, s>>>(bits, r0, r1, static_cast<int>(spw(k, xwb)),
-                                                             static_cast<int>(n), nmagic, tl, tp, logits, probs);
+                                                             static_cast<int>(n), nmagic, tl, tp, logits, probs,
+                                                             v4 ? 1 : 0);
   BG_LAUNCH_CHECK();
 }
 

@@ -84,3 +84,24 @@ def test_default_fbb_at_dispatch_sizes(mkn):
     got = bg.bmm("BMM.FBB", torch.from_numpy(A).cuda(), dw, 32)
     want = po.bmm("BMM.FBB", po.Mat.dense(A), ow, 32)
     assert bits_equal(got.bits.numpy(), want.bits)
+
+
+@pytest.mark.parametrize("mkn", [(1000, 602, 128), (300, 100, 128), (4096, 301, 96), (257, 33, 21)])
+def test_fbb_special_values(umma, mkn):
+    # the fp32 -> +-1 conversion of every kernel on the values a sign test
+    # can get wrong: -0.0 (>= 0), NaN (not >= 0, either sign), +-inf,
+    # subnormals of both signs, the smallest normals
+    m, k, n = mkn
+    rng = po.Rng(9090 + m + k + n)
+    A, W = rng.random_dense(m, k), rng.random_dense(k, n)
+    special = np.array([0.0, -0.0, np.nan, -np.nan, np.inf, -np.inf, 1e-45, -1e-45, 1e-40, -1e-40,
+                        np.finfo(np.float32).tiny, -np.finfo(np.float32).tiny], dtype=np.float32)
+    idx = rng.random_dense(1, m * k // 3).ravel()
+    pos = (np.abs(idx) * 1e6).astype(np.int64) % (m * k)
+    A.flat[pos] = special[np.arange(pos.size) % special.size]
+    wbits = po.binarize(W, 32)
+    dw = bg.BitOperand(bg.BitDenseMatrix.from_numpy(wbits, k, n, 32))
+    ow = po.Mat.binary(wbits, k, n, 32)
+    got = bg.bmm("BMM.FBB", torch.from_numpy(A).cuda(), dw, 32)
+    want = po.bmm("BMM.FBB", po.Mat.dense(A), ow, 32)
+    assert bits_equal(got.bits.numpy(), want.bits)
