@@ -121,15 +121,19 @@ __global__ void k_fbf_table(int64_t k, double pval, const uint32_t* __restrict__
 }
 
 // Block per kLookRows rows of [r0, r1): the rows' popcounts into shared
-// memory, then the block's contiguous output span element by element from
-// the table rows they pick (coalesced stores, 32-bit index arithmetic).
+// memory as the offset of each row's table row from its output span
+// (delta[r] = (popc_r - r) * n, so element e of the block's contiguous span
+// reads table element e + delta[e / n]), then the span element by element
+// (WL / WP: logits / probabilities wanted; V4: four consecutive elements and
+// one 16-byte streaming store per output per thread).
 constexpr int kLookRows = 256;
+template <bool WL, bool WP, bool V4>
 __global__ void __launch_bounds__(256) k_fbf_lookup(const uint32_t* __restrict__ bits, int64_t r0, int64_t r1,
                                                     int xspw, int n, uint32_t nmagic,
                                                     const float* __restrict__ tab_logits,
                                                     const float* __restrict__ tab_probs, float* __restrict__ logits,
-                                                    float* __restrict__ probs, int vec4) {
-  __shared__ int cnt[kLookRows];
+                                                    float* __restrict__ probs) {
+  __shared__ int delta[kLookRows];
   for (int64_t b0 = r0 + static_cast<int64_t>(blockIdx.x) * kLookRows; b0 < r1;
        b0 += static_cast<int64_t>(gridDim.x) * kLookRows) {
     const int nr = static_cast<int>(r1 - b0 < kLookRows ? r1 - b0 : kLookRows);
@@ -138,33 +142,38 @@ __global__ void __launch_bounds__(256) k_fbf_lookup(const uint32_t* __restrict__
       const uint32_t* row = bits + (b0 + threadIdx.x) * xspw;
       int c = 0;
       for (int q = 0; q < xspw; ++q) c += __popc(__ldg(row + q));
-      cnt[threadIdx.x] = c;
+      delta[threadIdx.x] = (c - static_cast<int>(threadIdx.x)) * n;
     }
     __syncthreads();
-    float* ol = logits ? logits + b0 * n : nullptr;  // null: the logits are not wanted
-    float* op = probs ? probs + b0 * n : nullptr;
+    float* ol = logits + (WL ? b0 * n : 0);
+    float* op = probs + (WP ? b0 * n : 0);
     const int total = nr * n;
-    if (vec4) {  // four consecutive elements per thread, one 16-byte store per output
-      for (int e = 4 * static_cast<int>(threadIdx.x); e < total; e += 4 * static_cast<int>(blockDim.x)) {
-        int r = static_cast<int>(__umulhi(static_cast<uint32_t>(e), nmagic)), j = e - r * n;
-        float vl[4], vp[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int src = cnt[r] * n + j;
-          if (ol) vl[i] = __ldg(tab_logits + src);
-          if (op) vp[i] = __ldg(tab_probs + src);
-          if (++j == n) j = 0, ++r;
-        }
-        if (ol) __stcs(reinterpret_cast<float4*>(ol + e), make_float4(vl[0], vl[1], vl[2], vl[3]));
-        if (op) __stcs(reinterpret_cast<float4*>(op + e), make_float4(vp[0], vp[1], vp[2], vp[3]));
+    if (V4) {
+      const int tail = total & ~3;  // the last (partial) block's 1-3 trailing elements: scalar, below
+      if (static_cast<int>(threadIdx.x) < total - tail) {
+        const int e = tail + threadIdx.x;
+        const int src = e + delta[__umulhi(static_cast<uint32_t>(e), nmagic)];
+        if (WL) ol[e] = __ldg(tab_logits + src);
+        if (WP) op[e] = __ldg(tab_probs + src);
       }
-      continue;
-    }
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {
-      const int r = static_cast<int>(__umulhi(static_cast<uint32_t>(e), nmagic)), j = e - r * n;  // e / n
-      const int src = cnt[r] * n + j;
-      if (ol) ol[e] = __ldg(tab_logits + src);
-      if (op) op[e] = __ldg(tab_probs + src);
+      for (int e = 4 * static_cast<int>(threadIdx.x); e < tail; e += 4 * kLookRows) {
+        int src[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)  // (e + i) / n by the magic multiply
+          src[i] = e + i + delta[__umulhi(static_cast<uint32_t>(e + i), nmagic)];
+        if (WL)
+          __stcs(reinterpret_cast<float4*>(ol + e), make_float4(__ldg(tab_logits + src[0]), __ldg(tab_logits + src[1]),
+                                                                __ldg(tab_logits + src[2]), __ldg(tab_logits + src[3])));
+        if (WP)
+          __stcs(reinterpret_cast<float4*>(op + e), make_float4(__ldg(tab_probs + src[0]), __ldg(tab_probs + src[1]),
+                                                                __ldg(tab_probs + src[2]), __ldg(tab_probs + src[3])));
+      }
+    } else {
+      for (int e = threadIdx.x; e < total; e += kLookRows) {
+        const int src = e + delta[__umulhi(static_cast<uint32_t>(e), nmagic)];
+        if (WL) ol[e] = __ldg(tab_logits + src);
+        if (WP) op[e] = __ldg(tab_probs + src);
+      }
     }
   }
 }
@@ -213,14 +222,22 @@ void packed_fbf(const uint32_t* bits, int64_t r0, int64_t r1, int64_t k, int xwb
   const int64_t blocks = std::min<int64_t>(cdiv(r1 - r0, kLookRows), 16LL * sm_count());
   // e / n == umulhi(e, ceil(2^32 / n)) for e < kLookRows * n (e * n < 2^32)
   const uint32_t nmagic = static_cast<uint32_t>(((uint64_t{1} << 32) + n - 1) / n);
-  // 16-byte stores when every block's span starts 16-byte aligned (kLookRows * n
-  // floats per full block; the last block's tail is a multiple of 4 too)
+  // 16-byte stores when every block's span starts 16-byte aligned (a full
+  // block is kLookRows * n floats; the last block's 1-3 odd elements go scalar)
   auto al16 = [](const float* p) { return p == nullptr || reinterpret_cast<uintptr_t>(p) % 16 == 0; };
-  const bool v4 = !std::getenv("BG_LOOKUP_SCALAR") && (r1 - r0) * n % 4 == 0 && al16(logits ? logits + r0 * n : nullptr) &&
-                  al16(probs ? probs + r0 * n : nullptr);
-  k_fbf_lookup<<<static_cast<unsigned>(blocks), 256, 0, s>>>(bits, r0, r1, static_cast<int>(spw(k, xwb)),
-                                                             static_cast<int>(n), nmagic, tl, tp, logits, probs,
-                                                             v4 ? 1 : 0);
+  const bool v4 = al16(logits ? logits + r0 * n : nullptr) && al16(probs ? probs + r0 * n : nullptr);
+  const unsigned g = static_cast<unsigned>(blocks);
+  const int xs = static_cast<int>(spw(k, xwb)), nn = static_cast<int>(n);
+#define BG_LOOKUP(WL, WP, V4) \
+  k_fbf_lookup<WL, WP, V4><<<g, kLookRows, 0, s>>>(bits, r0, r1, xs, nn, nmagic, tl, tp, logits, probs)
+  if (logits && probs) {
+    if (v4) BG_LOOKUP(true, true, true); else BG_LOOKUP(true, true, false);
+  } else if (probs) {
+    if (v4) BG_LOOKUP(false, true, true); else BG_LOOKUP(false, true, false);
+  } else if (logits) {
+    if (v4) BG_LOOKUP(true, false, true); else BG_LOOKUP(true, false, false);
+  }
+#undef BG_LOOKUP
   BG_LAUNCH_CHECK();
 }
 
