@@ -90,11 +90,19 @@ __global__ void k_const_rows(const uint32_t* __restrict__ wt, int64_t k, int64_t
 // logit rows (and their softmax rows) are computed once (one thread per c,
 // the reference's arithmetic), and every output element is a table lookup --
 // the pass is bound by writing the outputs.
-__global__ void k_fbf_table(int64_t k, double pval, const uint32_t* __restrict__ wt, int64_t kspw,
-                            const float* __restrict__ beta, int64_t n, int want_probs,
-                            float* __restrict__ tab_logits, float* __restrict__ tab_probs) {
-  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (c > k) return;
+// Warp per c: the lanes take the columns j = lane, lane + 32, ... of row c
+// (logits in parallel; a column's popcount does not depend on c), the max by
+// a warp reduction (order-free), then the softmax sum in the reference's
+// sequential column order -- each exp broadcast from its lane and added in
+// turn -- and the probabilities in parallel again.
+constexpr int kTabWarps = 4;
+__global__ void __launch_bounds__(kTabWarps * 32)
+    k_fbf_table(int64_t k, double pval, const uint32_t* __restrict__ wt, int64_t kspw,
+                const float* __restrict__ beta, int64_t n, int want_probs, float* __restrict__ tab_logits,
+                float* __restrict__ tab_probs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * kTabWarps + (threadIdx.x >> 5);
+  if (c > k) return;  // warp-uniform
   // binarize_with_scale row scale (bitdense.cpp:95-102): sum |x| in double
   // (pval c, exact for pval = 2), / cols, floor 1e-12, float
   double s = pval * static_cast<double>(c);
@@ -102,21 +110,27 @@ __global__ void k_fbf_table(int64_t k, double pval, const uint32_t* __restrict__
   const double a = static_cast<double>(static_cast<float>(s > 1e-12 ? s : 1e-12));
   float* yl = tab_logits + c * n;
   float mx = -INFINITY;
-  for (int64_t j = 0; j < n; ++j) {
+  for (int64_t j = lane; j < n; j += 32) {
     int64_t pc = 0;
-    for (int64_t q = 0; q < kspw; ++q) pc += __popc(wt[j * kspw + q]);
+    for (int64_t q = 0; q < kspw; ++q) pc += __popc(__ldg(wt + j * kspw + q));
     const double dot = static_cast<double>(2 * pc - k);  // the all-ones row against w_j
     // float((alpha dot) beta)  (kernels.cpp:179-190)
     yl[j] = __double2float_rn(__dmul_rn(__dmul_rn(a, dot), static_cast<double>(beta[j])));
     mx = fmaxf(mx, yl[j]);
   }
   if (!want_probs) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
   // softmax_rows (graphops.cpp:372-386): double max, sequential double sum of
   // exp(x - max), float(exp(x - max) / sum)
   const double m = static_cast<double>(mx);
   double sum = 0.0;
-  for (int64_t j = 0; j < n; ++j) sum = __dadd_rn(sum, exp(static_cast<double>(yl[j]) - m));
-  for (int64_t j = 0; j < n; ++j)
+  for (int64_t j0 = 0; j0 < n; j0 += 32) {
+    const double ej = j0 + lane < n ? exp(static_cast<double>(yl[j0 + lane]) - m) : 0.0;
+    const int cnt = static_cast<int>(n - j0 < 32 ? n - j0 : 32);
+    for (int q = 0; q < cnt; ++q) sum = __dadd_rn(sum, __shfl_sync(0xFFFFFFFFu, ej, q));
+  }
+  for (int64_t j = lane; j < n; j += 32)
     tab_probs[c * n + j] = __double2float_rn(__ddiv_rn(exp(static_cast<double>(yl[j]) - m), sum));
 }
 
@@ -216,8 +230,8 @@ void packed_fbf(const uint32_t* bits, int64_t r0, int64_t r1, int64_t k, int xwb
   // the (K+1) x n tables (a few KB, caller's workspace) are rebuilt per call
   float* tl = table;
   float* tp = tl + (k + 1) * n;
-  k_fbf_table<<<static_cast<unsigned>(cdiv(k + 1, 64)), 64, 0, s>>>(k, static_cast<double>(pval), wt, spw(k, wb),
-                                                                   beta, n, probs ? 1 : 0, tl, tp);
+  k_fbf_table<<<static_cast<unsigned>(cdiv(k + 1, kTabWarps)), kTabWarps * 32, 0, s>>>(
+      k, static_cast<double>(pval), wt, spw(k, wb), beta, n, probs ? 1 : 0, tl, tp);
   BG_LAUNCH_CHECK();
   const int64_t blocks = std::min<int64_t>(cdiv(r1 - r0, kLookRows), 16LL * sm_count());
   // e / n == umulhi(e, ceil(2^32 / n)) for e < kLookRows * n (e * n < 2^32)
